@@ -1,1 +1,30 @@
-"""B200-native CaRtGS mapping hot path (placeholder, filled below)."""
+"""B200-native CaRtGS mapping hot path (arxiv 2410.00486).
+
+Drop-in for the mapping path of the reference package ``splatstream``:
+the same render / loss / optimise API names (``__init__.py:45-79`` and
+``rasterizer/__init__.py:21-36`` of the reference), computing in
+hand-written sm_100a kernels (libss_b200.so, C ABI in
+include/splatstream_b200.h).  There is no CPU fallback: operators raise if
+the CUDA library or device is missing.
+"""
+
+from .core import Camera, GaussianMap, logistic, logit
+from .densify import (DensifyConfig, DensifyResult, accumulate_grad_stats, densify_and_prune,
+                      opacity_reset)
+from .engine import EngineConfig, MappingEngine
+from .losses import LossBreakdown, compute_losses, depth_l1, opacity_reg, total_loss
+from .optimizer import AdamState, LearningRates, adam_step, resize_for_densify
+from .rasterizer import (ParamGrads, Projection, RasterOpts, RenderOutput, TileIndex,
+                         backward_splatwise, rasterize_forward, screen_space_grads)
+from .scene import CONFIGS, survey_camera, survey_scene
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AdamState", "Camera", "CONFIGS", "DensifyConfig", "DensifyResult", "EngineConfig",
+    "GaussianMap", "LearningRates", "LossBreakdown", "MappingEngine", "ParamGrads", "Projection",
+    "RasterOpts", "RenderOutput", "TileIndex", "accumulate_grad_stats", "adam_step",
+    "backward_splatwise", "compute_losses", "densify_and_prune", "depth_l1", "logistic", "logit",
+    "opacity_reg", "opacity_reset", "rasterize_forward", "resize_for_densify",
+    "screen_space_grads", "survey_camera", "survey_scene", "total_loss",
+]

@@ -1,0 +1,484 @@
+// binning.cu -- K2-K4b: duplicate-with-keys, onesweep radix sort, tile ranges.
+//
+// Replaces build_tile_index (rasterizer/tiles.py:29-65), whose order is
+// np.lexsort((splat, depth, tile)) (tiles.py:58): pairs sorted by tile,
+// then camera depth, then splat index.  That order equals a STABLE sort of
+// 64-bit keys tile<<32 | float_bits(depth) over pairs emitted in splat
+// order (depth > near > 0, so the float bits are monotone).  An LSD radix
+// sort of those keys processes the 32 depth bits first; because the depth
+// half of a pair's key is a function of its splat alone, those passes are
+// run here over the N splats instead of the P ~ 12 N pairs:
+//
+//   1. onesweep LSD sort of the N depth keys (4 x 8-bit passes), stable,
+//      values = splat index                     -> splats in (depth, index) order
+//   2. exclusive scan of touched-tile counts in that order  -> pair offsets, P
+//   3. emission of (tile, splat) pairs in that order, with the tile-digit
+//      histograms accumulated on the fly
+//   4. onesweep LSD sort of the pair tile ids (ceil(log2 T / 8) passes),
+//      stable                                   -> (tile, depth, index) order
+//   5. tile ranges by boundary detection; checkpoint slot bases by scan.
+//
+// The result is bit-identical to the reference order (tests/test_gpu_parity.py
+// compares it with the oracle's build_tile_index fed this projection).
+//
+// Onesweep pass: one CTA per 256*ITEMS keys with a dynamic tile id, warp-
+// level stable ranking with __match_any_sync, per-digit decoupled look-back
+// through a (block, digit) status array, direct scatter.
+#include "common.cuh"
+
+namespace ss {
+
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagInc = 2u << 30;
+constexpr uint32_t kValMask = (1u << 30) - 1;
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_volatile64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ------------------------------------------------------------- histogram
+// 256-bin histograms of `npass` consecutive 8-bit digits starting at shift0.
+__global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys,
+                                                         uint32_t n, int npass, int shift0,
+                                                         uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[4][256];
+    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) (&h[0][0])[k] = 0;
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint32_t k = keys[i];
+        for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(k >> (shift0 + 8 * p)) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < npass * 256; k += blockDim.x) {
+        uint32_t v = (&h[0][0])[k];
+        if (v) atomicAdd(&hist[k], v);
+    }
+}
+
+// --------------------------------------------------------------- onesweep
+// keys_in == nullptr is not allowed; vals_in == nullptr means "values are
+// the item indices" (first pass over splats).  d_count: number of items
+// (device), clamped to cap.
+template <int ITEMS>
+__global__ void __launch_bounds__(256) onesweep_kernel(
+    const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+    uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, const uint32_t* d_count,
+    uint32_t n_static, uint32_t cap, int shift, const uint32_t* __restrict__ hist,
+    uint32_t* status, uint32_t* counter) {
+    constexpr int WARP_ITEMS = 32 * ITEMS;
+    constexpr int TILE = 256 * ITEMS;
+    __shared__ uint32_t s_bid;
+    __shared__ uint32_t s_cnt[8][256];
+    __shared__ uint32_t s_base[256];
+    __shared__ uint32_t s_warp_tot[8];
+    const int t = threadIdx.x, w = t >> 5, l = t & 31;
+    if (t == 0) s_bid = atomicAdd(counter, 1u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s_cnt[k][t] = 0;
+    __syncthreads();
+    const uint32_t bid = s_bid;
+    uint32_t n = d_count ? min(*d_count, cap) : n_static;
+    const uint32_t base = bid * TILE;
+    if (base >= n) return;
+
+    uint32_t key[ITEMS], val[ITEMS], rank[ITEMS];
+    const uint32_t wbase = base + w * WARP_ITEMS;
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+        uint32_t idx = wbase + r * 32 + l;
+        bool v = idx < n;
+        key[r] = v ? keys_in[idx] : 0u;
+        val[r] = v ? (vals_in ? vals_in[idx] : idx) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+        uint32_t idx = wbase + r * 32 + l;
+        uint32_t d = idx < n ? ((key[r] >> shift) & 255u) : 256u;
+        unsigned peers = __match_any_sync(0xffffffffu, d);
+        uint32_t before = d < 256u ? s_cnt[w][d] : 0u;
+        rank[r] = before + __popc(peers & lanemask_lt());
+        __syncwarp();
+        if (d < 256u && (peers & lanemask_lt()) == 0) s_cnt[w][d] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // exclusive scan over warps for digit t, block total
+    uint32_t run = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        uint32_t c = s_cnt[k][t];
+        s_cnt[k][t] = run;
+        run += c;
+    }
+    const uint32_t total = run;
+    // global digit start: exclusive scan of hist over digits (block scan)
+    uint32_t hv = hist[t];
+    uint32_t incl = hv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += y;
+    }
+    if (l == 31) s_warp_tot[w] = incl;
+    // decoupled look-back for digit t
+    uint32_t* my = status + (size_t)bid * 256 + t;
+    uint32_t excl = 0;
+    if (bid == 0) {
+        st_volatile(my, kFlagInc | total);
+    } else {
+        st_volatile(my, kFlagAgg | total);
+        int64_t j = (int64_t)bid - 1;
+        while (j >= 0) {
+            uint32_t v = ld_volatile(status + (size_t)j * 256 + t);
+            uint32_t f = v & ~kValMask;
+            if (f == 0) continue;
+            excl += v & kValMask;
+            if (f == kFlagInc) break;
+            --j;
+        }
+        st_volatile(my, kFlagInc | (excl + total));
+    }
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (int k = 0; k < w; ++k) wpre += s_warp_tot[k];
+    s_base[t] = wpre + incl - hv + excl;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+        uint32_t idx = wbase + r * 32 + l;
+        if (idx < n) {
+            uint32_t d = (key[r] >> shift) & 255u;
+            uint32_t pos = s_base[d] + s_cnt[w][d] + rank[r];
+            vals_out[pos] = val[r];
+            if (keys_out) keys_out[pos] = key[r];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ scan
+// Exclusive scan of in[gather ? gather[i] : i] (u32), 64-bit look-back
+// words (2 flag bits + 62-bit sum).  total_out (u64, optional) and
+// optional capacity check writing the overflow flag.
+constexpr int kScanItems = 8;
+constexpr unsigned long long kSFlagAgg = 1ull << 62;
+constexpr unsigned long long kSFlagInc = 2ull << 62;
+constexpr unsigned long long kSValMask = (1ull << 62) - 1;
+
+template <bool CEIL_DIV32>
+__global__ void __launch_bounds__(256) scan_kernel(const uint32_t* __restrict__ in,
+                                                   const uint32_t* __restrict__ gather,
+                                                   const uint32_t* __restrict__ in_end, uint32_t n,
+                                                   uint32_t* __restrict__ out,
+                                                   unsigned long long* status, uint32_t* counter,
+                                                   int64_t* total_out, int64_t* overflow_out,
+                                                   int64_t capacity) {
+    constexpr int TILE = 256 * kScanItems;
+    __shared__ uint32_t s_bid;
+    __shared__ unsigned long long s_warp[8];
+    __shared__ unsigned long long s_excl;
+    const int t = threadIdx.x, w = t >> 5, l = t & 31;
+    if (t == 0) s_bid = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t bid = s_bid;
+    const uint32_t base = bid * TILE + t * kScanItems;
+    uint32_t v[kScanItems];
+    unsigned long long sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        uint32_t i = base + k;
+        uint32_t x = 0;
+        if (i < n) {
+            uint32_t src = gather ? gather[i] : i;
+            if (CEIL_DIV32)
+                x = (i + 1 < n) ? (in_end[src] - in[src] + 31u) >> 5 : 0u;
+            else
+                x = in[src];
+        }
+        v[k] = x;
+        sum += x;
+    }
+    unsigned long long incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += y;
+    }
+    if (l == 31) s_warp[w] = incl;
+    __syncthreads();
+    if (t == 0) {
+        unsigned long long tot = 0;
+        for (int k = 0; k < 8; ++k) {
+            unsigned long long c = s_warp[k];
+            s_warp[k] = tot;
+            tot += c;
+        }
+        unsigned long long* my = status + bid;
+        unsigned long long excl = 0;
+        if (bid == 0) {
+            st_volatile64(my, kSFlagInc | tot);
+        } else {
+            st_volatile64(my, kSFlagAgg | tot);
+            int64_t j = (int64_t)bid - 1;
+            while (j >= 0) {
+                unsigned long long x = ld_volatile64(status + j);
+                unsigned long long f = x & ~kSValMask;
+                if (f == 0) continue;
+                excl += x & kSValMask;
+                if (f == kSFlagInc) break;
+                --j;
+            }
+            st_volatile64(my, kSFlagInc | (excl + tot));
+        }
+        s_excl = excl;
+        if ((bid + 1) * (uint32_t)TILE >= n) {  // last block writes the total
+            if (total_out) *total_out = (int64_t)(excl + tot);
+            if (overflow_out && (int64_t)(excl + tot) > capacity) *overflow_out = 1;  // sticky
+        }
+    }
+    __syncthreads();
+    unsigned long long run = s_excl + s_warp[w] + incl - sum;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        uint32_t i = base + k;
+        if (i < n) out[i] = (uint32_t)run;
+        run += v[k];
+    }
+}
+
+// ------------------------------------------------------------------- emit
+// One thread per splat in (depth, index) order: write its touched tiles'
+// (tile, splat) pairs at its scanned offset; accumulate the 8-bit tile
+// digit histograms of the pair sort.
+__global__ void __launch_bounds__(256) emit_pairs_kernel(
+    uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restrict__ tiles,
+    const uint2* __restrict__ rect, const uint32_t* __restrict__ offsets, int tiles_x,
+    const int64_t* total, int64_t cap, int npass, uint32_t* __restrict__ keys,
+    uint32_t* __restrict__ vals, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[3][256];
+    for (int k = threadIdx.x; k < 3 * 256; k += blockDim.x) (&h[0][0])[k] = 0;
+    __syncthreads();
+    const bool ok = *total <= cap;
+    uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ok && j < n) {
+        uint32_t s = order[j];
+        uint32_t c = tiles[s];
+        if (c) {
+            uint2 rc = rect[s];
+            uint32_t x0 = rc.x & 0xffffu, y0 = rc.x >> 16, x1 = rc.y & 0xffffu, y1 = rc.y >> 16;
+            uint32_t o = offsets[j];
+            for (uint32_t ty = y0; ty <= y1; ++ty)
+                for (uint32_t tx = x0; tx <= x1; ++tx) {
+                    uint32_t tid = ty * tiles_x + tx;
+                    keys[o] = tid;
+                    vals[o] = s;
+                    ++o;
+                    for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(tid >> (8 * p)) & 255u], 1u);
+                }
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < npass * 256; k += blockDim.x) {
+        uint32_t v = (&h[0][0])[k];
+        if (v) atomicAdd(&hist[k], v);
+    }
+}
+
+// ----------------------------------------------------------------- ranges
+__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, const int64_t* total,
+                                   int64_t cap, uint32_t* __restrict__ start,
+                                   uint32_t* __restrict__ end) {
+    int64_t P = min(*total, cap);
+    if (*total > cap) P = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t t = keys[i];
+        if (i == 0 || keys[i - 1] != t) start[t] = (uint32_t)i;
+        if (i == P - 1 || keys[i + 1] != t) end[t] = (uint32_t)(i + 1);
+    }
+}
+
+// Copy a device int64 (clamped) into a u32 count for the onesweep passes.
+__global__ void clamp_count_kernel(const int64_t* total, int64_t cap, uint32_t* out) {
+    int64_t P = *total;
+    *out = (P > cap) ? 0u : (uint32_t)P;
+}
+
+// ------------------------------------------------------------ workspace
+struct BinWorkspace {
+    size_t off = 0;
+    char* base = nullptr;
+    template <typename T>
+    T* take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+        off += count * sizeof(T);
+        return p;
+    }
+};
+
+constexpr int kDepthItems = 4;   // 1024 splats per onesweep CTA
+constexpr int kPairItems = 16;   // 4096 pairs per onesweep CTA
+
+struct BinLayout {
+    // zero-initialised control region first
+    uint32_t* ctrl;            // counters
+    uint32_t* hist_depth;      // 4*256
+    uint32_t* hist_tile;       // 3*256
+    uint32_t* st_depth;        // 4 passes * blocks * 256
+    uint32_t* st_pair;         // npass * blocks * 256
+    unsigned long long* st_scan1;
+    unsigned long long* st_scan2;
+    size_t ctrl_bytes;
+    // data
+    uint32_t *kA, *vA, *kB, *vB;      // N
+    uint32_t* offsets;                // N
+    uint32_t *pk0, *pk1, *pv0, *pv1;  // pair capacity
+    uint32_t* pcount;                 // 1
+};
+
+inline int tile_passes(int n_tiles) {
+    int bits = 1;
+    while ((1ll << bits) < n_tiles) ++bits;
+    return (bits + 7) / 8;
+}
+
+BinLayout bin_layout(int64_t n, int64_t cap, int n_tiles, void* ws, size_t* bytes) {
+    BinWorkspace w;
+    w.base = reinterpret_cast<char*>(ws);
+    BinLayout L;
+    int db = div_up(n > 0 ? n : 1, 256 * kDepthItems);
+    int pb = div_up(cap > 0 ? cap : 1, 256 * kPairItems);
+    int np = tile_passes(n_tiles);
+    L.ctrl = w.take<uint32_t>(16);
+    L.hist_depth = w.take<uint32_t>(4 * 256);
+    L.hist_tile = w.take<uint32_t>(3 * 256);
+    L.st_depth = w.take<uint32_t>((size_t)4 * db * 256);
+    L.st_pair = w.take<uint32_t>((size_t)np * pb * 256);
+    L.st_scan1 = w.take<unsigned long long>(div_up(n > 0 ? n : 1, 256 * kScanItems) + 1);
+    L.st_scan2 = w.take<unsigned long long>(div_up(n_tiles + 1, 256 * kScanItems) + 1);
+    w.off = (w.off + 255) & ~size_t(255);
+    L.ctrl_bytes = w.off;
+    L.kA = w.take<uint32_t>(n);
+    L.vA = w.take<uint32_t>(n);
+    L.kB = w.take<uint32_t>(n);
+    L.vB = w.take<uint32_t>(n);
+    L.offsets = w.take<uint32_t>(n);
+    L.pk0 = w.take<uint32_t>(cap);
+    L.pk1 = w.take<uint32_t>(cap);
+    L.pv0 = w.take<uint32_t>(cap);
+    L.pv1 = w.take<uint32_t>(cap);
+    L.pcount = w.take<uint32_t>(4);
+    if (bytes) *bytes = w.off + 256;
+    return L;
+}
+
+size_t bin_workspace_bytes(int64_t n, int64_t cap, int n_tiles) {
+    size_t b = 0;
+    bin_layout(n, cap, n_tiles, nullptr, &b);
+    return b;
+}
+
+cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam,
+                            const ss_bins* bins, void* ws, size_t ws_bytes, ss_status* st,
+                            cudaStream_t s) {
+    int tiles_x = div_up(cam->width, kTile), tiles_y = div_up(cam->height, kTile);
+    int n_tiles = tiles_x * tiles_y;
+    int64_t cap = bins->pair_capacity;
+    size_t need = 0;
+    BinLayout L = bin_layout(n, cap, n_tiles, ws, &need);
+    if (need > ws_bytes) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(L.ctrl, 0, L.ctrl_bytes, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(bins->d_tile_start, 0, sizeof(uint32_t) * n_tiles, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(bins->d_tile_end, 0, sizeof(uint32_t) * n_tiles, s);
+    if (e != cudaSuccess) return e;
+    int64_t* P = &st->pair_count;
+    if (n > 0) {
+        uint32_t nn = (uint32_t)n;
+        // 1. depth sort of splats (4 stable 8-bit passes)
+        radix_hist_kernel<<<min(div_up(n, 256 * 8), 1024), 256, 0, s>>>(sp->d_depth_key, nn, 4, 0,
+                                                                        L.hist_depth);
+        int db = div_up(n, 256 * kDepthItems);
+        const uint32_t* kin = sp->d_depth_key;
+        const uint32_t* vin = nullptr;
+        uint32_t *ko[2] = {L.kA, L.kB}, *vo[2] = {L.vA, L.vB};
+        for (int p = 0; p < 4; ++p) {
+            onesweep_kernel<kDepthItems><<<db, 256, 0, s>>>(
+                kin, vin, p < 3 ? ko[p & 1] : nullptr, vo[p & 1], nullptr, nn, nn, 8 * p,
+                L.hist_depth + 256 * p, L.st_depth + (size_t)p * db * 256, L.ctrl + p);
+            kin = ko[p & 1];
+            vin = vo[p & 1];
+        }
+        const uint32_t* order = vo[1];  // pass 3 wrote vB
+        // 2. offsets of each splat's pairs in depth order, total P
+        scan_kernel<false><<<div_up(n, 256 * kScanItems), 256, 0, s>>>(
+            sp->d_tiles, order, nullptr, nn, L.offsets, L.st_scan1, L.ctrl + 8, P,
+            &st->pair_overflow, cap);
+        // 3. emission + tile digit histograms
+        int np = tile_passes(n_tiles);
+        emit_pairs_kernel<<<div_up(n, 256), 256, 0, s>>>(
+            nn, order, sp->d_tiles, reinterpret_cast<const uint2*>(sp->d_rect), L.offsets, tiles_x,
+            P, cap, np, L.pk0, L.pv0, L.hist_tile);
+        clamp_count_kernel<<<1, 1, 0, s>>>(P, cap, L.pcount);
+        // 4. stable sort of pairs by tile id; the last pass lands in d_pair_splat
+        int pb = div_up(cap > 0 ? cap : 1, 256 * kPairItems);
+        const uint32_t* pk = L.pk0;
+        const uint32_t* pv = L.pv0;
+        for (int p = 0; p < np; ++p) {
+            bool last = p == np - 1;
+            uint32_t* kdst = (pk == L.pk0) ? L.pk1 : L.pk0;
+            uint32_t* vdst = last ? bins->d_pair_splat : ((pv == L.pv0) ? L.pv1 : L.pv0);
+            onesweep_kernel<kPairItems><<<pb, 256, 0, s>>>(
+                pk, pv, kdst, vdst, L.pcount, 0u, (uint32_t)cap, 8 * p, L.hist_tile + 256 * p,
+                L.st_pair + (size_t)p * pb * 256, L.ctrl + 4 + p);
+            pk = kdst;
+            pv = vdst;
+        }
+        // 5. ranges by boundary detection on the sorted tile ids
+        tile_ranges_kernel<<<592, 256, 0, s>>>(pk, P, cap, bins->d_tile_start, bins->d_tile_end);
+    } else {
+        e = cudaMemsetAsync(P, 0, sizeof(int64_t) * 2, s);
+        if (e != cudaSuccess) return e;
+    }
+    // checkpoint slot bases: exclusive scan of ceil(len/32), n_tiles+1 entries
+    scan_kernel<true><<<div_up(n_tiles + 1, 256 * kScanItems), 256, 0, s>>>(
+        bins->d_tile_start, nullptr, bins->d_tile_end, (uint32_t)n_tiles + 1, bins->d_ckpt_base,
+        L.st_scan2, L.ctrl + 9, nullptr, nullptr, 0);
+    return cudaGetLastError();
+}
+
+}  // namespace ss
+
+namespace ss {
+// Generic exclusive scan of u32 (used by densification's compaction).
+size_t scan_ws_bytes(int64_t n) {
+    return sizeof(unsigned long long) * (size_t)(div_up(n > 0 ? n : 1, 256 * kScanItems) + 1) + 256;
+}
+
+cudaError_t launch_scan_u32(const uint32_t* in, int64_t n, uint32_t* out, int64_t* total,
+                            void* ws, cudaStream_t s) {
+    if (n <= 0) return cudaMemsetAsync(total, 0, sizeof(int64_t), s);
+    int nb = div_up(n, 256 * kScanItems);
+    unsigned long long* st = reinterpret_cast<unsigned long long*>(ws);
+    uint32_t* counter = reinterpret_cast<uint32_t*>(st + nb);
+    cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(unsigned long long) * (nb + 1), s);
+    if (e != cudaSuccess) return e;
+    scan_kernel<false><<<nb, 256, 0, s>>>(in, nullptr, nullptr, (uint32_t)n, out, st, counter,
+                                          total, nullptr, 0);
+    return cudaGetLastError();
+}
+}  // namespace ss

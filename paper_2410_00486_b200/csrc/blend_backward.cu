@@ -1,0 +1,218 @@
+// blend_backward.cu -- K7: CaRtGS splat-wise backward on B200.
+//
+// Restates backward_splatwise (rasterizer/api.py:275-337) over
+// backward_splat_tile / _splat_bucket_inner (rasterizer/kernels.py:271-373).
+// The reference's work unit is a (tile, bucket of 32 list positions) pair
+// that restores pixel states from the bucket's checkpoint and lets each
+// splat accumulate its gradient privately over the tile's pixels.  On B200
+// that unit is one WARP, lane i owning list position 32 b + i:
+//
+//   - the pixels still blending at the bucket start (n_contrib > 32 b) are
+//     compacted into a per-warp shared-memory list with their gradient,
+//     g . image and checkpoint state;
+//   - the pixel states then flow down the warp as a diagonal wavefront:
+//     at step t lane i handles list pixel t - i, receiving that pixel's
+//     state after splats 32b..32b+i-1 from lane i-1 by __shfl_up_sync, so
+//     every (pixel, splat) term sees exactly the state the reference's
+//     sequential replay produces (kernels.py:322-333);
+//   - each lane keeps its splat's 9 screen-space gradients in registers
+//     (no per-pixel atomics) and adds them to g2d with one red.add row per
+//     (tile, splat) at the end -- the float32 counterpart of the
+//     reference's ordered per-tile merge (api.py:331-336).
+//
+// Pixel state carried between lanes: (T, G) with G = g . c_acc, the
+// gradient-weighted accumulated colour.  The reference's dL/dalpha
+//   sum_c (rgb_c T - (image_c - c_acc_c)/(1 - a)) g_c     (kernels.py:344-352)
+// equals T (g . rgb) - (g . image - G_after) / (1 - a), so two floats move
+// per shuffle instead of four.  Warps are persistent and pull work units
+// from the list the forward appended.
+#include "common.cuh"
+
+namespace ss {
+
+struct PixA {  // per active pixel, gradient side
+    float g0, g1, g2, gimg;
+};
+struct PixB {  // per active pixel, state side
+    float T0, G0;
+    int nc, p;
+};
+
+template <bool DEPTH>
+__global__ void __launch_bounds__(128) backward_splat_kernel(
+    int W, int H, int tiles_x, const uint32_t* __restrict__ tile_start,
+    const uint32_t* __restrict__ ckpt_base, const int32_t* __restrict__ k_eff,
+    const uint32_t* __restrict__ pairs, const SplatRec* __restrict__ rec, float amin, float amax,
+    const float* __restrict__ image, const float* __restrict__ grad_image,
+    const float* __restrict__ depth_img, const float* __restrict__ grad_depth,
+    const int32_t* __restrict__ n_contrib, const float4* __restrict__ ckpt,
+    const float* __restrict__ ckpt_depth, const uint2* __restrict__ work,
+    const int64_t* __restrict__ work_count, int64_t work_cap, uint32_t* work_counter,
+    float* __restrict__ g2d, uint8_t* __restrict__ contributed) {
+    extern __shared__ float4 smem[];
+    constexpr int NC = DEPTH ? 10 : 9;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    PixA* sA = reinterpret_cast<PixA*>(smem) + wid * kTilePx;
+    PixB* sB = reinterpret_cast<PixB*>(smem + (blockDim.x >> 5) * kTilePx) + wid * kTilePx;
+    float* sD = reinterpret_cast<float*>(smem + 2 * (blockDim.x >> 5) * kTilePx) + wid * kTilePx;
+    const int64_t count = min(*work_count, work_cap);
+
+    for (;;) {
+        uint32_t item = 0;
+        if (lane == 0) item = atomicAdd(work_counter, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if ((int64_t)item >= count) break;
+        const uint2 wk = work[item];
+        const int tile = (int)wk.x, b = (int)wk.y;
+        const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
+        const uint32_t start = tile_start[tile];
+        const int ke = k_eff[tile];
+        const int kbase = b * kBucket;
+        const int k = kbase + lane;
+        const bool valid = k < ke;
+        uint32_t s = 0;
+        float4 A = make_float4(0.f, 0.f, 0.f, 0.f), B = make_float4(0.f, 0.f, -1.f, 1.f),
+               C = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) {
+            s = pairs[start + k];
+            const SplatRec r = rec[s];
+            A = r.a;
+            B = r.b;
+            C = r.c;
+        }
+        // ---- compact the pixels still blending at this bucket
+        const size_t slot0 = (size_t)(ckpt_base[tile] + b) * kTilePx;
+        int nact = 0;
+#pragma unroll 1
+        for (int c = 0; c < kTilePx / 32; ++c) {
+            const int p = c * 32 + lane;
+            const int ix = x0 + (p & 15), iy = y0 + (p >> 4);
+            const bool inside = ix < W && iy < H;
+            const size_t o = (size_t)iy * W + ix;
+            const int nc = inside ? n_contrib[o] : 0;
+            const bool act = nc > kbase;
+            const unsigned bal = __ballot_sync(0xffffffffu, act);
+            if (act) {
+                const int pos = nact + __popc(bal & lanemask_lt());
+                const float g0 = grad_image[3 * o], g1 = grad_image[3 * o + 1],
+                            g2 = grad_image[3 * o + 2];
+                float gimg = g0 * image[3 * o] + g1 * image[3 * o + 1] + g2 * image[3 * o + 2];
+                const float4 ck = ckpt[slot0 + p];
+                float G0 = g0 * ck.y + g1 * ck.z + g2 * ck.w;
+                if (DEPTH) {
+                    const float gd = grad_depth ? grad_depth[o] : 0.f;
+                    gimg += gd * depth_img[o];
+                    G0 += gd * ckpt_depth[slot0 + p];
+                    sD[pos] = gd;
+                }
+                sA[pos] = PixA{g0, g1, g2, gimg};
+                sB[pos] = PixB{ck.x, G0, nc, p};
+            }
+            nact += __popc(bal);
+        }
+        __syncwarp();
+        // ---- diagonal wavefront over the active pixels
+        float acc[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) acc[q] = 0.f;
+        float T = 0.f, G = 0.f;
+        bool blended = false;
+        const float inv_sigma = 1.0f / B.y;
+        const int steps = nact + 31;
+#pragma unroll 1
+        for (int st = 0; st < steps; ++st) {
+            float Tin = __shfl_up_sync(0xffffffffu, T, 1);
+            float Gin = __shfl_up_sync(0xffffffffu, G, 1);
+            const int j = st - lane;
+            if (j < 0 || j >= nact) continue;
+            const PixB pb = sB[j];
+            if (lane == 0) {
+                Tin = pb.T0;
+                Gin = pb.G0;
+            }
+            T = Tin;
+            G = Gin;
+            if (!valid || k >= pb.nc) continue;
+            const float px = (float)(x0 + (pb.p & 15)), py = (float)(y0 + (pb.p >> 4));
+            float dx, dy;
+            const float a = splat_alpha(px, py, A, B, amin, amax, dx, dy);
+            if (a < 0.f) continue;
+            blended = true;
+            const PixA pa = sA[j];
+            const float gd = DEPTH ? sD[j] : 0.f;
+            const float w = __fmul_rn(a, T);
+            float grgb = pa.g0 * C.x + pa.g1 * C.y + pa.g2 * C.z;
+            if (DEPTH) grgb += gd * B.w;
+            const float Gafter = G + grgb * w;
+            const float Tafter = __fmul_rn(T, __fsub_rn(1.0f, a));
+            if (pa.g0 != 0.f || pa.g1 != 0.f || pa.g2 != 0.f || (DEPTH && gd != 0.f)) {
+                acc[0] += w * pa.g0;
+                acc[1] += w * pa.g1;
+                acc[2] += w * pa.g2;
+                if (DEPTH) acc[9] += w * gd;
+                const float am1 = 1.0f - a;
+                if (am1 > 0.f && a != amax) {
+                    const float dal = T * grgb - (pa.gimg - Gafter) / am1;
+                    acc[8] += dal * (a * inv_sigma);
+                    const float da = dal * a;
+                    acc[3] += da * (A.z * dx + A.w * dy);
+                    acc[4] += da * (A.w * dx + B.x * dy);
+                    const float h = -0.5f * da;
+                    acc[5] += h * dx * dx;
+                    acc[6] += h * 2.0f * dx * dy;
+                    acc[7] += h * dy * dy;
+                }
+            }
+            T = Tafter;
+            G = Gafter;
+        }
+        if (valid) {
+            float* row = g2d + (size_t)s * NC;
+#pragma unroll
+            for (int q = 0; q < NC; ++q)
+                if (acc[q] != 0.f) atomicAdd(row + q, acc[q]);
+            if (contributed && blended) contributed[s] = 1;
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
+                                  const ss_splats* sp, const ss_bins* bins, const float* image,
+                                  const float* grad_image, const float* depth,
+                                  const float* grad_depth, const int32_t* n_contrib,
+                                  const int32_t* k_eff, const void* ckpt, const float* ckpt_depth,
+                                  const uint32_t* work, int64_t work_cap, int64_t n, float* g2d,
+                                  uint8_t* contributed, const ss_status* st, uint32_t* counter,
+                                  cudaStream_t s) {
+    const bool depthf = o->with_depth != 0;
+    const int ncol = depthf ? 10 : 9;
+    cudaError_t e = cudaMemsetAsync(g2d, 0, sizeof(float) * (size_t)n * ncol, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(counter, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+    int tx = div_up(cam->width, kTile);
+    const int threads = 128, warps = threads / 32;
+    size_t smem = (size_t)warps * kTilePx * (sizeof(PixA) + sizeof(PixB) + (depthf ? 4 : 0));
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    auto go = [&](auto kern) -> cudaError_t {
+        cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem);
+        if (e2 != cudaSuccess) return e2;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+        if (per_sm < 1) per_sm = 1;
+        kern<<<sms * per_sm, threads, smem, s>>>(
+            cam->width, cam->height, tx, bins->d_tile_start, bins->d_ckpt_base, k_eff,
+            bins->d_pair_splat, reinterpret_cast<const SplatRec*>(sp->d_rec), o->alpha_min,
+            o->alpha_max, image, grad_image, depth, grad_depth, n_contrib,
+            reinterpret_cast<const float4*>(ckpt), ckpt_depth,
+            reinterpret_cast<const uint2*>(work), &st->bucket_count, work_cap, counter, g2d,
+            contributed);
+        return cudaGetLastError();
+    };
+    return depthf ? go(backward_splat_kernel<true>) : go(backward_splat_kernel<false>);
+}
+
+}  // namespace ss

@@ -1,0 +1,84 @@
+// common.cuh -- shared device definitions for the B200 mapping hot path.
+//
+// Semantics follow the reference `splatstream` package (paths relative to
+// /root/reference/pkg/src/splatstream); every threshold decision that the
+// forward blend, the checkpoint replay and the splat-wise backward must agree
+// on is made by ONE inline function (`splat_alpha`) built from explicit
+// round-to-nearest intrinsics, so the compiler cannot contract it differently
+// in the two kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/splatstream_b200.h"
+
+namespace ss {
+
+constexpr int kTile = 16;                 // RasterOpts.tile_size (api.py:41)
+constexpr int kTilePx = kTile * kTile;    // 256 pixels = 256 threads per tile CTA
+constexpr int kBucket = 32;               // RasterOpts.bucket_size (api.py:42) = warp width
+constexpr float kLog2e = 1.4426950408889634f;
+
+// Per-Gaussian screen-space record written by the preprocess kernel and
+// gathered by the blend kernels through the sorted pair list (48 B, one
+// 16-B-aligned struct so a gather is three LDG.128 from one 64-B window).
+struct __align__(16) SplatRec {
+    float4 a;  // mean2d.x, mean2d.y, conic[0], conic[1]
+    float4 b;  // conic[2], sigma, m_cut, depth (camera-frame z)
+    float4 c;  // r, g, b, unused
+};
+
+// Pixel-state checkpoint (T, r, g, b) archived before every 32nd list
+// position (kernels.py:61-67); the depth channel adds a second plane.
+// Layout: ckpt[(ckpt_base[tile] + bucket) * 256 + pixel].
+
+// ------------------------------------------------------------------ alpha
+// _alpha (kernels.py:14-31): m = c0 dx^2 + 2 c1 dx dy + c2 dy^2; skip when
+// m > m_cut; a = sigma exp(-m/2); skip when a < alpha_min; clamp alpha_max.
+// Returns a < 0 for "skip".  Pixel coordinates are integers (api.py:108-115).
+__device__ __forceinline__ float splat_alpha(float px, float py, const float4& A, const float4& B,
+                                             float amin, float amax, float& dx, float& dy) {
+    dx = __fsub_rn(px, A.x);
+    dy = __fsub_rn(py, A.y);
+    float m = __fmaf_rn(__fmul_rn(A.z, dx), dx,
+                        __fmaf_rn(__fmul_rn(__fmul_rn(2.0f, A.w), dx), dy,
+                                  __fmul_rn(__fmul_rn(B.x, dy), dy)));
+    if (m > B.z) return -1.0f;
+    float a = __fmul_rn(B.y, exp2f(__fmul_rn(m, -0.5f * kLog2e)));
+    if (a < amin) return -1.0f;
+    return fminf(a, amax);
+}
+
+// ----------------------------------------------------------- error words
+// Device error word layout (ss_error): first failing index via atomicMin.
+__device__ __forceinline__ void report_first(int64_t* word, int64_t idx) {
+    atomicMin(reinterpret_cast<unsigned long long*>(word), static_cast<unsigned long long>(idx));
+}
+
+__device__ __forceinline__ bool finitef(float x) { return isfinite(x); }
+
+// ------------------------------------------------------------ warp utils
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ int warp_max(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+inline int div_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace ss

@@ -1,0 +1,211 @@
+// preprocess.cu -- K1: per-Gaussian EWA projection, SH colour, footprint
+// radius and inclusive tile rectangle, over the SoA map.
+//
+// Restates project_map (rasterizer/projection.py:73-163) in float32, one
+// thread per Gaussian (no compaction: culled Gaussians get tiles = 0 and a
+// max depth key, so every later stage indexes by Gaussian id), and the
+// tile-rectangle half of build_tile_index (rasterizer/tiles.py:40-48).
+// Also folds rasterize_forward's finite-parameter check (api.py:127-129,
+// core.py:231-241) and the zero-quaternion check (projection.py:99-102)
+// into device error words.
+#include "common.cuh"
+#include "sh.cuh"
+
+namespace ss {
+
+struct CamF {
+    float fx, fy, cx, cy;
+    int W, H;
+    float R[9], t[3], c[3];
+};
+
+__device__ __forceinline__ float sigmoid_stable(float x) {
+    // projection.py:68-70
+    float e = expf(-fabsf(x));
+    return x >= 0.f ? 1.0f / (1.0f + e) : e / (1.0f + e);
+}
+
+// Camera-frame covariance and the dilated 2D covariance (projection.py:98-121).
+struct Proj2D {
+    float t[3];
+    float a, b, c;
+};
+
+__device__ __forceinline__ void project_cov(const float p[3], const float4 q, const float ls[3],
+                                            const CamF& cam, float dilation, Proj2D& o,
+                                            float qhat[4], float rot[9], float s2[3],
+                                            float covc[9], float& qn) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        o.t[i] = p[0] * cam.R[3 * i] + p[1] * cam.R[3 * i + 1] + p[2] * cam.R[3 * i + 2] + cam.t[i];
+    qn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+    float inv = 1.0f / qn;
+    qhat[0] = q.x * inv;
+    qhat[1] = q.y * inv;
+    qhat[2] = q.z * inv;
+    qhat[3] = q.w * inv;
+    quat_to_rot(qhat, rot);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s2[k] = expf(2.0f * ls[k]);
+    // cov3 = R diag(s2) R^T ; covc = Rcw cov3 Rcw^T
+    float M[9];  // M = Rcw * R  -> covc = M diag(s2) M^T
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            M[3 * i + j] = cam.R[3 * i] * rot[j] + cam.R[3 * i + 1] * rot[3 + j] +
+                           cam.R[3 * i + 2] * rot[6 + j];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int l = 0; l < 3; ++l)
+            covc[3 * i + l] = M[3 * i] * s2[0] * M[3 * l] + M[3 * i + 1] * s2[1] * M[3 * l + 1] +
+                              M[3 * i + 2] * s2[2] * M[3 * l + 2];
+    float iz = 1.0f / o.t[2], iz2 = iz * iz;
+    float j00 = cam.fx * iz, j02 = -cam.fx * o.t[0] * iz2;
+    float j11 = cam.fy * iz, j12 = -cam.fy * o.t[1] * iz2;
+    // c2 = J covc J^T with J = [[j00,0,j02],[0,j11,j12]]
+    float r0[3] = {j00 * covc[0] + j02 * covc[6], j00 * covc[1] + j02 * covc[7],
+                   j00 * covc[2] + j02 * covc[8]};
+    float r1[3] = {j11 * covc[3] + j12 * covc[6], j11 * covc[4] + j12 * covc[7],
+                   j11 * covc[5] + j12 * covc[8]};
+    o.a = r0[0] * j00 + r0[2] * j02 + dilation;
+    o.b = r0[1] * j11 + r0[2] * j12;
+    o.c = r1[1] * j11 + r1[2] * j12 + dilation;
+}
+
+__global__ void __launch_bounds__(256) preprocess_kernel(
+    int64_t n, const float* __restrict__ pos, const float4* __restrict__ rot,
+    const float* __restrict__ ls, const float* __restrict__ opl, const float* __restrict__ sh_dc,
+    const float* __restrict__ sh_rest, CamF cam, int sh_degree, float near_plane, float dilation,
+    float log_amin, int tiles_x, int tiles_y, SplatRec* __restrict__ rec,
+    uint32_t* __restrict__ depth_key, uint32_t* __restrict__ tiles, uint2* __restrict__ rect,
+    uint8_t* __restrict__ flags, float* __restrict__ aux, ss_status* status) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool vis = false;
+    if (i < n) {
+        float p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+        float4 q = rot[i];
+        float l[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
+        float o = opl[i];
+        float dc[3] = {sh_dc[3 * i], sh_dc[3 * i + 1], sh_dc[3 * i + 2]};
+        bool fin = finitef(p[0]) && finitef(p[1]) && finitef(p[2]) && finitef(q.x) &&
+                   finitef(q.y) && finitef(q.z) && finitef(q.w) && finitef(l[0]) &&
+                   finitef(l[1]) && finitef(l[2]) && finitef(o) && finitef(dc[0]) &&
+                   finitef(dc[1]) && finitef(dc[2]);
+        if (sh_degree > 0) {
+            // sh_rest only changes when it is optimised (sh_degree > 0); at
+            // degree 0 the host validates it once on upload.
+            for (int k = 0; k < 45; ++k) fin = fin && finitef(sh_rest[45 * i + k]);
+        }
+        if (!fin) report_first(&status->first_nonfinite_param, i);
+
+        float z = p[0] * cam.R[6] + p[1] * cam.R[7] + p[2] * cam.R[8] + cam.t[2];
+        uint32_t ntiles = 0;
+        uint2 rc = make_uint2(0u, 0u);
+        uint8_t fl = 0;
+        SplatRec r;
+        r.a = make_float4(0.f, 0.f, 0.f, 0.f);
+        r.b = make_float4(0.f, 0.f, -1.f, 0.f);
+        r.c = make_float4(0.f, 0.f, 0.f, 0.f);
+        float auxv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (z > near_plane) {
+            float qn2 = q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w;
+            if (qn2 == 0.0f) report_first(&status->first_zero_quat, i);
+            Proj2D P;
+            float qhat[4], R9[9], s2[3], covc[9], qn;
+            project_cov(p, q, l, cam, dilation, P, qhat, R9, s2, covc, qn);
+            float mx = cam.fx * P.t[0] / P.t[2] + cam.cx;
+            float my = cam.fy * P.t[1] / P.t[2] + cam.cy;
+            float det = P.a * P.c - P.b * P.b;
+            float mid = (P.a + P.c) / 2.0f;
+            float disc = mid * mid - det;
+            float lmax = mid + sqrtf(fmaxf(disc, 0.0f));
+            float sg = sigmoid_stable(o);
+            float mcut = 2.0f * (logf(sg) - log_amin);
+            float rad = ceilf(sqrtf(fmaxf(mcut, 0.0f) * lmax));
+            vis = (det > 0.f) && (mcut > 0.f) && (mx + rad >= 0.f) &&
+                  (mx - rad <= (float)(cam.W - 1)) && (my + rad >= 0.f) &&
+                  (my - rad <= (float)(cam.H - 1)) && (qn2 != 0.0f);
+            if (vis) {
+                // tiles.py:42-47: inclusive rect, float32 arithmetic as numpy
+                float fx0 = floorf(__fdiv_rn(__fsub_rn(mx, rad), (float)kTile));
+                float fx1 = floorf(__fdiv_rn(__fadd_rn(mx, rad), (float)kTile));
+                float fy0 = floorf(__fdiv_rn(__fsub_rn(my, rad), (float)kTile));
+                float fy1 = floorf(__fdiv_rn(__fadd_rn(my, rad), (float)kTile));
+                int x0 = (int)fminf(fmaxf(fx0, 0.f), (float)(tiles_x - 1));
+                int x1 = (int)fminf(fmaxf(fx1, 0.f), (float)(tiles_x - 1));
+                int y0 = (int)fminf(fmaxf(fy0, 0.f), (float)(tiles_y - 1));
+                int y1 = (int)fminf(fmaxf(fy1, 0.f), (float)(tiles_y - 1));
+                ntiles = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+                rc = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 16),
+                                (uint32_t)x1 | ((uint32_t)y1 << 16));
+                // colour (projection.py:147-155)
+                float u[3] = {p[0] - cam.c[0], p[1] - cam.c[1], p[2] - cam.c[2]};
+                float vl = fmaxf(sqrtf(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]), 1e-12f);
+                float d[3] = {u[0] / vl, u[1] / vl, u[2] / vl};
+                float rgb[3];
+                bool act[3];
+                sh_color(d, sh_degree, dc, sh_rest + 45 * i, rgb, act);
+                fl = 1u | (act[0] ? 2u : 0u) | (act[1] ? 4u : 0u) | (act[2] ? 8u : 0u);
+                r.a = make_float4(mx, my, P.c / det, -P.b / det);
+                r.b = make_float4(P.a / det, sg, mcut, P.t[2]);
+                r.c = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+                auxv[0] = P.t[0];
+                auxv[1] = P.t[1];
+                auxv[2] = P.t[2];
+                auxv[3] = P.a;
+                auxv[4] = P.b;
+                auxv[5] = P.c;
+                auxv[6] = rad;
+            }
+        }
+        rec[i] = r;
+        depth_key[i] = vis ? __float_as_uint(z) : 0xFFFFFFFFu;
+        tiles[i] = ntiles;
+        rect[i] = rc;
+        flags[i] = fl;
+        if (aux) {
+            float4* a4 = reinterpret_cast<float4*>(aux + 8 * i);
+            a4[0] = make_float4(auxv[0], auxv[1], auxv[2], auxv[3]);
+            a4[1] = make_float4(auxv[4], auxv[5], auxv[6], auxv[7]);
+        }
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, vis);
+    if (lane_id() == 0 && bal)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&status->visible_count),
+                  (unsigned long long)__popc(bal));
+}
+
+void fill_camf(const ss_camera* c, CamF& f) {
+    f.fx = c->fx;
+    f.fy = c->fy;
+    f.cx = c->cx;
+    f.cy = c->cy;
+    f.W = c->width;
+    f.H = c->height;
+    for (int k = 0; k < 9; ++k) f.R[k] = c->R[k];
+    for (int k = 0; k < 3; ++k) {
+        f.t[k] = c->t[k];
+        f.c[k] = c->center[k];
+    }
+}
+
+cudaError_t launch_preprocess(const ss_map* map, const ss_camera* cam, const ss_raster_opts* o,
+                              const ss_splats* out, ss_status* st, cudaStream_t s) {
+    if (map->n == 0) return cudaSuccess;
+    CamF cf;
+    fill_camf(cam, cf);
+    int tx = div_up(cam->width, kTile), ty = div_up(cam->height, kTile);
+    int threads = 256;
+    int blocks = div_up(map->n, threads);
+    preprocess_kernel<<<blocks, threads, 0, s>>>(
+        map->n, map->d_positions, reinterpret_cast<const float4*>(map->d_rotations),
+        map->d_log_scales, map->d_opacity_logits, map->d_sh_dc, map->d_sh_rest, cf,
+        o->sh_degree, o->near_plane, o->dilation, logf(o->alpha_min), tx, ty,
+        reinterpret_cast<SplatRec*>(out->d_rec), out->d_depth_key, out->d_tiles,
+        reinterpret_cast<uint2*>(out->d_rect), out->d_flags, out->d_aux, st);
+    return cudaGetLastError();
+}
+
+}  // namespace ss

@@ -1,0 +1,421 @@
+"""The mapping iteration as one stream-ordered sequence of B200 kernels.
+
+``MappingEngine.step`` is ``_Trainer.train_one`` (trainer.py:180-215) for
+one keyframe view, without host synchronisation:
+
+  K1 preprocess -> K2-K4b binning -> K5 blend -> K6 L1+SSIM (+depth) ->
+  K7 splat-wise backward -> K8+K9 fused chain + opacity-reg grad + stats +
+  Adam (one kernel; the per-Gaussian gradients never reach HBM)
+
+All buffers are allocated once for the map size, image size and pair
+capacity.  Data-dependent sizes stay on the device: the pair count P only
+has to fit the capacity; if it does not, the binning sets a sticky
+overflow word, the fused update becomes a no-op, and the host -- which
+reads each step's status block two steps late through pinned memory --
+grows the buffers and replays the skipped steps in order.  The loss
+scalars are read the same way (``losses()``), so the scheduler-style
+consumer never stalls the GPU.
+
+``multiview_step`` is the builder-defined keyframe batch (SURVEY 8a A17,
+8e): per-view K1-K7 + accumulate-mode K8 into one flat gradient buffer
+(grads + densify-statistics increments), an optional all-reduce hook
+(torch.distributed / NCCL over NVLink), then K9 Adam and the statistics
+update -- identical on every rank.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .core import Camera, GaussianMap
+from .densify import DensifyConfig, densify_and_prune, opacity_reset
+from .optimizer import AdamState, LearningRates
+from .rasterizer import BinBuffers, P, RasterOpts, SplatBuffers, bin_workspace, stream_handle
+
+STATUS_LAG = 2
+
+# kernels each C-ABI call enqueues (counted for bench.py's gpu_launches)
+KERNELS_PER_CALL = {
+    # status_begin 1 + preprocess 1 + binning (hist 1, 4 depth passes, scan 1,
+    # emit 1, clamp 1, 2 tile passes, ranges 1, ckpt scan 1) 13 + blend 1 +
+    # loss (ssim fwd, ssim bwd, reduce) 3 + backward 1
+    "step_fb": 1 + 1 + 13 + 1 + 3 + 1,
+    "chain_adam": 1,
+    "opacity_reg": 2,
+}
+
+
+@dataclass
+class StepRecord:
+    index: int
+    camera: Camera
+    target: torch.Tensor
+    target_depth: torch.Tensor | None
+    hp: _lib.SSAdamHP
+    slot: int
+    event: torch.cuda.Event
+    replayed: int = 0
+
+
+@dataclass
+class EngineConfig:
+    lambda_ssim: float = 0.2
+    lambda_o: float = 0.001
+    depth_weight: float = 0.0          # builder extension A15 (RGB-D configs)
+    densify: DensifyConfig | None = None
+    scene_extent: float = 1.0
+    opacity_reset_interval: int = 0    # builder extension A16 (0 = off)
+    opacity_reset_ceiling: float = 0.01
+    pair_margin: float = 1.3
+    lrs: LearningRates = field(default_factory=LearningRates)
+    horizon: int = 30000
+
+
+class MappingEngine:
+    """Owns the device buffers of the fused mapping iteration for one map."""
+
+    def __init__(self, gmap: GaussianMap, width: int, height: int, opts: RasterOpts | None = None,
+                 config: EngineConfig | None = None, pair_capacity: int | None = None):
+        self.gmap = gmap
+        self.opts = opts or RasterOpts(sh_degree=0)
+        self.cfg = config or EngineConfig()
+        self.W, self.H = int(width), int(height)
+        self.dev = gmap.device
+        self.state = AdamState.for_map(gmap, self.cfg.lrs, self.cfg.horizon)
+        self.tiles_x, self.tiles_y = (self.W + 15) // 16, (self.H + 15) // 16
+        self.n_tiles = self.tiles_x * self.tiles_y
+        self.iteration = 0
+        self.since_densify = 0
+        self._records: list[StepRecord] = []
+        self._loss_log: list[tuple[int, float, float]] = []
+        self._cap = int(pair_capacity) if pair_capacity else max(16 * len(gmap), 4096)
+        self.status = torch.empty(_lib.STATUS_WORDS, dtype=torch.int64, device=self.dev)
+        check(lib().ss_status_reset(P(self.status), stream_handle()), "ss_status_reset")
+        self._slots = 8
+        self._host = torch.zeros((self._slots, _lib.STATUS_WORDS + 4), dtype=torch.float64,
+                                 pin_memory=True)
+        self._alloc_map_buffers()
+        self._alloc_pair_buffers(self._cap)
+        self.profile = None  # list of (stage, start event, end event) when profiling
+        self.launches = 0    # kernels launched by this engine (see KERNELS_PER_CALL)
+
+    def _mark(self, name):
+        """Stage boundary for the per-kernel timing bench.py reports."""
+        if self.profile is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.profile.append((name, ev))
+
+    # ------------------------------------------------------------ buffers
+    def _alloc_map_buffers(self):
+        n = len(self.gmap)
+        dev = self.dev
+        self.splats = SplatBuffers.alloc(n, dev, aux=False)
+        ncol = 10 if self.opts.with_depth else 9
+        self.g2d = torch.empty((max(n, 1), ncol), dtype=torch.float32, device=dev)
+        self.contributed = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.image = torch.empty((self.H, self.W, 3), **f32)
+        self.final_t = torch.empty((self.H, self.W), **f32)
+        self.n_contrib = torch.empty((self.H, self.W), dtype=torch.int32, device=dev)
+        self.depth = torch.empty((self.H, self.W), **f32) if self.opts.with_depth else None
+        self.grad_depth = torch.empty((self.H, self.W), **f32) if self.opts.with_depth else None
+        self.grad_image = torch.empty((self.H, self.W, 3), **f32)
+        self.k_eff = torch.empty(self.n_tiles, dtype=torch.int32, device=dev)
+        self.sums = torch.zeros(_lib.SS_REDUCE_DOUBLES, dtype=torch.float64, device=dev)
+        self.osum = torch.zeros(_lib.SS_REDUCE_DOUBLES, dtype=torch.float64, device=dev)
+        self.dsum = torch.zeros(_lib.SS_REDUCE_DOUBLES, dtype=torch.float64, device=dev)
+        self.loss_ws = torch.empty(int(lib().ss_loss_workspace_bytes(self.H, self.W)),
+                                   dtype=torch.uint8, device=dev)
+        self._flat = None
+
+    def _alloc_pair_buffers(self, cap):
+        n = len(self.gmap)
+        self._cap = int(cap)
+        self.bins = BinBuffers.alloc(self._cap, self.n_tiles, self.dev)
+        self.bin_ws = bin_workspace(n, self._cap, self.n_tiles, self.dev)
+        slots = self._cap // 32 + self.n_tiles + 1
+        self.ckpt = torch.empty((slots * 256, 4), dtype=torch.float32, device=self.dev)
+        self.ckpt_depth = (torch.empty(slots * 256, dtype=torch.float32, device=self.dev)
+                           if self.opts.with_depth else None)
+        self.work_cap = slots
+        self.work = torch.empty((slots, 2), dtype=torch.int32, device=self.dev)
+
+    @property
+    def pair_capacity(self):
+        return self._cap
+
+    # -------------------------------------------------------------- pieces
+    def _forward_backward(self, cam: Camera, target: torch.Tensor, target_depth, view_mode):
+        """K1..K7 for one view; view_mode None = fused single view."""
+        L = lib()
+        s = stream_handle()
+        mp, cm, op = self.gmap.ss(), cam.to_ss(), self.opts.to_ss()
+        spss, bss = self.splats.ss(), self.bins.ss()
+        n = len(self.gmap)
+        self._mark("begin")
+        check(L.ss_status_begin_step(P(self.status), s), "ss_status_begin_step")
+        check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op),
+                              ctypes.byref(spss), P(self.status), s), "ss_preprocess")
+        self._mark("preprocess")
+        check(L.ss_bin_sort(n, ctypes.byref(spss), ctypes.byref(cm), ctypes.byref(bss),
+                            P(self.bin_ws), self.bin_ws.numel(), P(self.status), s),
+              "ss_bin_sort")
+        self._mark("binning")
+        check(L.ss_blend_forward(ctypes.byref(cm), ctypes.byref(op), ctypes.byref(spss),
+                                 ctypes.byref(bss), P(self.image), P(self.final_t),
+                                 P(self.n_contrib), P(self.depth), P(self.k_eff), None,
+                                 P(self.ckpt), P(self.ckpt_depth), P(self.work), self.work_cap,
+                                 P(self.status), s), "ss_blend_forward")
+        self._mark("blend_forward")
+        check(L.ss_loss_l1_ssim(self.H, self.W, P(self.image), P(target),
+                                float(self.cfg.lambda_ssim), P(self.grad_image), P(self.sums),
+                                P(self.loss_ws), self.loss_ws.numel(), s), "ss_loss_l1_ssim")
+        if self.opts.with_depth:
+            if target_depth is not None and self.cfg.depth_weight != 0.0:
+                check(L.ss_depth_l1(self.H, self.W, P(self.depth), P(target_depth),
+                                    float(self.cfg.depth_weight), P(self.grad_depth),
+                                    P(self.dsum), s), "ss_depth_l1")
+            else:
+                self.grad_depth.zero_()
+        self._mark("loss")
+        self.contributed.zero_()
+        check(L.ss_backward_splat(ctypes.byref(cm), ctypes.byref(op), ctypes.byref(spss),
+                                  ctypes.byref(bss), P(self.image), P(self.grad_image),
+                                  P(self.depth), P(self.grad_depth), P(self.n_contrib),
+                                  P(self.k_eff), P(self.ckpt), P(self.ckpt_depth), P(self.work),
+                                  self.work_cap, n, P(self.g2d), P(self.contributed),
+                                  P(self.status), s), "ss_backward_splat")
+        self._mark("backward")
+        self.launches += (KERNELS_PER_CALL["step_fb"] + (3 if self.opts.with_depth and
+                                                        self.cfg.depth_weight else 0))
+        return mp, cm, op
+
+    def _finish_record(self, rec: StepRecord):
+        """Snapshot status + loss sums into the record's pinned slot."""
+        L = lib()
+        s = stream_handle()
+        n = len(self.gmap)
+        check(L.ss_opacity_reg(n, P(self.gmap.opacity_logits), 0.0, None, 0, P(self.osum), s),
+              "ss_opacity_reg")
+        row = self._host[rec.slot]
+        row[:_lib.STATUS_WORDS].copy_(self.status.double(), non_blocking=True)
+        row[_lib.STATUS_WORDS:_lib.STATUS_WORDS + 2].copy_(self.sums[:2], non_blocking=True)
+        row[_lib.STATUS_WORDS + 2:_lib.STATUS_WORDS + 3].copy_(self.osum[:1], non_blocking=True)
+        rec.event.record()
+
+    # ---------------------------------------------------------- main step
+    def step(self, camera, target: torch.Tensor, target_depth: torch.Tensor | None = None):
+        """One fused mapping iteration (single view, single GPU)."""
+        self._maybe_densify()
+        cam = Camera.of(camera)
+        self.state.step_count += 1
+        hp = self.state.hparams(self.opts.sh_degree > 0)
+        rec = StepRecord(self.iteration, cam, target, target_depth, hp,
+                         self.iteration % self._slots, torch.cuda.Event())
+        self._run(rec)
+        self._records.append(rec)
+        self.iteration += 1
+        self.since_densify += 1
+        self._drain(STATUS_LAG)
+        return rec.index
+
+    def _run(self, rec: StepRecord):
+        L = lib()
+        n = len(self.gmap)
+        mp, cm, op = self._forward_backward(rec.camera, rec.target, rec.target_depth, None)
+        lon = float(self.cfg.lambda_o / n) if n else 0.0
+        check(L.ss_chain_adam(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op), P(self.g2d),
+                              P(self.splats.flags), P(self.contributed), lon,
+                              ctypes.byref(self.state.planes("m")),
+                              ctypes.byref(self.state.planes("v")), ctypes.byref(rec.hp),
+                              P(self.status), stream_handle()), "ss_chain_adam")
+        self._mark("chain_adam")
+        self._finish_record(rec)
+        self.launches += KERNELS_PER_CALL["chain_adam"] + KERNELS_PER_CALL["opacity_reg"]
+
+    def _drain(self, lag: int):
+        """Consume status snapshots older than `lag` steps; recover overflow."""
+        while len(self._records) > lag:
+            rec = self._records[0]
+            rec.event.synchronize()
+            row = self._host[rec.slot].numpy().copy()
+            if int(row[_lib.ST_OVERFLOW]):
+                self._recover(int(row[_lib.ST_PAIRS]))
+                continue
+            self._check_errors(row)
+            self._log(rec, row)
+            self._records.pop(0)
+
+    def _check_errors(self, row):
+        if int(row[_lib.ST_BAD_PARAM]) < len(self.gmap) and row[_lib.ST_BAD_PARAM] < 2 ** 62:
+            raise ValueError(f"non-finite parameter in primitive {int(row[_lib.ST_BAD_PARAM])}")
+        if row[_lib.ST_BAD_GRAD] < 2 ** 62:
+            raise FloatingPointError("non-finite gradient (primitive "
+                                     f"{int(row[_lib.ST_BAD_GRAD])})")
+
+    def _log(self, rec, row):
+        npx = self.H * self.W * 3
+        l1 = row[_lib.STATUS_WORDS] / npx
+        ssim = row[_lib.STATUS_WORDS + 1] / npx
+        lam = self.cfg.lambda_ssim
+        rendered = (1 - lam) * l1 + lam * (1 - ssim)
+        reg = row[_lib.STATUS_WORDS + 2] / max(len(self.gmap), 1)
+        self._loss_log.append((rec.index, rendered + self.cfg.lambda_o * reg, rendered))
+
+    def _recover(self, pairs_seen: int):
+        """Grow pair buffers and replay every pending (skipped) step in order."""
+        torch.cuda.current_stream().synchronize()
+        pending = list(self._records)
+        self._records.clear()
+        newcap = max(int(pairs_seen * self.cfg.pair_margin) + 4096, self._cap * 2)
+        self._alloc_pair_buffers(newcap)
+        check(lib().ss_status_reset(P(self.status), stream_handle()), "ss_status_reset")
+        for rec in pending:
+            rec.replayed += 1
+            self._run(rec)
+        torch.cuda.current_stream().synchronize()
+        self._records = pending
+
+    def synchronize(self):
+        self._drain(0)
+
+    def losses(self):
+        """(iteration, total loss, rendered loss) of every consumed step."""
+        self.synchronize()
+        return list(self._loss_log)
+
+    def last_pair_count(self) -> int:
+        return int(self.status[_lib.ST_PAIRS].item())
+
+    def fit_capacity(self, camera, margin: float | None = None):
+        """Size the pair buffers for `camera` (one binning + sync, no update)."""
+        cam = Camera.of(camera)
+        L = lib()
+        s = stream_handle()
+        mp, cm, op = self.gmap.ss(), cam.to_ss(), self.opts.to_ss()
+        st = torch.empty(_lib.STATUS_WORDS, dtype=torch.int64, device=self.dev)
+        check(L.ss_status_reset(P(st), s), "ss_status_reset")
+        check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op),
+                              ctypes.byref(self.splats.ss()), P(st), s), "ss_preprocess")
+        tiny = BinBuffers.alloc(0, self.n_tiles, self.dev)
+        ws = bin_workspace(len(self.gmap), 0, self.n_tiles, self.dev)
+        check(L.ss_bin_sort(len(self.gmap), ctypes.byref(self.splats.ss()), ctypes.byref(cm),
+                            ctypes.byref(tiny.ss()), P(ws), ws.numel(), P(st), s), "ss_bin_sort")
+        p = int(st[_lib.ST_PAIRS].item())
+        m = self.cfg.pair_margin if margin is None else margin
+        self._alloc_pair_buffers(int(p * m) + 4096)
+        return p
+
+    # ------------------------------------------------- densify / reset (K10)
+    def _maybe_densify(self):
+        cfg = self.cfg
+        if cfg.densify is not None and self.since_densify >= cfg.densify.interval:
+            self.densify()
+        if (cfg.opacity_reset_interval and self.iteration > 0
+                and self.iteration % cfg.opacity_reset_interval == 0):
+            self.synchronize()
+            opacity_reset(self.gmap, self.state, cfg.opacity_reset_ceiling)
+
+    def densify(self, normals=None):
+        """densify_and_prune + resize_for_densify as one compaction
+        (trainer.py:187-193)."""
+        self.synchronize()
+        n = len(self.gmap)
+        planes = []
+        new_m, new_v = {}, {}
+        # the engine's moments ride through the compaction as extra planes
+        from .densify import densify_count
+        _, c, _ = densify_count(self.gmap, self.cfg.densify, self.cfg.scene_extent)
+        n_out = int(c[0] + c[4])
+        for d, nd in ((self.state.m, new_m), (self.state.v, new_v)):
+            for k, t in d.items():
+                out = torch.zeros((n_out,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+                planes.append((t.contiguous(), out))
+                nd[k] = out
+        res = densify_and_prune(self.gmap, self.cfg.densify, self.cfg.scene_extent,
+                                normals=normals, rng=None if normals is not None else
+                                int(np.random.default_rng(self.iteration).integers(1, 2 ** 62)),
+                                extra_planes=planes)
+        self.state.m, self.state.v = new_m, new_v
+        self.since_densify = 0
+        if len(self.gmap) != n:
+            self._alloc_map_buffers()
+            self._alloc_pair_buffers(max(self._cap * len(self.gmap) // max(n, 1), 4096))
+        return res
+
+    # ------------------------------------------------------- multi-view
+    def _flat_grads(self):
+        n = len(self.gmap)
+        rest = 45 if self.opts.sh_degree > 0 else 0
+        if self._flat is None or self._flat_n != n:
+            per = 3 + 4 + 3 + 1 + 3 + rest + 1 + 1 + 3 + 1
+            self._flat = torch.zeros(per * max(n, 1), dtype=torch.float32, device=self.dev)
+            self._flat_n = n
+            views, off = {}, 0
+            for name, k in (("position", 3), ("rotation", 4), ("log_scale", 3), ("opacity", 1),
+                            ("sh_dc", 3), ("sh_rest", rest), ("pos2d", 1), ("stat_g2d", 1),
+                            ("stat_g3d", 3), ("stat_cnt", 1)):
+                views[name] = self._flat[off * n:(off + k) * n]
+                off += k
+            self._fv = views
+            g = _lib.SSParamGrads()
+            g.d_position, g.d_rotation = P(views["position"]), P(views["rotation"])
+            g.d_log_scale, g.d_opacity = P(views["log_scale"]), P(views["opacity"])
+            g.d_sh_dc, g.d_sh_rest = P(views["sh_dc"]), P(views["sh_rest"])
+            g.d_pos2d_norm = P(views["pos2d"])
+            g.d_stat_g2d, g.d_stat_g3d, g.d_stat_cnt = (P(views["stat_g2d"]),
+                                                        P(views["stat_g3d"]),
+                                                        P(views["stat_cnt"]))
+            self._fss = g
+        return self._flat, self._fss
+
+    def multiview_step(self, cameras, targets, target_depths=None, allreduce=None,
+                       add_reg: bool = True):
+        """Keyframe batch: sum of per-view gradients (+ the opacity-reg
+        gradient once), optional all-reduce of the flat buffer, then Adam and
+        the statistics update.  Synchronous on the status (overflow check)."""
+        self._maybe_densify()
+        L = lib()
+        s = stream_handle()
+        n = len(self.gmap)
+        flat, fss = self._flat_grads()
+        flat.zero_()
+        lon = float(self.cfg.lambda_o / n) if (n and add_reg) else 0.0
+        losses = []
+        for v, (cam, tgt) in enumerate(zip(cameras, targets)):
+            cam = Camera.of(cam)
+            td = target_depths[v] if target_depths is not None else None
+            while True:
+                mp, cm, op = self._forward_backward(cam, tgt, td, v)
+                sh = self.status.cpu()
+                if not int(sh[_lib.ST_OVERFLOW]):
+                    break
+                self._alloc_pair_buffers(int(int(sh[_lib.ST_PAIRS]) * self.cfg.pair_margin) + 4096)
+                check(L.ss_status_reset(P(self.status), s), "ss_status_reset")
+            check(L.ss_chain_backward(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op),
+                                      P(self.g2d), P(self.splats.flags), P(self.contributed),
+                                      lon if v == 0 else 0.0,
+                                      _lib.SS_CHAIN_ACCUMULATE | _lib.SS_CHAIN_STAT_PLANES,
+                                      ctypes.byref(fss), P(self.status), s), "ss_chain_backward")
+            losses.append(self.sums[:2].clone())
+        if allreduce is not None:
+            allreduce(flat)
+        self.state.step_count += 1
+        hp = self.state.hparams(self.opts.sh_degree > 0)
+        mp = self.gmap.ss()
+        check(L.ss_adam_step(ctypes.byref(mp), ctypes.byref(fss),
+                             ctypes.byref(self.state.planes("m")),
+                             ctypes.byref(self.state.planes("v")), ctypes.byref(hp),
+                             P(self.status), s), "ss_adam_step")
+        check(L.ss_apply_stat_planes(ctypes.byref(mp), ctypes.byref(fss), s),
+              "ss_apply_stat_planes")
+        self.iteration += 1
+        self.since_densify += 1
+        return losses

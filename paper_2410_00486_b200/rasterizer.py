@@ -1,0 +1,418 @@
+"""Forward rendering and the splat-wise backward on B200.
+
+Drop-in for ``splatstream.rasterizer`` (rasterizer/api.py:37-368): same
+names (``RasterOpts``, ``RenderOutput``, ``ParamGrads``,
+``rasterize_forward``, ``backward_splatwise``), same argument meaning and
+error behaviour; outputs are float32 CUDA tensors.  All compute runs in
+libss_b200.so (K1 preprocess, K2-K4b binning, K5 blend, K7 splat-wise
+backward, K8 chain); this module only allocates buffers and sequences the
+C-ABI calls on the current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .core import Camera, GaussianMap
+
+G2D_COLS = 9
+EAGER_CKPT_MAX_LIST = 1024  # api.py:23 -- the GPU always checkpoints in the forward pass
+
+
+@dataclass
+class RasterOpts:
+    """api.py:37-52.  ``dtype`` and ``n_workers`` are accepted for drop-in
+    compatibility; the B200 path always computes in float32 on the GPU."""
+
+    tile_size: int = 16
+    bucket_size: int = 32
+    t_min: float = 1e-4
+    alpha_min: float = 1.0 / 255.0
+    alpha_max: float = 0.99
+    background: tuple = (0.0, 0.0, 0.0)
+    sh_degree: int = 3
+    near: float = 0.01
+    dilation: float = 0.3
+    dtype: type = np.float32
+    with_checkpoints: bool = True
+    n_workers: int = 1
+    with_depth: bool = False  # builder extension A15
+
+    def to_ss(self) -> _lib.SSRasterOpts:
+        if self.tile_size != 16 or self.bucket_size != 32:
+            raise ValueError("the B200 kernels are specialised for tile_size=16, bucket_size=32")
+        o = _lib.SSRasterOpts()
+        o.tile_size, o.bucket_size = 16, 32
+        o.t_min, o.alpha_min, o.alpha_max = self.t_min, self.alpha_min, self.alpha_max
+        o.background[:] = [float(b) for b in self.background]
+        o.sh_degree = int(self.sh_degree)
+        o.near_plane, o.dilation = self.near, self.dilation
+        o.with_depth = 1 if self.with_depth else 0
+        return o
+
+
+def stream_handle():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def P(t):
+    """Device pointer of a tensor (None for empty / missing)."""
+    if t is None or t.numel() == 0:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+@dataclass
+class SplatBuffers:
+    """Per-Gaussian K1 outputs (ss_splats)."""
+
+    rec: torch.Tensor       # (n, 12) float32: SplatRec
+    depth_key: torch.Tensor  # (n,) int32 (u32 bits)
+    tiles: torch.Tensor     # (n,) int32
+    rect: torch.Tensor      # (n, 2) int32
+    flags: torch.Tensor     # (n,) uint8
+    aux: torch.Tensor | None  # (n, 8) float32
+
+    @classmethod
+    def alloc(cls, n, dev, aux=True):
+        return cls(torch.empty((n, 12), dtype=torch.float32, device=dev),
+                   torch.empty(n, dtype=torch.int32, device=dev),
+                   torch.empty(n, dtype=torch.int32, device=dev),
+                   torch.empty((n, 2), dtype=torch.int32, device=dev),
+                   torch.empty(n, dtype=torch.uint8, device=dev),
+                   torch.empty((n, 8), dtype=torch.float32, device=dev) if aux else None)
+
+    def ss(self):
+        s = _lib.SSSplats()
+        s.d_rec, s.d_depth_key, s.d_tiles = P(self.rec), P(self.depth_key), P(self.tiles)
+        s.d_rect, s.d_flags, s.d_aux = P(self.rect), P(self.flags), P(self.aux)
+        return s
+
+
+@dataclass
+class BinBuffers:
+    """K2-K4b outputs (ss_bins)."""
+
+    capacity: int
+    pairs: torch.Tensor      # (capacity,) int32 Gaussian ids
+    tile_start: torch.Tensor  # (T,)
+    tile_end: torch.Tensor    # (T,)
+    ckpt_base: torch.Tensor   # (T+1,)
+
+    @classmethod
+    def alloc(cls, cap, n_tiles, dev):
+        i32 = dict(dtype=torch.int32, device=dev)
+        return cls(cap, torch.empty(max(cap, 1), **i32), torch.empty(n_tiles, **i32),
+                   torch.empty(n_tiles, **i32), torch.empty(n_tiles + 1, **i32))
+
+    def ss(self):
+        b = _lib.SSBins()
+        b.pair_capacity = self.capacity
+        b.d_pair_splat, b.d_tile_start = P(self.pairs), P(self.tile_start)
+        b.d_tile_end, b.d_ckpt_base = P(self.tile_end), P(self.ckpt_base)
+        return b
+
+
+_CAP_HINT: dict = {}
+
+
+def new_status(dev):
+    st = torch.empty(_lib.STATUS_WORDS, dtype=torch.int64, device=dev)
+    check(lib().ss_status_reset(P(st), stream_handle()), "ss_status_reset")
+    return st
+
+
+def raise_param_errors(st_host):
+    bad = int(st_host[_lib.ST_BAD_PARAM])
+    if bad != _lib.INT64_MAX:
+        raise ValueError(f"non-finite parameter in primitive {bad}")
+    zq = int(st_host[_lib.ST_ZERO_QUAT])
+    if zq != _lib.INT64_MAX:
+        raise ValueError(f"zero-norm quaternion at primitive {zq}")
+
+
+def bin_workspace(n, cap, n_tiles, dev):
+    nbytes = int(lib().ss_bin_workspace_bytes(n, cap, n_tiles))
+    return torch.empty(nbytes, dtype=torch.uint8, device=dev)
+
+
+@dataclass
+class Projection:
+    """Reference-shaped view of the K1 output (projection.py:40-65), built
+    on request: rows are the visible Gaussians in index order."""
+
+    map_index: np.ndarray
+    t_cam: np.ndarray
+    depth: np.ndarray
+    mean2d: np.ndarray
+    cov2d: np.ndarray
+    conic: np.ndarray
+    radius: np.ndarray
+    sigma: np.ndarray
+    rgb: np.ndarray
+    rgb_active: np.ndarray
+    m_cut: np.ndarray
+    sh_degree: int
+
+    def __len__(self):
+        return int(self.map_index.shape[0])
+
+
+@dataclass
+class TileIndex:
+    """tiles.py:15-26 view; ``pair_splat`` holds projection-row indices like
+    the reference (``pair_gaussian`` the Gaussian ids the kernels use)."""
+
+    tile_size: int
+    tiles_x: int
+    tiles_y: int
+    pair_splat: np.ndarray
+    pair_gaussian: np.ndarray
+    tile_range: np.ndarray
+    active_tiles: np.ndarray
+
+    def tile_origin(self, tile_id):
+        ty, tx = divmod(int(tile_id), self.tiles_x)
+        return tx * self.tile_size, ty * self.tile_size
+
+
+@dataclass
+class RenderOutput:
+    """api.py:82-105 plus the device buffers the splat-wise backward reads."""
+
+    image: torch.Tensor      # (H, W, 3)
+    final_t: torch.Tensor    # (H, W)
+    n_contrib: torch.Tensor  # (H, W) int32
+    k_eff_tiles: torch.Tensor  # (T,) int32, per tile (all tiles)
+    contributed: torch.Tensor  # (N,) bool
+    opts: RasterOpts
+    camera: Camera
+    n_primitives: int
+    gmap: GaussianMap
+    splats: SplatBuffers
+    bins: BinBuffers
+    pair_count: int
+    ckpt: torch.Tensor | None
+    ckpt_depth: torch.Tensor | None
+    work: torch.Tensor
+    work_capacity: int
+    status: torch.Tensor
+    depth: torch.Tensor | None = None
+    _cache: dict = field(default_factory=dict)
+
+    @property
+    def acc_rgb(self) -> torch.Tensor:
+        bg = torch.tensor(self.opts.background, dtype=torch.float32, device=self.image.device)
+        return self.image - bg * self.final_t[..., None]
+
+    @property
+    def alpha(self) -> torch.Tensor:
+        """Builder extension A15: 1 - final_T (kernels.py:102)."""
+        return 1.0 - self.final_t
+
+    @property
+    def checkpoints(self):
+        return None if self.ckpt is None else self.ckpt
+
+    @property
+    def proj(self) -> Projection:
+        if "proj" not in self._cache:
+            fl = self.splats.flags.cpu().numpy()
+            vis = np.flatnonzero(fl & 1).astype(np.int32)
+            rec = self.splats.rec.cpu().numpy()[vis]
+            aux = self.splats.aux.cpu().numpy()[vis] if self.splats.aux is not None else None
+            act = np.stack([(fl[vis] >> 1) & 1, (fl[vis] >> 2) & 1, (fl[vis] >> 3) & 1], 1)
+            self._cache["proj"] = Projection(
+                map_index=vis, t_cam=aux[:, 0:3] if aux is not None else None,
+                depth=rec[:, 7].copy(), mean2d=rec[:, 0:2].copy(),
+                cov2d=aux[:, 3:6] if aux is not None else None,
+                conic=np.stack([rec[:, 2], rec[:, 3], rec[:, 4]], 1), radius=aux[:, 6].copy()
+                if aux is not None else None, sigma=rec[:, 5].copy(), rgb=rec[:, 8:11].copy(),
+                rgb_active=act.astype(bool), m_cut=rec[:, 6].copy(),
+                sh_degree=self.opts.sh_degree)
+        return self._cache["proj"]
+
+    @property
+    def tile_index(self) -> TileIndex:
+        if "ti" not in self._cache:
+            W, H = self.camera.width, self.camera.height
+            tx, ty = (W + 15) // 16, (H + 15) // 16
+            pg = self.bins.pairs[:self.pair_count].cpu().numpy().astype(np.int64)
+            st = self.bins.tile_start.cpu().numpy().astype(np.int64)
+            en = self.bins.tile_end.cpu().numpy().astype(np.int64)
+            ln = en - st
+            rng = np.zeros(tx * ty + 1, dtype=np.int64)
+            np.cumsum(ln, out=rng[1:])
+            row = np.full(self.n_primitives, -1, dtype=np.int64)
+            row[self.proj.map_index] = np.arange(len(self.proj))
+            self._cache["ti"] = TileIndex(16, tx, ty, row[pg].astype(np.int32), pg, rng,
+                                          np.flatnonzero(ln > 0).astype(np.int64))
+        return self._cache["ti"]
+
+    @property
+    def k_eff(self) -> np.ndarray:
+        """Per active tile, in active-tile order (api.py:195)."""
+        ke = self.k_eff_tiles.cpu().numpy().astype(np.int64)
+        return ke[self.tile_index.active_tiles]
+
+
+def _as_image(x, shape, dev, name="grad_image"):
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+    x = x.to(device=dev, dtype=torch.float32).contiguous()
+    return x
+
+
+def rasterize_forward(gmap: GaussianMap, camera, opts: RasterOpts | None = None) -> RenderOutput:
+    """api.py:118-206 on the GPU: K1 preprocess -> K2-K4b binning -> K5 blend."""
+    if opts is None:
+        opts = RasterOpts()
+    cam = Camera.of(camera)
+    L = lib()
+    dev = gmap.device
+    n = len(gmap)
+    H, W = cam.height, cam.width
+    tx, ty = cam.tiles
+    n_tiles = tx * ty
+    s = stream_handle()
+    st = new_status(dev)
+    sp = SplatBuffers.alloc(n, dev)
+    mp, cm, op = gmap.ss(), cam.to_ss(), opts.to_ss()
+    check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op),
+                          ctypes.byref(sp.ss()), P(st), s), "ss_preprocess")
+    key = (str(dev), n_tiles)
+    cap = max(_CAP_HINT.get(key, 0), 4 * n, 1024)
+    while True:
+        bins = BinBuffers.alloc(cap, n_tiles, dev)
+        ws = bin_workspace(n, cap, n_tiles, dev)
+        check(L.ss_bin_sort(n, ctypes.byref(sp.ss()), ctypes.byref(cm), ctypes.byref(bins.ss()),
+                            P(ws), ws.numel(), P(st), s), "ss_bin_sort")
+        sh = st.cpu()
+        raise_param_errors(sh)
+        pcount = int(sh[_lib.ST_PAIRS])
+        if not int(sh[_lib.ST_OVERFLOW]):
+            break
+        cap = int(pcount * 1.25) + 1024
+    _CAP_HINT[key] = cap
+    n_slots = int(bins.ckpt_base[n_tiles].item())
+    f32 = dict(dtype=torch.float32, device=dev)
+    ckpt = torch.empty((max(n_slots, 1) * 256, 4), **f32)
+    ckpt_depth = torch.empty(max(n_slots, 1) * 256, **f32) if opts.with_depth else None
+    image = torch.empty((H, W, 3), **f32)
+    final_t = torch.empty((H, W), **f32)
+    n_contrib = torch.empty((H, W), dtype=torch.int32, device=dev)
+    depth = torch.empty((H, W), **f32) if opts.with_depth else None
+    k_eff = torch.empty(n_tiles, dtype=torch.int32, device=dev)
+    contributed = torch.zeros(n, dtype=torch.uint8, device=dev)
+    work_cap = max(n_slots, 1)
+    work = torch.empty((work_cap, 2), dtype=torch.int32, device=dev)
+    check(L.ss_blend_forward(ctypes.byref(cm), ctypes.byref(op), ctypes.byref(sp.ss()),
+                             ctypes.byref(bins.ss()), P(image), P(final_t), P(n_contrib), P(depth),
+                             P(k_eff), P(contributed), P(ckpt), P(ckpt_depth), P(work), work_cap,
+                             P(st), s), "ss_blend_forward")
+    return RenderOutput(image=image, final_t=final_t, n_contrib=n_contrib, k_eff_tiles=k_eff,
+                        contributed=contributed.bool(), opts=opts, camera=cam, n_primitives=n,
+                        gmap=gmap, splats=sp, bins=bins, pair_count=pcount,
+                        ckpt=ckpt if opts.with_checkpoints else None, ckpt_depth=ckpt_depth,
+                        work=work, work_capacity=work_cap, status=st, depth=depth)
+
+
+@dataclass
+class ParamGrads:
+    """api.py:55-79, float32 device tensors; ``sh`` is assembled on request."""
+
+    position: torch.Tensor
+    rotation: torch.Tensor
+    log_scale: torch.Tensor
+    opacity_logit: torch.Tensor
+    sh_dc: torch.Tensor
+    sh_rest: torch.Tensor
+    pos2d_grad_norm: torch.Tensor
+    contributed: torch.Tensor
+
+    def __len__(self):
+        return int(self.position.shape[0])
+
+    @property
+    def sh(self) -> torch.Tensor:
+        n = len(self)
+        return torch.cat([self.sh_dc.view(n, 1, 3), self.sh_rest.view(n, 15, 3)], 1)
+
+    @classmethod
+    def alloc(cls, n, dev, zero=False):
+        mk = torch.zeros if zero else torch.empty
+        f = dict(dtype=torch.float32, device=dev)
+        return cls(mk((n, 3), **f), mk((n, 4), **f), mk((n, 3), **f), mk(n, **f), mk((n, 3), **f),
+                   torch.zeros((n, 45), **f), mk(n, **f), torch.zeros(n, dtype=torch.bool,
+                                                                     device=dev))
+
+    def ss(self):
+        g = _lib.SSParamGrads()
+        g.d_position, g.d_rotation, g.d_log_scale = P(self.position), P(self.rotation), P(
+            self.log_scale)
+        g.d_opacity, g.d_sh_dc, g.d_sh_rest = P(self.opacity_logit), P(self.sh_dc), P(self.sh_rest)
+        g.d_pos2d_norm = P(self.pos2d_grad_norm)
+        return g
+
+    def validate_finite(self):
+        """api.py:74-79."""
+        for name in ("position", "rotation", "log_scale", "opacity_logit"):
+            if not bool(torch.isfinite(getattr(self, name)).all()):
+                raise FloatingPointError(f"non-finite gradient in {name}")
+        if not (bool(torch.isfinite(self.sh_dc).all()) and bool(torch.isfinite(self.sh_rest).all())):
+            raise FloatingPointError("non-finite gradient in sh")
+        return self
+
+
+def screen_space_grads(render: RenderOutput, grad_image, grad_depth=None):
+    """K7 only: the per-Gaussian screen-space rows g2d (N, 9|10) float32 the
+    reference merges before chain_backward (api.py:331-336)."""
+    if render.ckpt is None:
+        raise RuntimeError("render output has no checkpoints; re-run rasterize_forward "
+                           "with with_checkpoints=True to use the splat-wise backward")
+    dev = render.image.device
+    if tuple(grad_image.shape) != tuple(render.image.shape):
+        raise ValueError(f"grad_image shape {tuple(grad_image.shape)} does not match "
+                         f"rendered image shape {tuple(render.image.shape)}")
+    g = _as_image(grad_image, render.image.shape, dev)
+    gd = None
+    if render.opts.with_depth:
+        gd = (_as_image(grad_depth, render.depth.shape, dev) if grad_depth is not None
+              else torch.zeros_like(render.depth))
+    ncol = 10 if render.opts.with_depth else 9
+    n = render.n_primitives
+    g2d = torch.empty((max(n, 1), ncol), dtype=torch.float32, device=dev)
+    cm, op = render.camera.to_ss(), render.opts.to_ss()
+    check(lib().ss_backward_splat(
+        ctypes.byref(cm), ctypes.byref(op), ctypes.byref(render.splats.ss()),
+        ctypes.byref(render.bins.ss()), P(render.image), P(g), P(render.depth), P(gd),
+        P(render.n_contrib), P(render.k_eff_tiles), P(render.ckpt), P(render.ckpt_depth),
+        P(render.work), render.work_capacity, n, P(g2d), None, P(render.status),
+        stream_handle()), "ss_backward_splat")
+    return g2d[:n]
+
+
+def backward_splatwise(render: RenderOutput, grad_image, n_workers=None,
+                       grad_depth=None) -> ParamGrads:
+    """api.py:275-337: K7 splat-wise backward + K8 chain to parameters."""
+    g2d = screen_space_grads(render, grad_image, grad_depth)
+    return _finish_backward(render, g2d)
+
+
+def _finish_backward(render: RenderOutput, g2d) -> ParamGrads:
+    """api.py:217-224: chain_backward + validate_finite."""
+    n = render.n_primitives
+    dev = render.image.device
+    grads = ParamGrads.alloc(n, dev)
+    grads.contributed = render.contributed.clone()
+    mp, cm, op = render.gmap.ss(), render.camera.to_ss(), render.opts.to_ss()
+    check(lib().ss_chain_backward(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op), P(g2d),
+                                  P(render.splats.flags), None, 0.0, 0, ctypes.byref(grads.ss()),
+                                  P(render.status), stream_handle()), "ss_chain_backward")
+    return grads.validate_finite()

@@ -1,0 +1,401 @@
+"""CUDA path vs the CPU oracle, stage by stage (SURVEY.md 8c protocol).
+
+Every comparison feeds the oracle the GPU's own upstream float32 values,
+so bit-exact stages (tile assignment, sort order, ranges, densify masks)
+are compared exactly and floating-point stages with the tolerances
+north_star states: colour/depth/alpha 1e-4 absolute, gradients and
+post-Adam parameters 1e-3 relative (norm-wise).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+import oracle as orc  # noqa: E402
+from helpers import (expand_sh, fixture_camera, fixture_scene, floored_rel, load,  # noqa: E402
+                     normwise)
+
+FIXTURES = ["iter_sh0_small", "iter_sh3_small", "iter_tiny_config"]
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.fixture(scope="module", params=FIXTURES)
+def case(request):
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    d = load(request.param)
+    cam = fixture_camera(d)
+    arrs = fixture_scene(d)
+    g = ss.GaussianMap.from_arrays(*arrs)
+    deg = int(d["sh_degree"])
+    opts = ss.RasterOpts(sh_degree=deg)
+    out = ss.rasterize_forward(g, cam, opts)
+    torch.cuda.synchronize()
+    return dict(d=d, cam=cam, arrs=arrs, g=g, out=out, deg=deg, ss=ss, opts=opts)
+
+
+def _f32_map(g):
+    """The GPU map's float32 values as a float64 oracle map."""
+    h = g.to_numpy()
+    return orc.OMap(h["positions"], h["rotations"], h["log_scales"], h["opacity_logits"], h["sh"])
+
+
+def _gpu_proj_as_oracle(out):
+    p = out.proj
+    return orc.OProjection(map_index=p.map_index, t_cam=p.t_cam.astype(np.float64),
+                           depth=p.depth.astype(np.float64), mean2d=p.mean2d.astype(np.float64),
+                           cov2d=p.cov2d.astype(np.float64), conic=p.conic.astype(np.float64),
+                           radius=p.radius.astype(np.float64), sigma=p.sigma.astype(np.float64),
+                           rgb=p.rgb.astype(np.float64), rgb_active=p.rgb_active,
+                           sh_degree=p.sh_degree)
+
+
+def test_preprocess_matches_oracle(case):
+    out, cam, deg = case["out"], case["cam"], case["deg"]
+    ref = orc.project(_f32_map(case["g"]), cam, sh_degree=deg)
+    p = out.proj
+    np.testing.assert_array_equal(p.map_index, ref.map_index)
+    assert np.abs(p.mean2d - ref.mean2d).max() <= 1e-3
+    for name in ("conic", "cov2d"):
+        a, b = getattr(p, name), getattr(ref, name)
+        assert (np.abs(a - b) / np.abs(b).max(axis=0)).max() <= 1e-5, name
+    for name in ("depth", "sigma"):
+        a, b = getattr(p, name), getattr(ref, name)
+        assert (np.abs(a - b) / np.abs(b)).max() <= 1e-5, name
+    assert np.abs(p.rgb - ref.rgb).max() <= 1e-5
+    assert (p.radius != ref.radius).sum() <= max(2, len(ref) // 50000)
+    np.testing.assert_array_equal(p.rgb_active, ref.rgb_active)
+
+
+def test_binning_bit_exact(case):
+    """K2-K4b == build_tile_index fed the GPU's float32 projection."""
+    out, cam = case["out"], case["cam"]
+    p = out.proj
+    ti = orc.tile_index(p.mean2d.astype(np.float32), p.radius.astype(np.float32),
+                        p.depth.astype(np.float32), cam.width, cam.height, 16)
+    g = out.tile_index
+    assert out.pair_count == ti.pair_splat.size
+    np.testing.assert_array_equal(g.pair_splat, ti.pair_splat)
+    np.testing.assert_array_equal(g.tile_range, ti.tile_range)
+    np.testing.assert_array_equal(g.active_tiles, ti.active_tiles)
+
+
+def _oracle_render_on_gpu_inputs(case):
+    out, cam = case["out"], case["cam"]
+    po = _gpu_proj_as_oracle(out)
+    ti = out.tile_index
+    oti = orc.OTileIndex(16, ti.tiles_x, ti.tiles_y, ti.pair_splat, ti.tile_range,
+                         ti.active_tiles)
+    return orc.forward(po, oti, cam.width, cam.height, out.n_primitives,
+                       m_cut=out.proj.m_cut.astype(np.float64))
+
+
+def test_forward_matches_oracle(case):
+    out = case["out"]
+    r = _oracle_render_on_gpu_inputs(case)
+    img = out.image.cpu().numpy()
+    assert np.abs(img - r.image).max() <= 1e-4
+    assert np.abs(out.final_t.cpu().numpy() - r.final_t).max() <= 1e-4
+    flips = (out.n_contrib.cpu().numpy() != r.n_contrib).sum()
+    assert flips <= max(2, r.n_contrib.size // 20000)
+    assert (out.contributed.cpu().numpy() != r.contributed).sum() <= max(2, flips * 4)
+    if flips == 0:
+        np.testing.assert_array_equal(out.k_eff, r.k_eff)
+
+
+def test_losses_match_oracle(case):
+    ss, out, d = case["ss"], case["out"], case["d"]
+    tgt = torch.as_tensor(d["target"], dtype=torch.float32, device="cuda")
+    lb = ss.compute_losses(out.image, tgt, case["g"].opacity_logits, 0.2, 0.001)
+    ref = orc.losses(out.image.cpu().numpy().astype(np.float64),
+                     tgt.cpu().numpy().astype(np.float64),
+                     case["g"].opacity_logits.cpu().numpy().astype(np.float64), 0.2, 0.001)
+    for k in ("l1", "ssim_loss", "rendered", "opacity_reg", "total"):
+        a, b = getattr(lb, k), getattr(ref, k)
+        assert abs(a - b) <= 1e-6 * max(abs(b), 1e-3), (k, a, b)
+    gi = lb.grad_image.cpu().numpy()
+    assert normwise(gi, ref.grad_image) <= 1e-5
+    assert np.abs(gi - ref.grad_image).max() <= 1e-5 * np.abs(ref.grad_image).max()
+    np.testing.assert_allclose(lb.grad_opacity_logit.cpu().numpy(), ref.grad_opacity_logit,
+                               rtol=1e-5, atol=1e-12)
+
+
+def test_backward_g2d_matches_oracle(case):
+    """K7 vs backward_splat on the same render, same grad_image."""
+    ss, out = case["ss"], case["out"]
+    rng = np.random.default_rng(3)
+    gimg = rng.standard_normal(out.image.shape).astype(np.float32) * 1e-3
+    g2d = ss.screen_space_grads(out, torch.as_tensor(gimg, device="cuda")).cpu().numpy()
+    r = _oracle_render_on_gpu_inputs(case)
+    ref = orc.backward_splat(r, gimg.astype(np.float64))
+    mine = g2d[out.proj.map_index]
+    for cols in ((0, 3), (3, 5), (5, 8), (8, 9)):
+        a, b = mine[:, cols[0]:cols[1]], ref[:, cols[0]:cols[1]]
+        assert normwise(a, b) <= 1e-3, cols
+
+
+def test_chain_matches_oracle(case):
+    """K8 vs chain_backward on the same g2d."""
+    ss, out, cam, deg = case["ss"], case["out"], case["cam"], case["deg"]
+    rng = np.random.default_rng(4)
+    gimg = rng.standard_normal(out.image.shape).astype(np.float32) * 1e-3
+    g2d = ss.screen_space_grads(out, torch.as_tensor(gimg, device="cuda"))
+    grads = ss.rasterizer._finish_backward(out, g2d)
+    mi = out.proj.map_index
+    po = orc.project(_f32_map(case["g"]), cam, sh_degree=deg)
+    ref = orc.chain(_f32_map(case["g"]), cam, po, g2d.cpu().numpy().astype(np.float64)[mi],
+                    out.contributed.cpu().numpy())
+    for name in ("position", "rotation", "log_scale", "opacity_logit", "pos2d_grad_norm"):
+        a = getattr(grads, name).cpu().numpy()
+        assert normwise(a, getattr(ref, name)) <= 1e-3, name
+    assert normwise(grads.sh.cpu().numpy(), ref.sh) <= 1e-3
+
+
+def test_full_iteration_matches_reference_golden(case):
+    """End to end against the REFERENCE's own float64 iteration (fixture)."""
+    ss, d, cam, deg = case["ss"], case["d"], case["cam"], case["deg"]
+    g = ss.GaussianMap.from_arrays(*case["arrs"])
+    opts = ss.RasterOpts(sh_degree=deg)
+    out = ss.rasterize_forward(g, cam, opts)
+    assert np.abs(out.image.cpu().numpy() - d["image"]).max() <= 1e-4
+    tgt = torch.as_tensor(d["target"], dtype=torch.float32, device="cuda")
+    lb = ss.compute_losses(out.image, tgt, g.opacity_logits, 0.2, 0.001)
+    assert abs(lb.total - d["loss"][4]) <= 1e-4 * abs(d["loss"][4])
+    gr = ss.backward_splatwise(out, lb.grad_image)
+    gr.opacity_logit += lb.grad_opacity_logit
+    for name in ("position", "rotation", "log_scale", "opacity_logit"):
+        a = getattr(gr, name).cpu().numpy()
+        assert normwise(a, d["g_" + name]) <= 1e-3, name
+        assert floored_rel(a, d["g_" + name], 1e-2) <= 5e-2, name
+    assert normwise(gr.sh.cpu().numpy(), expand_sh(d["g_sh"])) <= 1e-3
+    st = ss.AdamState.for_map(g)
+    ss.adam_step(g, gr, st)
+    ss.accumulate_grad_stats(g, gr)
+    h = g.to_numpy()
+    # first Adam step moves every element by ~lr*sign(g): compare where the
+    # reference gradient is not within float32 noise of zero
+    for name, gname in (("positions", "g_position"), ("log_scales", "g_log_scale"),
+                        ("opacity_logits", "g_opacity_logit")):
+        ref_g = d[gname]
+        ok = np.abs(ref_g) > 1e-3 * np.abs(ref_g).max()
+        a, b = h[name][ok], d["post_" + name][ok]
+        assert np.abs(a - b).max() <= 1e-3 * np.abs(b).max(), name
+    np.testing.assert_array_equal(h["obs_count"], d["post_obs_count"])
+
+
+def test_engine_step_matches_api_sequence(case):
+    ss, d, cam, deg = case["ss"], case["d"], case["cam"], case["deg"]
+    tgt = torch.as_tensor(d["target"], dtype=torch.float32, device="cuda")
+    g1 = ss.GaussianMap.from_arrays(*case["arrs"])
+    g2 = ss.GaussianMap.from_arrays(*case["arrs"])
+    opts = ss.RasterOpts(sh_degree=deg)
+    # API sequence (trainer.py:199-208)
+    st = ss.AdamState.for_map(g1)
+    for _ in range(2):
+        out = ss.rasterize_forward(g1, cam, opts)
+        lb = ss.compute_losses(out.image, tgt, g1.opacity_logits)
+        gr = ss.backward_splatwise(out, lb.grad_image)
+        gr.opacity_logit += lb.grad_opacity_logit
+        ss.adam_step(g1, gr, st)
+        ss.accumulate_grad_stats(g1, gr)
+    eng = ss.MappingEngine(g2, cam.width, cam.height, opts)
+    for _ in range(2):
+        eng.step(cam, tgt)
+    eng.synchronize()
+    for f in ("positions", "rotations", "log_scales", "opacity_logits", "sh_dc",
+              "grad2d_accum"):
+        a, b = getattr(g2, f).cpu().numpy(), getattr(g1, f).cpu().numpy()
+        assert np.abs(a - b).max() <= 1e-3 * max(np.abs(b).max(), 1e-6), f
+    np.testing.assert_array_equal(g2.obs_count.cpu().numpy(), g1.obs_count.cpu().numpy())
+    losses = eng.losses()
+    assert len(losses) == 2 and np.isfinite(losses[0][1])
+
+
+def test_engine_recovers_from_pair_overflow():
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    d = load("iter_sh0_small")
+    cam = fixture_camera(d)
+    arrs = fixture_scene(d)
+    tgt = torch.as_tensor(d["target"], dtype=torch.float32, device="cuda")
+    ga = ss.GaussianMap.from_arrays(*arrs)
+    gb = ss.GaussianMap.from_arrays(*arrs)
+    ea = ss.MappingEngine(ga, cam.width, cam.height, ss.RasterOpts(sh_degree=0),
+                          pair_capacity=64)
+    eb = ss.MappingEngine(gb, cam.width, cam.height, ss.RasterOpts(sh_degree=0))
+    eb.fit_capacity(cam)
+    for _ in range(3):
+        ea.step(cam, tgt)
+        eb.step(cam, tgt)
+    ea.synchronize()
+    eb.synchronize()
+    assert ea.pair_capacity > 64
+    np.testing.assert_allclose(ga.positions.cpu().numpy(), gb.positions.cpu().numpy(),
+                               rtol=0, atol=1e-6)
+
+
+def test_depth_extension_matches_oracle():
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    d = load("iter_sh0_small")
+    cam = fixture_camera(d)
+    g = ss.GaussianMap.from_arrays(*fixture_scene(d))
+    out = ss.rasterize_forward(g, cam, ss.RasterOpts(sh_degree=0, with_depth=True))
+    po = _gpu_proj_as_oracle(out)
+    ti = out.tile_index
+    oti = orc.OTileIndex(16, ti.tiles_x, ti.tiles_y, ti.pair_splat, ti.tile_range,
+                         ti.active_tiles)
+    r = orc.forward(po, oti, cam.width, cam.height, out.n_primitives, with_depth=True,
+                    m_cut=out.proj.m_cut.astype(np.float64))
+    assert np.abs(out.depth.cpu().numpy() - r.depth).max() <= 1e-4 * max(1.0, r.depth.max())
+    assert np.abs(out.alpha.cpu().numpy() - r.alpha).max() <= 1e-4
+    rng = np.random.default_rng(9)
+    gi = rng.standard_normal(out.image.shape).astype(np.float32) * 1e-3
+    gd = rng.standard_normal(out.depth.shape).astype(np.float32) * 1e-3
+    g2d = ss.screen_space_grads(out, torch.as_tensor(gi, device="cuda"),
+                                torch.as_tensor(gd, device="cuda")).cpu().numpy()
+    ref = orc.backward_splat(r, gi.astype(np.float64), gd.astype(np.float64))
+    mine = g2d[out.proj.map_index]
+    assert normwise(mine, ref) <= 1e-3
+    assert normwise(mine[:, 9], ref[:, 9]) <= 1e-3
+
+
+def test_densify_masks_and_indices_bit_exact():
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    d = load("densify")
+    g = ss.GaussianMap.from_arrays(d["pre_positions"], d["pre_rotations"], d["pre_log_scales"],
+                                   d["pre_opacity_logits"], d["pre_sh"])
+    g.grad2d_accum = torch.as_tensor(d["pre_grad2d_accum"], dtype=torch.float32, device="cuda")
+    g.grad3d_accum = torch.as_tensor(d["pre_grad3d_accum"], dtype=torch.float32, device="cuda")
+    g.obs_count = torch.as_tensor(d["pre_obs_count"], dtype=torch.int32, device="cuda")
+    h = g.to_numpy()
+    om = orc.OMap(h["positions"], h["rotations"], h["log_scales"], h["opacity_logits"], h["sh"],
+                  h["grad2d_accum"], h["grad3d_accum"], h["obs_count"])
+    ext = float(d["extent"])
+    small, large, keep = orc.densify_masks(om, scene_extent=ext)
+    normals = np.random.default_rng(7).standard_normal((2 * int(large.sum()), 3))
+    onew, ores = orc.densify_and_prune(om, normals=normals, scene_extent=ext)
+    cfg = ss.DensifyConfig()
+    res = ss.densify_and_prune(g, cfg, ext, normals=normals)
+    np.testing.assert_array_equal(res.survivors.cpu().numpy(), ores["survivors"])
+    assert (res.n_new, res.n_cloned, res.n_split, res.n_pruned) == (
+        ores["n_new"], ores["n_cloned"], ores["n_split"], ores["n_pruned"])
+    hn = g.to_numpy()
+    assert len(g) == len(onew)
+    np.testing.assert_allclose(hn["positions"], onew.positions, rtol=0, atol=1e-5)
+    np.testing.assert_allclose(hn["log_scales"], onew.log_scales, rtol=0, atol=1e-5)
+    np.testing.assert_array_equal(hn["opacity_logits"].astype(np.float32),
+                                  onew.opacity_logits.astype(np.float32))
+    assert hn["obs_count"].sum() == 0
+    # and the reference's own result on its float64 values (golden): same indices
+    np.testing.assert_array_equal(res.survivors.cpu().numpy(), d["survivors"])
+
+
+def test_opacity_reset():
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    d = load("iter_sh0_small")
+    g = ss.GaussianMap.from_arrays(*fixture_scene(d))
+    st = ss.AdamState.for_map(g)
+    st.m["opacity_logit"].fill_(1.0)
+    h = g.to_numpy()
+    om = orc.OMap(h["positions"], h["rotations"], h["log_scales"], h["opacity_logits"], h["sh"])
+    orc.opacity_reset(om, ceiling=0.01)
+    ss.opacity_reset(g, st, 0.01)
+    np.testing.assert_allclose(g.opacity_logits.cpu().numpy(), om.opacity_logits, rtol=1e-6)
+    assert float(st.m["opacity_logit"].abs().max()) == 0.0
+
+
+def test_multiview_is_sum_of_views():
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    from paper_2410_00486_b200.scene import survey_camera, survey_scene
+    sc = survey_scene(3000, 5)
+    cams = [survey_camera(96, 64, v, 3) for v in range(3)]
+    gm = ss.GaussianMap.from_scene(sc)
+    tg = [ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(3000, 105)), c,
+                               ss.RasterOpts(sh_degree=0)).image for c in cams]
+    eng = ss.MappingEngine(gm, 96, 64, ss.RasterOpts(sh_degree=0))
+    eng._flat_grads()
+    flat, fss = eng._flat_grads()
+    # reference: per-view API grads summed, reg grad once
+    gsum = None
+    g0 = ss.GaussianMap.from_scene(sc)
+    for v, c in enumerate(cams):
+        out = ss.rasterize_forward(g0, c, ss.RasterOpts(sh_degree=0))
+        lb = ss.compute_losses(out.image, tg[v], g0.opacity_logits)
+        gr = ss.backward_splatwise(out, lb.grad_image)
+        if v == 0:
+            gr.opacity_logit += lb.grad_opacity_logit
+        gsum = gr.position.clone() if gsum is None else gsum + gr.position
+    captured = {}
+    eng.multiview_step(cams, tg, allreduce=lambda f: captured.setdefault("flat", f.clone()))
+    n = len(gm)
+    pos = captured["flat"][:3 * n].view(n, 3).cpu().numpy()
+    assert normwise(pos, gsum.cpu().numpy()) <= 1e-4
+    obs = gm.obs_count.cpu().numpy()
+    assert obs.max() <= 3 and obs.sum() > 0
+
+
+def test_edge_cases_empty_and_culled():
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    cam = ss.Camera(50.0, 50.0, 16.0, 12.0, 32, 24)
+    g = ss.GaussianMap.from_arrays(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)),
+                                   np.zeros(0), np.zeros((0, 16, 3)))
+    out = ss.rasterize_forward(g, cam)
+    assert float(out.image.abs().max()) == 0.0 and float(out.final_t.min()) == 1.0
+    # every splat behind the camera: culled, background, zero gradients
+    gb = ss.GaussianMap.from_arrays(np.array([[0, 0, -1.0], [0.1, 0, -2.0]]),
+                                    np.array([[1.0, 0, 0, 0]] * 2), np.zeros((2, 3)),
+                                    np.zeros(2), np.zeros((2, 16, 3)))
+    out = ss.rasterize_forward(gb, cam, ss.RasterOpts(background=(0.2, 0.3, 0.4)))
+    np.testing.assert_allclose(out.image.cpu().numpy()[0, 0], [0.2, 0.3, 0.4], rtol=1e-6)
+    gr = ss.backward_splatwise(out, torch.ones_like(out.image))
+    assert float(gr.position.abs().max()) == 0.0
+
+
+def test_nonfinite_and_shape_errors():
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    d = load("iter_sh0_small")
+    cam = fixture_camera(d)
+    pos, rot, ls, op, sh = (a.copy() for a in fixture_scene(d))
+    pos[5, 1] = np.nan
+    g = ss.GaussianMap.from_arrays(pos, rot, ls, op, sh)
+    with pytest.raises(ValueError, match="non-finite parameter in primitive 5"):
+        ss.rasterize_forward(g, cam, ss.RasterOpts(sh_degree=0))
+    g = ss.GaussianMap.from_arrays(*fixture_scene(d))
+    out = ss.rasterize_forward(g, cam, ss.RasterOpts(sh_degree=0, with_checkpoints=False))
+    with pytest.raises(RuntimeError, match="no checkpoints"):
+        ss.backward_splatwise(out, torch.zeros_like(out.image))
+    out = ss.rasterize_forward(g, cam, ss.RasterOpts(sh_degree=0))
+    with pytest.raises(ValueError, match="does not match"):
+        ss.backward_splatwise(out, torch.zeros((3, 3, 3), device="cuda"))
+
+
+def test_two_splat_known_answer():
+    """SPEC.md:127 on the GPU: (1,0,0)@0.5 over (0,1,0)@0.5 -> (0.5, 0.25, 0)."""
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    from paper_2410_00486_b200.scene import SH_C0
+    cam = ss.Camera(100.0, 100.0, 8.0, 8.0, 16, 16)
+    sh = np.zeros((2, 16, 3))
+    sh[0, 0] = (np.array([1.0, 0, 0]) - 0.5) / SH_C0
+    sh[1, 0] = (np.array([0, 1.0, 0]) - 0.5) / SH_C0
+    g = ss.GaussianMap.from_arrays(np.array([[0, 0, 5.0], [0, 0, 6.0]]),
+                                   np.array([[1.0, 0, 0, 0]] * 2), np.full((2, 3), -1.0),
+                                   np.zeros(2), sh)
+    out = ss.rasterize_forward(g, cam, ss.RasterOpts(sh_degree=0))
+    # at the centre pixel (8,8) both splats have alpha = sigma = 0.5
+    np.testing.assert_allclose(out.image.cpu().numpy()[8, 8], [0.5, 0.25, 0.0], atol=1e-6)
+    assert abs(float(out.final_t[8, 8]) - 0.25) < 1e-6
+    assert int(out.n_contrib[8, 8]) == 2
