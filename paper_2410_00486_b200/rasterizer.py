@@ -298,6 +298,7 @@ def rasterize_forward(gmap: GaussianMap, camera, opts: RasterOpts | None = None)
         pcount = int(sh[_lib.ST_PAIRS])
         if not int(sh[_lib.ST_OVERFLOW]):
             break
+        st[_lib.ST_OVERFLOW] = 0  # the overflow word is sticky; clear it for the retry
         cap = int(pcount * 1.25) + 1024
     _CAP_HINT[key] = cap
     n_slots = int(bins.ckpt_base[n_tiles].item())
