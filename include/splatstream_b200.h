@@ -134,25 +134,30 @@ int ss_bin_sort(int64_t n, const ss_splats *splats, const ss_camera *cam, const 
 /* ------------------------------------------------------------ blend fwd */
 /* Replaces rasterize_forward's blend (api.py:135-206; forward_tile
  * kernels.py:34-109 and checkpoint_tile kernels.py:112-152).
- * d_ckpt holds (T,r,g,b) float4 per pixel per checkpoint slot; with depth,
- * d_ckpt_depth holds D.  d_contributed (optional, [n] uint8) marks splats
- * blended into >= 1 pixel.  d_work/d_status->bucket_count receive the
- * (tile, bucket) work units of the splat-wise backward. */
+ * Checkpoint slots (d_bins->d_ckpt_base): d_ckpt holds (T,r,g,b) float4 per
+ * pixel per slot; d_ckpt_depth (depth extension) holds D; d_ckpt_mask holds,
+ * per pixel per slot, the 32-bit mask of the bucket's list positions that
+ * were blended into the pixel (read by the backward).  d_contributed
+ * (optional, [n] uint8) marks splats blended into >= 1 pixel.
+ * d_work/d_status->bucket_count receive the (tile, bucket) work units of
+ * the splat-wise backward. */
 int ss_blend_forward(const ss_camera *cam, const ss_raster_opts *opts, const ss_splats *splats,
                      const ss_bins *bins, float *d_image, float *d_final_t, int32_t *d_n_contrib,
                      float *d_depth, int32_t *d_k_eff, uint8_t *d_contributed, void *d_ckpt,
-                     float *d_ckpt_depth, uint32_t *d_work, int64_t work_capacity,
-                     ss_status *d_status, void *stream);
+                     float *d_ckpt_depth, uint32_t *d_ckpt_mask, uint32_t *d_work,
+                     int64_t work_capacity, ss_status *d_status, void *stream);
 
 /* -------------------------------------------------------------- losses */
 /* Replaces compute_losses' photometric part (losses.py:137-154,198-218):
  * (1-l) mean|x-y| + l (1 - SSIM), 11x11 Gaussian window, mirror padding.
  * d_sums receives (sum |x-y|, sum SSIM) as doubles; d_grad (h,w,3) the
- * analytic gradient.  Needs height, width >= 6. */
+ * analytic gradient; optional d_pixgrad (h,w,4) float4 (g_r, g_g, g_b,
+ * g . x) for ss_backward_splat (lambda_ssim != 0 only).  Needs height,
+ * width >= 6 when lambda_ssim != 0. */
 size_t ss_loss_workspace_bytes(int32_t height, int32_t width);
 int ss_loss_l1_ssim(int32_t height, int32_t width, const float *d_x, const float *d_y,
-                    float lambda_ssim, float *d_grad, double *d_sums, void *d_workspace,
-                    size_t workspace_bytes, void *stream);
+                    float lambda_ssim, float *d_grad, float *d_pixgrad, double *d_sums,
+                    void *d_workspace, size_t workspace_bytes, void *stream);
 /* opacity_reg (losses.py:157-168) chained through the logistic
  * (losses.py:220-223): d_grad[i] = lambda_o sigma(1-sigma)/n (written or
  * added; d_grad may be NULL); d_sum[0] receives sum sigma.  d_sum must hold
@@ -169,14 +174,17 @@ int ss_depth_l1(int32_t height, int32_t width, const float *d_depth, const float
 /* --------------------------------------------------------- backward */
 /* Replaces backward_splatwise up to the screen-space rows g2d
  * (api.py:275-336; backward_splat_tile / _splat_bucket_inner
- * kernels.py:271-373).  d_g2d [n * g2d_cols] float, g2d_cols = 9 (10 with
+ * kernels.py:271-373).  d_pixgrad (optional, from ss_loss_l1_ssim; its .w
+ * must include g_D . D with depth) replaces reading d_grad_image/d_image.
+ * d_g2d [n * g2d_cols] float, g2d_cols = 9 (10 with
  * depth), columns [rgb(3), mean2d(2), conic(3), opacity(, z)], zeroed
  * here and accumulated with one red.add row per (tile, splat). */
 int ss_backward_splat(const ss_camera *cam, const ss_raster_opts *opts, const ss_splats *splats,
                       const ss_bins *bins, const float *d_image, const float *d_grad_image,
-                      const float *d_depth, const float *d_grad_depth,
+                      const float *d_pixgrad, const float *d_depth, const float *d_grad_depth,
                       const int32_t *d_n_contrib, const int32_t *d_k_eff, const void *d_ckpt,
-                      const float *d_ckpt_depth, const uint32_t *d_work, int64_t work_capacity,
+                      const float *d_ckpt_depth, const uint32_t *d_ckpt_mask,
+                      const uint32_t *d_work, int64_t work_capacity,
                       int64_t n, float *d_g2d, uint8_t *d_contributed, const ss_status *d_status,
                       void *stream);
 

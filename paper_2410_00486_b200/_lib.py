@@ -92,13 +92,13 @@ _SIGS = {
     "ss_bin_workspace_bytes": (SZ, [I64, I64, I32]),
     "ss_bin_sort": (I32, [I64, P(SSSplats), P(SSCamera), P(SSBins), VP, SZ, VP, VP]),
     "ss_blend_forward": (I32, [P(SSCamera), P(SSRasterOpts), P(SSSplats), P(SSBins), VP, VP, VP,
-                               VP, VP, VP, VP, VP, VP, I64, VP, VP]),
+                               VP, VP, VP, VP, VP, VP, VP, I64, VP, VP]),
     "ss_loss_workspace_bytes": (SZ, [I32, I32]),
-    "ss_loss_l1_ssim": (I32, [I32, I32, VP, VP, F32, VP, VP, VP, SZ, VP]),
+    "ss_loss_l1_ssim": (I32, [I32, I32, VP, VP, F32, VP, VP, VP, VP, SZ, VP]),
     "ss_opacity_reg": (I32, [I64, VP, F32, VP, I32, VP, VP]),
     "ss_depth_l1": (I32, [I32, I32, VP, VP, F32, VP, VP, VP]),
     "ss_backward_splat": (I32, [P(SSCamera), P(SSRasterOpts), P(SSSplats), P(SSBins), VP, VP,
-                                VP, VP, VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP]),
+                                VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP]),
     "ss_chain_backward": (I32, [P(SSMap), P(SSCamera), P(SSRasterOpts), VP, VP, VP, F32, I32,
                                 P(SSParamGrads), VP, VP]),
     "ss_adam_step": (I32, [P(SSMap), P(SSParamGrads), P(SSParamGrads), P(SSParamGrads),

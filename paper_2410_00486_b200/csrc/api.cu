@@ -14,16 +14,17 @@ cudaError_t launch_bin_sort(int64_t, const ss_splats*, const ss_camera*, const s
                             size_t, ss_status*, cudaStream_t);
 cudaError_t launch_blend_forward(const ss_camera*, const ss_raster_opts*, const ss_splats*,
                                  const ss_bins*, float*, float*, int32_t*, float*, int32_t*,
-                                 uint8_t*, void*, float*, uint32_t*, int64_t, ss_status*,
-                                 cudaStream_t);
+                                 uint8_t*, void*, float*, uint32_t*, uint32_t*, int64_t,
+                                 ss_status*, cudaStream_t);
 cudaError_t launch_backward_splat(const ss_camera*, const ss_raster_opts*, const ss_splats*,
-                                  const ss_bins*, const float*, const float*, const float*,
-                                  const float*, const int32_t*, const int32_t*, const void*,
-                                  const float*, const uint32_t*, int64_t, int64_t, float*,
-                                  uint8_t*, const ss_status*, uint32_t*, cudaStream_t);
+                                  const ss_bins*, const float*, const float*, const float4*,
+                                  const float*, const float*, const int32_t*, const int32_t*,
+                                  const void*, const float*, const uint32_t*, const uint32_t*,
+                                  int64_t, int64_t, float*, uint8_t*, const ss_status*, uint32_t*,
+                                  cudaStream_t);
 size_t loss_workspace_bytes(int, int);
-cudaError_t launch_loss(int, int, const float*, const float*, float, float*, double*, void*,
-                        size_t, cudaStream_t);
+cudaError_t launch_loss(int, int, const float*, const float*, float, float*, float*, double*,
+                        void*, size_t, cudaStream_t);
 cudaError_t launch_opacity_reg(int64_t, const float*, float, float*, int, double*, double*,
                                cudaStream_t);
 cudaError_t launch_depth_l1(int, int, const float*, const float*, float, float*, double*,
@@ -123,15 +124,15 @@ int ss_bin_sort(int64_t n, const ss_splats* splats, const ss_camera* cam, const 
 int ss_blend_forward(const ss_camera* cam, const ss_raster_opts* opts, const ss_splats* splats,
                      const ss_bins* bins, float* d_image, float* d_final_t, int32_t* d_n_contrib,
                      float* d_depth, int32_t* d_k_eff, uint8_t* d_contributed, void* d_ckpt,
-                     float* d_ckpt_depth, uint32_t* d_work, int64_t work_capacity,
-                     ss_status* d_status, void* stream) {
+                     float* d_ckpt_depth, uint32_t* d_ckpt_mask, uint32_t* d_work,
+                     int64_t work_capacity, ss_status* d_status, void* stream) {
     if (!cam || !opts_ok(opts) || !splats || !bins || !d_image || !d_final_t || !d_n_contrib ||
-        !d_k_eff || !d_ckpt || !d_status)
+        !d_k_eff || !d_ckpt || !d_ckpt_mask || !d_status)
         return SS_EINVAL;
     if (opts->with_depth && (!d_depth || !d_ckpt_depth)) return SS_EINVAL;
     return rc(launch_blend_forward(cam, opts, splats, bins, d_image, d_final_t, d_n_contrib,
-                                   d_depth, d_k_eff, d_contributed, d_ckpt, d_ckpt_depth, d_work,
-                                   work_capacity, d_status, S(stream)));
+                                   d_depth, d_k_eff, d_contributed, d_ckpt, d_ckpt_depth,
+                                   d_ckpt_mask, d_work, work_capacity, d_status, S(stream)));
 }
 
 size_t ss_loss_workspace_bytes(int32_t height, int32_t width) {
@@ -139,13 +140,14 @@ size_t ss_loss_workspace_bytes(int32_t height, int32_t width) {
 }
 
 int ss_loss_l1_ssim(int32_t height, int32_t width, const float* d_x, const float* d_y,
-                    float lambda_ssim, float* d_grad, double* d_sums, void* d_workspace,
-                    size_t workspace_bytes, void* stream) {
+                    float lambda_ssim, float* d_grad, float* d_pixgrad, double* d_sums,
+                    void* d_workspace, size_t workspace_bytes, void* stream) {
     if (!d_x || !d_y || !d_grad || !d_sums || height <= 0 || width <= 0) return SS_EINVAL;
     if (lambda_ssim != 0.0f && (height < 6 || width < 6)) return SS_EINVAL;
     if (workspace_bytes < loss_workspace_bytes(height, width)) return SS_ECAPACITY;
-    return rc(launch_loss(height, width, d_x, d_y, lambda_ssim, d_grad, d_sums, d_workspace,
-                          workspace_bytes, S(stream)));
+    if (d_pixgrad && lambda_ssim == 0.0f) return SS_EINVAL;
+    return rc(launch_loss(height, width, d_x, d_y, lambda_ssim, d_grad, d_pixgrad, d_sums,
+                          d_workspace, workspace_bytes, S(stream)));
 }
 
 int ss_opacity_reg(int64_t n, const float* d_logits, float lambda_o, float* d_grad,
@@ -166,21 +168,23 @@ int ss_depth_l1(int32_t height, int32_t width, const float* d_depth, const float
 
 int ss_backward_splat(const ss_camera* cam, const ss_raster_opts* opts, const ss_splats* splats,
                       const ss_bins* bins, const float* d_image, const float* d_grad_image,
-                      const float* d_depth, const float* d_grad_depth,
+                      const float* d_pixgrad, const float* d_depth, const float* d_grad_depth,
                       const int32_t* d_n_contrib, const int32_t* d_k_eff, const void* d_ckpt,
-                      const float* d_ckpt_depth, const uint32_t* d_work, int64_t work_capacity,
+                      const float* d_ckpt_depth, const uint32_t* d_ckpt_mask,
+                      const uint32_t* d_work, int64_t work_capacity,
                       int64_t n, float* d_g2d, uint8_t* d_contributed, const ss_status* d_status,
                       void* stream) {
     if (!cam || !opts_ok(opts) || !splats || !bins || !d_image || !d_grad_image ||
-        !d_n_contrib || !d_k_eff || !d_ckpt || !d_work || !d_g2d || !d_status)
+        !d_n_contrib || !d_k_eff || !d_ckpt || !d_ckpt_mask || !d_work || !d_g2d || !d_status)
         return SS_EINVAL;
     if (opts->with_depth && (!d_depth || !d_ckpt_depth)) return SS_EINVAL;
     // the work counter lives in the status block's reserved word
     uint32_t* counter = reinterpret_cast<uint32_t*>(const_cast<int64_t*>(&d_status->reserved));
-    return rc(launch_backward_splat(cam, opts, splats, bins, d_image, d_grad_image, d_depth,
+    return rc(launch_backward_splat(cam, opts, splats, bins, d_image, d_grad_image,
+                                    reinterpret_cast<const float4*>(d_pixgrad), d_depth,
                                     d_grad_depth, d_n_contrib, d_k_eff, d_ckpt, d_ckpt_depth,
-                                    d_work, work_capacity, n, d_g2d, d_contributed, d_status,
-                                    counter, S(stream)));
+                                    d_ckpt_mask, d_work, work_capacity, n, d_g2d, d_contributed,
+                                    d_status, counter, S(stream)));
 }
 
 int ss_chain_backward(const ss_map* map, const ss_camera* cam, const ss_raster_opts* opts,

@@ -49,6 +49,68 @@ __device__ __forceinline__ void st_volatile64(unsigned long long* p, unsigned lo
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Decoupled look-back with a window: each step loads the status words of up
+// to LB_WIN predecessors at once (independent loads in flight), then
+// consumes them nearest-first -- adding aggregates until an inclusive
+// prefix is found, or stopping at the first not-yet-published word and
+// retrying from there.  With hundreds of co-resident CTAs the walk length
+// is ~k/2 predecessors; the window divides the serial L2 round trips by
+// LB_WIN.
+constexpr int LB_WIN = 16;
+
+__device__ __forceinline__ uint32_t lookback_u32(const uint32_t* status, int64_t j, int stride) {
+    uint32_t excl = 0;
+    while (j >= 0) {
+        uint32_t v[LB_WIN];
+#pragma unroll
+        for (int i = 0; i < LB_WIN; ++i)
+            v[i] = (j - i >= 0) ? ld_volatile(status + (size_t)(j - i) * stride) : kFlagInc;
+        int used = 0;
+        bool done = false;
+#pragma unroll
+        for (int i = 0; i < LB_WIN; ++i) {
+            if (done || used != i) break;
+            const uint32_t f = v[i] & ~kValMask;
+            if (f == 0) break;
+            excl += v[i] & kValMask;
+            ++used;
+            if (f == kFlagInc) done = true;
+        }
+        if (done) break;
+        j -= used;
+        if (used < LB_WIN) __nanosleep(32);
+    }
+    return excl;
+}
+
+__device__ __forceinline__ unsigned long long lookback_u64(const unsigned long long* status,
+                                                           int64_t j, unsigned long long flag_agg,
+                                                           unsigned long long flag_inc,
+                                                           unsigned long long mask) {
+    unsigned long long excl = 0;
+    while (j >= 0) {
+        unsigned long long v[LB_WIN];
+#pragma unroll
+        for (int i = 0; i < LB_WIN; ++i) v[i] = (j - i >= 0) ? ld_volatile64(status + (j - i)) : flag_inc;
+        int used = 0;
+        bool done = false;
+#pragma unroll
+        for (int i = 0; i < LB_WIN; ++i) {
+            if (done || used != i) break;
+            const unsigned long long f = v[i] & ~mask;
+            if (f == 0) break;
+            excl += v[i] & mask;
+            ++used;
+            if (f == flag_inc) done = true;
+        }
+        if (done) break;
+        j -= used;
+        if (used < LB_WIN) __nanosleep(32);
+    }
+    (void)flag_agg;
+    return excl;
+}
+
 // ------------------------------------------------------------- histogram
 // 256-bin histograms of `npass` consecutive 8-bit digits starting at shift0.
 __global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys,
@@ -69,9 +131,28 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restr
 }
 
 // --------------------------------------------------------------- onesweep
-// keys_in == nullptr is not allowed; vals_in == nullptr means "values are
-// the item indices" (first pass over splats).  d_count: number of items
-// (device), clamped to cap.
+// Block-wide exclusive scan of one value per thread (256 threads).
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* s_warp) {
+    const int t = threadIdx.x, w = t >> 5, l = t & 31;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += y;
+    }
+    if (l == 31) s_warp[w] = incl;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int k = 0; k < w; ++k) pre += s_warp[k];
+    __syncthreads();
+    return pre + incl - v;
+}
+
+// One stable LSD pass on an 8-bit digit: per-warp ranking with
+// __match_any_sync, per-digit windowed decoupled look-back, block-local
+// reorder in shared memory, then coalesced runs written to the global digit
+// ranges.  vals_in == nullptr means "values are the item indices" (first
+// pass over splats).  d_count: number of items (device), clamped to cap.
 template <int ITEMS>
 __global__ void __launch_bounds__(256) onesweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
@@ -83,30 +164,32 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
     __shared__ uint32_t s_bid;
     __shared__ uint32_t s_cnt[8][256];
     __shared__ uint32_t s_base[256];
-    __shared__ uint32_t s_warp_tot[8];
+    __shared__ uint32_t s_local[256];
+    __shared__ uint32_t s_warp[8];
+    __shared__ uint32_t s_keys[TILE];
+    __shared__ uint32_t s_vals[TILE];
     const int t = threadIdx.x, w = t >> 5, l = t & 31;
     if (t == 0) s_bid = atomicAdd(counter, 1u);
 #pragma unroll
     for (int k = 0; k < 8; ++k) s_cnt[k][t] = 0;
     __syncthreads();
     const uint32_t bid = s_bid;
-    uint32_t n = d_count ? min(*d_count, cap) : n_static;
+    const uint32_t n = d_count ? min(*d_count, cap) : n_static;
     const uint32_t base = bid * TILE;
     if (base >= n) return;
+    const uint32_t nloc = min((uint32_t)TILE, n - base);
 
-    uint32_t key[ITEMS], val[ITEMS], rank[ITEMS];
-    const uint32_t wbase = base + w * WARP_ITEMS;
+    uint32_t key[ITEMS], rank[ITEMS];
+    const uint32_t wbase = w * WARP_ITEMS;
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
-        uint32_t idx = wbase + r * 32 + l;
-        bool v = idx < n;
-        key[r] = v ? keys_in[idx] : 0u;
-        val[r] = v ? (vals_in ? vals_in[idx] : idx) : 0u;
+        uint32_t li = wbase + r * 32 + l;
+        key[r] = li < nloc ? keys_in[base + li] : 0u;
     }
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
-        uint32_t idx = wbase + r * 32 + l;
-        uint32_t d = idx < n ? ((key[r] >> shift) & 255u) : 256u;
+        uint32_t li = wbase + r * 32 + l;
+        uint32_t d = li < nloc ? ((key[r] >> shift) & 255u) : 256u;
         unsigned peers = __match_any_sync(0xffffffffu, d);
         uint32_t before = d < 256u ? s_cnt[w][d] : 0u;
         rank[r] = before + __popc(peers & lanemask_lt());
@@ -115,7 +198,6 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
         __syncwarp();
     }
     __syncthreads();
-    // exclusive scan over warps for digit t, block total
     uint32_t run = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -124,47 +206,41 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
         run += c;
     }
     const uint32_t total = run;
-    // global digit start: exclusive scan of hist over digits (block scan)
-    uint32_t hv = hist[t];
-    uint32_t incl = hv;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (l >= o) incl += y;
-    }
-    if (l == 31) s_warp_tot[w] = incl;
-    // decoupled look-back for digit t
+    // publish + look back for digit t
     uint32_t* my = status + (size_t)bid * 256 + t;
     uint32_t excl = 0;
     if (bid == 0) {
         st_volatile(my, kFlagInc | total);
     } else {
         st_volatile(my, kFlagAgg | total);
-        int64_t j = (int64_t)bid - 1;
-        while (j >= 0) {
-            uint32_t v = ld_volatile(status + (size_t)j * 256 + t);
-            uint32_t f = v & ~kValMask;
-            if (f == 0) continue;
-            excl += v & kValMask;
-            if (f == kFlagInc) break;
-            --j;
-        }
+        excl = lookback_u32(status + t, (int64_t)bid - 1, 256);
         st_volatile(my, kFlagInc | (excl + total));
     }
+    const uint32_t hv = hist[t];
+    const uint32_t gstart = block_excl_scan256(hv, s_warp);
+    const uint32_t lstart = block_excl_scan256(total, s_warp);
+    s_base[t] = gstart + excl;
+    s_local[t] = lstart;
     __syncthreads();
-    uint32_t wpre = 0;
-    for (int k = 0; k < w; ++k) wpre += s_warp_tot[k];
-    s_base[t] = wpre + incl - hv + excl;
-    __syncthreads();
+    // block-local reorder by digit (stable)
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
-        uint32_t idx = wbase + r * 32 + l;
-        if (idx < n) {
+        uint32_t li = wbase + r * 32 + l;
+        if (li < nloc) {
             uint32_t d = (key[r] >> shift) & 255u;
-            uint32_t pos = s_base[d] + s_cnt[w][d] + rank[r];
-            vals_out[pos] = val[r];
-            if (keys_out) keys_out[pos] = key[r];
+            uint32_t lp = s_local[d] + s_cnt[w][d] + rank[r];
+            s_keys[lp] = key[r];
+            s_vals[lp] = vals_in ? vals_in[base + li] : base + li;
         }
+    }
+    __syncthreads();
+    // coalesced runs to the global digit ranges
+    for (uint32_t i = t; i < nloc; i += 256) {
+        uint32_t k = s_keys[i];
+        uint32_t d = (k >> shift) & 255u;
+        uint32_t gp = s_base[d] + (i - s_local[d]);
+        vals_out[gp] = s_vals[i];
+        if (keys_out) keys_out[gp] = k;
     }
 }
 
@@ -231,15 +307,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t* __restrict__ 
             st_volatile64(my, kSFlagInc | tot);
         } else {
             st_volatile64(my, kSFlagAgg | tot);
-            int64_t j = (int64_t)bid - 1;
-            while (j >= 0) {
-                unsigned long long x = ld_volatile64(status + j);
-                unsigned long long f = x & ~kSValMask;
-                if (f == 0) continue;
-                excl += x & kSValMask;
-                if (f == kSFlagInc) break;
-                --j;
-            }
+            excl = lookback_u64(status, (int64_t)bid - 1, kSFlagAgg, kSFlagInc, kSValMask);
             st_volatile64(my, kSFlagInc | (excl + tot));
         }
         s_excl = excl;
@@ -259,9 +327,11 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t* __restrict__ 
 }
 
 // ------------------------------------------------------------------- emit
-// One thread per splat in (depth, index) order: write its touched tiles'
-// (tile, splat) pairs at its scanned offset; accumulate the 8-bit tile
-// digit histograms of the pair sort.
+// One warp per 32 consecutive splats in (depth, index) order: the warp's
+// pairs form one contiguous output range, written lane-strided (coalesced);
+// each output element finds its splat by a 5-step shuffle binary search
+// over the 32 exclusive offsets.  The 8-bit tile-digit histograms of the
+// pair sort are accumulated in shared memory on the way.
 __global__ void __launch_bounds__(256) emit_pairs_kernel(
     uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restrict__ tiles,
     const uint2* __restrict__ rect, const uint32_t* __restrict__ offsets, int tiles_x,
@@ -271,22 +341,44 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
     for (int k = threadIdx.x; k < 3 * 256; k += blockDim.x) (&h[0][0])[k] = 0;
     __syncthreads();
     const bool ok = *total <= cap;
-    uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const uint32_t j = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32 + lane;
+    uint32_t s = 0, c = 0, o = 0, x0 = 0, y0 = 0, wx = 1;
     if (ok && j < n) {
-        uint32_t s = order[j];
-        uint32_t c = tiles[s];
+        s = order[j];
+        c = tiles[s];
+        o = offsets[j];
         if (c) {
             uint2 rc = rect[s];
-            uint32_t x0 = rc.x & 0xffffu, y0 = rc.x >> 16, x1 = rc.y & 0xffffu, y1 = rc.y >> 16;
-            uint32_t o = offsets[j];
-            for (uint32_t ty = y0; ty <= y1; ++ty)
-                for (uint32_t tx = x0; tx <= x1; ++tx) {
-                    uint32_t tid = ty * tiles_x + tx;
-                    keys[o] = tid;
-                    vals[o] = s;
-                    ++o;
-                    for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(tid >> (8 * p)) & 255u], 1u);
-                }
+            x0 = rc.x & 0xffffu;
+            y0 = rc.x >> 16;
+            wx = (rc.y & 0xffffu) - x0 + 1;
+        }
+    }
+    const uint32_t base = __shfl_sync(0xffffffffu, o, 0);
+    const uint32_t rel = (ok && j < n) ? o - base : 0x7fffffffu;
+    uint32_t endw = (ok && j < n) ? rel + c : 0u;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) endw = max(endw, __shfl_xor_sync(0xffffffffu, endw, d));
+    // warp-uniform trip count: every lane reaches every __shfl_sync
+    for (uint32_t e0 = 0; e0 < endw; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        // owner = largest lane with rel <= e (never an empty lane for e < endw)
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            uint32_t r = __shfl_sync(0xffffffffu, rel, lo + step);
+            if (r <= e) lo += step;
+        }
+        const uint32_t li = e - __shfl_sync(0xffffffffu, rel, lo);
+        const uint32_t ox = __shfl_sync(0xffffffffu, x0, lo), oy = __shfl_sync(0xffffffffu, y0, lo);
+        const uint32_t ow = __shfl_sync(0xffffffffu, wx, lo), sid = __shfl_sync(0xffffffffu, s, lo);
+        if (e < endw) {
+            const uint32_t ry = li / ow;
+            const uint32_t tid = (oy + ry) * tiles_x + ox + (li - ry * ow);
+            keys[base + e] = tid;
+            vals[base + e] = sid;
+            for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(tid >> (8 * p)) & 255u], 1u);
         }
     }
     __syncthreads();
@@ -329,7 +421,7 @@ struct BinWorkspace {
     }
 };
 
-constexpr int kDepthItems = 4;   // 1024 splats per onesweep CTA
+constexpr int kDepthItems = 8;   // 2048 splats per onesweep CTA
 constexpr int kPairItems = 16;   // 4096 pairs per onesweep CTA
 
 struct BinLayout {
@@ -449,7 +541,8 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
             pv = vdst;
         }
         // 5. ranges by boundary detection on the sorted tile ids
-        tile_ranges_kernel<<<592, 256, 0, s>>>(pk, P, cap, bins->d_tile_start, bins->d_tile_end);
+        tile_ranges_kernel<<<div_up(cap > 0 ? cap : 1, 1024), 256, 0, s>>>(
+            pk, P, cap, bins->d_tile_start, bins->d_tile_end);
     } else {
         e = cudaMemsetAsync(P, 0, sizeof(int64_t) * 2, s);
         if (e != cudaSuccess) return e;

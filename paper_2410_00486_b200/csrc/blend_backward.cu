@@ -30,31 +30,27 @@
 
 namespace ss {
 
-struct PixA {  // per active pixel, gradient side
-    float g0, g1, g2, gimg;
-};
-struct PixB {  // per active pixel, state side
-    float T0, G0;
-    int nc, p;
-};
-
 template <bool DEPTH>
 __global__ void __launch_bounds__(128) backward_splat_kernel(
     int W, int H, int tiles_x, const uint32_t* __restrict__ tile_start,
     const uint32_t* __restrict__ ckpt_base, const int32_t* __restrict__ k_eff,
-    const uint32_t* __restrict__ pairs, const SplatRec* __restrict__ rec, float amin, float amax,
+    const uint32_t* __restrict__ pairs, const SplatRec* __restrict__ rec, float amax,
     const float* __restrict__ image, const float* __restrict__ grad_image,
-    const float* __restrict__ depth_img, const float* __restrict__ grad_depth,
-    const int32_t* __restrict__ n_contrib, const float4* __restrict__ ckpt,
-    const float* __restrict__ ckpt_depth, const uint2* __restrict__ work,
+    const float4* __restrict__ pixgrad, const float* __restrict__ depth_img,
+    const float* __restrict__ grad_depth, const int32_t* __restrict__ n_contrib,
+    const float4* __restrict__ ckpt, const float* __restrict__ ckpt_depth,
+    const uint32_t* __restrict__ ckpt_mask, const uint2* __restrict__ work,
     const int64_t* __restrict__ work_count, int64_t work_cap, uint32_t* work_counter,
     float* __restrict__ g2d, uint8_t* __restrict__ contributed) {
     extern __shared__ float4 smem[];
     constexpr int NC = DEPTH ? 10 : 9;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    PixA* sA = reinterpret_cast<PixA*>(smem) + wid * kTilePx;
-    PixB* sB = reinterpret_cast<PixB*>(smem + (blockDim.x >> 5) * kTilePx) + wid * kTilePx;
-    float* sD = reinterpret_cast<float*>(smem + 2 * (blockDim.x >> 5) * kTilePx) + wid * kTilePx;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // per-warp compacted pixel list: gradient side, coordinates, state, blend mask
+    float4* sG = smem + wid * kTilePx;
+    float2* sXY = reinterpret_cast<float2*>(smem + nw * kTilePx) + wid * kTilePx;
+    float2* sS = reinterpret_cast<float2*>(smem + nw * kTilePx) + (nw + wid) * kTilePx;
+    uint32_t* sM = reinterpret_cast<uint32_t*>(smem + 2 * nw * kTilePx) + wid * kTilePx;
+    float* sD = reinterpret_cast<float*>(smem + 2 * nw * kTilePx) + (nw + wid) * kTilePx;
     const int64_t count = min(*work_count, work_cap);
 
     for (;;) {
@@ -69,18 +65,17 @@ __global__ void __launch_bounds__(128) backward_splat_kernel(
         const int ke = k_eff[tile];
         const int kbase = b * kBucket;
         const int k = kbase + lane;
-        const bool valid = k < ke;
         uint32_t s = 0;
-        float4 A = make_float4(0.f, 0.f, 0.f, 0.f), B = make_float4(0.f, 0.f, -1.f, 1.f),
+        float4 A = make_float4(0.f, 0.f, 0.f, 0.f), B = make_float4(0.f, 1.f, -1.f, 0.f),
                C = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) {
+        if (k < ke) {
             s = pairs[start + k];
             const SplatRec r = rec[s];
             A = r.a;
             B = r.b;
             C = r.c;
         }
-        // ---- compact the pixels still blending at this bucket
+        // ---- compact the pixels that blended any splat of this bucket
         const size_t slot0 = (size_t)(ckpt_base[tile] + b) * kTilePx;
         int nact = 0;
 #pragma unroll 1
@@ -90,23 +85,31 @@ __global__ void __launch_bounds__(128) backward_splat_kernel(
             const bool inside = ix < W && iy < H;
             const size_t o = (size_t)iy * W + ix;
             const int nc = inside ? n_contrib[o] : 0;
-            const bool act = nc > kbase;
-            const unsigned bal = __ballot_sync(0xffffffffu, act);
-            if (act) {
+            const uint32_t mask = nc > kbase ? ckpt_mask[slot0 + p] : 0u;
+            const unsigned bal = __ballot_sync(0xffffffffu, mask != 0u);
+            if (mask) {
                 const int pos = nact + __popc(bal & lanemask_lt());
-                const float g0 = grad_image[3 * o], g1 = grad_image[3 * o + 1],
-                            g2 = grad_image[3 * o + 2];
-                float gimg = g0 * image[3 * o] + g1 * image[3 * o + 1] + g2 * image[3 * o + 2];
+                float4 pg;
+                if (pixgrad) {
+                    pg = pixgrad[o];
+                } else {
+                    pg.x = grad_image[3 * o];
+                    pg.y = grad_image[3 * o + 1];
+                    pg.z = grad_image[3 * o + 2];
+                    pg.w = pg.x * image[3 * o] + pg.y * image[3 * o + 1] + pg.z * image[3 * o + 2];
+                }
                 const float4 ck = ckpt[slot0 + p];
-                float G0 = g0 * ck.y + g1 * ck.z + g2 * ck.w;
+                float G0 = pg.x * ck.y + pg.y * ck.z + pg.z * ck.w;
                 if (DEPTH) {
                     const float gd = grad_depth ? grad_depth[o] : 0.f;
-                    gimg += gd * depth_img[o];
+                    if (!pixgrad) pg.w += gd * depth_img[o];
                     G0 += gd * ckpt_depth[slot0 + p];
                     sD[pos] = gd;
                 }
-                sA[pos] = PixA{g0, g1, g2, gimg};
-                sB[pos] = PixB{ck.x, G0, nc, p};
+                sG[pos] = pg;
+                sXY[pos] = make_float2((float)ix, (float)iy);
+                sS[pos] = make_float2(ck.x, G0);
+                sM[pos] = mask;
             }
             nact += __popc(bal);
         }
@@ -124,49 +127,49 @@ __global__ void __launch_bounds__(128) backward_splat_kernel(
             float Tin = __shfl_up_sync(0xffffffffu, T, 1);
             float Gin = __shfl_up_sync(0xffffffffu, G, 1);
             const int j = st - lane;
-            if (j < 0 || j >= nact) continue;
-            const PixB pb = sB[j];
+            if ((unsigned)j >= (unsigned)nact) continue;
+            const uint32_t m = sM[j];
             if (lane == 0) {
-                Tin = pb.T0;
-                Gin = pb.G0;
+                const float2 s0 = sS[j];
+                Tin = s0.x;
+                Gin = s0.y;
             }
             T = Tin;
             G = Gin;
-            if (!valid || k >= pb.nc) continue;
-            const float px = (float)(x0 + (pb.p & 15)), py = (float)(y0 + (pb.p >> 4));
-            float dx, dy;
-            const float a = splat_alpha(px, py, A, B, amin, amax, dx, dy);
-            if (a < 0.f) continue;
+            if (!((m >> lane) & 1u)) continue;
+            // this (pixel, splat) pair was blended in the forward
             blended = true;
-            const PixA pa = sA[j];
-            const float gd = DEPTH ? sD[j] : 0.f;
+            const float2 xy = sXY[j];
+            const float4 pg = sG[j];
+            float dx, dy;
+            const float a = splat_alpha_blended(xy.x, xy.y, A, B, amax, dx, dy);
             const float w = __fmul_rn(a, T);
-            float grgb = pa.g0 * C.x + pa.g1 * C.y + pa.g2 * C.z;
-            if (DEPTH) grgb += gd * B.w;
-            const float Gafter = G + grgb * w;
-            const float Tafter = __fmul_rn(T, __fsub_rn(1.0f, a));
-            if (pa.g0 != 0.f || pa.g1 != 0.f || pa.g2 != 0.f || (DEPTH && gd != 0.f)) {
-                acc[0] += w * pa.g0;
-                acc[1] += w * pa.g1;
-                acc[2] += w * pa.g2;
-                if (DEPTH) acc[9] += w * gd;
-                const float am1 = 1.0f - a;
-                if (am1 > 0.f && a != amax) {
-                    const float dal = T * grgb - (pa.gimg - Gafter) / am1;
-                    acc[8] += dal * (a * inv_sigma);
-                    const float da = dal * a;
-                    acc[3] += da * (A.z * dx + A.w * dy);
-                    acc[4] += da * (A.w * dx + B.x * dy);
-                    const float h = -0.5f * da;
-                    acc[5] += h * dx * dx;
-                    acc[6] += h * 2.0f * dx * dy;
-                    acc[7] += h * dy * dy;
-                }
+            float grgb = pg.x * C.x + pg.y * C.y + pg.z * C.z;
+            float gd = 0.f;
+            if (DEPTH) {
+                gd = sD[j];
+                grgb += gd * B.w;
             }
-            T = Tafter;
+            const float Gafter = G + grgb * w;
+            acc[0] += w * pg.x;
+            acc[1] += w * pg.y;
+            acc[2] += w * pg.z;
+            if (DEPTH) acc[9] += w * gd;
+            if (a != amax) {  // alpha-path gradient (kernels.py:342-364); 1 - a > 0 here
+                const float dal = T * grgb - __fdividef(pg.w - Gafter, 1.0f - a);
+                acc[8] += dal * (a * inv_sigma);
+                const float da = dal * a;
+                acc[3] += da * (A.z * dx + A.w * dy);
+                acc[4] += da * (A.w * dx + B.x * dy);
+                const float h = -0.5f * da;
+                acc[5] += h * dx * dx;
+                acc[6] += (h + h) * dx * dy;
+                acc[7] += h * dy * dy;
+            }
+            T = __fmul_rn(T, __fsub_rn(1.0f, a));
             G = Gafter;
         }
-        if (valid) {
+        if (k < ke) {
             float* row = g2d + (size_t)s * NC;
 #pragma unroll
             for (int q = 0; q < NC; ++q)
@@ -179,9 +182,10 @@ __global__ void __launch_bounds__(128) backward_splat_kernel(
 
 cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
                                   const ss_splats* sp, const ss_bins* bins, const float* image,
-                                  const float* grad_image, const float* depth,
-                                  const float* grad_depth, const int32_t* n_contrib,
-                                  const int32_t* k_eff, const void* ckpt, const float* ckpt_depth,
+                                  const float* grad_image, const float4* pixgrad,
+                                  const float* depth, const float* grad_depth,
+                                  const int32_t* n_contrib, const int32_t* k_eff, const void* ckpt,
+                                  const float* ckpt_depth, const uint32_t* ckpt_mask,
                                   const uint32_t* work, int64_t work_cap, int64_t n, float* g2d,
                                   uint8_t* contributed, const ss_status* st, uint32_t* counter,
                                   cudaStream_t s) {
@@ -193,7 +197,7 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
     if (e != cudaSuccess) return e;
     int tx = div_up(cam->width, kTile);
     const int threads = 128, warps = threads / 32;
-    size_t smem = (size_t)warps * kTilePx * (sizeof(PixA) + sizeof(PixB) + (depthf ? 4 : 0));
+    size_t smem = (size_t)warps * kTilePx * (16 + 8 + 8 + 4 + 4);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -205,9 +209,9 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
         if (per_sm < 1) per_sm = 1;
         kern<<<sms * per_sm, threads, smem, s>>>(
             cam->width, cam->height, tx, bins->d_tile_start, bins->d_ckpt_base, k_eff,
-            bins->d_pair_splat, reinterpret_cast<const SplatRec*>(sp->d_rec), o->alpha_min,
-            o->alpha_max, image, grad_image, depth, grad_depth, n_contrib,
-            reinterpret_cast<const float4*>(ckpt), ckpt_depth,
+            bins->d_pair_splat, reinterpret_cast<const SplatRec*>(sp->d_rec), o->alpha_max, image,
+            grad_image, pixgrad, depth, grad_depth, n_contrib,
+            reinterpret_cast<const float4*>(ckpt), ckpt_depth, ckpt_mask,
             reinterpret_cast<const uint2*>(work), &st->bucket_count, work_cap, counter, g2d,
             contributed);
         return cudaGetLastError();

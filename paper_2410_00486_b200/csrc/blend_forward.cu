@@ -2,11 +2,12 @@
 //
 // Restates rasterize_forward's tile loop (rasterizer/api.py:153-196) and
 // forward_tile (rasterizer/kernels.py:34-109) with checkpoint_tile
-// (kernels.py:112-152) folded in: one 256-thread CTA per 16x16 tile, one
-// thread per pixel.  The tile's depth-sorted list is walked in batches of
-// 256 splat records staged in shared memory (one coalesced gather per
-// batch, each thread loading one record); every thread walks the batch
-// from shared memory with broadcast reads.  Reference semantics kept:
+// (kernels.py:112-152) folded in: one 128-thread CTA per 16x16 tile, two
+// pixels per thread (rows r and r+8, two independent blend chains per
+// thread for ILP).  The tile's depth-sorted list is walked in batches of
+// 256 splat records staged in shared memory (each thread gathers two
+// records; every thread then reads the batch with broadcast LDS.128).
+// Reference semantics kept:
 //  - a splat is skipped when m > m_cut or alpha < alpha_min, alpha clamped
 //    at alpha_max (kernels.py:14-31);
 //  - the splat that drives T below t_min is blended, then the pixel stops
@@ -17,6 +18,9 @@
 //    stopped pixel has n_contrib <= that position and the backward never
 //    reads its later checkpoints;
 //  - image = acc + background * T (kernels.py:98-108).
+// B200 addition: per (pixel, bucket) a 32-bit mask of the bucket positions
+// that were blended into the pixel.  The backward replays exactly these
+// pairs (identical arithmetic, so identical decisions) and skips the rest.
 // Extension A15 (builder-defined): D = sum z a T in a 4th accumulator.
 // The CTA also emits k_eff (kernels.py:86-87,109) and appends its
 // ceil(k_eff/32) (tile, bucket) units to the splat-wise backward work list.
@@ -24,100 +28,152 @@
 
 namespace ss {
 
+struct PixState {
+    float T, c0, c1, c2, D;
+    int last;
+    uint32_t bm;
+    bool done, live;
+};
+
+template <bool DEPTH>
+__device__ __forceinline__ void blend_one(PixState& s, float px, float py, const float4& A,
+                                          const float4& B, const SplatRec* rec, int j, int q,
+                                          float t_min, float amin, float amax, bool& hit) {
+    if (s.done) return;
+    float dx, dy;
+    float a = splat_alpha(px, py, A, B, amin, amax, dx, dy);
+    if (a < 0.f) return;
+    const float4 C = rec[j].c;
+    float w = __fmul_rn(a, s.T);
+    s.c0 = __fmaf_rn(C.x, w, s.c0);
+    s.c1 = __fmaf_rn(C.y, w, s.c1);
+    s.c2 = __fmaf_rn(C.z, w, s.c2);
+    if (DEPTH) s.D = __fmaf_rn(B.w, w, s.D);
+    s.T = __fmul_rn(s.T, __fsub_rn(1.0f, a));
+    s.last = q + 1;
+    s.bm |= 1u << (q & 31);
+    hit = true;
+    if (s.T < t_min) s.done = true;
+}
+
 template <bool DEPTH, bool CONTRIB>
-__global__ void __launch_bounds__(256) blend_forward_kernel(
+__global__ void __launch_bounds__(128) blend_forward_kernel(
     int W, int H, int tiles_x, const uint32_t* __restrict__ tile_start,
     const uint32_t* __restrict__ tile_end, const uint32_t* __restrict__ ckpt_base,
     const uint32_t* __restrict__ pairs, const SplatRec* __restrict__ rec, float t_min, float amin,
     float amax, float bg0, float bg1, float bg2, float* __restrict__ image,
     float* __restrict__ final_t, int32_t* __restrict__ n_contrib, float* __restrict__ depth_img,
     int32_t* __restrict__ k_eff, uint8_t* __restrict__ contributed, float4* __restrict__ ckpt,
-    float* __restrict__ ckpt_depth, uint2* __restrict__ work, int64_t work_cap,
-    int64_t* bucket_count) {
+    float* __restrict__ ckpt_depth, uint32_t* __restrict__ ckpt_mask, uint2* __restrict__ work,
+    int64_t work_cap, int64_t* bucket_count) {
     __shared__ SplatRec s_rec[256];
     __shared__ uint32_t s_id[256];
     __shared__ int s_hit[CONTRIB ? 256 : 1];
-    __shared__ int s_kmax[8];
+    __shared__ int s_kmax[4];
+    __shared__ unsigned long long s_wbase;
     const int tile = blockIdx.x;
     const int t = threadIdx.x;
     const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
-    const int ix = x0 + (t & 15), iy = y0 + (t >> 4);
-    const bool inside = ix < W && iy < H;
-    const float px = (float)ix, py = (float)iy;
+    const int ix = x0 + (t & 15), iy0 = y0 + (t >> 4), iy1 = iy0 + 8;
+    const int p0 = t, p1 = t + 128;  // tile-local pixel ids (row-major 16x16)
+    const float px = (float)ix, py0 = (float)iy0, py1 = (float)iy1;
     const uint32_t start = tile_start[tile];
     const uint32_t len = tile_end[tile] - start;
     const uint32_t cbase = ckpt_base[tile];
 
-    float T = 1.0f, c0 = 0.f, c1 = 0.f, c2 = 0.f, D = 0.f;
-    bool done = !inside;
-    int last = 0;
+    PixState s0 = {1.f, 0.f, 0.f, 0.f, 0.f, 0, 0u, !(ix < W && iy0 < H), false};
+    PixState s1 = {1.f, 0.f, 0.f, 0.f, 0.f, 0, 0u, !(ix < W && iy1 < H), false};
+    int open_bucket = -1;
     for (uint32_t b0 = 0; b0 < len; b0 += 256) {
-        if (__syncthreads_count(!done) == 0) break;
-        if (b0 + t < len) {
-            uint32_t s = pairs[start + b0 + t];
-            s_id[t] = s;
-            s_rec[t] = rec[s];
-            if (CONTRIB) s_hit[t] = 0;
+        if (__syncthreads_count(!(s0.done && s1.done)) == 0) break;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const uint32_t k = b0 + t + 128 * r;
+            if (k < len) {
+                uint32_t s = pairs[start + k];
+                s_id[t + 128 * r] = s;
+                s_rec[t + 128 * r] = rec[s];
+                if (CONTRIB) s_hit[t + 128 * r] = 0;
+            }
         }
         __syncthreads();
         const int nb = (int)min(256u, len - b0);
         for (int j0 = 0; j0 < nb; j0 += 32) {
-            if (__all_sync(0xffffffffu, done)) break;  // whole warp stopped
-            const uint32_t q0 = b0 + j0;                 // multiple of 32
-            if (!done) {
-                size_t slot = (size_t)(cbase + (q0 >> 5)) * kTilePx + t;
-                ckpt[slot] = make_float4(T, c0, c1, c2);
-                if (DEPTH) ckpt_depth[slot] = D;
+            const int bucket = (int)((b0 + j0) >> 5);
+            // close the previous bucket's blend masks, open this bucket
+            if (open_bucket >= 0) {
+                const size_t prev = (size_t)(cbase + open_bucket) * kTilePx;
+                if (s0.live) ckpt_mask[prev + p0] = s0.bm;
+                if (s1.live) ckpt_mask[prev + p1] = s1.bm;
             }
+            open_bucket = bucket;
+            s0.live = !s0.done;
+            s1.live = !s1.done;
+            s0.bm = s1.bm = 0u;
+            const size_t slot = (size_t)(cbase + bucket) * kTilePx;
+            if (s0.live) {
+                ckpt[slot + p0] = make_float4(s0.T, s0.c0, s0.c1, s0.c2);
+                if (DEPTH) ckpt_depth[slot + p0] = s0.D;
+            }
+            if (s1.live) {
+                ckpt[slot + p1] = make_float4(s1.T, s1.c0, s1.c1, s1.c2);
+                if (DEPTH) ckpt_depth[slot + p1] = s1.D;
+            }
+            if (__all_sync(0xffffffffu, s0.done && s1.done)) continue;  // whole warp stopped
             const int jn = min(nb, j0 + 32);
             for (int j = j0; j < jn; ++j) {
-                if (done) continue;
                 const float4 A = s_rec[j].a, B = s_rec[j].b;
-                float dx, dy;
-                float a = splat_alpha(px, py, A, B, amin, amax, dx, dy);
-                if (a < 0.f) continue;
-                const float4 C = s_rec[j].c;
-                float w = __fmul_rn(a, T);
-                c0 = __fmaf_rn(C.x, w, c0);
-                c1 = __fmaf_rn(C.y, w, c1);
-                c2 = __fmaf_rn(C.z, w, c2);
-                if (DEPTH) D = __fmaf_rn(B.w, w, D);
-                T = __fmul_rn(T, __fsub_rn(1.0f, a));
-                last = (int)(b0 + j) + 1;
-                if (CONTRIB) s_hit[j] = 1;
-                if (T < t_min) done = true;
+                const int q = (int)b0 + j;
+                bool hit = false;
+                blend_one<DEPTH>(s0, px, py0, A, B, s_rec, j, q, t_min, amin, amax, hit);
+                blend_one<DEPTH>(s1, px, py1, A, B, s_rec, j, q, t_min, amin, amax, hit);
+                if (CONTRIB && hit) s_hit[j] = 1;
             }
         }
         if (CONTRIB) {
             __syncthreads();
-            if (b0 + t < len && s_hit[t]) contributed[s_id[t]] = 1;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const uint32_t k = b0 + t + 128 * r;
+                if (k < len && s_hit[t + 128 * r]) contributed[s_id[t + 128 * r]] = 1;
+            }
         }
     }
-    if (inside) {
-        const size_t o = (size_t)iy * W + ix;
-        final_t[o] = T;
-        image[3 * o] = c0 + bg0 * T;
-        image[3 * o + 1] = c1 + bg1 * T;
-        image[3 * o + 2] = c2 + bg2 * T;
-        n_contrib[o] = last;
-        if (DEPTH) depth_img[o] = D;
+    if (open_bucket >= 0) {
+        const size_t prev = (size_t)(cbase + open_bucket) * kTilePx;
+        if (s0.live) ckpt_mask[prev + p0] = s0.bm;
+        if (s1.live) ckpt_mask[prev + p1] = s1.bm;
     }
-    int km = warp_max(last);
+    if (ix < W) {
+        if (iy0 < H) {
+            const size_t o = (size_t)iy0 * W + ix;
+            final_t[o] = s0.T;
+            image[3 * o] = s0.c0 + bg0 * s0.T;
+            image[3 * o + 1] = s0.c1 + bg1 * s0.T;
+            image[3 * o + 2] = s0.c2 + bg2 * s0.T;
+            n_contrib[o] = s0.last;
+            if (DEPTH) depth_img[o] = s0.D;
+        }
+        if (iy1 < H) {
+            const size_t o = (size_t)iy1 * W + ix;
+            final_t[o] = s1.T;
+            image[3 * o] = s1.c0 + bg0 * s1.T;
+            image[3 * o + 1] = s1.c1 + bg1 * s1.T;
+            image[3 * o + 2] = s1.c2 + bg2 * s1.T;
+            n_contrib[o] = s1.last;
+            if (DEPTH) depth_img[o] = s1.D;
+        }
+    }
+    int km = warp_max(max(s0.last, s1.last));
     if ((t & 31) == 0) s_kmax[t >> 5] = km;
     __syncthreads();
-    if (t < 32) {
-        int v = t < 8 ? s_kmax[t] : 0;
-        v = warp_max(v);
-        if (t == 0) s_kmax[0] = v;
-    }
-    __syncthreads();
-    const int kmax = s_kmax[0];
+    const int kmax = max(max(s_kmax[0], s_kmax[1]), max(s_kmax[2], s_kmax[3]));
     if (t == 0) k_eff[tile] = kmax;
     const int nbk = (kmax + kBucket - 1) / kBucket;
     if (nbk > 0 && work) {
-        __shared__ unsigned long long s_wbase;
-        if (t == 0) s_wbase = atomicAdd(reinterpret_cast<unsigned long long*>(bucket_count),
-                                        (unsigned long long)nbk);
+        if (t == 0)
+            s_wbase = atomicAdd(reinterpret_cast<unsigned long long*>(bucket_count),
+                                (unsigned long long)nbk);
         __syncthreads();
         for (int b = t; b < nbk; b += blockDim.x) {
             long long idx = (long long)s_wbase + b;
@@ -130,19 +186,19 @@ cudaError_t launch_blend_forward(const ss_camera* cam, const ss_raster_opts* o,
                                  const ss_splats* sp, const ss_bins* bins, float* image,
                                  float* final_t, int32_t* n_contrib, float* depth,
                                  int32_t* k_eff, uint8_t* contributed, void* ckpt,
-                                 float* ckpt_depth, uint32_t* work, int64_t work_cap,
-                                 ss_status* st, cudaStream_t s) {
+                                 float* ckpt_depth, uint32_t* ckpt_mask, uint32_t* work,
+                                 int64_t work_cap, ss_status* st, cudaStream_t s) {
     int tx = div_up(cam->width, kTile), ty = div_up(cam->height, kTile);
     int n_tiles = tx * ty;
     const bool depthf = o->with_depth != 0;
     const bool contribf = contributed != nullptr;
     auto args = [&](auto kern) {
-        kern<<<n_tiles, 256, 0, s>>>(
+        kern<<<n_tiles, 128, 0, s>>>(
             cam->width, cam->height, tx, bins->d_tile_start, bins->d_tile_end, bins->d_ckpt_base,
             bins->d_pair_splat, reinterpret_cast<const SplatRec*>(sp->d_rec), o->t_min,
             o->alpha_min, o->alpha_max, o->background[0], o->background[1], o->background[2],
             image, final_t, n_contrib, depth, k_eff, contributed, reinterpret_cast<float4*>(ckpt),
-            ckpt_depth, reinterpret_cast<uint2*>(work), work_cap, &st->bucket_count);
+            ckpt_depth, ckpt_mask, reinterpret_cast<uint2*>(work), work_cap, &st->bucket_count);
     };
     if (depthf && contribf)
         args(blend_forward_kernel<true, true>);

@@ -405,19 +405,20 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t n, float* pos, float4
 }
 
 // ----------------------------------------------------------- chain+adam
-template <int NC>
+template <int NC, bool REST>
 __global__ void __launch_bounds__(256) chain_adam_kernel(
-    int64_t n, float* pos, float4* rot, float* ls, float* opl, float* shdc, float* shrest,
-    CamC cam, int deg, float dilation, const float* __restrict__ g2d,
-    const uint8_t* __restrict__ flags, const uint8_t* __restrict__ contributed, float lo_over_n,
-    ss_param_grads M, ss_param_grads V, AdamHP hp, int upd_rest, float* grad2d_accum,
-    float* grad3d_accum, int32_t* obs_count, ss_status* st) {
+    int64_t n, float* __restrict__ pos, float4* __restrict__ rot, float* __restrict__ ls,
+    float* __restrict__ opl, float* __restrict__ shdc, float* __restrict__ shrest, CamC cam,
+    int deg, float dilation, const float* __restrict__ g2d, const uint8_t* __restrict__ flags,
+    const uint8_t* __restrict__ contributed, float lo_over_n, ss_param_grads M, ss_param_grads V,
+    AdamHP hp, float* __restrict__ grad2d_accum, float* __restrict__ grad3d_accum,
+    int32_t* __restrict__ obs_count, ss_status* st) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n || st->pair_overflow) return;
     GaussGrad o = {};
-    uint8_t fl = flags[i];
-    float rest_g[45];
-    bool have_rest = false;
+    const uint8_t fl = flags[i];
+    const float opi = opl[i];
+    float rest_g[REST ? 45 : 1];
     if (fl & 1) {
         float p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
         float l[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
@@ -425,12 +426,14 @@ __global__ void __launch_bounds__(256) chain_adam_kernel(
         float g[NC];
 #pragma unroll
         for (int k = 0; k < NC; ++k) g[k] = g2d[NC * i + k];
-        chain_one<NC>(p, rot[i], l, opl[i], dc, shrest + 45 * i, cam, deg, dilation, g, fl, o,
-                      upd_rest ? rest_g : nullptr);
-        have_rest = upd_rest != 0;
+        chain_one<NC>(p, rot[i], l, opi, dc, shrest + 45 * i, cam, deg, dilation, g, fl, o,
+                      REST ? rest_g : nullptr);
+    } else if (REST) {
+#pragma unroll
+        for (int k = 0; k < (REST ? 45 : 1); ++k) rest_g[k] = 0.f;
     }
     if (lo_over_n != 0.f) {
-        float sg = sigm(opl[i]);
+        float sg = sigm(opi);
         o.op += lo_over_n * sg * (1.f - sg);
     }
     if (!grad_finite(o)) report_first(&st->first_nonfinite_grad, i);
@@ -441,8 +444,8 @@ __global__ void __launch_bounds__(256) chain_adam_kernel(
         grad3d_accum[3 * i + 2] += o.pos[2];
         obs_count[i] += 1;
     }
-    adam_gaussian(i, o, have_rest ? rest_g : nullptr, pos, rot, ls, opl, shdc, shrest, M, V, hp,
-                  upd_rest != 0, st);
+    adam_gaussian(i, o, REST ? rest_g : nullptr, pos, rot, ls, opl, shdc, shrest, M, V, hp, REST,
+                  st);
 }
 
 // ---------------------------------------------------------------- stats
@@ -541,13 +544,14 @@ cudaError_t launch_chain_adam(const ss_map* mp, const ss_camera* cam, const ss_r
         kern<<<div_up(mp->n, 256), 256, 0, s>>>(
             mp->n, mp->d_positions, reinterpret_cast<float4*>(mp->d_rotations), mp->d_log_scales,
             mp->d_opacity_logits, mp->d_sh_dc, mp->d_sh_rest, cc, o->sh_degree, o->dilation, g2d,
-            flags, contributed, lo_over_n, *M, *V, make_hp(h), h->update_sh_rest,
-            mp->d_grad2d_accum, mp->d_grad3d_accum, mp->d_obs_count, st);
+            flags, contributed, lo_over_n, *M, *V, make_hp(h), mp->d_grad2d_accum,
+            mp->d_grad3d_accum, mp->d_obs_count, st);
     };
+    const bool rest = h->update_sh_rest != 0;
     if (o->with_depth)
-        go(chain_adam_kernel<10>);
+        rest ? go(chain_adam_kernel<10, true>) : go(chain_adam_kernel<10, false>);
     else
-        go(chain_adam_kernel<9>);
+        rest ? go(chain_adam_kernel<9, true>) : go(chain_adam_kernel<9, false>);
     return cudaGetLastError();
 }
 

@@ -36,17 +36,43 @@ struct __align__(16) SplatRec {
 // _alpha (kernels.py:14-31): m = c0 dx^2 + 2 c1 dx dy + c2 dy^2; skip when
 // m > m_cut; a = sigma exp(-m/2); skip when a < alpha_min; clamp alpha_max.
 // Returns a < 0 for "skip".  Pixel coordinates are integers (api.py:108-115).
-__device__ __forceinline__ float splat_alpha(float px, float py, const float4& A, const float4& B,
-                                             float amin, float amax, float& dx, float& dy) {
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Quadratic form m = c0 dx^2 + 2 c1 dx dy + c2 dy^2 with pinned rounding.
+__device__ __forceinline__ float splat_power(float px, float py, const float4& A, const float4& B,
+                                             float& dx, float& dy) {
     dx = __fsub_rn(px, A.x);
     dy = __fsub_rn(py, A.y);
-    float m = __fmaf_rn(__fmul_rn(A.z, dx), dx,
-                        __fmaf_rn(__fmul_rn(__fmul_rn(2.0f, A.w), dx), dy,
-                                  __fmul_rn(__fmul_rn(B.x, dy), dy)));
+    return __fmaf_rn(__fmul_rn(A.z, dx), dx,
+                     __fmaf_rn(__fmul_rn(__fmul_rn(2.0f, A.w), dx), dy,
+                               __fmul_rn(__fmul_rn(B.x, dy), dy)));
+}
+
+// sigma * exp(-m/2) with pinned rounding (MUFU.EX2, flush-to-zero: values
+// that small are far below alpha_min anyway).
+__device__ __forceinline__ float splat_falloff(float m, const float4& B) {
+    return __fmul_rn(B.y, ex2_approx(__fmul_rn(m, -0.5f * kLog2e)));
+}
+
+__device__ __forceinline__ float splat_alpha(float px, float py, const float4& A, const float4& B,
+                                             float amin, float amax, float& dx, float& dy) {
+    float m = splat_power(px, py, A, B, dx, dy);
     if (m > B.z) return -1.0f;
-    float a = __fmul_rn(B.y, exp2f(__fmul_rn(m, -0.5f * kLog2e)));
+    float a = splat_falloff(m, B);
     if (a < amin) return -1.0f;
     return fminf(a, amax);
+}
+
+// Alpha of a pair the forward already recorded as blended (same
+// arithmetic, no skip tests: they passed in the forward).
+__device__ __forceinline__ float splat_alpha_blended(float px, float py, const float4& A,
+                                                     const float4& B, float amax, float& dx,
+                                                     float& dy) {
+    return fminf(splat_falloff(splat_power(px, py, A, B, dx, dy), B), amax);
 }
 
 // ----------------------------------------------------------- error words

@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(int H, int W, const float
                                                        const float* __restrict__ gmu,
                                                        const float* __restrict__ gxx,
                                                        const float* __restrict__ gxy, float lam,
-                                                       float* __restrict__ grad) {
+                                                       float* __restrict__ grad,
+                                                       float4* __restrict__ pixgrad) {
     __shared__ float sg[3][LHH][LHW + 1];
     __shared__ float sh[3][LHH][LTW];
     const int t = threadIdx.x;
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(int H, int W, const float
     const int x0 = blockIdx.x * LTW, y0 = blockIdx.y * LTH;
     const int ox = x0 + tx, oy = y0 + ty;
     const float inv_n = 1.0f / (float)((double)H * W * 3);
+    float gsave[3] = {0.f, 0.f, 0.f}, gdot = 0.f;
     for (int c = 0; c < 3; ++c) {
         for (int k = t; k < LHH * LHW; k += 256) {
             int r = k / LHW, q = k % LHW;
@@ -193,10 +195,15 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(int H, int W, const float
             float d = xv - yv;
             float sg0 = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);  // np.sign: sign(0) = 0
             float gx = adj[0] + adj[1] * 2.f * xv + adj[2] * yv;
-            grad[o] = (1.0f - lam) * sg0 * inv_n - lam * gx;
+            float gv = (1.0f - lam) * sg0 * inv_n - lam * gx;
+            grad[o] = gv;
+            gsave[c] = gv;
+            gdot += gv * xv;
         }
         __syncthreads();
     }
+    if (pixgrad && ox < W && oy < H)
+        pixgrad[(size_t)oy * W + ox] = make_float4(gsave[0], gsave[1], gsave[2], gdot);
 }
 
 // L1-only variant (lambda_ssim == 0): losses.py:147-153
@@ -267,7 +274,7 @@ size_t loss_workspace_bytes(int H, int W) {
 }
 
 cudaError_t launch_loss(int H, int W, const float* x, const float* y, float lam, float* grad,
-                        double* sums, void* ws, size_t ws_bytes, cudaStream_t s) {
+                        float* pixgrad, double* sums, void* ws, size_t ws_bytes, cudaStream_t s) {
     if (ws_bytes < loss_workspace_bytes(H, W)) return cudaErrorInvalidValue;
     size_t plane = (size_t)H * W * 3;
     float* gmu = reinterpret_cast<float*>(ws);
@@ -285,7 +292,8 @@ cudaError_t launch_loss(int H, int W, const float* x, const float* y, float lam,
     SsimWindow win = make_window();
     dim3 grid(div_up(W, LTW), div_up(H, LTH));
     ssim_fwd_kernel<<<grid, 256, 0, s>>>(H, W, x, y, win, gmu, gxx, gxy, partials);
-    ssim_bwd_kernel<<<grid, 256, 0, s>>>(H, W, x, y, win, gmu, gxx, gxy, lam, grad);
+    ssim_bwd_kernel<<<grid, 256, 0, s>>>(H, W, x, y, win, gmu, gxx, gxy, lam, grad,
+                                         reinterpret_cast<float4*>(pixgrad));
     reduce_pairs_kernel<<<1, 256, 0, s>>>(grid.x * grid.y, partials, sums);
     return cudaGetLastError();
 }

@@ -127,6 +127,7 @@ class MappingEngine:
         self.depth = torch.empty((self.H, self.W), **f32) if self.opts.with_depth else None
         self.grad_depth = torch.empty((self.H, self.W), **f32) if self.opts.with_depth else None
         self.grad_image = torch.empty((self.H, self.W, 3), **f32)
+        self.pixgrad = torch.empty((self.H, self.W, 4), **f32)
         self.k_eff = torch.empty(self.n_tiles, dtype=torch.int32, device=dev)
         self.sums = torch.zeros(_lib.SS_REDUCE_DOUBLES, dtype=torch.float64, device=dev)
         self.osum = torch.zeros(_lib.SS_REDUCE_DOUBLES, dtype=torch.float64, device=dev)
@@ -144,6 +145,7 @@ class MappingEngine:
         self.ckpt = torch.empty((slots * 256, 4), dtype=torch.float32, device=self.dev)
         self.ckpt_depth = (torch.empty(slots * 256, dtype=torch.float32, device=self.dev)
                            if self.opts.with_depth else None)
+        self.ckpt_mask = torch.empty(slots * 256, dtype=torch.int32, device=self.dev)
         self.work_cap = slots
         self.work = torch.empty((slots, 2), dtype=torch.int32, device=self.dev)
 
@@ -171,11 +173,14 @@ class MappingEngine:
         check(L.ss_blend_forward(ctypes.byref(cm), ctypes.byref(op), ctypes.byref(spss),
                                  ctypes.byref(bss), P(self.image), P(self.final_t),
                                  P(self.n_contrib), P(self.depth), P(self.k_eff), None,
-                                 P(self.ckpt), P(self.ckpt_depth), P(self.work), self.work_cap,
-                                 P(self.status), s), "ss_blend_forward")
+                                 P(self.ckpt), P(self.ckpt_depth), P(self.ckpt_mask),
+                                 P(self.work), self.work_cap, P(self.status), s),
+              "ss_blend_forward")
         self._mark("blend_forward")
+        use_pg = self.cfg.lambda_ssim != 0.0 and not self.opts.with_depth
         check(L.ss_loss_l1_ssim(self.H, self.W, P(self.image), P(target),
-                                float(self.cfg.lambda_ssim), P(self.grad_image), P(self.sums),
+                                float(self.cfg.lambda_ssim), P(self.grad_image),
+                                P(self.pixgrad) if use_pg else None, P(self.sums),
                                 P(self.loss_ws), self.loss_ws.numel(), s), "ss_loss_l1_ssim")
         if self.opts.with_depth:
             if target_depth is not None and self.cfg.depth_weight != 0.0:
@@ -188,10 +193,11 @@ class MappingEngine:
         self.contributed.zero_()
         check(L.ss_backward_splat(ctypes.byref(cm), ctypes.byref(op), ctypes.byref(spss),
                                   ctypes.byref(bss), P(self.image), P(self.grad_image),
-                                  P(self.depth), P(self.grad_depth), P(self.n_contrib),
-                                  P(self.k_eff), P(self.ckpt), P(self.ckpt_depth), P(self.work),
-                                  self.work_cap, n, P(self.g2d), P(self.contributed),
-                                  P(self.status), s), "ss_backward_splat")
+                                  P(self.pixgrad) if use_pg else None, P(self.depth),
+                                  P(self.grad_depth), P(self.n_contrib), P(self.k_eff),
+                                  P(self.ckpt), P(self.ckpt_depth), P(self.ckpt_mask),
+                                  P(self.work), self.work_cap, n, P(self.g2d),
+                                  P(self.contributed), P(self.status), s), "ss_backward_splat")
         self._mark("backward")
         self.launches += (KERNELS_PER_CALL["step_fb"] + (3 if self.opts.with_depth and
                                                         self.cfg.depth_weight else 0))

@@ -50,7 +50,7 @@ def photometric(rendered: torch.Tensor, target: torch.Tensor, lambda_ssim: float
     if ws is None:
         ws = torch.empty(int(lib().ss_loss_workspace_bytes(H, W)), dtype=torch.uint8,
                          device=rendered.device)
-    check(lib().ss_loss_l1_ssim(H, W, P(rendered), P(target), float(lambda_ssim), P(grad),
+    check(lib().ss_loss_l1_ssim(H, W, P(rendered), P(target), float(lambda_ssim), P(grad), None,
                                 P(sums), P(ws), ws.numel(), stream_handle()), "ss_loss_l1_ssim")
     return ws
 

@@ -200,6 +200,7 @@ class RenderOutput:
     pair_count: int
     ckpt: torch.Tensor | None
     ckpt_depth: torch.Tensor | None
+    ckpt_mask: torch.Tensor
     work: torch.Tensor
     work_capacity: int
     status: torch.Tensor
@@ -305,6 +306,7 @@ def rasterize_forward(gmap: GaussianMap, camera, opts: RasterOpts | None = None)
     f32 = dict(dtype=torch.float32, device=dev)
     ckpt = torch.empty((max(n_slots, 1) * 256, 4), **f32)
     ckpt_depth = torch.empty(max(n_slots, 1) * 256, **f32) if opts.with_depth else None
+    ckpt_mask = torch.empty(max(n_slots, 1) * 256, dtype=torch.int32, device=dev)
     image = torch.empty((H, W, 3), **f32)
     final_t = torch.empty((H, W), **f32)
     n_contrib = torch.empty((H, W), dtype=torch.int32, device=dev)
@@ -315,13 +317,13 @@ def rasterize_forward(gmap: GaussianMap, camera, opts: RasterOpts | None = None)
     work = torch.empty((work_cap, 2), dtype=torch.int32, device=dev)
     check(L.ss_blend_forward(ctypes.byref(cm), ctypes.byref(op), ctypes.byref(sp.ss()),
                              ctypes.byref(bins.ss()), P(image), P(final_t), P(n_contrib), P(depth),
-                             P(k_eff), P(contributed), P(ckpt), P(ckpt_depth), P(work), work_cap,
-                             P(st), s), "ss_blend_forward")
+                             P(k_eff), P(contributed), P(ckpt), P(ckpt_depth), P(ckpt_mask),
+                             P(work), work_cap, P(st), s), "ss_blend_forward")
     return RenderOutput(image=image, final_t=final_t, n_contrib=n_contrib, k_eff_tiles=k_eff,
                         contributed=contributed.bool(), opts=opts, camera=cam, n_primitives=n,
                         gmap=gmap, splats=sp, bins=bins, pair_count=pcount,
                         ckpt=ckpt if opts.with_checkpoints else None, ckpt_depth=ckpt_depth,
-                        work=work, work_capacity=work_cap, status=st, depth=depth)
+                        ckpt_mask=ckpt_mask, work=work, work_capacity=work_cap, status=st, depth=depth)
 
 
 @dataclass
@@ -392,9 +394,10 @@ def screen_space_grads(render: RenderOutput, grad_image, grad_depth=None):
     cm, op = render.camera.to_ss(), render.opts.to_ss()
     check(lib().ss_backward_splat(
         ctypes.byref(cm), ctypes.byref(op), ctypes.byref(render.splats.ss()),
-        ctypes.byref(render.bins.ss()), P(render.image), P(g), P(render.depth), P(gd),
+        ctypes.byref(render.bins.ss()), P(render.image), P(g), None, P(render.depth), P(gd),
         P(render.n_contrib), P(render.k_eff_tiles), P(render.ckpt), P(render.ckpt_depth),
-        P(render.work), render.work_capacity, n, P(g2d), None, P(render.status),
+        P(render.ckpt_mask), P(render.work), render.work_capacity, n, P(g2d), None,
+        P(render.status),
         stream_handle()), "ss_backward_splat")
     return g2d[:n]
 

@@ -209,10 +209,18 @@ def test_engine_step_matches_api_sequence(case):
     for _ in range(2):
         eng.step(cam, tgt)
     eng.synchronize()
-    for f in ("positions", "rotations", "log_scales", "opacity_logits", "sh_dc",
-              "grad2d_accum"):
+    # Adam moves each element by at most lr per step; near-zero gradients may
+    # flip sign between two float32 reduction orders, so the
+    # bound is 2 steps * 2 lr, and such flips must be rare.
+    lr = dict(positions=1.6e-4, rotations=1e-3, log_scales=5e-3, opacity_logits=5e-2,
+              sh_dc=2.5e-3)
+    for f, r in lr.items():
         a, b = getattr(g2, f).cpu().numpy(), getattr(g1, f).cpu().numpy()
-        assert np.abs(a - b).max() <= 1e-3 * max(np.abs(b).max(), 1e-6), f
+        d = np.abs(a - b)
+        assert d.max() <= 4 * r + 1e-5, f
+        assert (d > 1e-3 * r + 1e-6).mean() < 0.01, f
+    a, b = g2.grad2d_accum.cpu().numpy(), g1.grad2d_accum.cpu().numpy()
+    assert normwise(a, b) <= 1e-3
     np.testing.assert_array_equal(g2.obs_count.cpu().numpy(), g1.obs_count.cpu().numpy())
     losses = eng.losses()
     assert len(losses) == 2 and np.isfinite(losses[0][1])
