@@ -230,6 +230,8 @@ def main():
     del tmap
     eng = ss.MappingEngine(gmap, W, H, opts)
     pcount = eng.fit_capacity(cams[rank % views])
+    if world == 1:
+        eng.enable_graph()  # the whole iteration is replayed as one CUDA graph
     my_cam, my_tgt = cams[rank % views], targets[rank % views]
 
     def allreduce(flat):
@@ -312,27 +314,51 @@ def main():
     ach = per_kernel[dom] / (stage_ms[dom] / 1000.0) / 1e9
     it_bytes = sum(algo.values())
 
-    # ---- end to end through the public API with host buffers (N=1)
+    # ---- end to end through the public API with host buffers (N=1): every
+    # step uploads its keyframe target from pinned host memory (on a copy
+    # stream, double-buffered so the upload of step k+1 overlaps step k) and
+    # the step's loss/status snapshot comes back to the host
     e2e = None
     if world == 1 and not args.no_e2e:
         host_tgt = my_tgt.cpu().pin_memory()
-        dev_tgt = torch.empty_like(my_tgt)
+        bufs = [torch.empty_like(my_tgt), torch.empty_like(my_tgt)]
+        copy_stream = torch.cuda.Stream()
+        uploaded = [torch.cuda.Event(), torch.cuda.Event()]
+        consumed = [torch.cuda.Event(), torch.cuda.Event()]
+        main = torch.cuda.current_stream()
+
+        def upload(k):
+            b = k % 2
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(consumed[b])
+                bufs[b].copy_(host_tgt, non_blocking=True)
+                uploaded[b].record(copy_stream)
+
+        def e2e_step(k):
+            b = k % 2
+            main.wait_event(uploaded[b])
+            eng.step(my_cam, bufs[b])
+            consumed[b].record(main)
+            upload(k + 2)
+
+        for b in range(2):
+            consumed[b].record(main)
+        upload(0)
+        upload(1)
+        for k in range(2):  # capture the graphs of both input buffers
+            e2e_step(k)
+        eng.synchronize()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for k in range(args.steps):
-            dev_tgt.copy_(host_tgt, non_blocking=True)   # H2D of the step's keyframe target
-            eng.step(my_cam, dev_tgt)                       # D2H: per-step status+loss snapshot
-        e1.record()
-        eng.synchronize()                                   # last losses on the host
+        for k in range(2, 2 + args.steps):
+            e2e_step(k)
+        eng.synchronize()  # every step's loss is on the host
         wall = time.perf_counter() - t0
-        ev_ms = e0.elapsed_time(e1)
-        e2e = {"value": args.steps / max(wall, ev_ms / 1000.0), "unit": "it/s",
+        e2e = {"value": args.steps / wall, "unit": "it/s",
                "h2d_bytes_per_step": int(host_tgt.numel() * 4),
                "d2h_bytes_per_step": int(eng._host.shape[1] * 8),
-               "timing": "wall clock incl. host sync of the last step's loss"}
+               "timing": "wall clock, host pinned target upload per step (copy stream, "
+                         "double-buffered) + per-step loss/status read back"}
 
     # ---- CPU baseline (rank 0, N = 1): bounded oracle sample
     cpu = None

@@ -118,9 +118,13 @@ int ss_status_reset(ss_status *d_status, void *stream);
 
 /* ------------------------------------------------------------ preprocess */
 /* Replaces project_map (projection.py:73-163) + the finite check of
- * rasterize_forward (api.py:127-129, core.py:231-241). */
-int ss_preprocess(const ss_map *map, const ss_camera *cam, const ss_raster_opts *opts,
-                  const ss_splats *out, ss_status *d_status, void *stream);
+ * rasterize_forward (api.py:127-129, core.py:231-241).  d_cam (optional):
+ * a DEVICE copy of the camera read by the kernel instead of *cam, so a
+ * captured CUDA graph can be replayed for a new view after a host->device
+ * copy of the camera. */
+int ss_preprocess(const ss_map *map, const ss_camera *cam, const ss_camera *d_cam,
+                  const ss_raster_opts *opts, const ss_splats *out, ss_status *d_status,
+                  void *stream);
 
 /* ----------------------------------------------------------------- binning */
 /* Replaces build_tile_index (tiles.py:29-65): duplicate-with-keys, stable
@@ -245,10 +249,12 @@ int ss_adam_step(const ss_map *map, const ss_param_grads *grads, const ss_param_
 /* Fused K8+K9 (+stats, +opacity reg): chain -> Adam for one view without
  * materialising the gradients (single-GPU mapping iteration).  Does nothing
  * while d_status->pair_overflow is set. */
-int ss_chain_adam(const ss_map *map, const ss_camera *cam, const ss_raster_opts *opts,
-                  const float *d_g2d, const uint8_t *d_flags, const uint8_t *d_contributed,
-                  float lambda_o_over_n, const ss_param_grads *m, const ss_param_grads *v,
-                  const ss_adam_hparams *hp, ss_status *d_status, void *stream);
+int ss_chain_adam(const ss_map *map, const ss_camera *cam, const ss_camera *d_cam,
+                  const ss_raster_opts *opts, const float *d_g2d, const uint8_t *d_flags,
+                  const uint8_t *d_contributed, float lambda_o_over_n, const ss_param_grads *m,
+                  const ss_param_grads *v, const ss_adam_hparams *hp,
+                  const ss_adam_hparams *d_hp /* optional device copy, as d_cam */,
+                  ss_status *d_status, void *stream);
 
 /* accumulate_grad_stats (densify.py:86-100). */
 int ss_accumulate_grad_stats(const ss_map *map, const ss_param_grads *grads,

@@ -88,7 +88,7 @@ _SIGS = {
     "ss_status_reset": (I32, [VP, VP]),
     "ss_status_begin_step": (I32, [VP, VP]),
     "ss_apply_stat_planes": (I32, [P(SSMap), P(SSParamGrads), VP]),
-    "ss_preprocess": (I32, [P(SSMap), P(SSCamera), P(SSRasterOpts), P(SSSplats), VP, VP]),
+    "ss_preprocess": (I32, [P(SSMap), P(SSCamera), VP, P(SSRasterOpts), P(SSSplats), VP, VP]),
     "ss_bin_workspace_bytes": (SZ, [I64, I64, I32]),
     "ss_bin_sort": (I32, [I64, P(SSSplats), P(SSCamera), P(SSBins), VP, SZ, VP, VP]),
     "ss_blend_forward": (I32, [P(SSCamera), P(SSRasterOpts), P(SSSplats), P(SSBins), VP, VP, VP,
@@ -103,8 +103,8 @@ _SIGS = {
                                 P(SSParamGrads), VP, VP]),
     "ss_adam_step": (I32, [P(SSMap), P(SSParamGrads), P(SSParamGrads), P(SSParamGrads),
                            P(SSAdamHP), VP, VP]),
-    "ss_chain_adam": (I32, [P(SSMap), P(SSCamera), P(SSRasterOpts), VP, VP, VP, F32,
-                            P(SSParamGrads), P(SSParamGrads), P(SSAdamHP), VP, VP]),
+    "ss_chain_adam": (I32, [P(SSMap), P(SSCamera), VP, P(SSRasterOpts), VP, VP, VP, F32,
+                            P(SSParamGrads), P(SSParamGrads), P(SSAdamHP), VP, VP, VP]),
     "ss_accumulate_grad_stats": (I32, [P(SSMap), P(SSParamGrads), VP, VP]),
     "ss_densify_workspace_bytes": (SZ, [I64]),
     "ss_densify_count": (I32, [P(SSMap), F32, F32, F64, VP, SZ, VP, VP, VP]),

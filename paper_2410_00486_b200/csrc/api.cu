@@ -7,8 +7,8 @@
 #include "common.cuh"
 
 namespace ss {
-cudaError_t launch_preprocess(const ss_map*, const ss_camera*, const ss_raster_opts*,
-                              const ss_splats*, ss_status*, cudaStream_t);
+cudaError_t launch_preprocess(const ss_map*, const ss_camera*, const ss_camera*,
+                              const ss_raster_opts*, const ss_splats*, ss_status*, cudaStream_t);
 size_t bin_workspace_bytes(int64_t, int64_t, int);
 cudaError_t launch_bin_sort(int64_t, const ss_splats*, const ss_camera*, const ss_bins*, void*,
                             size_t, ss_status*, cudaStream_t);
@@ -34,10 +34,11 @@ cudaError_t launch_chain(const ss_map*, const ss_camera*, const ss_raster_opts*,
                          ss_status*, cudaStream_t);
 cudaError_t launch_adam(const ss_map*, const ss_param_grads*, const ss_param_grads*,
                         const ss_param_grads*, const ss_adam_hparams*, ss_status*, cudaStream_t);
-cudaError_t launch_chain_adam(const ss_map*, const ss_camera*, const ss_raster_opts*,
-                              const float*, const uint8_t*, const uint8_t*, float,
-                              const ss_param_grads*, const ss_param_grads*,
-                              const ss_adam_hparams*, ss_status*, cudaStream_t);
+cudaError_t launch_chain_adam(const ss_map*, const ss_camera*, const ss_camera*,
+                              const ss_raster_opts*, const float*, const uint8_t*, const uint8_t*,
+                              float, const ss_param_grads*, const ss_param_grads*,
+                              const ss_adam_hparams*, const ss_adam_hparams*, ss_status*,
+                              cudaStream_t);
 cudaError_t launch_stats(const ss_map*, const ss_param_grads*, const uint8_t*, cudaStream_t);
 cudaError_t launch_apply_stat_planes(const ss_map*, const ss_param_grads*, cudaStream_t);
 cudaError_t launch_opacity_reset(const ss_map*, float, float*, float*, cudaStream_t);
@@ -99,11 +100,12 @@ int ss_apply_stat_planes(const ss_map* map, const ss_param_grads* grads, void* s
     return rc(launch_apply_stat_planes(map, grads, S(stream)));
 }
 
-int ss_preprocess(const ss_map* map, const ss_camera* cam, const ss_raster_opts* opts,
-                  const ss_splats* out, ss_status* d_status, void* stream) {
+int ss_preprocess(const ss_map* map, const ss_camera* cam, const ss_camera* d_cam,
+                  const ss_raster_opts* opts, const ss_splats* out, ss_status* d_status,
+                  void* stream) {
     if (!map || !cam || !opts_ok(opts) || !out || !d_status) return SS_EINVAL;
     if (map->n < 0 || map->n > 0x7fffffffLL) return SS_EINVAL;
-    return rc(launch_preprocess(map, cam, opts, out, d_status, S(stream)));
+    return rc(launch_preprocess(map, cam, d_cam, opts, out, d_status, S(stream)));
 }
 
 size_t ss_bin_workspace_bytes(int64_t n, int64_t pair_capacity, int32_t n_tiles) {
@@ -204,14 +206,15 @@ int ss_adam_step(const ss_map* map, const ss_param_grads* grads, const ss_param_
     return rc(launch_adam(map, grads, m, v, hp, d_status, S(stream)));
 }
 
-int ss_chain_adam(const ss_map* map, const ss_camera* cam, const ss_raster_opts* opts,
-                  const float* d_g2d, const uint8_t* d_flags, const uint8_t* d_contributed,
-                  float lambda_o_over_n, const ss_param_grads* m, const ss_param_grads* v,
-                  const ss_adam_hparams* hp, ss_status* d_status, void* stream) {
+int ss_chain_adam(const ss_map* map, const ss_camera* cam, const ss_camera* d_cam,
+                  const ss_raster_opts* opts, const float* d_g2d, const uint8_t* d_flags,
+                  const uint8_t* d_contributed, float lambda_o_over_n, const ss_param_grads* m,
+                  const ss_param_grads* v, const ss_adam_hparams* hp,
+                  const ss_adam_hparams* d_hp, ss_status* d_status, void* stream) {
     if (!map || !cam || !opts_ok(opts) || !d_g2d || !d_flags || !m || !v || !hp || !d_status)
         return SS_EINVAL;
-    return rc(launch_chain_adam(map, cam, opts, d_g2d, d_flags, d_contributed, lambda_o_over_n,
-                                m, v, hp, d_status, S(stream)));
+    return rc(launch_chain_adam(map, cam, d_cam, opts, d_g2d, d_flags, d_contributed,
+                                lambda_o_over_n, m, v, hp, d_hp, d_status, S(stream)));
 }
 
 int ss_accumulate_grad_stats(const ss_map* map, const ss_param_grads* grads,

@@ -1,4 +1,4 @@
-// binning.cu -- K2-K4b: duplicate-with-keys, onesweep radix sort, tile ranges.
+// binning.cu -- K2-K4b: duplicate-with-keys, radix sort, tile ranges.
 //
 // Replaces build_tile_index (rasterizer/tiles.py:29-65), whose order is
 // np.lexsort((splat, depth, tile)) (tiles.py:58): pairs sorted by tile,
@@ -9,37 +9,26 @@
 // half of a pair's key is a function of its splat alone, those passes are
 // run here over the N splats instead of the P ~ 12 N pairs:
 //
-//   1. onesweep LSD sort of the N depth keys (4 x 8-bit passes), stable,
-//      values = splat index                     -> splats in (depth, index) order
+//   1. LSD sort of the N depth keys (4 x 8-bit passes), stable, values =
+//      splat index                               -> splats in (depth, index) order
 //   2. exclusive scan of touched-tile counts in that order  -> pair offsets, P
-//   3. emission of (tile, splat) pairs in that order, with the tile-digit
-//      histograms accumulated on the fly
-//   4. onesweep LSD sort of the pair tile ids (ceil(log2 T / 8) passes),
-//      stable                                   -> (tile, depth, index) order
+//   3. coalesced emission of (tile, splat) pairs in that order
+//   4. LSD sort of the pair tile ids (ceil(log2 T / 8) passes), stable
+//                                                -> (tile, depth, index) order
 //   5. tile ranges by boundary detection; checkpoint slot bases by scan.
 //
 // The result is bit-identical to the reference order (tests/test_gpu_parity.py
 // compares it with the oracle's build_tile_index fed this projection).
 //
-// Onesweep pass: one CTA per 256*ITEMS keys with a dynamic tile id, warp-
-// level stable ranking with __match_any_sync, per-digit decoupled look-back
-// through a (block, digit) status array, direct scatter.
+// Each radix pass is reduce-then-scan (upsweep counts, per-digit scan,
+// downsweep with warp ballot ranking and a shared-memory reorder so the
+// scatter writes coalesced runs).  A one-sweep pass with decoupled look-back
+// was measured first and was latency-bound here: with hundreds of CTAs
+// co-resident, each CTA walks back over all its predecessors' aggregates.
 #include "common.cuh"
 
 namespace ss {
 
-constexpr uint32_t kFlagAgg = 1u << 30;
-constexpr uint32_t kFlagInc = 2u << 30;
-constexpr uint32_t kValMask = (1u << 30) - 1;
-
-__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
-    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ unsigned long long ld_volatile64(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -49,39 +38,12 @@ __device__ __forceinline__ void st_volatile64(unsigned long long* p, unsigned lo
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Decoupled look-back with a window: each step loads the status words of up
-// to LB_WIN predecessors at once (independent loads in flight), then
-// consumes them nearest-first -- adding aggregates until an inclusive
-// prefix is found, or stopping at the first not-yet-published word and
-// retrying from there.  With hundreds of co-resident CTAs the walk length
-// is ~k/2 predecessors; the window divides the serial L2 round trips by
-// LB_WIN.
+// Decoupled look-back (used by the scans) with a window: each step loads
+// the status words of up to LB_WIN predecessors at once (independent loads
+// in flight), then consumes them nearest-first -- adding aggregates until an
+// inclusive prefix is found, or stopping at the first not-yet-published word
+// and retrying from there.
 constexpr int LB_WIN = 16;
-
-__device__ __forceinline__ uint32_t lookback_u32(const uint32_t* status, int64_t j, int stride) {
-    uint32_t excl = 0;
-    while (j >= 0) {
-        uint32_t v[LB_WIN];
-#pragma unroll
-        for (int i = 0; i < LB_WIN; ++i)
-            v[i] = (j - i >= 0) ? ld_volatile(status + (size_t)(j - i) * stride) : kFlagInc;
-        int used = 0;
-        bool done = false;
-#pragma unroll
-        for (int i = 0; i < LB_WIN; ++i) {
-            if (done || used != i) break;
-            const uint32_t f = v[i] & ~kValMask;
-            if (f == 0) break;
-            excl += v[i] & kValMask;
-            ++used;
-            if (f == kFlagInc) done = true;
-        }
-        if (done) break;
-        j -= used;
-        if (used < LB_WIN) __nanosleep(32);
-    }
-    return excl;
-}
 
 __device__ __forceinline__ unsigned long long lookback_u64(const unsigned long long* status,
                                                            int64_t j, unsigned long long flag_agg,
@@ -111,26 +73,20 @@ __device__ __forceinline__ unsigned long long lookback_u64(const unsigned long l
     return excl;
 }
 
-// ------------------------------------------------------------- histogram
-// 256-bin histograms of `npass` consecutive 8-bit digits starting at shift0.
-__global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys,
-                                                         uint32_t n, int npass, int shift0,
-                                                         uint32_t* __restrict__ hist) {
-    __shared__ uint32_t h[4][256];
-    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) (&h[0][0])[k] = 0;
-    __syncthreads();
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        uint32_t k = keys[i];
-        for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(k >> (shift0 + 8 * p)) & 255u], 1u);
+// Lanes holding the same 8-bit digit (warp multi-split by 8 ballots; the
+// ballots are independent, unlike the serialised MATCH.ANY).  Invalid lanes
+// (valid == false) get an empty mask and are excluded from everyone's mask.
+__device__ __forceinline__ unsigned peers8(uint32_t d, bool valid) {
+    unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const unsigned bal = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bal : ~bal;
     }
-    __syncthreads();
-    for (int k = threadIdx.x; k < npass * 256; k += blockDim.x) {
-        uint32_t v = (&h[0][0])[k];
-        if (v) atomicAdd(&hist[k], v);
-    }
+    return valid ? peers : 0u;
 }
 
-// --------------------------------------------------------------- onesweep
 // Block-wide exclusive scan of one value per thread (256 threads).
 __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* s_warp) {
     const int t = threadIdx.x, w = t >> 5, l = t & 31;
@@ -148,20 +104,80 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* s_w
     return pre + incl - v;
 }
 
-// One stable LSD pass on an 8-bit digit: per-warp ranking with
-// __match_any_sync, per-digit windowed decoupled look-back, block-local
-// reorder in shared memory, then coalesced runs written to the global digit
-// ranges.  vals_in == nullptr means "values are the item indices" (first
-// pass over splats).  d_count: number of items (device), clamped to cap.
+// ------------------------------------------------------- reduce-then-scan
+// Chain-free LSD pass in three launches (the one-sweep look-back above is
+// latency-bound when hundreds of CTAs are co-resident: every CTA walks back
+// over all its predecessors' aggregates):
+//   rs_upsweep   : per-block digit counts -> counts[digit][block]
+//   rs_scan      : one CTA per digit, exclusive scan over blocks (in place)
+//                  and the digit total
+//   rs_downsweep : digit starts from the 256 totals, stable warp ranking,
+//                  block-local reorder, coalesced scatter
 template <int ITEMS>
-__global__ void __launch_bounds__(256) onesweep_kernel(
+__global__ void __launch_bounds__(256) rs_upsweep_kernel(const uint32_t* __restrict__ keys,
+                                                         const uint32_t* d_count,
+                                                         uint32_t n_static, uint32_t cap,
+                                                         int shift, uint32_t nblk,
+                                                         uint32_t* __restrict__ counts) {
+    constexpr int TILE = 256 * ITEMS;
+    __shared__ uint32_t h[8][256];
+    const int t = threadIdx.x, w = t >> 5;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) h[k][t] = 0;
+    __syncthreads();
+    const uint32_t n = d_count ? min(*d_count, cap) : n_static;
+    const uint32_t base = blockIdx.x * TILE;
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+        const uint32_t i = base + r * 256 + t;
+        if (i < n) atomicAdd(&h[w][(keys[i] >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c += h[k][t];
+    counts[(size_t)t * nblk + blockIdx.x] = c;
+}
+
+__global__ void __launch_bounds__(256) rs_scan_kernel(uint32_t nblk, uint32_t* __restrict__ counts,
+                                                      uint32_t* __restrict__ totals) {
+    __shared__ uint32_t s_warp[8];
+    uint32_t* row = counts + (size_t)blockIdx.x * nblk;
+    const int t = threadIdx.x;
+    uint32_t carry = 0;
+    for (uint32_t b0 = 0; b0 < nblk; b0 += 256 * 4) {
+        uint32_t v[4], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = b0 + t * 4 + k;
+            v[k] = i < nblk ? row[i] : 0u;
+            sum += v[k];
+        }
+        const uint32_t ex = block_excl_scan256(sum, s_warp);
+        __shared__ uint32_t s_tot;
+        if (t == 255) s_tot = ex + sum;
+        uint32_t run = carry + ex;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = b0 + t * 4 + k;
+            if (i < nblk) row[i] = run;
+            run += v[k];
+        }
+        __syncthreads();
+        carry += s_tot;
+        __syncthreads();
+    }
+    if (t == 0) totals[blockIdx.x] = carry;
+}
+
+template <int ITEMS>
+__global__ void __launch_bounds__(256) rs_downsweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, const uint32_t* d_count,
-    uint32_t n_static, uint32_t cap, int shift, const uint32_t* __restrict__ hist,
-    uint32_t* status, uint32_t* counter) {
+    uint32_t n_static, uint32_t cap, int shift, uint32_t nblk,
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ totals) {
     constexpr int WARP_ITEMS = 32 * ITEMS;
     constexpr int TILE = 256 * ITEMS;
-    __shared__ uint32_t s_bid;
     __shared__ uint32_t s_cnt[8][256];
     __shared__ uint32_t s_base[256];
     __shared__ uint32_t s_local[256];
@@ -169,79 +185,73 @@ __global__ void __launch_bounds__(256) onesweep_kernel(
     __shared__ uint32_t s_keys[TILE];
     __shared__ uint32_t s_vals[TILE];
     const int t = threadIdx.x, w = t >> 5, l = t & 31;
-    if (t == 0) s_bid = atomicAdd(counter, 1u);
 #pragma unroll
     for (int k = 0; k < 8; ++k) s_cnt[k][t] = 0;
-    __syncthreads();
-    const uint32_t bid = s_bid;
     const uint32_t n = d_count ? min(*d_count, cap) : n_static;
-    const uint32_t base = bid * TILE;
-    if (base >= n) return;
+    const uint32_t base = blockIdx.x * TILE;
+    if (base >= n) return;  // uniform per block
     const uint32_t nloc = min((uint32_t)TILE, n - base);
-
+    const uint32_t gstart = block_excl_scan256(totals[t], s_warp);  // also syncs s_cnt
+    s_base[t] = gstart + offsets[(size_t)t * nblk + blockIdx.x];
     uint32_t key[ITEMS], rank[ITEMS];
     const uint32_t wbase = w * WARP_ITEMS;
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
-        uint32_t li = wbase + r * 32 + l;
+        const uint32_t li = wbase + r * 32 + l;
         key[r] = li < nloc ? keys_in[base + li] : 0u;
     }
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
-        uint32_t li = wbase + r * 32 + l;
-        uint32_t d = li < nloc ? ((key[r] >> shift) & 255u) : 256u;
-        unsigned peers = __match_any_sync(0xffffffffu, d);
-        uint32_t before = d < 256u ? s_cnt[w][d] : 0u;
+        const uint32_t li = wbase + r * 32 + l;
+        const bool valid = li < nloc;
+        const uint32_t d = (key[r] >> shift) & 255u;
+        const unsigned peers = peers8(d, valid);
+        const uint32_t before = valid ? s_cnt[w][d] : 0u;
         rank[r] = before + __popc(peers & lanemask_lt());
         __syncwarp();
-        if (d < 256u && (peers & lanemask_lt()) == 0) s_cnt[w][d] = before + __popc(peers);
+        if (valid && (peers & lanemask_lt()) == 0) s_cnt[w][d] = before + __popc(peers);
         __syncwarp();
     }
     __syncthreads();
     uint32_t run = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        uint32_t c = s_cnt[k][t];
+        const uint32_t c = s_cnt[k][t];
         s_cnt[k][t] = run;
         run += c;
     }
-    const uint32_t total = run;
-    // publish + look back for digit t
-    uint32_t* my = status + (size_t)bid * 256 + t;
-    uint32_t excl = 0;
-    if (bid == 0) {
-        st_volatile(my, kFlagInc | total);
-    } else {
-        st_volatile(my, kFlagAgg | total);
-        excl = lookback_u32(status + t, (int64_t)bid - 1, 256);
-        st_volatile(my, kFlagInc | (excl + total));
-    }
-    const uint32_t hv = hist[t];
-    const uint32_t gstart = block_excl_scan256(hv, s_warp);
-    const uint32_t lstart = block_excl_scan256(total, s_warp);
-    s_base[t] = gstart + excl;
-    s_local[t] = lstart;
+    s_local[t] = block_excl_scan256(run, s_warp);
     __syncthreads();
-    // block-local reorder by digit (stable)
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
-        uint32_t li = wbase + r * 32 + l;
+        const uint32_t li = wbase + r * 32 + l;
         if (li < nloc) {
-            uint32_t d = (key[r] >> shift) & 255u;
-            uint32_t lp = s_local[d] + s_cnt[w][d] + rank[r];
+            const uint32_t d = (key[r] >> shift) & 255u;
+            const uint32_t lp = s_local[d] + s_cnt[w][d] + rank[r];
             s_keys[lp] = key[r];
             s_vals[lp] = vals_in ? vals_in[base + li] : base + li;
         }
     }
     __syncthreads();
-    // coalesced runs to the global digit ranges
     for (uint32_t i = t; i < nloc; i += 256) {
-        uint32_t k = s_keys[i];
-        uint32_t d = (k >> shift) & 255u;
-        uint32_t gp = s_base[d] + (i - s_local[d]);
+        const uint32_t k = s_keys[i];
+        const uint32_t d = (k >> shift) & 255u;
+        const uint32_t gp = s_base[d] + (i - s_local[d]);
         vals_out[gp] = s_vals[i];
         if (keys_out) keys_out[gp] = k;
     }
+}
+
+// One reduce-then-scan pass (3 launches).
+template <int ITEMS>
+static void rs_pass(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                    const uint32_t* d_count, uint32_t n_static, uint32_t cap, int shift,
+                    uint32_t* counts, uint32_t* totals, cudaStream_t s) {
+    const uint32_t nblk = (uint32_t)div_up(cap > 0 ? cap : 1, 256 * ITEMS);
+    rs_upsweep_kernel<ITEMS><<<nblk, 256, 0, s>>>(kin, d_count, n_static, cap, shift, nblk, counts);
+    rs_scan_kernel<<<256, 256, 0, s>>>(nblk, counts, totals);
+    rs_downsweep_kernel<ITEMS><<<nblk, 256, 0, s>>>(kin, vin, kout, vout, d_count, n_static, cap,
+                                                    shift, nblk, counts, totals);
 }
 
 // ------------------------------------------------------------------ scan
@@ -330,16 +340,12 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t* __restrict__ 
 // One warp per 32 consecutive splats in (depth, index) order: the warp's
 // pairs form one contiguous output range, written lane-strided (coalesced);
 // each output element finds its splat by a 5-step shuffle binary search
-// over the 32 exclusive offsets.  The 8-bit tile-digit histograms of the
-// pair sort are accumulated in shared memory on the way.
+// over the 32 exclusive offsets.
 __global__ void __launch_bounds__(256) emit_pairs_kernel(
     uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restrict__ tiles,
     const uint2* __restrict__ rect, const uint32_t* __restrict__ offsets, int tiles_x,
-    const int64_t* total, int64_t cap, int npass, uint32_t* __restrict__ keys,
-    uint32_t* __restrict__ vals, uint32_t* __restrict__ hist) {
-    __shared__ uint32_t h[3][256];
-    for (int k = threadIdx.x; k < 3 * 256; k += blockDim.x) (&h[0][0])[k] = 0;
-    __syncthreads();
+    const int64_t* total, int64_t cap, uint32_t* __restrict__ keys,
+    uint32_t* __restrict__ vals) {
     const bool ok = *total <= cap;
     const int lane = threadIdx.x & 31;
     const uint32_t j = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32 + lane;
@@ -378,13 +384,7 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
             const uint32_t tid = (oy + ry) * tiles_x + ox + (li - ry * ow);
             keys[base + e] = tid;
             vals[base + e] = sid;
-            for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(tid >> (8 * p)) & 255u], 1u);
         }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < npass * 256; k += blockDim.x) {
-        uint32_t v = (&h[0][0])[k];
-        if (v) atomicAdd(&hist[k], v);
     }
 }
 
@@ -402,7 +402,7 @@ __global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, const int6
     }
 }
 
-// Copy a device int64 (clamped) into a u32 count for the onesweep passes.
+// Copy a device int64 (clamped) into a u32 count for the pair passes.
 __global__ void clamp_count_kernel(const int64_t* total, int64_t cap, uint32_t* out) {
     int64_t P = *total;
     *out = (P > cap) ? 0u : (uint32_t)P;
@@ -421,16 +421,12 @@ struct BinWorkspace {
     }
 };
 
-constexpr int kDepthItems = 8;   // 2048 splats per onesweep CTA
-constexpr int kPairItems = 16;   // 4096 pairs per onesweep CTA
+constexpr int kDepthItems = 8;  // 2048 splats per radix CTA
+constexpr int kPairItems = 8;   // 2048 pairs per radix CTA
 
 struct BinLayout {
     // zero-initialised control region first
     uint32_t* ctrl;            // counters
-    uint32_t* hist_depth;      // 4*256
-    uint32_t* hist_tile;       // 3*256
-    uint32_t* st_depth;        // 4 passes * blocks * 256
-    uint32_t* st_pair;         // npass * blocks * 256
     unsigned long long* st_scan1;
     unsigned long long* st_scan2;
     size_t ctrl_bytes;
@@ -439,6 +435,8 @@ struct BinLayout {
     uint32_t* offsets;                // N
     uint32_t *pk0, *pk1, *pv0, *pv1;  // pair capacity
     uint32_t* pcount;                 // 1
+    uint32_t* rs_counts;              // 256 * max blocks
+    uint32_t* rs_totals;              // 256
 };
 
 inline int tile_passes(int n_tiles) {
@@ -451,14 +449,8 @@ BinLayout bin_layout(int64_t n, int64_t cap, int n_tiles, void* ws, size_t* byte
     BinWorkspace w;
     w.base = reinterpret_cast<char*>(ws);
     BinLayout L;
-    int db = div_up(n > 0 ? n : 1, 256 * kDepthItems);
-    int pb = div_up(cap > 0 ? cap : 1, 256 * kPairItems);
-    int np = tile_passes(n_tiles);
+    (void)n_tiles;
     L.ctrl = w.take<uint32_t>(16);
-    L.hist_depth = w.take<uint32_t>(4 * 256);
-    L.hist_tile = w.take<uint32_t>(3 * 256);
-    L.st_depth = w.take<uint32_t>((size_t)4 * db * 256);
-    L.st_pair = w.take<uint32_t>((size_t)np * pb * 256);
     L.st_scan1 = w.take<unsigned long long>(div_up(n > 0 ? n : 1, 256 * kScanItems) + 1);
     L.st_scan2 = w.take<unsigned long long>(div_up(n_tiles + 1, 256 * kScanItems) + 1);
     w.off = (w.off + 255) & ~size_t(255);
@@ -473,6 +465,14 @@ BinLayout bin_layout(int64_t n, int64_t cap, int n_tiles, void* ws, size_t* byte
     L.pv0 = w.take<uint32_t>(cap);
     L.pv1 = w.take<uint32_t>(cap);
     L.pcount = w.take<uint32_t>(4);
+    {
+        int64_t mx = cap > n ? cap : n;
+        L.rs_counts = w.take<uint32_t>(
+            (size_t)256 * (div_up(mx > 0 ? mx : 1, 256 * (kDepthItems < kPairItems ? kDepthItems
+                                                                               : kPairItems)) +
+                           1));
+        L.rs_totals = w.take<uint32_t>(256);
+    }
     if (bytes) *bytes = w.off + 256;
     return L;
 }
@@ -501,17 +501,13 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
     int64_t* P = &st->pair_count;
     if (n > 0) {
         uint32_t nn = (uint32_t)n;
-        // 1. depth sort of splats (4 stable 8-bit passes)
-        radix_hist_kernel<<<min(div_up(n, 256 * 8), 1024), 256, 0, s>>>(sp->d_depth_key, nn, 4, 0,
-                                                                        L.hist_depth);
-        int db = div_up(n, 256 * kDepthItems);
+        // 1. depth sort of splats (4 stable 8-bit reduce-then-scan passes)
         const uint32_t* kin = sp->d_depth_key;
         const uint32_t* vin = nullptr;
         uint32_t *ko[2] = {L.kA, L.kB}, *vo[2] = {L.vA, L.vB};
         for (int p = 0; p < 4; ++p) {
-            onesweep_kernel<kDepthItems><<<db, 256, 0, s>>>(
-                kin, vin, p < 3 ? ko[p & 1] : nullptr, vo[p & 1], nullptr, nn, nn, 8 * p,
-                L.hist_depth + 256 * p, L.st_depth + (size_t)p * db * 256, L.ctrl + p);
+            rs_pass<kDepthItems>(kin, vin, p < 3 ? ko[p & 1] : nullptr, vo[p & 1], nullptr, nn, nn,
+                                 8 * p, L.rs_counts, L.rs_totals, s);
             kin = ko[p & 1];
             vin = vo[p & 1];
         }
@@ -520,23 +516,21 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
         scan_kernel<false><<<div_up(n, 256 * kScanItems), 256, 0, s>>>(
             sp->d_tiles, order, nullptr, nn, L.offsets, L.st_scan1, L.ctrl + 8, P,
             &st->pair_overflow, cap);
-        // 3. emission + tile digit histograms
-        int np = tile_passes(n_tiles);
+        // 3. emission of (tile, splat) pairs in depth order
         emit_pairs_kernel<<<div_up(n, 256), 256, 0, s>>>(
             nn, order, sp->d_tiles, reinterpret_cast<const uint2*>(sp->d_rect), L.offsets, tiles_x,
-            P, cap, np, L.pk0, L.pv0, L.hist_tile);
+            P, cap, L.pk0, L.pv0);
         clamp_count_kernel<<<1, 1, 0, s>>>(P, cap, L.pcount);
         // 4. stable sort of pairs by tile id; the last pass lands in d_pair_splat
-        int pb = div_up(cap > 0 ? cap : 1, 256 * kPairItems);
+        const int np = tile_passes(n_tiles);
         const uint32_t* pk = L.pk0;
         const uint32_t* pv = L.pv0;
         for (int p = 0; p < np; ++p) {
             bool last = p == np - 1;
             uint32_t* kdst = (pk == L.pk0) ? L.pk1 : L.pk0;
             uint32_t* vdst = last ? bins->d_pair_splat : ((pv == L.pv0) ? L.pv1 : L.pv0);
-            onesweep_kernel<kPairItems><<<pb, 256, 0, s>>>(
-                pk, pv, kdst, vdst, L.pcount, 0u, (uint32_t)cap, 8 * p, L.hist_tile + 256 * p,
-                L.st_pair + (size_t)p * pb * 256, L.ctrl + 4 + p);
+            rs_pass<kPairItems>(pk, pv, kdst, vdst, L.pcount, 0u, (uint32_t)cap, 8 * p,
+                                L.rs_counts, L.rs_totals, s);
             pk = kdst;
             pv = vdst;
         }

@@ -39,6 +39,22 @@ void fill_camc(const ss_camera* c, CamC& f) {
     }
 }
 
+__device__ __forceinline__ void load_camc(const ss_camera* __restrict__ c, CamC& f) {
+    f.fx = c->fx;
+    f.fy = c->fy;
+    f.cx = c->cx;
+    f.cy = c->cy;
+    f.W = c->width;
+    f.H = c->height;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) f.R[k] = c->R[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        f.t[k] = c->t[k];
+        f.c[k] = c->center[k];
+    }
+}
+
 struct GaussGrad {
     float pos[3], rot[4], ls[3], op, dc[3];
     float n2d;
@@ -325,6 +341,20 @@ struct AdamHP {
     float b1, b2, eps, bc1, bc2;
 };
 
+__device__ __forceinline__ void load_hp(const ss_adam_hparams* __restrict__ h, AdamHP& hp) {
+    hp.lr[0] = h->lr_position;
+    hp.lr[1] = h->lr_rotation;
+    hp.lr[2] = h->lr_log_scale;
+    hp.lr[3] = h->lr_opacity;
+    hp.lr[4] = h->lr_sh_dc;
+    hp.lr[5] = h->lr_sh_rest;
+    hp.b1 = h->beta1;
+    hp.b2 = h->beta2;
+    hp.eps = h->eps;
+    hp.bc1 = h->bias1;
+    hp.bc2 = h->bias2;
+}
+
 __device__ __forceinline__ float adam_elem(float& p, float g, float& m, float& v, float lr,
                                            const AdamHP& hp) {
     m = m * hp.b1 + (1.f - hp.b1) * g;
@@ -408,13 +438,18 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t n, float* pos, float4
 template <int NC, bool REST>
 __global__ void __launch_bounds__(256) chain_adam_kernel(
     int64_t n, float* __restrict__ pos, float4* __restrict__ rot, float* __restrict__ ls,
-    float* __restrict__ opl, float* __restrict__ shdc, float* __restrict__ shrest, CamC cam,
-    int deg, float dilation, const float* __restrict__ g2d, const uint8_t* __restrict__ flags,
-    const uint8_t* __restrict__ contributed, float lo_over_n, ss_param_grads M, ss_param_grads V,
-    AdamHP hp, float* __restrict__ grad2d_accum, float* __restrict__ grad3d_accum,
+    float* __restrict__ opl, float* __restrict__ shdc, float* __restrict__ shrest, CamC cam_v,
+    const ss_camera* __restrict__ d_cam, int deg, float dilation, const float* __restrict__ g2d,
+    const uint8_t* __restrict__ flags, const uint8_t* __restrict__ contributed, float lo_over_n,
+    ss_param_grads M, ss_param_grads V, AdamHP hp_v, const ss_adam_hparams* __restrict__ d_hp,
+    float* __restrict__ grad2d_accum, float* __restrict__ grad3d_accum,
     int32_t* __restrict__ obs_count, ss_status* st) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n || st->pair_overflow) return;
+    CamC cam = cam_v;
+    AdamHP hp = hp_v;
+    if (d_cam) load_camc(d_cam, cam);  // graph replay: per-step values from device memory
+    if (d_hp) load_hp(d_hp, hp);
     GaussGrad o = {};
     const uint8_t fl = flags[i];
     const float opi = opl[i];
@@ -533,18 +568,20 @@ cudaError_t launch_adam(const ss_map* mp, const ss_param_grads* G, const ss_para
     return cudaGetLastError();
 }
 
-cudaError_t launch_chain_adam(const ss_map* mp, const ss_camera* cam, const ss_raster_opts* o,
-                              const float* g2d, const uint8_t* flags, const uint8_t* contributed,
-                              float lo_over_n, const ss_param_grads* M, const ss_param_grads* V,
-                              const ss_adam_hparams* h, ss_status* st, cudaStream_t s) {
+cudaError_t launch_chain_adam(const ss_map* mp, const ss_camera* cam, const ss_camera* d_cam,
+                              const ss_raster_opts* o, const float* g2d, const uint8_t* flags,
+                              const uint8_t* contributed, float lo_over_n,
+                              const ss_param_grads* M, const ss_param_grads* V,
+                              const ss_adam_hparams* h, const ss_adam_hparams* d_hp,
+                              ss_status* st, cudaStream_t s) {
     if (mp->n == 0) return cudaSuccess;
     CamC cc;
     fill_camc(cam, cc);
     auto go = [&](auto kern) {
         kern<<<div_up(mp->n, 256), 256, 0, s>>>(
             mp->n, mp->d_positions, reinterpret_cast<float4*>(mp->d_rotations), mp->d_log_scales,
-            mp->d_opacity_logits, mp->d_sh_dc, mp->d_sh_rest, cc, o->sh_degree, o->dilation, g2d,
-            flags, contributed, lo_over_n, *M, *V, make_hp(h), mp->d_grad2d_accum,
+            mp->d_opacity_logits, mp->d_sh_dc, mp->d_sh_rest, cc, d_cam, o->sh_degree, o->dilation,
+            g2d, flags, contributed, lo_over_n, *M, *V, make_hp(h), d_hp, mp->d_grad2d_accum,
             mp->d_grad3d_accum, mp->d_obs_count, st);
     };
     const bool rest = h->update_sh_rest != 0;

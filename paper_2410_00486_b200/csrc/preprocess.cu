@@ -19,6 +19,22 @@ struct CamF {
     float R[9], t[3], c[3];
 };
 
+__device__ __forceinline__ void load_camf(const ss_camera* __restrict__ c, CamF& f) {
+    f.fx = c->fx;
+    f.fy = c->fy;
+    f.cx = c->cx;
+    f.cy = c->cy;
+    f.W = c->width;
+    f.H = c->height;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) f.R[k] = c->R[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        f.t[k] = c->t[k];
+        f.c[k] = c->center[k];
+    }
+}
+
 __device__ __forceinline__ float sigmoid_stable(float x) {
     // projection.py:68-70
     float e = expf(-fabsf(x));
@@ -77,11 +93,14 @@ __device__ __forceinline__ void project_cov(const float p[3], const float4 q, co
 __global__ void __launch_bounds__(256) preprocess_kernel(
     int64_t n, const float* __restrict__ pos, const float4* __restrict__ rot,
     const float* __restrict__ ls, const float* __restrict__ opl, const float* __restrict__ sh_dc,
-    const float* __restrict__ sh_rest, CamF cam, int sh_degree, float near_plane, float dilation,
-    float log_amin, int tiles_x, int tiles_y, SplatRec* __restrict__ rec,
+    const float* __restrict__ sh_rest, CamF cam_v, const ss_camera* __restrict__ d_cam,
+    int sh_degree, float near_plane, float dilation, float log_amin, int tiles_x, int tiles_y,
+    SplatRec* __restrict__ rec,
     uint32_t* __restrict__ depth_key, uint32_t* __restrict__ tiles, uint2* __restrict__ rect,
     uint8_t* __restrict__ flags, float* __restrict__ aux, ss_status* status) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    CamF cam = cam_v;
+    if (d_cam) load_camf(d_cam, cam);  // graph replay: camera from device memory
     bool vis = false;
     if (i < n) {
         float p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
@@ -191,8 +210,9 @@ void fill_camf(const ss_camera* c, CamF& f) {
     }
 }
 
-cudaError_t launch_preprocess(const ss_map* map, const ss_camera* cam, const ss_raster_opts* o,
-                              const ss_splats* out, ss_status* st, cudaStream_t s) {
+cudaError_t launch_preprocess(const ss_map* map, const ss_camera* cam, const ss_camera* d_cam,
+                              const ss_raster_opts* o, const ss_splats* out, ss_status* st,
+                              cudaStream_t s) {
     if (map->n == 0) return cudaSuccess;
     CamF cf;
     fill_camf(cam, cf);
@@ -201,7 +221,7 @@ cudaError_t launch_preprocess(const ss_map* map, const ss_camera* cam, const ss_
     int blocks = div_up(map->n, threads);
     preprocess_kernel<<<blocks, threads, 0, s>>>(
         map->n, map->d_positions, reinterpret_cast<const float4*>(map->d_rotations),
-        map->d_log_scales, map->d_opacity_logits, map->d_sh_dc, map->d_sh_rest, cf,
+        map->d_log_scales, map->d_opacity_logits, map->d_sh_dc, map->d_sh_rest, cf, d_cam,
         o->sh_degree, o->near_plane, o->dilation, logf(o->alpha_min), tx, ty,
         reinterpret_cast<SplatRec*>(out->d_rec), out->d_depth_key, out->d_tiles,
         reinterpret_cast<uint2*>(out->d_rect), out->d_flags, out->d_aux, st);

@@ -42,13 +42,19 @@ STATUS_LAG = 2
 
 # kernels each C-ABI call enqueues (counted for bench.py's gpu_launches)
 KERNELS_PER_CALL = {
-    # status_begin 1 + preprocess 1 + binning (hist 1, 4 depth passes, scan 1,
-    # emit 1, clamp 1, 2 tile passes, ranges 1, ckpt scan 1) 13 + blend 1 +
-    # loss (ssim fwd, ssim bwd, reduce) 3 + backward 1
-    "step_fb": 1 + 1 + 13 + 1 + 3 + 1,
+    # status_begin 1 + preprocess 1 + blend 1 + loss (ssim fwd, ssim bwd,
+    # reduce) 3 + backward 1; binning is counted separately (binning_kernels)
+    "step_fb": 1 + 1 + 1 + 3 + 1,
     "chain_adam": 1,
     "opacity_reg": 2,
 }
+
+
+def binning_kernels(n_tiles: int) -> int:
+    """4 depth passes x 3 + scan + emit + clamp + tile passes x 3 + ranges +
+    checkpoint-base scan (binning.cu)."""
+    bits = max(1, (n_tiles - 1).bit_length())
+    return 4 * 3 + 1 + 1 + 1 + 3 * ((bits + 7) // 8) + 1 + 1
 
 
 @dataclass
@@ -100,10 +106,40 @@ class MappingEngine:
         self._slots = 8
         self._host = torch.zeros((self._slots, _lib.STATUS_WORDS + 4), dtype=torch.float64,
                                  pin_memory=True)
+        self._graphs: dict = {}
         self._alloc_map_buffers()
         self._alloc_pair_buffers(self._cap)
         self.profile = None  # list of (stage, start event, end event) when profiling
         self.launches = 0    # kernels launched by this engine (see KERNELS_PER_CALL)
+        # per-step parameters (camera, Adam step values) live in device memory
+        # so one captured CUDA graph serves every step; they are filled from a
+        # ring of pinned host slots (a slot is reused only after its step drained)
+        self._pslots = 8
+        self._pbytes = 256
+        self._phost = torch.zeros((self._pslots, self._pbytes), dtype=torch.uint8,
+                                  pin_memory=True)
+        self._pdev = torch.zeros(self._pbytes, dtype=torch.uint8, device=self.dev)
+        self.use_graph = False
+
+    def enable_graph(self, on: bool = True):
+        """Replay the iteration body from a captured CUDA graph (one per
+        target buffer); buffers reallocated by densify or capacity growth
+        drop the captures."""
+        self.use_graph = on
+        self._graphs.clear()
+
+    def _params_ptrs(self):
+        base = self._pdev.data_ptr()
+        return ctypes.c_void_p(base), ctypes.c_void_p(base + 128)
+
+    def _stage_params(self, rec):
+        """Write the step's camera + Adam values into its pinned slot and
+        enqueue the host->device copy."""
+        slot = self._phost[rec.slot % self._pslots]
+        cm = rec.camera.to_ss()
+        ctypes.memmove(slot.data_ptr(), ctypes.addressof(cm), ctypes.sizeof(cm))
+        ctypes.memmove(slot.data_ptr() + 128, ctypes.addressof(rec.hp), ctypes.sizeof(rec.hp))
+        self._pdev.copy_(slot, non_blocking=True)
 
     def _mark(self, name):
         """Stage boundary for the per-kernel timing bench.py reports."""
@@ -114,6 +150,7 @@ class MappingEngine:
 
     # ------------------------------------------------------------ buffers
     def _alloc_map_buffers(self):
+        self._graphs.clear()
         n = len(self.gmap)
         dev = self.dev
         self.splats = SplatBuffers.alloc(n, dev, aux=False)
@@ -137,6 +174,7 @@ class MappingEngine:
         self._flat = None
 
     def _alloc_pair_buffers(self, cap):
+        self._graphs.clear()
         n = len(self.gmap)
         self._cap = int(cap)
         self.bins = BinBuffers.alloc(self._cap, self.n_tiles, self.dev)
@@ -163,7 +201,8 @@ class MappingEngine:
         n = len(self.gmap)
         self._mark("begin")
         check(L.ss_status_begin_step(P(self.status), s), "ss_status_begin_step")
-        check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op),
+        d_cam = self._params_ptrs()[0] if view_mode is None else None
+        check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), d_cam, ctypes.byref(op),
                               ctypes.byref(spss), P(self.status), s), "ss_preprocess")
         self._mark("preprocess")
         check(L.ss_bin_sort(n, ctypes.byref(spss), ctypes.byref(cm), ctypes.byref(bss),
@@ -199,17 +238,10 @@ class MappingEngine:
                                   P(self.work), self.work_cap, n, P(self.g2d),
                                   P(self.contributed), P(self.status), s), "ss_backward_splat")
         self._mark("backward")
-        self.launches += (KERNELS_PER_CALL["step_fb"] + (3 if self.opts.with_depth and
-                                                        self.cfg.depth_weight else 0))
         return mp, cm, op
 
-    def _finish_record(self, rec: StepRecord):
-        """Snapshot status + loss sums into the record's pinned slot."""
-        L = lib()
-        s = stream_handle()
-        n = len(self.gmap)
-        check(L.ss_opacity_reg(n, P(self.gmap.opacity_logits), 0.0, None, 0, P(self.osum), s),
-              "ss_opacity_reg")
+    def _snapshot(self, rec: StepRecord):
+        """Copy the step's status block + loss sums into its pinned slot."""
         row = self._host[rec.slot]
         row[:_lib.STATUS_WORDS].copy_(self.status.double(), non_blocking=True)
         row[_lib.STATUS_WORDS:_lib.STATUS_WORDS + 2].copy_(self.sums[:2], non_blocking=True)
@@ -232,19 +264,48 @@ class MappingEngine:
         self._drain(STATUS_LAG)
         return rec.index
 
-    def _run(self, rec: StepRecord):
+    def _body(self, cam: Camera, target, target_depth):
+        """The iteration's kernels; the per-step camera / Adam values are read
+        from the device parameter block (graph-capturable)."""
         L = lib()
         n = len(self.gmap)
-        mp, cm, op = self._forward_backward(rec.camera, rec.target, rec.target_depth, None)
+        mp, cm, op = self._forward_backward(cam, target, target_depth, None)
         lon = float(self.cfg.lambda_o / n) if n else 0.0
-        check(L.ss_chain_adam(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op), P(self.g2d),
-                              P(self.splats.flags), P(self.contributed), lon,
+        d_cam, d_hp = self._params_ptrs()
+        hp0 = self.state.hparams(self.opts.sh_degree > 0)
+        check(L.ss_chain_adam(ctypes.byref(mp), ctypes.byref(cm), d_cam, ctypes.byref(op),
+                              P(self.g2d), P(self.splats.flags), P(self.contributed), lon,
                               ctypes.byref(self.state.planes("m")),
-                              ctypes.byref(self.state.planes("v")), ctypes.byref(rec.hp),
+                              ctypes.byref(self.state.planes("v")), ctypes.byref(hp0), d_hp,
                               P(self.status), stream_handle()), "ss_chain_adam")
         self._mark("chain_adam")
-        self._finish_record(rec)
-        self.launches += KERNELS_PER_CALL["chain_adam"] + KERNELS_PER_CALL["opacity_reg"]
+        check(L.ss_opacity_reg(n, P(self.gmap.opacity_logits), 0.0, None, 0, P(self.osum),
+                               stream_handle()), "ss_opacity_reg")
+
+    def _run(self, rec: StepRecord):
+        self._stage_params(rec)
+        if self.use_graph and self.profile is None:
+            key = (rec.target.data_ptr(),
+                   rec.target_depth.data_ptr() if rec.target_depth is not None else 0)
+            g = self._graphs.get(key)
+            if g is None:
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._body(rec.camera, rec.target, rec.target_depth)
+                self._graphs[key] = g
+            g.replay()
+        else:
+            self._body(rec.camera, rec.target, rec.target_depth)
+        self.launches += self._launches_per_step()
+        self._snapshot(rec)
+
+    def _launches_per_step(self):
+        k = (KERNELS_PER_CALL["step_fb"] + binning_kernels(self.n_tiles)
+             + KERNELS_PER_CALL["chain_adam"] + KERNELS_PER_CALL["opacity_reg"])
+        if self.opts.with_depth and self.cfg.depth_weight:
+            k += 3
+        return k
 
     def _drain(self, lag: int):
         """Consume status snapshots older than `lag` steps; recover overflow."""
@@ -308,7 +369,7 @@ class MappingEngine:
         mp, cm, op = self.gmap.ss(), cam.to_ss(), self.opts.to_ss()
         st = torch.empty(_lib.STATUS_WORDS, dtype=torch.int64, device=self.dev)
         check(L.ss_status_reset(P(st), s), "ss_status_reset")
-        check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op),
+        check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), None, ctypes.byref(op),
                               ctypes.byref(self.splats.ss()), P(st), s), "ss_preprocess")
         tiny = BinBuffers.alloc(0, self.n_tiles, self.dev)
         ws = bin_workspace(len(self.gmap), 0, self.n_tiles, self.dev)

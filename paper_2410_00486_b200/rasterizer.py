@@ -285,7 +285,7 @@ def rasterize_forward(gmap: GaussianMap, camera, opts: RasterOpts | None = None)
     st = new_status(dev)
     sp = SplatBuffers.alloc(n, dev)
     mp, cm, op = gmap.ss(), cam.to_ss(), opts.to_ss()
-    check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op),
+    check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), None, ctypes.byref(op),
                           ctypes.byref(sp.ss()), P(st), s), "ss_preprocess")
     key = (str(dev), n_tiles)
     cap = max(_CAP_HINT.get(key, 0), 4 * n, 1024)

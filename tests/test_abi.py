@@ -45,12 +45,12 @@ def test_workspace_queries_need_no_gpu():
 def test_invalid_arguments_rejected_without_launch():
     from paper_2410_00486_b200 import _lib
     L = _lib.lib()
-    assert L.ss_preprocess(None, None, None, None, None, None) == _lib.SS_EINVAL
+    assert L.ss_preprocess(None, None, None, None, None, None, None) == _lib.SS_EINVAL
     assert L.ss_loss_l1_ssim(4, 4, None, None, 0.2, None, None, None, None, 0, None) == _lib.SS_EINVAL
     opts = _lib.SSRasterOpts()
     opts.tile_size, opts.bucket_size = 8, 32  # the kernels are specialised for 16x16 tiles
     m, c, s = _lib.SSMap(), _lib.SSCamera(), _lib.SSSplats()
-    assert L.ss_preprocess(ctypes.byref(m), ctypes.byref(c), ctypes.byref(opts),
+    assert L.ss_preprocess(ctypes.byref(m), ctypes.byref(c), None, ctypes.byref(opts),
                            ctypes.byref(s), ctypes.c_void_p(8), None) == _lib.SS_EINVAL
 
 
