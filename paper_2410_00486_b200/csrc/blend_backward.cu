@@ -45,12 +45,15 @@ __global__ void __launch_bounds__(128) backward_splat_kernel(
     extern __shared__ float4 smem[];
     constexpr int NC = DEPTH ? 10 : 9;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    // per-warp compacted pixel list: gradient side, coordinates, state, blend mask
-    float4* sG = smem + wid * kTilePx;
-    float2* sXY = reinterpret_cast<float2*>(smem + nw * kTilePx) + wid * kTilePx;
-    float2* sS = reinterpret_cast<float2*>(smem + nw * kTilePx) + (nw + wid) * kTilePx;
-    uint32_t* sM = reinterpret_cast<uint32_t*>(smem + 2 * nw * kTilePx) + wid * kTilePx;
-    float* sD = reinterpret_cast<float*>(smem + 2 * nw * kTilePx) + (nw + wid) * kTilePx;
+    // per-warp compacted pixel list (36-40 B per pixel): gradient side
+    // (g, g . image), state at the bucket start (T0, G0), coordinates, blend mask
+    char* sbase = reinterpret_cast<char*>(smem);
+    const size_t plane = (size_t)nw * kTilePx;
+    float4* sG = reinterpret_cast<float4*>(sbase) + wid * kTilePx;
+    float2* sS = reinterpret_cast<float2*>(sbase + plane * 16) + wid * kTilePx;
+    float2* sXY = reinterpret_cast<float2*>(sbase + plane * 24) + wid * kTilePx;
+    uint32_t* sM = reinterpret_cast<uint32_t*>(sbase + plane * 32) + wid * kTilePx;
+    float* sD = reinterpret_cast<float*>(sbase + plane * 36) + wid * kTilePx;
     const int64_t count = min(*work_count, work_cap);
 
     for (;;) {
@@ -107,20 +110,22 @@ __global__ void __launch_bounds__(128) backward_splat_kernel(
                     sD[pos] = gd;
                 }
                 sG[pos] = pg;
-                sXY[pos] = make_float2((float)ix, (float)iy);
                 sS[pos] = make_float2(ck.x, G0);
                 sM[pos] = mask;
+                sXY[pos] = make_float2((float)ix, (float)iy);
             }
             nact += __popc(bal);
         }
         __syncwarp();
         // ---- diagonal wavefront over the active pixels
-        float acc[NC];
-#pragma unroll
-        for (int q = 0; q < NC; ++q) acc[q] = 0.f;
+        // per-lane sums; the splat-constant factors (conic, 1/sigma, -1/2)
+        // are applied once at the end:
+        //   d mean  = (c0 S_dx + c1 S_dy, c1 S_dx + c2 S_dy),  S_d. = sum da d.
+        //   d conic = -1/2 (S_dxdx, 2 S_dxdy, S_dydy),        d sigma = S_da / sigma
+        float acc_rgb0 = 0.f, acc_rgb1 = 0.f, acc_rgb2 = 0.f, acc_z = 0.f;
+        float s_da = 0.f, s_dx = 0.f, s_dy = 0.f, s_xx = 0.f, s_xy = 0.f, s_yy = 0.f;
         float T = 0.f, G = 0.f;
         bool blended = false;
-        const float inv_sigma = 1.0f / B.y;
         const int steps = nact + 31;
 #pragma unroll 1
         for (int st = 0; st < steps; ++st) {
@@ -149,26 +154,38 @@ __global__ void __launch_bounds__(128) backward_splat_kernel(
             if (DEPTH) {
                 gd = sD[j];
                 grgb += gd * B.w;
+                acc_z += w * gd;
             }
             const float Gafter = G + grgb * w;
-            acc[0] += w * pg.x;
-            acc[1] += w * pg.y;
-            acc[2] += w * pg.z;
-            if (DEPTH) acc[9] += w * gd;
+            acc_rgb0 += w * pg.x;
+            acc_rgb1 += w * pg.y;
+            acc_rgb2 += w * pg.z;
             if (a != amax) {  // alpha-path gradient (kernels.py:342-364); 1 - a > 0 here
-                const float dal = T * grgb - __fdividef(pg.w - Gafter, 1.0f - a);
-                acc[8] += dal * (a * inv_sigma);
+                const float dal = T * grgb - (pg.w - Gafter) * rcp_approx(1.0f - a);
                 const float da = dal * a;
-                acc[3] += da * (A.z * dx + A.w * dy);
-                acc[4] += da * (A.w * dx + B.x * dy);
-                const float h = -0.5f * da;
-                acc[5] += h * dx * dx;
-                acc[6] += (h + h) * dx * dy;
-                acc[7] += h * dy * dy;
+                const float tx = da * dx, ty = da * dy;
+                s_da += da;
+                s_dx += tx;
+                s_dy += ty;
+                s_xx += tx * dx;
+                s_xy += tx * dy;
+                s_yy += ty * dy;
             }
             T = __fmul_rn(T, __fsub_rn(1.0f, a));
             G = Gafter;
         }
+        const float c1 = 0.5f * A.w;
+        float acc[NC];
+        acc[0] = acc_rgb0;
+        acc[1] = acc_rgb1;
+        acc[2] = acc_rgb2;
+        acc[3] = A.z * s_dx + c1 * s_dy;
+        acc[4] = c1 * s_dx + B.x * s_dy;
+        acc[5] = -0.5f * s_xx;
+        acc[6] = -s_xy;
+        acc[7] = -0.5f * s_yy;
+        acc[8] = s_da / B.y;
+        if (DEPTH) acc[NC - 1] = acc_z;
         if (k < ke) {
             float* row = g2d + (size_t)s * NC;
 #pragma unroll
@@ -197,7 +214,7 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
     if (e != cudaSuccess) return e;
     int tx = div_up(cam->width, kTile);
     const int threads = 128, warps = threads / 32;
-    size_t smem = (size_t)warps * kTilePx * (16 + 8 + 8 + 4 + 4);
+    size_t smem = (size_t)warps * kTilePx * (16 + 8 + 8 + 4 + (depthf ? 4 : 0));
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -35,16 +35,14 @@ struct PixState {
     bool done, live;
 };
 
+// Blend splat q into one pixel whose quadratic form m passed m <= m_cut.
 template <bool DEPTH>
-__device__ __forceinline__ void blend_one(PixState& s, float px, float py, const float4& A,
-                                          const float4& B, const SplatRec* rec, int j, int q,
-                                          float t_min, float amin, float amax, bool& hit) {
-    if (s.done) return;
-    float dx, dy;
-    float a = splat_alpha(px, py, A, B, amin, amax, dx, dy);
-    if (a < 0.f) return;
-    const float4 C = rec[j].c;
-    float w = __fmul_rn(a, s.T);
+__device__ __forceinline__ bool blend_one(PixState& s, float m, const float4& B, const float4& C,
+                                          int q, float t_min, float amin, float amax) {
+    float a = splat_falloff(m, B);
+    if (a < amin) return false;
+    a = fminf(a, amax);
+    const float w = __fmul_rn(a, s.T);
     s.c0 = __fmaf_rn(C.x, w, s.c0);
     s.c1 = __fmaf_rn(C.y, w, s.c1);
     s.c2 = __fmaf_rn(C.z, w, s.c2);
@@ -52,8 +50,8 @@ __device__ __forceinline__ void blend_one(PixState& s, float px, float py, const
     s.T = __fmul_rn(s.T, __fsub_rn(1.0f, a));
     s.last = q + 1;
     s.bm |= 1u << (q & 31);
-    hit = true;
     if (s.T < t_min) s.done = true;
+    return true;
 }
 
 template <bool DEPTH, bool CONTRIB>
@@ -123,11 +121,21 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
             const int jn = min(nb, j0 + 32);
             for (int j = j0; j < jn; ++j) {
                 const float4 A = s_rec[j].a, B = s_rec[j].b;
-                const int q = (int)b0 + j;
-                bool hit = false;
-                blend_one<DEPTH>(s0, px, py0, A, B, s_rec, j, q, t_min, amin, amax, hit);
-                blend_one<DEPTH>(s1, px, py1, A, B, s_rec, j, q, t_min, amin, amax, hit);
-                if (CONTRIB && hit) s_hit[j] = 1;
+                // the two pixels share a column: dx-only terms once
+                const float dx = __fsub_rn(px, A.x);
+                const float q0 = quad_dx0(A, dx), q1 = quad_dx1(A, dx);
+                const float m0 = quad_finish(q0, q1, B, __fsub_rn(py0, A.y));
+                const float m1 = quad_finish(q0, q1, B, __fsub_rn(py1, A.y));
+                const bool in0 = !s0.done && !(m0 > B.z);
+                const bool in1 = !s1.done && !(m1 > B.z);
+                if (in0 || in1) {
+                    const float4 C = s_rec[j].c;
+                    const int q = (int)b0 + j;
+                    bool hit = false;
+                    if (in0) hit |= blend_one<DEPTH>(s0, m0, B, C, q, t_min, amin, amax);
+                    if (in1) hit |= blend_one<DEPTH>(s1, m1, B, C, q, t_min, amin, amax);
+                    if (CONTRIB && hit) s_hit[j] = 1;
+                }
             }
         }
         if (CONTRIB) {

@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t n, float* pos, float4
 
 // ----------------------------------------------------------- chain+adam
 template <int NC, bool REST>
-__global__ void __launch_bounds__(256) chain_adam_kernel(
+__global__ void __launch_bounds__(256, REST ? 2 : 4) chain_adam_kernel(
     int64_t n, float* __restrict__ pos, float4* __restrict__ rot, float* __restrict__ ls,
     float* __restrict__ opl, float* __restrict__ shdc, float* __restrict__ shrest, CamC cam_v,
     const ss_camera* __restrict__ d_cam, int deg, float dilation, const float* __restrict__ g2d,

@@ -23,7 +23,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 // gathered by the blend kernels through the sorted pair list (48 B, one
 // 16-B-aligned struct so a gather is three LDG.128 from one 64-B window).
 struct __align__(16) SplatRec {
-    float4 a;  // mean2d.x, mean2d.y, conic[0], conic[1]
+    float4 a;  // mean2d.x, mean2d.y, conic[0], 2 * conic[1]
     float4 b;  // conic[2], sigma, m_cut, depth (camera-frame z)
     float4 c;  // r, g, b, unused
 };
@@ -35,36 +35,45 @@ struct __align__(16) SplatRec {
 // ------------------------------------------------------------------ alpha
 // _alpha (kernels.py:14-31): m = c0 dx^2 + 2 c1 dx dy + c2 dy^2; skip when
 // m > m_cut; a = sigma exp(-m/2); skip when a < alpha_min; clamp alpha_max.
-// Returns a < 0 for "skip".  Pixel coordinates are integers (api.py:108-115).
+// The forward applies the two skip tests around quad_* / splat_falloff; the
+// backward recomputes alpha of recorded-blended pairs with the same
+// operations.  Pixel coordinates are integers (api.py:108-115).
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 
-// Quadratic form m = c0 dx^2 + 2 c1 dx dy + c2 dy^2 with pinned rounding.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Quadratic form m = c0 dx^2 + 2 c1 dx dy + c2 dy^2 with pinned rounding,
+// as fma(c2 dy, dy, fma(2c1 dx, dy, (c0 dx) dx)); the record stores 2 c1
+// (exact) in A.w.  The forward evaluates two pixels of one column with the
+// dx-only terms shared; every evaluation uses exactly these operations.
+__device__ __forceinline__ float quad_dx0(const float4& A, float dx) {
+    return __fmul_rn(__fmul_rn(A.z, dx), dx);
+}
+__device__ __forceinline__ float quad_dx1(const float4& A, float dx) {
+    return __fmul_rn(A.w, dx);
+}
+__device__ __forceinline__ float quad_finish(float q0, float q1, const float4& B, float dy) {
+    return __fmaf_rn(__fmul_rn(B.x, dy), dy, __fmaf_rn(q1, dy, q0));
+}
 __device__ __forceinline__ float splat_power(float px, float py, const float4& A, const float4& B,
                                              float& dx, float& dy) {
     dx = __fsub_rn(px, A.x);
     dy = __fsub_rn(py, A.y);
-    return __fmaf_rn(__fmul_rn(A.z, dx), dx,
-                     __fmaf_rn(__fmul_rn(__fmul_rn(2.0f, A.w), dx), dy,
-                               __fmul_rn(__fmul_rn(B.x, dy), dy)));
+    return quad_finish(quad_dx0(A, dx), quad_dx1(A, dx), B, dy);
 }
 
 // sigma * exp(-m/2) with pinned rounding (MUFU.EX2, flush-to-zero: values
 // that small are far below alpha_min anyway).
 __device__ __forceinline__ float splat_falloff(float m, const float4& B) {
     return __fmul_rn(B.y, ex2_approx(__fmul_rn(m, -0.5f * kLog2e)));
-}
-
-__device__ __forceinline__ float splat_alpha(float px, float py, const float4& A, const float4& B,
-                                             float amin, float amax, float& dx, float& dy) {
-    float m = splat_power(px, py, A, B, dx, dy);
-    if (m > B.z) return -1.0f;
-    float a = splat_falloff(m, B);
-    if (a < amin) return -1.0f;
-    return fminf(a, amax);
 }
 
 // Alpha of a pair the forward already recorded as blended (same

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
                 bool act[3];
                 sh_color(d, sh_degree, dc, sh_rest + 45 * i, rgb, act);
                 fl = 1u | (act[0] ? 2u : 0u) | (act[1] ? 4u : 0u) | (act[2] ? 8u : 0u);
-                r.a = make_float4(mx, my, P.c / det, -P.b / det);
+                r.a = make_float4(mx, my, P.c / det, 2.0f * (-P.b / det));
                 r.b = make_float4(P.a / det, sg, mcut, P.t[2]);
                 r.c = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
                 auxv[0] = P.t[0];

@@ -233,7 +233,7 @@ class RenderOutput:
                 map_index=vis, t_cam=aux[:, 0:3] if aux is not None else None,
                 depth=rec[:, 7].copy(), mean2d=rec[:, 0:2].copy(),
                 cov2d=aux[:, 3:6] if aux is not None else None,
-                conic=np.stack([rec[:, 2], rec[:, 3], rec[:, 4]], 1), radius=aux[:, 6].copy()
+                conic=np.stack([rec[:, 2], 0.5 * rec[:, 3], rec[:, 4]], 1), radius=aux[:, 6].copy()
                 if aux is not None else None, sigma=rec[:, 5].copy(), rgb=rec[:, 8:11].copy(),
                 rgb_active=act.astype(bool), m_cut=rec[:, 6].copy(),
                 sh_degree=self.opts.sh_degree)
