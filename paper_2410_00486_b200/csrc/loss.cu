@@ -10,7 +10,7 @@
 // n >= 6 that fold is
 //     out[i] = gp(i) + [1<=i<=5] gp(-i) + [n-6<=i<=n-2] gp(2n-2-i),
 //     gp(u)  = sum_m w[m] g[u-5+m]   (g zero outside [0, n)).
-// Two tiled kernels, 32x8 output pixels per CTA, 5-pixel halo in shared
+// Two tiled kernels, 32x32 output pixels per CTA, 5-pixel halo in shared
 // memory, channels processed in turn:
 //   ssim_fwd : moments (x, y, x^2, y^2, xy), SSIM map and the three
 //              gradient maps dS/d(mu_x), dS/d(F x^2), dS/d(F xy), per-CTA
@@ -21,8 +21,10 @@
 
 namespace ss {
 
-constexpr int LTW = 32, LTH = 8, LR = 5;
-constexpr int LHW = LTW + 2 * LR, LHH = LTH + 2 * LR;  // 42 x 18
+constexpr int LR = 5;                 // half window
+constexpr int LT = 32;                // output tile side
+constexpr int LH = LT + 2 * LR;       // 42: halo side
+constexpr int LP = 44;                // padded row pitch (float4 rows)
 
 struct SsimWindow {
     float w[11];
@@ -35,75 +37,107 @@ __device__ __forceinline__ int reflect1(int i, int n) {
     return i;
 }
 
+// 11-tap correlation of 4 consecutive outputs from 14 register values.
+__device__ __forceinline__ void taps4(const float* v, const SsimWindow& win, float out[4]) {
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+        float a = 0.f;
+#pragma unroll
+        for (int m = 0; m < 11; ++m) a += win.w[m] * v[o + m];
+        out[o] = a;
+    }
+}
+
+// Tiles of 32x32 output pixels, one channel at a time; both separable
+// passes give every thread 4 consecutive outputs from one register window
+// (14 loads per 4 outputs instead of 11 per output).
 __global__ void __launch_bounds__(256) ssim_fwd_kernel(int H, int W, const float* __restrict__ x,
                                                        const float* __restrict__ y,
                                                        SsimWindow win, float* __restrict__ gmu,
                                                        float* __restrict__ gxx,
                                                        float* __restrict__ gxy,
                                                        double* __restrict__ partials) {
-    __shared__ float sx[LHH][LHW + 1], sy[LHH][LHW + 1];
-    __shared__ float sh[5][LHH][LTW];
+    __shared__ __align__(16) float sx[LH][LP];
+    __shared__ __align__(16) float sy[LH][LP];
+    __shared__ __align__(16) float sh[5][LH][LT];
     __shared__ double red[2][8];
     const int t = threadIdx.x;
-    const int tx = t & 31, ty = t >> 5;
-    const int x0 = blockIdx.x * LTW, y0 = blockIdx.y * LTH;
-    const int ox = x0 + tx, oy = y0 + ty;
-    const bool inside = ox < W && oy < H;
+    const int x0 = blockIdx.x * LT, y0 = blockIdx.y * LT;
     const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
     const float gs = 1.0f / (float)((double)H * W * 3);
     double l1 = 0.0, ssum = 0.0;
+    // vertical-pass task of this thread: column q, rows 4 rg .. 4 rg + 3
+    const int q = t & 31, rg = t >> 5;
     for (int c = 0; c < 3; ++c) {
-        for (int k = t; k < LHH * LHW; k += 256) {
-            int r = k / LHW, q = k % LHW;
-            int gy = reflect1(y0 - LR + r, H), gx = reflect1(x0 - LR + q, W);
-            size_t o = ((size_t)gy * W + gx) * 3 + c;
-            sx[r][q] = x[o];
-            sy[r][q] = y[o];
+        for (int k = t; k < LH * LH; k += 256) {
+            const int r = k / LH, cc = k - r * LH;
+            const int gy = reflect1(y0 - LR + r, H), gx = reflect1(x0 - LR + cc, W);
+            const size_t o = ((size_t)gy * W + gx) * 3 + c;
+            sx[r][cc] = x[o];
+            sy[r][cc] = y[o];
         }
         __syncthreads();
-        for (int k = t; k < LHH * LTW; k += 256) {
-            int r = k / LTW, q = k % LTW;
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+        // horizontal (axis 1): 42 rows x 8 groups of 4 columns
+        for (int task = t; task < LH * 8; task += 256) {
+            const int r = task >> 3, c0 = (task & 7) * 4;
+            float xv[16], yv[16];
 #pragma unroll
-            for (int m = 0; m < 11; ++m) {
-                float xv = sx[r][q + m], yv = sy[r][q + m], wm = win.w[m];
-                a0 += wm * xv;
-                a1 += wm * yv;
-                a2 += wm * (xv * xv);
-                a3 += wm * (yv * yv);
-                a4 += wm * (xv * yv);
+            for (int k = 0; k < 4; ++k) {
+                const float4 a = *reinterpret_cast<const float4*>(&sx[r][c0 + 4 * k]);
+                const float4 b = *reinterpret_cast<const float4*>(&sy[r][c0 + 4 * k]);
+                xv[4 * k] = a.x, xv[4 * k + 1] = a.y, xv[4 * k + 2] = a.z, xv[4 * k + 3] = a.w;
+                yv[4 * k] = b.x, yv[4 * k + 1] = b.y, yv[4 * k + 2] = b.z, yv[4 * k + 3] = b.w;
             }
-            sh[0][r][q] = a0;
-            sh[1][r][q] = a1;
-            sh[2][r][q] = a2;
-            sh[3][r][q] = a3;
-            sh[4][r][q] = a4;
+            float o0[4], o1[4], o2[4], o3[4], o4[4];
+            taps4(xv, win, o0);
+            taps4(yv, win, o1);
+            float pxx[14], pyy[14], pxy[14];
+#pragma unroll
+            for (int k = 0; k < 14; ++k) {
+                pxx[k] = xv[k] * xv[k];
+                pyy[k] = yv[k] * yv[k];
+                pxy[k] = xv[k] * yv[k];
+            }
+            taps4(pxx, win, o2);
+            taps4(pyy, win, o3);
+            taps4(pxy, win, o4);
+            *reinterpret_cast<float4*>(&sh[0][r][c0]) = make_float4(o0[0], o0[1], o0[2], o0[3]);
+            *reinterpret_cast<float4*>(&sh[1][r][c0]) = make_float4(o1[0], o1[1], o1[2], o1[3]);
+            *reinterpret_cast<float4*>(&sh[2][r][c0]) = make_float4(o2[0], o2[1], o2[2], o2[3]);
+            *reinterpret_cast<float4*>(&sh[3][r][c0]) = make_float4(o3[0], o3[1], o3[2], o3[3]);
+            *reinterpret_cast<float4*>(&sh[4][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
         }
         __syncthreads();
-        if (inside) {
-            float mx = 0.f, my = 0.f, fxx = 0.f, fyy = 0.f, fxy = 0.f;
+        // vertical (axis 0): column q, 4 consecutive rows
+        float mom[5][4];
 #pragma unroll
-            for (int m = 0; m < 11; ++m) {
-                float wm = win.w[m];
-                mx += wm * sh[0][ty + m][tx];
-                my += wm * sh[1][ty + m][tx];
-                fxx += wm * sh[2][ty + m][tx];
-                fyy += wm * sh[3][ty + m][tx];
-                fxy += wm * sh[4][ty + m][tx];
+        for (int k = 0; k < 5; ++k) {
+            float v[14];
+#pragma unroll
+            for (int i = 0; i < 14; ++i) v[i] = sh[k][4 * rg + i][q];
+            taps4(v, win, mom[k]);
+        }
+        const int ox = x0 + q;
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            const int oy = y0 + 4 * rg + o;
+            if (ox < W && oy < H) {
+                const float mx = mom[0][o], my = mom[1][o];
+                const float sxx = mom[2][o] - mx * mx, syy = mom[3][o] - my * my;
+                const float sxy = mom[4][o] - mx * my;
+                const float a1 = 2.f * mx * my + C1, a2 = 2.f * sxy + C2;
+                const float b1 = mx * mx + my * my + C1, b2 = sxx + syy + C2;
+                const float bb = b1 * b2;
+                const float ss = a1 * a2 / bb;
+                const float ga1 = gs * a2 / bb, ga2 = gs * a1 / bb;
+                const float gb1 = -gs * ss / b1, gb2 = -gs * ss / b2;
+                const size_t go = ((size_t)oy * W + ox) * 3 + c;
+                gmu[go] = 2.f * my * ga1 + 2.f * mx * gb1 - 2.f * mx * gb2 - my * 2.f * ga2;
+                gxx[go] = gb2;
+                gxy[go] = 2.f * ga2;
+                ssum += (double)ss;
+                l1 += (double)fabsf(sx[LR + 4 * rg + o][LR + q] - sy[LR + 4 * rg + o][LR + q]);
             }
-            float sxx = fxx - mx * mx, syy = fyy - my * my, sxy = fxy - mx * my;
-            float a1 = 2.f * mx * my + C1, a2 = 2.f * sxy + C2;
-            float b1 = mx * mx + my * my + C1, b2 = sxx + syy + C2;
-            float bb = b1 * b2;
-            float s = a1 * a2 / bb;
-            float ga1 = gs * a2 / bb, ga2 = gs * a1 / bb;
-            float gb1 = -gs * s / b1, gb2 = -gs * s / b2;
-            size_t o = ((size_t)oy * W + ox) * 3 + c;
-            gmu[o] = 2.f * my * ga1 + 2.f * mx * gb1 - 2.f * mx * gb2 - my * 2.f * ga2;
-            gxx[o] = gb2;
-            gxy[o] = 2.f * ga2;
-            ssum += (double)s;
-            l1 += (double)fabsf(sx[ty + LR][tx + LR] - sy[ty + LR][tx + LR]);
         }
         __syncthreads();
     }
@@ -120,25 +154,32 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int H, int W, const float
             a += red[0][k];
             b += red[1][k];
         }
-        size_t bid = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+        const size_t bid = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
         partials[2 * bid] = a;
         partials[2 * bid + 1] = b;
     }
 }
 
-// gp(u) over a zero-extended shared row/column: v(k) returns g at local k.
-template <typename V>
-__device__ __forceinline__ float fold_gather(int i, int n, int org, const SsimWindow& win, V v) {
-    // i: global index on this axis; org: global index of local 0
-    auto gp = [&](int u) {
-        float acc = 0.f;
+// gp(u) = sum_m w[m] g[u - 5 + m] over a zero-extended shared line; lc is
+// the local index of u - 5, `at(k)` reads local element k (0 <= k < LH).
+template <typename AT>
+__device__ __forceinline__ float gp_line(int lc, const SsimWindow& win, AT at) {
+    float a = 0.f;
 #pragma unroll
-        for (int m = 0; m < 11; ++m) acc += win.w[m] * v(u - LR + m - org);
-        return acc;
-    };
-    float r = gp(i);
-    if (i >= 1 && i <= LR) r += gp(-i);
-    if (i >= n - 6 && i <= n - 2) r += gp(2 * n - 2 - i);
+    for (int m = 0; m < 11; ++m) {
+        const int k = lc + m;
+        a += (k >= 0 && k < LH) ? win.w[m] * at(k) : 0.f;
+    }
+    return a;
+}
+
+// Mirror-fold extras of the adjoint for global index i on an axis of
+// length n whose local index 0 is global org - 5.
+template <typename AT>
+__device__ __forceinline__ float fold_extra(int i, int n, int org, const SsimWindow& win, AT at) {
+    float r = 0.f;
+    if (i >= 1 && i <= LR) r += gp_line(-i - org, win, at);
+    if (i >= n - 6 && i <= n - 2) r += gp_line(2 * n - 2 - i - org, win, at);
     return r;
 }
 
@@ -150,60 +191,94 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(int H, int W, const float
                                                        const float* __restrict__ gxy, float lam,
                                                        float* __restrict__ grad,
                                                        float4* __restrict__ pixgrad) {
-    __shared__ float sg[3][LHH][LHW + 1];
-    __shared__ float sh[3][LHH][LTW];
+    __shared__ __align__(16) float sg[3][LH][LP];
+    __shared__ __align__(16) float sh[3][LH][LT];
     const int t = threadIdx.x;
-    const int tx = t & 31, ty = t >> 5;
-    const int x0 = blockIdx.x * LTW, y0 = blockIdx.y * LTH;
-    const int ox = x0 + tx, oy = y0 + ty;
+    const int x0 = blockIdx.x * LT, y0 = blockIdx.y * LT;
     const float inv_n = 1.0f / (float)((double)H * W * 3);
-    float gsave[3] = {0.f, 0.f, 0.f}, gdot = 0.f;
+    const int q = t & 31, rg = t >> 5;
+    const int ox = x0 + q;
+    float gsave[4][3], gdot[4] = {0.f, 0.f, 0.f, 0.f};
+    const bool xborder = x0 <= LR || x0 + LT - 1 >= W - 6;
+    const bool yborder = y0 <= LR || y0 + LT - 1 >= H - 6;
     for (int c = 0; c < 3; ++c) {
-        for (int k = t; k < LHH * LHW; k += 256) {
-            int r = k / LHW, q = k % LHW;
-            int gy = y0 - LR + r, gx = x0 - LR + q;
-            bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-            size_t o = ((size_t)(in ? gy : 0) * W + (in ? gx : 0)) * 3 + c;
-            sg[0][r][q] = in ? gmu[o] : 0.f;
-            sg[1][r][q] = in ? gxx[o] : 0.f;
-            sg[2][r][q] = in ? gxy[o] : 0.f;
+        for (int k = t; k < LH * LH; k += 256) {
+            const int r = k / LH, cc = k - r * LH;
+            const int gy = y0 - LR + r, gx = x0 - LR + cc;
+            const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+            const size_t o = ((size_t)(in ? gy : 0) * W + (in ? gx : 0)) * 3 + c;
+            sg[0][r][cc] = in ? gmu[o] : 0.f;
+            sg[1][r][cc] = in ? gxx[o] : 0.f;
+            sg[2][r][cc] = in ? gxy[o] : 0.f;
         }
         __syncthreads();
         // axis 1 (columns) first, as losses.py:87-88
-        for (int k = t; k < LHH * LTW; k += 256) {
-            int r = k / LTW, q = k % LTW;
-            int j = x0 + q;
-            if (j >= W) continue;
+        for (int task = t; task < LH * 8; task += 256) {
+            const int r = task >> 3, c0 = (task & 7) * 4;
 #pragma unroll
             for (int f = 0; f < 3; ++f) {
-                sh[f][r][q] = fold_gather(j, W, x0 - LR, win, [&](int loc) {
-                    return (loc >= 0 && loc < LHW) ? sg[f][r][loc] : 0.f;
-                });
+                float v[16];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float4 a = *reinterpret_cast<const float4*>(&sg[f][r][c0 + 4 * k]);
+                    v[4 * k] = a.x, v[4 * k + 1] = a.y, v[4 * k + 2] = a.z, v[4 * k + 3] = a.w;
+                }
+                float o4[4];
+                taps4(v, win, o4);
+                if (xborder) {
+#pragma unroll
+                    for (int o = 0; o < 4; ++o) {
+                        const int j = x0 + c0 + o;
+                        o4[o] += fold_extra(j, W, x0, win, [&](int k) { return sg[f][r][k]; });
+                    }
+                }
+                *reinterpret_cast<float4*>(&sh[f][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
             }
         }
         __syncthreads();
-        if (ox < W && oy < H) {
-            float adj[3];
+        // axis 0 (rows): column q, 4 consecutive rows; combine
+        float adj[3][4];
 #pragma unroll
-            for (int f = 0; f < 3; ++f) {
-                adj[f] = fold_gather(oy, H, y0 - LR, win, [&](int loc) {
-                    return (loc >= 0 && loc < LHH) ? sh[f][loc][tx] : 0.f;
-                });
+        for (int f = 0; f < 3; ++f) {
+            float v[14];
+#pragma unroll
+            for (int i = 0; i < 14; ++i) v[i] = sh[f][4 * rg + i][q];
+            taps4(v, win, adj[f]);
+            if (yborder) {
+#pragma unroll
+                for (int o = 0; o < 4; ++o) {
+                    const int i = y0 + 4 * rg + o;
+                    adj[f][o] += fold_extra(i, H, y0, win, [&](int k) { return sh[f][k][q]; });
+                }
             }
-            size_t o = ((size_t)oy * W + ox) * 3 + c;
-            float xv = x[o], yv = y[o];
-            float d = xv - yv;
-            float sg0 = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);  // np.sign: sign(0) = 0
-            float gx = adj[0] + adj[1] * 2.f * xv + adj[2] * yv;
-            float gv = (1.0f - lam) * sg0 * inv_n - lam * gx;
-            grad[o] = gv;
-            gsave[c] = gv;
-            gdot += gv * xv;
+        }
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            const int oy = y0 + 4 * rg + o;
+            gsave[o][c] = 0.f;
+            if (ox < W && oy < H) {
+                const size_t go = ((size_t)oy * W + ox) * 3 + c;
+                const float xv = x[go], yv = y[go];
+                const float d = xv - yv;
+                const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);  // np.sign(0) = 0
+                const float gx = adj[0][o] + adj[1][o] * 2.f * xv + adj[2][o] * yv;
+                const float gv = (1.0f - lam) * sgn * inv_n - lam * gx;
+                grad[go] = gv;
+                gsave[o][c] = gv;
+                gdot[o] += gv * xv;
+            }
         }
         __syncthreads();
     }
-    if (pixgrad && ox < W && oy < H)
-        pixgrad[(size_t)oy * W + ox] = make_float4(gsave[0], gsave[1], gsave[2], gdot);
+    if (pixgrad && ox < W) {
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            const int oy = y0 + 4 * rg + o;
+            if (oy < H)
+                pixgrad[(size_t)oy * W + ox] =
+                    make_float4(gsave[o][0], gsave[o][1], gsave[o][2], gdot[o]);
+        }
+    }
 }
 
 // L1-only variant (lambda_ssim == 0): losses.py:147-153
@@ -268,7 +343,7 @@ static SsimWindow make_window() {
 
 size_t loss_workspace_bytes(int H, int W) {
     size_t maps = (size_t)H * W * 3 * sizeof(float) * 3;
-    size_t nb = (size_t)div_up(W, LTW) * div_up(H, LTH);
+    size_t nb = (size_t)div_up(W, LT) * div_up(H, LT);
     size_t nb2 = 1184;
     return maps + 2 * sizeof(double) * (nb > nb2 ? nb : nb2) + 512;
 }
@@ -290,7 +365,7 @@ cudaError_t launch_loss(int H, int W, const float* x, const float* y, float lam,
     }
     if (H < 6 || W < 6) return cudaErrorInvalidValue;
     SsimWindow win = make_window();
-    dim3 grid(div_up(W, LTW), div_up(H, LTH));
+    dim3 grid(div_up(W, LT), div_up(H, LT));
     ssim_fwd_kernel<<<grid, 256, 0, s>>>(H, W, x, y, win, gmu, gxx, gxy, partials);
     ssim_bwd_kernel<<<grid, 256, 0, s>>>(H, W, x, y, win, gmu, gxx, gxy, lam, grad,
                                          reinterpret_cast<float4*>(pixgrad));
