@@ -124,6 +124,16 @@ def algorithmic_bytes(n, m, p, hw, t, c, e, G=14):
     return st
 
 
+def ncu_traffic(kernel):
+    """dram read+write bytes per launch of `kernel` from the committed ncu
+    --set full capture summary (profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -234,12 +244,12 @@ def main():
         eng.enable_graph()  # the whole iteration is replayed as one CUDA graph
     my_cam, my_tgt = cams[rank % views], targets[rank % views]
 
-    def allreduce(flat):
-        dist.all_reduce(flat)
+    from paper_2410_00486_b200.distributed import ShardedMapper
+    sharded = ShardedMapper(eng, rank, world) if world > 1 else None
 
     def one_step():
-        if world > 1:
-            eng.multiview_step([my_cam], [my_tgt], allreduce=allreduce, add_reg=(rank == 0))
+        if sharded is not None:
+            sharded.step(cams, targets)  # one view per rank, one NCCL all-reduce
         else:
             eng.step(my_cam, my_tgt)
 
@@ -384,7 +394,7 @@ def main():
                        "l2": "256 MB buffer written between timed steps (outside the events)",
                        "parallelism": f"keyframe-sharded x{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
-                         "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                         "unit": "GB/s", "frac": ach / peak, "traffic": ncu_traffic(dom),
                          "algorithmic_bytes": per_kernel[dom], "avg_ms": stage_ms[dom],
                          "peak_source": peak_src},
             "iteration_roofline": {"algorithmic_MB": it_bytes / 1e6,
