@@ -127,11 +127,15 @@ __global__ void __launch_bounds__(256) rs_upsweep_kernel(const uint32_t* __restr
     __syncthreads();
     const uint32_t n = d_count ? min(*d_count, cap) : n_static;
     const uint32_t base = blockIdx.x * TILE;
+    uint32_t k[ITEMS];  // all loads in flight before the shared-memory atomics
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
         const uint32_t i = base + r * 256 + t;
-        if (i < n) atomicAdd(&h[w][(keys[i] >> shift) & 255u], 1u);
+        k[r] = i < n ? keys[i] : 0xffffffffu;
     }
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r)
+        if (base + r * 256 + t < n) atomicAdd(&h[w][(k[r] >> shift) & 255u], 1u);
     __syncthreads();
     uint32_t c = 0;
 #pragma unroll
@@ -193,12 +197,13 @@ __global__ void __launch_bounds__(256) rs_downsweep_kernel(
     const uint32_t nloc = min((uint32_t)TILE, n - base);
     const uint32_t gstart = block_excl_scan256(totals[t], s_warp);  // also syncs s_cnt
     s_base[t] = gstart + offsets[(size_t)t * nblk + blockIdx.x];
-    uint32_t key[ITEMS], rank[ITEMS];
+    uint32_t key[ITEMS], val[ITEMS], rank[ITEMS];
     const uint32_t wbase = w * WARP_ITEMS;
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
         const uint32_t li = wbase + r * 32 + l;
         key[r] = li < nloc ? keys_in[base + li] : 0u;
+        val[r] = li < nloc ? (vals_in ? vals_in[base + li] : base + li) : 0u;
     }
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
@@ -229,7 +234,7 @@ __global__ void __launch_bounds__(256) rs_downsweep_kernel(
             const uint32_t d = (key[r] >> shift) & 255u;
             const uint32_t lp = s_local[d] + s_cnt[w][d] + rank[r];
             s_keys[lp] = key[r];
-            s_vals[lp] = vals_in ? vals_in[base + li] : base + li;
+            s_vals[lp] = val[r];
         }
     }
     __syncthreads();

@@ -131,7 +131,9 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int H, int W, const float
                 const float ss = a1 * a2 / bb;
                 const float ga1 = gs * a2 / bb, ga2 = gs * a1 / bb;
                 const float gb1 = -gs * ss / b1, gb2 = -gs * ss / b2;
-                const size_t go = ((size_t)oy * W + ox) * 3 + c;
+                // gradient maps are workspace: planar per channel, so the
+                // adjoint kernel's halo loads are coalesced
+                const size_t go = ((size_t)c * H + oy) * W + ox;
                 gmu[go] = 2.f * my * ga1 + 2.f * mx * gb1 - 2.f * mx * gb2 - my * 2.f * ga2;
                 gxx[go] = gb2;
                 gxy[go] = 2.f * ga2;
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(int H, int W, const float
             const int r = k / LH, cc = k - r * LH;
             const int gy = y0 - LR + r, gx = x0 - LR + cc;
             const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-            const size_t o = ((size_t)(in ? gy : 0) * W + (in ? gx : 0)) * 3 + c;
+            const size_t o = ((size_t)c * H + (in ? gy : 0)) * W + (in ? gx : 0);
             sg[0][r][cc] = in ? gmu[o] : 0.f;
             sg[1][r][cc] = in ? gxx[o] : 0.f;
             sg[2][r][cc] = in ? gxy[o] : 0.f;
