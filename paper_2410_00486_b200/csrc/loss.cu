@@ -69,12 +69,28 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int H, int W, const float
     // vertical-pass task of this thread: column q, rows 4 rg .. 4 rg + 3
     const int q = t & 31, rg = t >> 5;
     for (int c = 0; c < 3; ++c) {
-        for (int k = t; k < LH * LH; k += 256) {
-            const int r = k / LH, cc = k - r * LH;
-            const int gy = reflect1(y0 - LR + r, H), gx = reflect1(x0 - LR + cc, W);
-            const size_t o = ((size_t)gy * W + gx) * 3 + c;
-            sx[r][cc] = x[o];
-            sy[r][cc] = y[o];
+        {
+            // halo: all 7 loads per thread in flight before the stores
+            constexpr int NL = (LH * LH + 255) / 256;
+            float vx[NL], vy[NL];
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+                const int k = t + 256 * i;
+                const int r = k / LH, cc = k - r * LH;
+                const int gy = reflect1(y0 - LR + r, H), gx = reflect1(x0 - LR + cc, W);
+                const size_t o = ((size_t)gy * W + gx) * 3 + c;
+                vx[i] = k < LH * LH ? x[o] : 0.f;
+                vy[i] = k < LH * LH ? y[o] : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+                const int k = t + 256 * i;
+                if (k < LH * LH) {
+                    const int r = k / LH, cc = k - r * LH;
+                    sx[r][cc] = vx[i];
+                    sy[r][cc] = vy[i];
+                }
+            }
         }
         __syncthreads();
         // horizontal (axis 1): 42 rows x 8 groups of 4 columns
@@ -204,14 +220,31 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(int H, int W, const float
     const bool xborder = x0 <= LR || x0 + LT - 1 >= W - 6;
     const bool yborder = y0 <= LR || y0 + LT - 1 >= H - 6;
     for (int c = 0; c < 3; ++c) {
-        for (int k = t; k < LH * LH; k += 256) {
-            const int r = k / LH, cc = k - r * LH;
-            const int gy = y0 - LR + r, gx = x0 - LR + cc;
-            const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
-            const size_t o = ((size_t)c * H + (in ? gy : 0)) * W + (in ? gx : 0);
-            sg[0][r][cc] = in ? gmu[o] : 0.f;
-            sg[1][r][cc] = in ? gxx[o] : 0.f;
-            sg[2][r][cc] = in ? gxy[o] : 0.f;
+        {
+            // halo (zero outside the image): all loads in flight before the stores
+            constexpr int NL = (LH * LH + 255) / 256;
+            float v0[NL], v1[NL], v2[NL];
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+                const int k = t + 256 * i;
+                const int r = k / LH, cc = k - r * LH;
+                const int gy = y0 - LR + r, gx = x0 - LR + cc;
+                const bool in = k < LH * LH && gy >= 0 && gy < H && gx >= 0 && gx < W;
+                const size_t o = ((size_t)c * H + (in ? gy : 0)) * W + (in ? gx : 0);
+                v0[i] = in ? gmu[o] : 0.f;
+                v1[i] = in ? gxx[o] : 0.f;
+                v2[i] = in ? gxy[o] : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+                const int k = t + 256 * i;
+                if (k < LH * LH) {
+                    const int r = k / LH, cc = k - r * LH;
+                    sg[0][r][cc] = v0[i];
+                    sg[1][r][cc] = v1[i];
+                    sg[2][r][cc] = v2[i];
+                }
+            }
         }
         __syncthreads();
         // axis 1 (columns) first, as losses.py:87-88
