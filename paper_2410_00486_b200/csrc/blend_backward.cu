@@ -30,8 +30,49 @@
 
 namespace ss {
 
+// Per-warp pixel list capacity: a tile's 256 pixels as 128 (even, odd) pairs.
+constexpr int kBwdWarps = 4;
+constexpr int kPairs = kTilePx / 2;
+
+// One (pixel, splat) term of the wavefront.  `bit` is the forward's blend
+// mask bit; a pair that was not blended gets a = 0, which leaves T and G
+// bit-exactly unchanged and contributes nothing, so both pixels of a step
+// run branch-free as two independent dependency chains.
 template <bool DEPTH>
-__global__ void __launch_bounds__(128) backward_splat_kernel(
+__device__ __forceinline__ void bwd_term(bool bit, float px, float py, const float4& pg, float gd,
+                                         const float4& A, const float4& B, const float4& C,
+                                         float amax, float& T, float& G, float& r0, float& r1,
+                                         float& r2, float& rz, float& s_da, float& s_dx,
+                                         float& s_dy, float& s_xx, float& s_xy, float& s_yy) {
+    float dx, dy;
+    float a = splat_alpha_blended(px, py, A, B, amax, dx, dy);
+    a = bit ? a : 0.f;
+    const float w = __fmul_rn(a, T);
+    float grgb = pg.x * C.x + pg.y * C.y + pg.z * C.z;
+    if (DEPTH) {
+        grgb += gd * B.w;
+        rz += w * gd;
+    }
+    const float Gafter = G + grgb * w;
+    r0 += w * pg.x;
+    r1 += w * pg.y;
+    r2 += w * pg.z;
+    // alpha-path gradient (kernels.py:342-364); zero when clamped or not blended
+    const float dal = T * grgb - (pg.w - Gafter) * rcp_approx(1.0f - a);
+    const float da = (bit && a != amax) ? dal * a : 0.f;
+    const float tx = da * dx, ty = da * dy;
+    s_da += da;
+    s_dx += tx;
+    s_dy += ty;
+    s_xx += tx * dx;
+    s_xy += tx * dy;
+    s_yy += ty * dy;
+    T = __fmul_rn(T, __fsub_rn(1.0f, a));
+    G = Gafter;
+}
+
+template <bool DEPTH>
+__global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
     int W, int H, int tiles_x, const uint32_t* __restrict__ tile_start,
     const uint32_t* __restrict__ ckpt_base, const int32_t* __restrict__ k_eff,
     const uint32_t* __restrict__ pairs, const SplatRec* __restrict__ rec, float amax,
@@ -42,18 +83,16 @@ __global__ void __launch_bounds__(128) backward_splat_kernel(
     const uint32_t* __restrict__ ckpt_mask, const uint2* __restrict__ work,
     const int64_t* __restrict__ work_count, int64_t work_cap, uint32_t* work_counter,
     float* __restrict__ g2d, uint8_t* __restrict__ contributed) {
-    extern __shared__ float4 smem[];
     constexpr int NC = DEPTH ? 10 : 9;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    // per-warp compacted pixel list (36-40 B per pixel): gradient side
-    // (g, g . image), state at the bucket start (T0, G0), coordinates, blend mask
-    char* sbase = reinterpret_cast<char*>(smem);
-    const size_t plane = (size_t)nw * kTilePx;
-    float4* sG = reinterpret_cast<float4*>(sbase) + wid * kTilePx;
-    float2* sS = reinterpret_cast<float2*>(sbase + plane * 16) + wid * kTilePx;
-    float2* sXY = reinterpret_cast<float2*>(sbase + plane * 24) + wid * kTilePx;
-    uint32_t* sM = reinterpret_cast<uint32_t*>(sbase + plane * 32) + wid * kTilePx;
-    float* sD = reinterpret_cast<float*>(sbase + plane * 36) + wid * kTilePx;
+    // per-warp compacted pixel list, list position q -> pair q/2, half q&1:
+    // gradient side (g, g . image), state at the bucket start (T0, G0),
+    // coordinates, blend mask, depth gradient
+    __shared__ float4 sGe[kBwdWarps][kPairs], sGo[kBwdWarps][kPairs];
+    __shared__ float4 sS[kBwdWarps][kPairs];   // (T0, G0) even, (T0, G0) odd
+    __shared__ float4 sXY[kBwdWarps][kPairs];  // (x, y) even, (x, y) odd
+    __shared__ uint2 sM[kBwdWarps][kPairs];
+    __shared__ float2 sD[DEPTH ? kBwdWarps : 1][DEPTH ? kPairs : 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t count = min(*work_count, work_cap);
 
     for (;;) {
@@ -103,76 +142,71 @@ __global__ void __launch_bounds__(128) backward_splat_kernel(
                 }
                 const float4 ck = ckpt[slot0 + p];
                 float G0 = pg.x * ck.y + pg.y * ck.z + pg.z * ck.w;
+                const int h = pos & 1, q = pos >> 1;
                 if (DEPTH) {
                     const float gd = grad_depth ? grad_depth[o] : 0.f;
                     if (!pixgrad) pg.w += gd * depth_img[o];
                     G0 += gd * ckpt_depth[slot0 + p];
-                    sD[pos] = gd;
+                    reinterpret_cast<float*>(&sD[wid][q])[h] = gd;
                 }
-                sG[pos] = pg;
-                sS[pos] = make_float2(ck.x, G0);
-                sM[pos] = mask;
-                sXY[pos] = make_float2((float)ix, (float)iy);
+                (h ? sGo : sGe)[wid][q] = pg;
+                reinterpret_cast<float2*>(&sS[wid][q])[h] = make_float2(ck.x, G0);
+                reinterpret_cast<uint32_t*>(&sM[wid][q])[h] = mask;
+                reinterpret_cast<float2*>(&sXY[wid][q])[h] = make_float2((float)ix, (float)iy);
             }
             nact += __popc(bal);
         }
+        if ((nact & 1) && lane == 0) {  // pad the last pair with an empty pixel
+            const int q = nact >> 1;
+            sGo[wid][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            sS[wid][q].z = sS[wid][q].w = 0.f;
+            sXY[wid][q].z = sXY[wid][q].w = 0.f;
+            sM[wid][q].y = 0u;
+            if (DEPTH) sD[wid][q].y = 0.f;
+        }
         __syncwarp();
-        // ---- diagonal wavefront over the active pixels
+        // ---- diagonal wavefront over the active pixel pairs
         // per-lane sums; the splat-constant factors (conic, 1/sigma, -1/2)
         // are applied once at the end:
         //   d mean  = (c0 S_dx + c1 S_dy, c1 S_dx + c2 S_dy),  S_d. = sum da d.
         //   d conic = -1/2 (S_dxdx, 2 S_dxdy, S_dydy),        d sigma = S_da / sigma
         float acc_rgb0 = 0.f, acc_rgb1 = 0.f, acc_rgb2 = 0.f, acc_z = 0.f;
         float s_da = 0.f, s_dx = 0.f, s_dy = 0.f, s_xx = 0.f, s_xy = 0.f, s_yy = 0.f;
-        float T = 0.f, G = 0.f;
-        bool blended = false;
-        const int steps = nact + 31;
+        float T0 = 0.f, G0 = 0.f, T1 = 0.f, G1 = 0.f;
+        uint32_t any = 0u;
+        const int npair = (nact + 1) >> 1;
+        const int steps = npair + 31;
 #pragma unroll 1
         for (int st = 0; st < steps; ++st) {
-            float Tin = __shfl_up_sync(0xffffffffu, T, 1);
-            float Gin = __shfl_up_sync(0xffffffffu, G, 1);
-            const int j = st - lane;
-            if ((unsigned)j >= (unsigned)nact) continue;
-            const uint32_t m = sM[j];
+            float Ta = __shfl_up_sync(0xffffffffu, T0, 1);
+            float Ga = __shfl_up_sync(0xffffffffu, G0, 1);
+            float Tb = __shfl_up_sync(0xffffffffu, T1, 1);
+            float Gb = __shfl_up_sync(0xffffffffu, G1, 1);
+            const int q = st - lane;
+            if ((unsigned)q >= (unsigned)npair) continue;
+            const uint2 m = sM[wid][q];
             if (lane == 0) {
-                const float2 s0 = sS[j];
-                Tin = s0.x;
-                Gin = s0.y;
+                const float4 s0 = sS[wid][q];
+                Ta = s0.x;
+                Ga = s0.y;
+                Tb = s0.z;
+                Gb = s0.w;
             }
-            T = Tin;
-            G = Gin;
-            if (!((m >> lane) & 1u)) continue;
-            // this (pixel, splat) pair was blended in the forward
-            blended = true;
-            const float2 xy = sXY[j];
-            const float4 pg = sG[j];
-            float dx, dy;
-            const float a = splat_alpha_blended(xy.x, xy.y, A, B, amax, dx, dy);
-            const float w = __fmul_rn(a, T);
-            float grgb = pg.x * C.x + pg.y * C.y + pg.z * C.z;
-            float gd = 0.f;
-            if (DEPTH) {
-                gd = sD[j];
-                grgb += gd * B.w;
-                acc_z += w * gd;
-            }
-            const float Gafter = G + grgb * w;
-            acc_rgb0 += w * pg.x;
-            acc_rgb1 += w * pg.y;
-            acc_rgb2 += w * pg.z;
-            if (a != amax) {  // alpha-path gradient (kernels.py:342-364); 1 - a > 0 here
-                const float dal = T * grgb - (pg.w - Gafter) * rcp_approx(1.0f - a);
-                const float da = dal * a;
-                const float tx = da * dx, ty = da * dy;
-                s_da += da;
-                s_dx += tx;
-                s_dy += ty;
-                s_xx += tx * dx;
-                s_xy += tx * dy;
-                s_yy += ty * dy;
-            }
-            T = __fmul_rn(T, __fsub_rn(1.0f, a));
-            G = Gafter;
+            T0 = Ta;
+            G0 = Ga;
+            T1 = Tb;
+            G1 = Gb;
+            const bool b0 = (m.x >> lane) & 1u, b1 = (m.y >> lane) & 1u;
+            if (!(b0 || b1)) continue;
+            any = 1u;
+            const float4 xy = sXY[wid][q];
+            const float4 pe = sGe[wid][q], po = sGo[wid][q];
+            float2 gd = make_float2(0.f, 0.f);
+            if (DEPTH) gd = sD[wid][q];
+            bwd_term<DEPTH>(b0, xy.x, xy.y, pe, gd.x, A, B, C, amax, T0, G0, acc_rgb0, acc_rgb1,
+                            acc_rgb2, acc_z, s_da, s_dx, s_dy, s_xx, s_xy, s_yy);
+            bwd_term<DEPTH>(b1, xy.z, xy.w, po, gd.y, A, B, C, amax, T1, G1, acc_rgb0, acc_rgb1,
+                            acc_rgb2, acc_z, s_da, s_dx, s_dy, s_xx, s_xy, s_yy);
         }
         const float c1 = 0.5f * A.w;
         float acc[NC];
@@ -191,7 +225,7 @@ __global__ void __launch_bounds__(128) backward_splat_kernel(
 #pragma unroll
             for (int q = 0; q < NC; ++q)
                 if (acc[q] != 0.f) atomicAdd(row + q, acc[q]);
-            if (contributed && blended) contributed[s] = 1;
+            if (contributed && any) contributed[s] = 1;
         }
         __syncwarp();
     }
@@ -213,15 +247,12 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
     e = cudaMemsetAsync(counter, 0, sizeof(uint32_t), s);
     if (e != cudaSuccess) return e;
     int tx = div_up(cam->width, kTile);
-    const int threads = 128, warps = threads / 32;
-    size_t smem = (size_t)warps * kTilePx * (16 + 8 + 8 + 4 + (depthf ? 4 : 0));
+    const int threads = 32 * kBwdWarps;
+    const size_t smem = 0;
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     auto go = [&](auto kern) -> cudaError_t {
-        cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)smem);
-        if (e2 != cudaSuccess) return e2;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
         if (per_sm < 1) per_sm = 1;
         kern<<<sms * per_sm, threads, smem, s>>>(
