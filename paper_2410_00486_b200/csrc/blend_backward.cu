@@ -30,20 +30,20 @@
 
 namespace ss {
 
-// Per-warp pixel list capacity: a tile's 256 pixels as 128 (even, odd) pairs.
-constexpr int kBwdWarps = 4;
-constexpr int kPairs = kTilePx / 2;
+constexpr int kBwdWarps = 2;
 
 // One (pixel, splat) term of the wavefront.  `bit` is the forward's blend
 // mask bit; a pair that was not blended gets a = 0, which leaves T and G
-// bit-exactly unchanged and contributes nothing, so both pixels of a step
-// run branch-free as two independent dependency chains.
+// bit-exactly unchanged and contributes nothing, so a lane's two terms run
+// branch-free.
+struct SplatAcc {
+    float r0, r1, r2, rz, s_da, s_dx, s_dy, s_xx, s_xy, s_yy;
+};
+
 template <bool DEPTH>
 __device__ __forceinline__ void bwd_term(bool bit, float px, float py, const float4& pg, float gd,
                                          const float4& A, const float4& B, const float4& C,
-                                         float amax, float& T, float& G, float& r0, float& r1,
-                                         float& r2, float& rz, float& s_da, float& s_dx,
-                                         float& s_dy, float& s_xx, float& s_xy, float& s_yy) {
+                                         float amax, float& T, float& G, SplatAcc& q) {
     float dx, dy;
     float a = splat_alpha_blended(px, py, A, B, amax, dx, dy);
     a = bit ? a : 0.f;
@@ -51,24 +51,46 @@ __device__ __forceinline__ void bwd_term(bool bit, float px, float py, const flo
     float grgb = pg.x * C.x + pg.y * C.y + pg.z * C.z;
     if (DEPTH) {
         grgb += gd * B.w;
-        rz += w * gd;
+        q.rz += w * gd;
     }
     const float Gafter = G + grgb * w;
-    r0 += w * pg.x;
-    r1 += w * pg.y;
-    r2 += w * pg.z;
-    // alpha-path gradient (kernels.py:342-364); zero when clamped or not blended
+    q.r0 += w * pg.x;
+    q.r1 += w * pg.y;
+    q.r2 += w * pg.z;
+    // alpha-path gradient (kernels.py:342-364); zero when clamped (and when
+    // not blended: a = 0)
     const float dal = T * grgb - (pg.w - Gafter) * rcp_approx(1.0f - a);
-    const float da = (bit && a != amax) ? dal * a : 0.f;
+    const float da = dal * (a != amax ? a : 0.f);
     const float tx = da * dx, ty = da * dy;
-    s_da += da;
-    s_dx += tx;
-    s_dy += ty;
-    s_xx += tx * dx;
-    s_xy += tx * dy;
-    s_yy += ty * dy;
+    q.s_da += da;
+    q.s_dx += tx;
+    q.s_dy += ty;
+    q.s_xx += tx * dx;
+    q.s_xy += tx * dy;
+    q.s_yy += ty * dy;
     T = __fmul_rn(T, __fsub_rn(1.0f, a));
     G = Gafter;
+}
+
+// Commit one splat's sums as its 9 (10) screen-space gradients.
+template <int NC>
+__device__ __forceinline__ void bwd_commit(const SplatAcc& q, const float4& A, const float4& B,
+                                           float* __restrict__ row) {
+    const float c1 = 0.5f * A.w;
+    float acc[NC];
+    acc[0] = q.r0;
+    acc[1] = q.r1;
+    acc[2] = q.r2;
+    acc[3] = A.z * q.s_dx + c1 * q.s_dy;
+    acc[4] = c1 * q.s_dx + B.x * q.s_dy;
+    acc[5] = -0.5f * q.s_xx;
+    acc[6] = -q.s_xy;
+    acc[7] = -0.5f * q.s_yy;
+    acc[8] = q.s_da / B.y;
+    if (NC == 10) acc[NC - 1] = q.rz;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+        if (acc[c] != 0.f) atomicAdd(row + c, acc[c]);
 }
 
 template <bool DEPTH>
@@ -84,15 +106,17 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
     const int64_t* __restrict__ work_count, int64_t work_cap, uint32_t* work_counter,
     float* __restrict__ g2d, uint8_t* __restrict__ contributed) {
     constexpr int NC = DEPTH ? 10 : 9;
-    // per-warp compacted pixel list, list position q -> pair q/2, half q&1:
-    // gradient side (g, g . image), state at the bucket start (T0, G0),
-    // coordinates, blend mask, depth gradient
-    __shared__ float4 sGe[kBwdWarps][kPairs], sGo[kBwdWarps][kPairs];
-    __shared__ float4 sS[kBwdWarps][kPairs];   // (T0, G0) even, (T0, G0) odd
-    __shared__ float4 sXY[kBwdWarps][kPairs];  // (x, y) even, (x, y) odd
-    __shared__ uint2 sM[kBwdWarps][kPairs];
-    __shared__ float2 sD[DEPTH ? kBwdWarps : 1][DEPTH ? kPairs : 1];
+    // per-warp compacted pixel list: gradient side (g, g . image), state at
+    // the unit start (T0, G0), coordinates, the two buckets' blend masks,
+    // depth gradient
+    __shared__ float4 sG[kBwdWarps][kTilePx];
+    __shared__ float2 sS[kBwdWarps][kTilePx];
+    __shared__ float2 sXY[kBwdWarps][kTilePx];
+    __shared__ uint2 sM[kBwdWarps][kTilePx];
+    __shared__ float sD[DEPTH ? kBwdWarps : 1][DEPTH ? kTilePx : 1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool hi = lane >= 16;            // lane's splats live in the second bucket
+    const int sh = (2 * lane) & 31;        // their bit pair in that bucket's mask
     const int64_t count = min(*work_count, work_cap);
 
     for (;;) {
@@ -101,24 +125,32 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
         item = __shfl_sync(0xffffffffu, item, 0);
         if ((int64_t)item >= count) break;
         const uint2 wk = work[item];
-        const int tile = (int)wk.x, b = (int)wk.y;
+        const int tile = (int)wk.x, u = (int)wk.y;
         const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
         const uint32_t start = tile_start[tile];
         const int ke = k_eff[tile];
-        const int kbase = b * kBucket;
-        const int k = kbase + lane;
-        uint32_t s = 0;
-        float4 A = make_float4(0.f, 0.f, 0.f, 0.f), B = make_float4(0.f, 1.f, -1.f, 0.f),
-               C = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (k < ke) {
-            s = pairs[start + k];
-            const SplatRec r = rec[s];
-            A = r.a;
-            B = r.b;
-            C = r.c;
+        const int kbase = u * kUnit;
+        const int k0 = kbase + 2 * lane, k1 = k0 + 1;
+        uint32_t s0 = 0, s1 = 0;
+        float4 A0 = make_float4(0.f, 0.f, 0.f, 0.f), B0 = make_float4(0.f, 1.f, -1.f, 0.f),
+               C0 = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 A1 = A0, B1 = B0, C1 = C0;
+        if (k0 < ke) {
+            s0 = pairs[start + k0];
+            const SplatRec r = rec[s0];
+            A0 = r.a;
+            B0 = r.b;
+            C0 = r.c;
         }
-        // ---- compact the pixels that blended any splat of this bucket
-        const size_t slot0 = (size_t)(ckpt_base[tile] + b) * kTilePx;
+        if (k1 < ke) {
+            s1 = pairs[start + k1];
+            const SplatRec r = rec[s1];
+            A1 = r.a;
+            B1 = r.b;
+            C1 = r.c;
+        }
+        // ---- compact the pixels that blended any splat of this unit
+        const size_t slot0 = (size_t)(ckpt_base[tile] + 2 * u) * kTilePx;
         int nact = 0;
 #pragma unroll 1
         for (int c = 0; c < kTilePx / 32; ++c) {
@@ -127,9 +159,12 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
             const bool inside = ix < W && iy < H;
             const size_t o = (size_t)iy * W + ix;
             const int nc = inside ? n_contrib[o] : 0;
-            const uint32_t mask = nc > kbase ? ckpt_mask[slot0 + p] : 0u;
-            const unsigned bal = __ballot_sync(0xffffffffu, mask != 0u);
-            if (mask) {
+            // a bucket's mask exists for pixels still blending at its start
+            const uint32_t m0 = nc > kbase ? ckpt_mask[slot0 + p] : 0u;
+            const uint32_t m1 = nc > kbase + kBucket ? ckpt_mask[slot0 + kTilePx + p] : 0u;
+            const bool act = (m0 | m1) != 0u;
+            const unsigned bal = __ballot_sync(0xffffffffu, act);
+            if (act) {
                 const int pos = nact + __popc(bal & lanemask_lt());
                 float4 pg;
                 if (pixgrad) {
@@ -142,90 +177,58 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
                 }
                 const float4 ck = ckpt[slot0 + p];
                 float G0 = pg.x * ck.y + pg.y * ck.z + pg.z * ck.w;
-                const int h = pos & 1, q = pos >> 1;
                 if (DEPTH) {
                     const float gd = grad_depth ? grad_depth[o] : 0.f;
                     if (!pixgrad) pg.w += gd * depth_img[o];
                     G0 += gd * ckpt_depth[slot0 + p];
-                    reinterpret_cast<float*>(&sD[wid][q])[h] = gd;
+                    sD[wid][pos] = gd;
                 }
-                (h ? sGo : sGe)[wid][q] = pg;
-                reinterpret_cast<float2*>(&sS[wid][q])[h] = make_float2(ck.x, G0);
-                reinterpret_cast<uint32_t*>(&sM[wid][q])[h] = mask;
-                reinterpret_cast<float2*>(&sXY[wid][q])[h] = make_float2((float)ix, (float)iy);
+                sG[wid][pos] = pg;
+                sS[wid][pos] = make_float2(ck.x, G0);
+                sM[wid][pos] = make_uint2(m0, m1);
+                sXY[wid][pos] = make_float2((float)ix, (float)iy);
             }
             nact += __popc(bal);
         }
-        if ((nact & 1) && lane == 0) {  // pad the last pair with an empty pixel
-            const int q = nact >> 1;
-            sGo[wid][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-            sS[wid][q].z = sS[wid][q].w = 0.f;
-            sXY[wid][q].z = sXY[wid][q].w = 0.f;
-            sM[wid][q].y = 0u;
-            if (DEPTH) sD[wid][q].y = 0.f;
-        }
         __syncwarp();
-        // ---- diagonal wavefront over the active pixel pairs
-        // per-lane sums; the splat-constant factors (conic, 1/sigma, -1/2)
+        // ---- diagonal wavefront over the active pixels; lane i applies
+        // list positions 2i and 2i+1 to each pixel in turn.
+        // Per-splat sums; the splat-constant factors (conic, 1/sigma, -1/2)
         // are applied once at the end:
         //   d mean  = (c0 S_dx + c1 S_dy, c1 S_dx + c2 S_dy),  S_d. = sum da d.
         //   d conic = -1/2 (S_dxdx, 2 S_dxdy, S_dydy),        d sigma = S_da / sigma
-        float acc_rgb0 = 0.f, acc_rgb1 = 0.f, acc_rgb2 = 0.f, acc_z = 0.f;
-        float s_da = 0.f, s_dx = 0.f, s_dy = 0.f, s_xx = 0.f, s_xy = 0.f, s_yy = 0.f;
-        float T0 = 0.f, G0 = 0.f, T1 = 0.f, G1 = 0.f;
-        uint32_t any = 0u;
-        const int npair = (nact + 1) >> 1;
-        const int steps = npair + 31;
+        SplatAcc q0 = {}, q1 = {};
+        float T = 0.f, G = 0.f;
+        uint32_t seen = 0u;
+        const int steps = nact + 31;
 #pragma unroll 1
         for (int st = 0; st < steps; ++st) {
-            float Ta = __shfl_up_sync(0xffffffffu, T0, 1);
-            float Ga = __shfl_up_sync(0xffffffffu, G0, 1);
-            float Tb = __shfl_up_sync(0xffffffffu, T1, 1);
-            float Gb = __shfl_up_sync(0xffffffffu, G1, 1);
-            const int q = st - lane;
-            if ((unsigned)q >= (unsigned)npair) continue;
-            const uint2 m = sM[wid][q];
+            T = __shfl_up_sync(0xffffffffu, T, 1);
+            G = __shfl_up_sync(0xffffffffu, G, 1);
+            const int j = st - lane;
+            if ((unsigned)j >= (unsigned)nact) continue;
+            const uint2 m = sM[wid][j];
             if (lane == 0) {
-                const float4 s0 = sS[wid][q];
-                Ta = s0.x;
-                Ga = s0.y;
-                Tb = s0.z;
-                Gb = s0.w;
+                const float2 s = sS[wid][j];
+                T = s.x;
+                G = s.y;
             }
-            T0 = Ta;
-            G0 = Ga;
-            T1 = Tb;
-            G1 = Gb;
-            const bool b0 = (m.x >> lane) & 1u, b1 = (m.y >> lane) & 1u;
-            if (!(b0 || b1)) continue;
-            any = 1u;
-            const float4 xy = sXY[wid][q];
-            const float4 pe = sGe[wid][q], po = sGo[wid][q];
-            float2 gd = make_float2(0.f, 0.f);
-            if (DEPTH) gd = sD[wid][q];
-            bwd_term<DEPTH>(b0, xy.x, xy.y, pe, gd.x, A, B, C, amax, T0, G0, acc_rgb0, acc_rgb1,
-                            acc_rgb2, acc_z, s_da, s_dx, s_dy, s_xx, s_xy, s_yy);
-            bwd_term<DEPTH>(b1, xy.z, xy.w, po, gd.y, A, B, C, amax, T1, G1, acc_rgb0, acc_rgb1,
-                            acc_rgb2, acc_z, s_da, s_dx, s_dy, s_xx, s_xy, s_yy);
+            const uint32_t bits = ((hi ? m.y : m.x) >> sh) & 3u;
+            if (bits == 0u) continue;
+            seen |= bits;
+            const float2 xy = sXY[wid][j];
+            const float4 pg = sG[wid][j];
+            const float gd = DEPTH ? sD[wid][j] : 0.f;
+            bwd_term<DEPTH>(bits & 1u, xy.x, xy.y, pg, gd, A0, B0, C0, amax, T, G, q0);
+            bwd_term<DEPTH>(bits & 2u, xy.x, xy.y, pg, gd, A1, B1, C1, amax, T, G, q1);
         }
-        const float c1 = 0.5f * A.w;
-        float acc[NC];
-        acc[0] = acc_rgb0;
-        acc[1] = acc_rgb1;
-        acc[2] = acc_rgb2;
-        acc[3] = A.z * s_dx + c1 * s_dy;
-        acc[4] = c1 * s_dx + B.x * s_dy;
-        acc[5] = -0.5f * s_xx;
-        acc[6] = -s_xy;
-        acc[7] = -0.5f * s_yy;
-        acc[8] = s_da / B.y;
-        if (DEPTH) acc[NC - 1] = acc_z;
-        if (k < ke) {
-            float* row = g2d + (size_t)s * NC;
-#pragma unroll
-            for (int q = 0; q < NC; ++q)
-                if (acc[q] != 0.f) atomicAdd(row + q, acc[q]);
-            if (contributed && any) contributed[s] = 1;
+        if (k0 < ke) {
+            bwd_commit<NC>(q0, A0, B0, g2d + (size_t)s0 * NC);
+            if (contributed && (seen & 1u)) contributed[s0] = 1;
+        }
+        if (k1 < ke) {
+            bwd_commit<NC>(q1, A1, B1, g2d + (size_t)s1 * NC);
+            if (contributed && (seen & 2u)) contributed[s1] = 1;
         }
         __syncwarp();
     }

@@ -23,7 +23,8 @@
 // pairs (identical arithmetic, so identical decisions) and skips the rest.
 // Extension A15 (builder-defined): D = sum z a T in a 4th accumulator.
 // The CTA also emits k_eff (kernels.py:86-87,109) and appends its
-// ceil(k_eff/32) (tile, bucket) units to the splat-wise backward work list.
+// ceil(k_eff/64) (tile, unit) entries to the splat-wise backward work list
+// (a unit = two checkpoint buckets, one warp, two list positions per lane).
 #include "common.cuh"
 
 namespace ss {
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
     __syncthreads();
     const int kmax = max(max(s_kmax[0], s_kmax[1]), max(s_kmax[2], s_kmax[3]));
     if (t == 0) k_eff[tile] = kmax;
-    const int nbk = (kmax + kBucket - 1) / kBucket;
+    const int nbk = (kmax + kUnit - 1) / kUnit;  // backward units of 64 list positions
     if (nbk > 0 && work) {
         if (t == 0)
             s_wbase = atomicAdd(reinterpret_cast<unsigned long long*>(bucket_count),

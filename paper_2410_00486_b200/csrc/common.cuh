@@ -17,6 +17,7 @@ namespace ss {
 constexpr int kTile = 16;                 // RasterOpts.tile_size (api.py:41)
 constexpr int kTilePx = kTile * kTile;    // 256 pixels = 256 threads per tile CTA
 constexpr int kBucket = 32;               // RasterOpts.bucket_size (api.py:42) = warp width
+constexpr int kUnit = 2 * kBucket;        // list positions per backward work unit (2 per lane)
 constexpr float kLog2e = 1.4426950408889634f;
 
 // Per-Gaussian screen-space record written by the preprocess kernel and
