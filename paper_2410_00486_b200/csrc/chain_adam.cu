@@ -60,9 +60,25 @@ struct GaussGrad {
     float n2d;
 };
 
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// The chain and Adam math runs on MUFU reciprocals / square roots (relative
+// error ~1e-7, far inside the 1e-3 parity tolerance on gradients and
+// post-Adam parameters): the IEEE divide/sqrt sequences dominated the
+// fused kernel's instruction count.
 __device__ __forceinline__ float sigm(float x) {
     float e = expf(-fabsf(x));
-    return x >= 0.f ? 1.f / (1.f + e) : e / (1.f + e);
+    float r = rcp_approx(1.f + e);
+    return x >= 0.f ? r : e * r;
 }
 
 // Chain one visible Gaussian.  g: screen-space row (9 or 10 values).
@@ -78,8 +94,8 @@ __device__ __forceinline__ void chain_one(const float p[3], float4 q4, const flo
 #pragma unroll
     for (int i = 0; i < 3; ++i)
         t[i] = p[0] * cam.R[3 * i] + p[1] * cam.R[3 * i + 1] + p[2] * cam.R[3 * i + 2] + cam.t[i];
-    float qn = sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
-    float qh[4] = {q4.x / qn, q4.y / qn, q4.z / qn, q4.w / qn};
+    const float rqn = rsqrt_approx(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
+    float qh[4] = {q4.x * rqn, q4.y * rqn, q4.z * rqn, q4.w * rqn};
     float R[9];
     quat_to_rot(qh, R);
     float s2[3] = {expf(2.f * l[0]), expf(2.f * l[1]), expf(2.f * l[2])};
@@ -97,7 +113,7 @@ __device__ __forceinline__ void chain_one(const float p[3], float4 q4, const flo
             covc[3 * i + k] = M[3 * i] * s2[0] * M[3 * k] + M[3 * i + 1] * s2[1] * M[3 * k + 1] +
                               M[3 * i + 2] * s2[2] * M[3 * k + 2];
     const float fx = cam.fx, fy = cam.fy;
-    float iz = 1.f / t[2], iz2 = iz * iz;
+    float iz = rcp_approx(t[2]), iz2 = iz * iz;
     float J[6] = {fx * iz, 0.f, -fx * t[0] * iz2, 0.f, fy * iz, -fy * t[1] * iz2};
     float JC[6];
 #pragma unroll
@@ -109,7 +125,8 @@ __device__ __forceinline__ void chain_one(const float p[3], float4 q4, const flo
     float b = JC[0] * J[3] + JC[1] * J[4] + JC[2] * J[5];
     float c = JC[3] * J[3] + JC[4] * J[4] + JC[5] * J[5] + dilation;
     float det = a * c - b * b;
-    float Q00 = c / det, Q01 = -b / det, Q11 = a / det;
+    const float idet = rcp_approx(det);
+    float Q00 = c * idet, Q01 = -b * idet, Q11 = a * idet;
 
     // ---- opacity (projection.py:217-218)
     float sg = sigm(opl);
@@ -180,7 +197,7 @@ __device__ __forceinline__ void chain_one(const float p[3], float4 q4, const flo
                    dR[5] * y + dR[6] * x + dR[7] * y);
     float dot = qh[0] * gq[0] + qh[1] * gq[1] + qh[2] * gq[2] + qh[3] * gq[3];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) o.rot[k] = (gq[k] - qh[k] * dot) / qn;
+    for (int k = 0; k < 4; ++k) o.rot[k] = (gq[k] - qh[k] * dot) * rqn;
     // ---- position through mean2d and J (projection.py:253-265)
     float gm0 = g[3], gm1 = g[4];
     float gt0 = (fx * iz) * gm0 - dJ[2] * fx * iz2;
@@ -193,8 +210,9 @@ __device__ __forceinline__ void chain_one(const float p[3], float4 q4, const flo
     for (int k = 0; k < 3; ++k) o.pos[k] = gt0 * cam.R[k] + gt1 * cam.R[3 + k] + gt2 * cam.R[6 + k];
     // ---- colour (projection.py:267-277)
     float u[3] = {p[0] - cam.c[0], p[1] - cam.c[1], p[2] - cam.c[2]};
-    float vl = fmaxf(sqrtf(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]), 1e-12f);
-    float d[3] = {u[0] / vl, u[1] / vl, u[2] / vl};
+    // 1 / max(|u|, 1e-12)
+    const float ivl = rsqrt_approx(fmaxf(u[0] * u[0] + u[1] * u[1] + u[2] * u[2], 1e-24f));
+    float d[3] = {u[0] * ivl, u[1] * ivl, u[2] * ivl};
     float grgb[3] = {(flags & 2) ? g[0] : 0.f, (flags & 4) ? g[1] : 0.f, (flags & 8) ? g[2] : 0.f};
     float bs[16];
     sh_basis16(d, deg, bs);
@@ -225,7 +243,7 @@ __device__ __forceinline__ void chain_one(const float p[3], float4 q4, const flo
         sh_dir_grad(d, deg, coef, gdir);
         float vd = d[0] * gdir[0] + d[1] * gdir[1] + d[2] * gdir[2];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) o.pos[k] += (gdir[k] - d[k] * vd) / vl;
+        for (int k = 0; k < 3; ++k) o.pos[k] += (gdir[k] - d[k] * vd) * ivl;
     } else if (rest_grad) {
         for (int k = 0; k < 45; ++k) rest_grad[k] = 0.f;
     }
@@ -339,6 +357,7 @@ __global__ void apply_stat_planes_kernel(int64_t n, ss_param_grads G, float* gra
 struct AdamHP {
     float lr[6];  // position, rotation, log_scale, opacity, sh_dc, sh_rest
     float b1, b2, eps, bc1, bc2;
+    float ibc1, ibc2;  // 1 / bias corrections
 };
 
 __device__ __forceinline__ void load_hp(const ss_adam_hparams* __restrict__ h, AdamHP& hp) {
@@ -353,13 +372,15 @@ __device__ __forceinline__ void load_hp(const ss_adam_hparams* __restrict__ h, A
     hp.eps = h->eps;
     hp.bc1 = h->bias1;
     hp.bc2 = h->bias2;
+    hp.ibc1 = 1.f / hp.bc1;
+    hp.ibc2 = 1.f / hp.bc2;
 }
 
 __device__ __forceinline__ float adam_elem(float& p, float g, float& m, float& v, float lr,
                                            const AdamHP& hp) {
     m = m * hp.b1 + (1.f - hp.b1) * g;
     v = v * hp.b2 + (1.f - hp.b2) * g * g;
-    float step = lr * (m / hp.bc1) / (sqrtf(v / hp.bc2) + hp.eps);
+    float step = lr * (m * hp.ibc1) * rcp_approx(sqrt_approx(v * hp.ibc2) + hp.eps);
     step = fminf(fmaxf(step, -lr), lr);
     p -= step;
     return step;
@@ -389,12 +410,13 @@ __device__ __forceinline__ void adam_gaussian(int64_t i, const GaussGrad& o, con
     adam_elem(q.z, o.rot[2], mq.z, vq.z, hp.lr[1], hp);
     adam_elem(q.w, o.rot[3], mq.w, vq.w, hp.lr[1], hp);
     // normalize_rotations (core.py:225-229)
-    float nn = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
-    if (nn == 0.f) report_first(&st->first_zero_quat, i);
-    q.x /= nn;
-    q.y /= nn;
-    q.z /= nn;
-    q.w /= nn;
+    const float nn2 = q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w;
+    if (nn2 == 0.f) report_first(&st->first_zero_quat, i);
+    const float rn = rsqrt_approx(nn2);
+    q.x *= rn;
+    q.y *= rn;
+    q.z *= rn;
+    q.w *= rn;
     rot[i] = q;
     reinterpret_cast<float4*>(M.d_rotation)[i] = mq;
     reinterpret_cast<float4*>(V.d_rotation)[i] = vq;
@@ -523,6 +545,8 @@ static AdamHP make_hp(const ss_adam_hparams* h) {
     hp.eps = h->eps;
     hp.bc1 = h->bias1;
     hp.bc2 = h->bias2;
+    hp.ibc1 = 1.f / hp.bc1;
+    hp.ibc2 = 1.f / hp.bc2;
     return hp;
 }
 
