@@ -51,7 +51,7 @@ __device__ __forceinline__ void taps4(const float* v, const SsimWindow& win, flo
 // Tiles of 32x32 output pixels, one channel at a time; both separable
 // passes give every thread 4 consecutive outputs from one register window
 // (14 loads per 4 outputs instead of 11 per output).
-__global__ void __launch_bounds__(256) ssim_fwd_kernel(int H, int W, const float* __restrict__ x,
+__global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const float* __restrict__ x,
                                                        const float* __restrict__ y,
                                                        SsimWindow win, float* __restrict__ gmu,
                                                        float* __restrict__ gxx,
@@ -104,23 +104,23 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int H, int W, const float
                 xv[4 * k] = a.x, xv[4 * k + 1] = a.y, xv[4 * k + 2] = a.z, xv[4 * k + 3] = a.w;
                 yv[4 * k] = b.x, yv[4 * k + 1] = b.y, yv[4 * k + 2] = b.z, yv[4 * k + 3] = b.w;
             }
-            float o0[4], o1[4], o2[4], o3[4], o4[4];
-            taps4(xv, win, o0);
-            taps4(yv, win, o1);
-            float pxx[14], pyy[14], pxy[14];
+            // one quantity at a time (x, y, x^2, y^2, xy), stored before the next
+            float o4[4], pv[14];
+            taps4(xv, win, o4);
+            *reinterpret_cast<float4*>(&sh[0][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+            taps4(yv, win, o4);
+            *reinterpret_cast<float4*>(&sh[1][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
 #pragma unroll
-            for (int k = 0; k < 14; ++k) {
-                pxx[k] = xv[k] * xv[k];
-                pyy[k] = yv[k] * yv[k];
-                pxy[k] = xv[k] * yv[k];
-            }
-            taps4(pxx, win, o2);
-            taps4(pyy, win, o3);
-            taps4(pxy, win, o4);
-            *reinterpret_cast<float4*>(&sh[0][r][c0]) = make_float4(o0[0], o0[1], o0[2], o0[3]);
-            *reinterpret_cast<float4*>(&sh[1][r][c0]) = make_float4(o1[0], o1[1], o1[2], o1[3]);
-            *reinterpret_cast<float4*>(&sh[2][r][c0]) = make_float4(o2[0], o2[1], o2[2], o2[3]);
-            *reinterpret_cast<float4*>(&sh[3][r][c0]) = make_float4(o3[0], o3[1], o3[2], o3[3]);
+            for (int k = 0; k < 14; ++k) pv[k] = xv[k] * xv[k];
+            taps4(pv, win, o4);
+            *reinterpret_cast<float4*>(&sh[2][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+#pragma unroll
+            for (int k = 0; k < 14; ++k) pv[k] = yv[k] * yv[k];
+            taps4(pv, win, o4);
+            *reinterpret_cast<float4*>(&sh[3][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+#pragma unroll
+            for (int k = 0; k < 14; ++k) pv[k] = xv[k] * yv[k];
+            taps4(pv, win, o4);
             *reinterpret_cast<float4*>(&sh[4][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
         }
         __syncthreads();
@@ -143,10 +143,10 @@ __global__ void __launch_bounds__(256) ssim_fwd_kernel(int H, int W, const float
                 const float sxy = mom[4][o] - mx * my;
                 const float a1 = 2.f * mx * my + C1, a2 = 2.f * sxy + C2;
                 const float b1 = mx * mx + my * my + C1, b2 = sxx + syy + C2;
-                const float bb = b1 * b2;
-                const float ss = a1 * a2 / bb;
-                const float ga1 = gs * a2 / bb, ga2 = gs * a1 / bb;
-                const float gb1 = -gs * ss / b1, gb2 = -gs * ss / b2;
+                const float ibb = rcp_approx(b1 * b2);  // 1/b1 = b2/bb, 1/b2 = b1/bb
+                const float ss = a1 * a2 * ibb;
+                const float ga1 = gs * a2 * ibb, ga2 = gs * a1 * ibb;
+                const float gb1 = -gs * ss * (b2 * ibb), gb2 = -gs * ss * (b1 * ibb);
                 // gradient maps are workspace: planar per channel, so the
                 // adjoint kernel's halo loads are coalesced
                 const size_t go = ((size_t)c * H + oy) * W + ox;
@@ -201,7 +201,7 @@ __device__ __forceinline__ float fold_extra(int i, int n, int org, const SsimWin
     return r;
 }
 
-__global__ void __launch_bounds__(256) ssim_bwd_kernel(int H, int W, const float* __restrict__ x,
+__global__ void __launch_bounds__(256, 3) ssim_bwd_kernel(int H, int W, const float* __restrict__ x,
                                                        const float* __restrict__ y,
                                                        SsimWindow win,
                                                        const float* __restrict__ gmu,
@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(int H, int W, const float
     const float inv_n = 1.0f / (float)((double)H * W * 3);
     const int q = t & 31, rg = t >> 5;
     const int ox = x0 + q;
-    float gsave[4][3], gdot[4] = {0.f, 0.f, 0.f, 0.f};
+    float gdot[4] = {0.f, 0.f, 0.f, 0.f};
+    float* pg = reinterpret_cast<float*>(pixgrad);
     const bool xborder = x0 <= LR || x0 + LT - 1 >= W - 6;
     const bool yborder = y0 <= LR || y0 + LT - 1 >= H - 6;
     for (int c = 0; c < 3; ++c) {
@@ -290,7 +291,6 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(int H, int W, const float
 #pragma unroll
         for (int o = 0; o < 4; ++o) {
             const int oy = y0 + 4 * rg + o;
-            gsave[o][c] = 0.f;
             if (ox < W && oy < H) {
                 const size_t go = ((size_t)oy * W + ox) * 3 + c;
                 const float xv = x[go], yv = y[go];
@@ -299,19 +299,17 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(int H, int W, const float
                 const float gx = adj[0][o] + adj[1][o] * 2.f * xv + adj[2][o] * yv;
                 const float gv = (1.0f - lam) * sgn * inv_n - lam * gx;
                 grad[go] = gv;
-                gsave[o][c] = gv;
+                if (pg) pg[4 * ((size_t)oy * W + ox) + c] = gv;
                 gdot[o] += gv * xv;
             }
         }
         __syncthreads();
     }
-    if (pixgrad && ox < W) {
+    if (pg && ox < W) {
 #pragma unroll
         for (int o = 0; o < 4; ++o) {
             const int oy = y0 + 4 * rg + o;
-            if (oy < H)
-                pixgrad[(size_t)oy * W + ox] =
-                    make_float4(gsave[o][0], gsave[o][1], gsave[o][2], gdot[o]);
+            if (oy < H) pg[4 * ((size_t)oy * W + ox) + 3] = gdot[o];
         }
     }
 }
