@@ -59,7 +59,8 @@ __device__ __forceinline__ void bwd_term(bool bit, float px, float py, const flo
     q.r2 += w * pg.z;
     // alpha-path gradient (kernels.py:342-364); zero when clamped (and when
     // not blended: a = 0)
-    const float dal = T * grgb - (pg.w - Gafter) * rcp_approx(1.0f - a);
+    const float om = __fsub_rn(1.0f, a);
+    const float dal = T * grgb - (pg.w - Gafter) * rcp_approx(om);
     const float da = dal * (a != amax ? a : 0.f);
     const float tx = da * dx, ty = da * dy;
     q.s_da += da;
@@ -68,7 +69,7 @@ __device__ __forceinline__ void bwd_term(bool bit, float px, float py, const flo
     q.s_xx += tx * dx;
     q.s_xy += tx * dy;
     q.s_yy += ty * dy;
-    T = __fmul_rn(T, __fsub_rn(1.0f, a));
+    T = __fmul_rn(T, om);
     G = Gafter;
 }
 

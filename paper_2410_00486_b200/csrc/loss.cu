@@ -37,6 +37,21 @@ __device__ __forceinline__ int reflect1(int i, int n) {
     return i;
 }
 
+// 4-byte global -> shared copy that bypasses registers (zero-fills when
+// !valid); the halo of the next channel streams in under the current
+// channel's compute.
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src),
+                 "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // 11-tap correlation of 4 consecutive outputs from 14 register values.
 __device__ __forceinline__ void taps4(const float* v, const SsimWindow& win, float out[4]) {
 #pragma unroll
@@ -209,8 +224,9 @@ __global__ void __launch_bounds__(256, 3) ssim_bwd_kernel(int H, int W, const fl
                                                        const float* __restrict__ gxy, float lam,
                                                        float* __restrict__ grad,
                                                        float4* __restrict__ pixgrad) {
-    __shared__ __align__(16) float sg[3][LH][LP];
-    __shared__ __align__(16) float sh[3][LH][LT];
+    extern __shared__ __align__(16) float smem_b[];
+    float(*sgb)[3][LH][LP] = reinterpret_cast<float(*)[3][LH][LP]>(smem_b);          // [2]
+    float(*sh)[LH][LT] = reinterpret_cast<float(*)[LH][LT]>(smem_b + 6 * LH * LP);  // [3]
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * LT, y0 = blockIdx.y * LT;
     const float inv_n = 1.0f / (float)((double)H * W * 3);
@@ -220,34 +236,29 @@ __global__ void __launch_bounds__(256, 3) ssim_bwd_kernel(int H, int W, const fl
     float* pg = reinterpret_cast<float*>(pixgrad);
     const bool xborder = x0 <= LR || x0 + LT - 1 >= W - 6;
     const bool yborder = y0 <= LR || y0 + LT - 1 >= H - 6;
+    // halo of channel c (zero outside the image) into buffer b
+    auto issue = [&](int c, int b) {
+        for (int k = t; k < LH * LH; k += 256) {
+            const int r = k / LH, cc = k - r * LH;
+            const int gy = y0 - LR + r, gx = x0 - LR + cc;
+            const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+            const size_t o = ((size_t)c * H + (in ? gy : 0)) * W + (in ? gx : 0);
+            cp_async4(&sgb[b][0][r][cc], gmu + o, in);
+            cp_async4(&sgb[b][1][r][cc], gxx + o, in);
+            cp_async4(&sgb[b][2][r][cc], gxy + o, in);
+        }
+        cp_async_commit();
+    };
+    issue(0, 0);
     for (int c = 0; c < 3; ++c) {
-        {
-            // halo (zero outside the image): all loads in flight before the stores
-            constexpr int NL = (LH * LH + 255) / 256;
-            float v0[NL], v1[NL], v2[NL];
-#pragma unroll
-            for (int i = 0; i < NL; ++i) {
-                const int k = t + 256 * i;
-                const int r = k / LH, cc = k - r * LH;
-                const int gy = y0 - LR + r, gx = x0 - LR + cc;
-                const bool in = k < LH * LH && gy >= 0 && gy < H && gx >= 0 && gx < W;
-                const size_t o = ((size_t)c * H + (in ? gy : 0)) * W + (in ? gx : 0);
-                v0[i] = in ? gmu[o] : 0.f;
-                v1[i] = in ? gxx[o] : 0.f;
-                v2[i] = in ? gxy[o] : 0.f;
-            }
-#pragma unroll
-            for (int i = 0; i < NL; ++i) {
-                const int k = t + 256 * i;
-                if (k < LH * LH) {
-                    const int r = k / LH, cc = k - r * LH;
-                    sg[0][r][cc] = v0[i];
-                    sg[1][r][cc] = v1[i];
-                    sg[2][r][cc] = v2[i];
-                }
-            }
+        if (c < 2) {
+            issue(c + 1, (c + 1) & 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
+        float(*sg)[LH][LP] = sgb[c & 1];
         // axis 1 (columns) first, as losses.py:87-88
         for (int task = t; task < LH * 8; task += 256) {
             const int r = task >> 3, c0 = (task & 7) * 4;
@@ -399,9 +410,13 @@ cudaError_t launch_loss(int H, int W, const float* x, const float* y, float lam,
     if (H < 6 || W < 6) return cudaErrorInvalidValue;
     SsimWindow win = make_window();
     dim3 grid(div_up(W, LT), div_up(H, LT));
+    const int smem_b = (6 * LH * LP + 3 * LH * LT) * (int)sizeof(float);
+    cudaError_t e =
+        cudaFuncSetAttribute(ssim_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_b);
+    if (e != cudaSuccess) return e;
     ssim_fwd_kernel<<<grid, 256, 0, s>>>(H, W, x, y, win, gmu, gxx, gxy, partials);
-    ssim_bwd_kernel<<<grid, 256, 0, s>>>(H, W, x, y, win, gmu, gxx, gxy, lam, grad,
-                                         reinterpret_cast<float4*>(pixgrad));
+    ssim_bwd_kernel<<<grid, 256, smem_b, s>>>(H, W, x, y, win, gmu, gxx, gxy, lam, grad,
+                                              reinterpret_cast<float4*>(pixgrad));
     reduce_pairs_kernel<<<1, 256, 0, s>>>(grid.x * grid.y, partials, sums);
     return cudaGetLastError();
 }
