@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(256) rs_scan_kernel(uint32_t nblk, uint32_t* _
     if (t == 0) totals[blockIdx.x] = carry;
 }
 
-template <int ITEMS>
+template <int ITEMS, bool KEYS_ONLY>
 __global__ void __launch_bounds__(256) rs_downsweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, const uint32_t* d_count,
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(256) rs_downsweep_kernel(
     __shared__ uint32_t s_local[256];
     __shared__ uint32_t s_warp[8];
     __shared__ uint32_t s_keys[TILE];
-    __shared__ uint32_t s_vals[TILE];
+    __shared__ uint32_t s_vals[KEYS_ONLY ? 1 : TILE];
     const int t = threadIdx.x, w = t >> 5, l = t & 31;
 #pragma unroll
     for (int k = 0; k < 8; ++k) s_cnt[k][t] = 0;
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) rs_downsweep_kernel(
     for (int r = 0; r < ITEMS; ++r) {
         const uint32_t li = wbase + r * 32 + l;
         key[r] = li < nloc ? keys_in[base + li] : 0u;
-        val[r] = li < nloc ? (vals_in ? vals_in[base + li] : base + li) : 0u;
+        if (!KEYS_ONLY) val[r] = li < nloc ? (vals_in ? vals_in[base + li] : base + li) : 0u;
     }
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256) rs_downsweep_kernel(
             const uint32_t d = (key[r] >> shift) & 255u;
             const uint32_t lp = s_local[d] + s_cnt[w][d] + rank[r];
             s_keys[lp] = key[r];
-            s_vals[lp] = val[r];
+            if (!KEYS_ONLY) s_vals[lp] = val[r];
         }
     }
     __syncthreads();
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(256) rs_downsweep_kernel(
         const uint32_t k = s_keys[i];
         const uint32_t d = (k >> shift) & 255u;
         const uint32_t gp = s_base[d] + (i - s_local[d]);
-        vals_out[gp] = s_vals[i];
+        if (!KEYS_ONLY) vals_out[gp] = s_vals[i];
         if (keys_out) keys_out[gp] = k;
     }
 }
@@ -255,8 +255,14 @@ static void rs_pass(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, ui
     const uint32_t nblk = (uint32_t)div_up(cap > 0 ? cap : 1, 256 * ITEMS);
     rs_upsweep_kernel<ITEMS><<<nblk, 256, 0, s>>>(kin, d_count, n_static, cap, shift, nblk, counts);
     rs_scan_kernel<<<256, 256, 0, s>>>(nblk, counts, totals);
-    rs_downsweep_kernel<ITEMS><<<nblk, 256, 0, s>>>(kin, vin, kout, vout, d_count, n_static, cap,
-                                                    shift, nblk, counts, totals);
+    if (vout)
+        rs_downsweep_kernel<ITEMS, false><<<nblk, 256, 0, s>>>(kin, vin, kout, vout, d_count,
+                                                               n_static, cap, shift, nblk, counts,
+                                                               totals);
+    else
+        rs_downsweep_kernel<ITEMS, true><<<nblk, 256, 0, s>>>(kin, nullptr, kout, nullptr, d_count,
+                                                              n_static, cap, shift, nblk, counts,
+                                                              totals);
 }
 
 // ------------------------------------------------------------------ scan
@@ -350,7 +356,7 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
     uint32_t n, const uint32_t* __restrict__ order, const uint32_t* __restrict__ tiles,
     const uint2* __restrict__ rect, const uint32_t* __restrict__ offsets, int tiles_x,
     const int64_t* total, int64_t cap, uint32_t* __restrict__ keys,
-    uint32_t* __restrict__ vals) {
+    uint32_t* __restrict__ vals, int sb) {
     const bool ok = *total <= cap;
     const int lane = threadIdx.x & 31;
     const uint32_t j = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32 + lane;
@@ -387,23 +393,60 @@ __global__ void __launch_bounds__(256) emit_pairs_kernel(
         if (e < endw) {
             const uint32_t ry = li / ow;
             const uint32_t tid = (oy + ry) * tiles_x + ox + (li - ry * ow);
-            keys[base + e] = tid;
-            vals[base + e] = sid;
+            if (vals) {
+                keys[base + e] = tid;
+                vals[base + e] = sid;
+            } else {
+                keys[base + e] = (tid << sb) | sid;  // packed (tile, splat)
+            }
         }
     }
 }
 
 // ----------------------------------------------------------------- ranges
-__global__ void tile_ranges_kernel(const uint32_t* __restrict__ keys, const int64_t* total,
-                                   int64_t cap, uint32_t* __restrict__ start,
-                                   uint32_t* __restrict__ end) {
-    int64_t P = min(*total, cap);
-    if (*total > cap) P = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t t = keys[i];
-        if (i == 0 || keys[i - 1] != t) start[t] = (uint32_t)i;
-        if (i == P - 1 || keys[i + 1] != t) end[t] = (uint32_t)(i + 1);
+// Tile ranges by boundary detection on the sorted keys, 4 keys per thread
+// (16-byte loads).  Packed keys (sb > 0) hold tile << sb | splat: the splat
+// ids are unpacked into the pair list in the same pass.
+__global__ void __launch_bounds__(256) tile_ranges_kernel(const uint32_t* __restrict__ keys,
+                                                          const int64_t* total, int64_t cap,
+                                                          int sb, uint32_t* __restrict__ start,
+                                                          uint32_t* __restrict__ end,
+                                                          uint32_t* __restrict__ splat_out) {
+    int64_t P = *total;
+    if (P > cap) P = 0;
+    const uint32_t smask = sb ? (1u << sb) - 1u : 0u;
+    for (int64_t i0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); i0 < P;
+         i0 += 4 * (int64_t)gridDim.x * blockDim.x) {
+        uint32_t k[6];
+        if (i0 + 4 <= P) {
+            const uint4 v = *reinterpret_cast<const uint4*>(keys + i0);
+            k[1] = v.x, k[2] = v.y, k[3] = v.z, k[4] = v.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) k[1 + j] = (i0 + j < P) ? keys[i0 + j] : 0u;
+        }
+        k[0] = i0 > 0 ? keys[i0 - 1] : 0u;
+        k[5] = i0 + 4 < P ? keys[i0 + 4] : 0u;
+        uint32_t tl[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) tl[j] = sb ? k[j] >> sb : k[j];
+#pragma unroll
+        for (int j = 1; j <= 4; ++j) {
+            const int64_t i = i0 + j - 1;
+            if (i >= P) break;
+            if (i == 0 || tl[j - 1] != tl[j]) start[tl[j]] = (uint32_t)i;
+            if (i == P - 1 || tl[j + 1] != tl[j]) end[tl[j]] = (uint32_t)(i + 1);
+        }
+        if (sb) {
+            if (i0 + 4 <= P) {
+                *reinterpret_cast<uint4*>(splat_out + i0) =
+                    make_uint4(k[1] & smask, k[2] & smask, k[3] & smask, k[4] & smask);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (i0 + j < P) splat_out[i0 + j] = k[1 + j] & smask;
+            }
+        }
     }
 }
 
@@ -521,27 +564,39 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
         scan_kernel<false><<<div_up(n, 256 * kScanItems), 256, 0, s>>>(
             sp->d_tiles, order, nullptr, nn, L.offsets, L.st_scan1, L.ctrl + 8, P,
             &st->pair_overflow, cap);
-        // 3. emission of (tile, splat) pairs in depth order
+        // 3. emission of (tile, splat) pairs in depth order; one packed
+        //    32-bit word per pair when tile and splat ids fit
+        int sbits = 1, tbits = 1;
+        while ((1ll << sbits) < n) ++sbits;
+        while ((1ll << tbits) < n_tiles) ++tbits;
+        const bool packed = sbits + tbits <= 32;
         emit_pairs_kernel<<<div_up(n, 256), 256, 0, s>>>(
             nn, order, sp->d_tiles, reinterpret_cast<const uint2*>(sp->d_rect), L.offsets, tiles_x,
-            P, cap, L.pk0, L.pv0);
+            P, cap, L.pk0, packed ? nullptr : L.pv0, sbits);
         clamp_count_kernel<<<1, 1, 0, s>>>(P, cap, L.pcount);
-        // 4. stable sort of pairs by tile id; the last pass lands in d_pair_splat
+        // 4. stable sort of pairs by tile id
         const int np = tile_passes(n_tiles);
         const uint32_t* pk = L.pk0;
         const uint32_t* pv = L.pv0;
         for (int p = 0; p < np; ++p) {
             bool last = p == np - 1;
             uint32_t* kdst = (pk == L.pk0) ? L.pk1 : L.pk0;
-            uint32_t* vdst = last ? bins->d_pair_splat : ((pv == L.pv0) ? L.pv1 : L.pv0);
-            rs_pass<kPairItems>(pk, pv, kdst, vdst, L.pcount, 0u, (uint32_t)cap, 8 * p,
-                                L.rs_counts, L.rs_totals, s);
+            if (packed) {
+                rs_pass<kPairItems>(pk, nullptr, kdst, nullptr, L.pcount, 0u, (uint32_t)cap,
+                                    sbits + 8 * p, L.rs_counts, L.rs_totals, s);
+            } else {
+                // the last pass lands in d_pair_splat
+                uint32_t* vdst = last ? bins->d_pair_splat : ((pv == L.pv0) ? L.pv1 : L.pv0);
+                rs_pass<kPairItems>(pk, pv, kdst, vdst, L.pcount, 0u, (uint32_t)cap, 8 * p,
+                                    L.rs_counts, L.rs_totals, s);
+                pv = vdst;
+            }
             pk = kdst;
-            pv = vdst;
         }
-        // 5. ranges by boundary detection on the sorted tile ids
-        tile_ranges_kernel<<<div_up(cap > 0 ? cap : 1, 1024), 256, 0, s>>>(
-            pk, P, cap, bins->d_tile_start, bins->d_tile_end);
+        // 5. ranges by boundary detection on the sorted tile ids (+ unpack)
+        tile_ranges_kernel<<<div_up(cap > 0 ? cap : 1, 4 * 256), 256, 0, s>>>(
+            pk, P, cap, packed ? sbits : 0, bins->d_tile_start, bins->d_tile_end,
+            bins->d_pair_splat);
     } else {
         e = cudaMemsetAsync(P, 0, sizeof(int64_t) * 2, s);
         if (e != cudaSuccess) return e;
