@@ -51,7 +51,11 @@ typedef struct ss_status {
     int64_t pair_overflow;          /* 1 when P exceeded the caller's pair capacity */
     int64_t bucket_count;           /* number of (tile, bucket) backward work units */
     int64_t visible_count;          /* M = rows of the reference's Projection */
-    int64_t reserved;
+    int64_t reserved;               /* backward work-unit counter */
+    double opacity_sum;             /* sum of sigmoid(opacity logit) over all Gaussians at
+                                       ss_preprocess, i.e. before the step's update
+                                       (opacity regulariser value, losses.py:157-168) */
+    int64_t reserved2;
 } ss_status;
 
 /* Gaussian map in structure-of-arrays float32 (core.py:120-128; SH split
@@ -230,6 +234,15 @@ int ss_apply_stat_planes(const ss_map *map, const ss_param_grads *grads, void *s
  * pair-overflow words (the fused step skips its update while overflow is
  * set, so the host can grow the buffers and replay). */
 int ss_status_begin_step(ss_status *d_status, void *stream);
+
+/* Host snapshot of one step, for reading the step's outcome without
+ * stalling the stream: h_row (page-locked host memory, 11 doubles) receives
+ * the 8 status words as doubles, opacity_sum, and the two loss sums of
+ * ss_loss_l1_ssim (sum |x - y|, sum SSIM; zeros when d_loss_sums is NULL).
+ * One kernel writes through the mapped host pointer. */
+#define SS_SNAPSHOT_DOUBLES 11
+int ss_step_snapshot(const ss_status *d_status, const double *d_loss_sums, double *h_row,
+                     void *stream);
 
 /* Adam hyper-parameters of one step (optimizer.py:40-76,101-133), resolved
  * on the host for the post-increment step count t. */

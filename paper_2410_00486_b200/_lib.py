@@ -30,10 +30,13 @@ SZ = ctypes.c_size_t
 class SSStatus(ctypes.Structure):
     _fields_ = [("first_nonfinite_param", I64), ("first_zero_quat", I64),
                 ("first_nonfinite_grad", I64), ("pair_count", I64), ("pair_overflow", I64),
-                ("bucket_count", I64), ("visible_count", I64), ("reserved", I64)]
+                ("bucket_count", I64), ("visible_count", I64), ("reserved", I64),
+                ("opacity_sum", F64), ("reserved2", I64)]
 
 
-STATUS_WORDS = 8
+STATUS_WORDS = 10  # 80-byte ss_status as int64 words (word 8 holds a double)
+SNAPSHOT_DOUBLES = 11  # ss_step_snapshot row: 8 status words, opacity sum, 2 loss sums
+SN_OPACITY_SUM, SN_L1_SUM, SN_SSIM_SUM = 8, 9, 10
 ST_BAD_PARAM, ST_ZERO_QUAT, ST_BAD_GRAD, ST_PAIRS, ST_OVERFLOW, ST_BUCKETS, ST_VISIBLE = range(7)
 INT64_MAX = (1 << 63) - 1
 
@@ -87,6 +90,7 @@ _SIGS = {
     "ss_abi_version": (I32, []),
     "ss_status_reset": (I32, [VP, VP]),
     "ss_status_begin_step": (I32, [VP, VP]),
+    "ss_step_snapshot": (I32, [VP, VP, VP, VP]),
     "ss_apply_stat_planes": (I32, [P(SSMap), P(SSParamGrads), VP]),
     "ss_preprocess": (I32, [P(SSMap), P(SSCamera), VP, P(SSRasterOpts), P(SSSplats), VP, VP]),
     "ss_bin_workspace_bytes": (SZ, [I64, I64, I32]),

@@ -58,6 +58,8 @@ __global__ void status_reset_kernel(ss_status* st) {
     st->bucket_count = 0;
     st->visible_count = 0;
     st->reserved = 0;
+    st->opacity_sum = 0.0;
+    st->reserved2 = 0;
 }
 
 __global__ void status_begin_step_kernel(ss_status* st) {
@@ -65,6 +67,15 @@ __global__ void status_begin_step_kernel(ss_status* st) {
     st->bucket_count = 0;
     st->visible_count = 0;
     st->reserved = 0;
+    st->opacity_sum = 0.0;
+}
+
+__global__ void step_snapshot_kernel(const ss_status* st, const double* sums, double* row) {
+    const int t = threadIdx.x;
+    const int64_t* w = reinterpret_cast<const int64_t*>(st);
+    if (t < 8) row[t] = (double)w[t];
+    if (t == 8) row[8] = st->opacity_sum;
+    if (t == 9 || t == 10) row[t] = sums ? sums[t - 9] : 0.0;
 }
 }  // namespace ss
 
@@ -91,6 +102,19 @@ int ss_status_reset(ss_status* d_status, void* stream) {
 int ss_status_begin_step(ss_status* d_status, void* stream) {
     if (!d_status) return SS_EINVAL;
     status_begin_step_kernel<<<1, 1, 0, S(stream)>>>(d_status);
+    return rc(cudaGetLastError());
+}
+
+int ss_step_snapshot(const ss_status* d_status, const double* d_loss_sums, double* h_row,
+                     void* stream) {
+    if (!d_status || !h_row) return SS_EINVAL;
+    void* dev_row = nullptr;
+    if (cudaHostGetDevicePointer(&dev_row, h_row, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return SS_EINVAL;  // not page-locked / mapped host memory
+    }
+    step_snapshot_kernel<<<1, 32, 0, S(stream)>>>(d_status, d_loss_sums,
+                                                  reinterpret_cast<double*>(dev_row));
     return rc(cudaGetLastError());
 }
 

@@ -38,48 +38,46 @@ __device__ __forceinline__ void st_volatile64(unsigned long long* p, unsigned lo
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Decoupled look-back (used by the scans) with a window: each step loads
-// the status words of up to LB_WIN predecessors at once (independent loads
-// in flight), then consumes them nearest-first -- adding aggregates until an
-// inclusive prefix is found, or stopping at the first not-yet-published word
-// and retrying from there.
-constexpr int LB_WIN = 16;
-
-__device__ __forceinline__ unsigned long long lookback_u64(const unsigned long long* status,
-                                                           int64_t j, unsigned long long flag_agg,
-                                                           unsigned long long flag_inc,
-                                                           unsigned long long mask) {
+// Decoupled look-back (used by the scans), executed by one full warp: lane
+// l reads the status word of predecessor j - l, so each round covers 32
+// predecessors with independent loads.  The nearest-first run of published
+// words is consumed up to (and including) the first inclusive prefix; when
+// an unpublished word interrupts the run, the published part is added and
+// the walk resumes from there.  Returns the exclusive prefix (all lanes).
+__device__ __forceinline__ unsigned long long lookback_warp(const unsigned long long* status,
+                                                            int64_t j,
+                                                            unsigned long long flag_inc,
+                                                            unsigned long long mask) {
+    const int l = threadIdx.x & 31;
     unsigned long long excl = 0;
     while (j >= 0) {
-        unsigned long long v[LB_WIN];
+        const unsigned long long v = (j - l >= 0) ? ld_volatile64(status + (j - l)) : flag_inc;
+        const unsigned long long f = v & ~mask;
+        const unsigned not_ready = __ballot_sync(0xffffffffu, f == 0);
+        const unsigned inc = __ballot_sync(0xffffffffu, f == flag_inc);
+        const int limit = not_ready ? __ffs(not_ready) - 1 : 32;  // lanes [0, limit) published
+        const int first_inc = inc ? __ffs(inc) - 1 : 32;
+        const bool done = first_inc < limit;
+        const int take = done ? first_inc + 1 : limit;
+        unsigned long long part = l < take ? (v & mask) : 0ull;
 #pragma unroll
-        for (int i = 0; i < LB_WIN; ++i) v[i] = (j - i >= 0) ? ld_volatile64(status + (j - i)) : flag_inc;
-        int used = 0;
-        bool done = false;
-#pragma unroll
-        for (int i = 0; i < LB_WIN; ++i) {
-            if (done || used != i) break;
-            const unsigned long long f = v[i] & ~mask;
-            if (f == 0) break;
-            excl += v[i] & mask;
-            ++used;
-            if (f == flag_inc) done = true;
-        }
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        excl += part;
         if (done) break;
-        j -= used;
-        if (used < LB_WIN) __nanosleep(32);
+        j -= take;
+        if (take < 32) __nanosleep(32);
     }
-    (void)flag_agg;
     return excl;
 }
 
 // Lanes holding the same 8-bit digit (warp multi-split by 8 ballots; the
 // ballots are independent, unlike the serialised MATCH.ANY).  Invalid lanes
 // (valid == false) get an empty mask and are excluded from everyone's mask.
+template <int BITS = 8>
 __device__ __forceinline__ unsigned peers8(uint32_t d, bool valid) {
     unsigned peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
+    for (int b = 0; b < BITS; ++b) {
         const bool bit = (d >> b) & 1u;
         const unsigned bal = __ballot_sync(0xffffffffu, bit);
         peers &= bit ? bal : ~bal;
@@ -174,7 +172,7 @@ __global__ void __launch_bounds__(256) rs_scan_kernel(uint32_t nblk, uint32_t* _
     if (t == 0) totals[blockIdx.x] = carry;
 }
 
-template <int ITEMS, bool KEYS_ONLY>
+template <int ITEMS, bool KEYS_ONLY, int BITS>
 __global__ void __launch_bounds__(256) rs_downsweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, const uint32_t* d_count,
@@ -210,7 +208,7 @@ __global__ void __launch_bounds__(256) rs_downsweep_kernel(
         const uint32_t li = wbase + r * 32 + l;
         const bool valid = li < nloc;
         const uint32_t d = (key[r] >> shift) & 255u;
-        const unsigned peers = peers8(d, valid);
+        const unsigned peers = peers8<BITS>(d, valid);
         const uint32_t before = valid ? s_cnt[w][d] : 0u;
         rank[r] = before + __popc(peers & lanemask_lt());
         __syncwarp();
@@ -251,25 +249,30 @@ __global__ void __launch_bounds__(256) rs_downsweep_kernel(
 template <int ITEMS>
 static void rs_pass(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
                     const uint32_t* d_count, uint32_t n_static, uint32_t cap, int shift,
-                    uint32_t* counts, uint32_t* totals, cudaStream_t s) {
+                    uint32_t* counts, uint32_t* totals, cudaStream_t s, int bits = 8) {
     const uint32_t nblk = (uint32_t)div_up(cap > 0 ? cap : 1, 256 * ITEMS);
     rs_upsweep_kernel<ITEMS><<<nblk, 256, 0, s>>>(kin, d_count, n_static, cap, shift, nblk, counts);
     rs_scan_kernel<<<256, 256, 0, s>>>(nblk, counts, totals);
+    // digits narrower than 8 bits (a last partial pass) rank with fewer ballots
     if (vout)
-        rs_downsweep_kernel<ITEMS, false><<<nblk, 256, 0, s>>>(kin, vin, kout, vout, d_count,
-                                                               n_static, cap, shift, nblk, counts,
-                                                               totals);
+        rs_downsweep_kernel<ITEMS, false, 8><<<nblk, 256, 0, s>>>(kin, vin, kout, vout, d_count,
+                                                                  n_static, cap, shift, nblk,
+                                                                  counts, totals);
+    else if (bits <= 4)
+        rs_downsweep_kernel<ITEMS, true, 4><<<nblk, 256, 0, s>>>(kin, nullptr, kout, nullptr,
+                                                                 d_count, n_static, cap, shift,
+                                                                 nblk, counts, totals);
     else
-        rs_downsweep_kernel<ITEMS, true><<<nblk, 256, 0, s>>>(kin, nullptr, kout, nullptr, d_count,
-                                                              n_static, cap, shift, nblk, counts,
-                                                              totals);
+        rs_downsweep_kernel<ITEMS, true, 8><<<nblk, 256, 0, s>>>(kin, nullptr, kout, nullptr,
+                                                                 d_count, n_static, cap, shift,
+                                                                 nblk, counts, totals);
 }
 
 // ------------------------------------------------------------------ scan
 // Exclusive scan of in[gather ? gather[i] : i] (u32), 64-bit look-back
 // words (2 flag bits + 62-bit sum).  total_out (u64, optional) and
 // optional capacity check writing the overflow flag.
-constexpr int kScanItems = 8;
+constexpr int kScanItems = 16;
 constexpr unsigned long long kSFlagAgg = 1ull << 62;
 constexpr unsigned long long kSFlagInc = 2ull << 62;
 constexpr unsigned long long kSValMask = (1ull << 62) - 1;
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t* __restrict__ 
                                                    int64_t capacity) {
     constexpr int TILE = 256 * kScanItems;
     __shared__ uint32_t s_bid;
-    __shared__ unsigned long long s_warp[8];
+    __shared__ unsigned long long s_warp[8], s_wpre[8];
     __shared__ unsigned long long s_excl;
     const int t = threadIdx.x, w = t >> 5, l = t & 31;
     if (t == 0) s_bid = atomicAdd(counter, 1u);
@@ -315,30 +318,34 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t* __restrict__ 
     }
     if (l == 31) s_warp[w] = incl;
     __syncthreads();
-    if (t == 0) {
+    if (w == 0) {
         unsigned long long tot = 0;
-        for (int k = 0; k < 8; ++k) {
-            unsigned long long c = s_warp[k];
-            s_warp[k] = tot;
-            tot += c;
-        }
+        for (int k = 0; k < 8; ++k) tot += s_warp[k];
         unsigned long long* my = status + bid;
         unsigned long long excl = 0;
         if (bid == 0) {
-            st_volatile64(my, kSFlagInc | tot);
+            if (l == 0) st_volatile64(my, kSFlagInc | tot);
         } else {
-            st_volatile64(my, kSFlagAgg | tot);
-            excl = lookback_u64(status, (int64_t)bid - 1, kSFlagAgg, kSFlagInc, kSValMask);
-            st_volatile64(my, kSFlagInc | (excl + tot));
+            if (l == 0) st_volatile64(my, kSFlagAgg | tot);
+            excl = lookback_warp(status, (int64_t)bid - 1, kSFlagInc, kSValMask);
+            if (l == 0) st_volatile64(my, kSFlagInc | (excl + tot));
         }
-        s_excl = excl;
-        if ((bid + 1) * (uint32_t)TILE >= n) {  // last block writes the total
-            if (total_out) *total_out = (int64_t)(excl + tot);
-            if (overflow_out && (int64_t)(excl + tot) > capacity) *overflow_out = 1;  // sticky
+        if (l == 0) {
+            s_excl = excl;
+            if ((bid + 1) * (uint32_t)TILE >= n) {  // last block writes the total
+                if (total_out) *total_out = (int64_t)(excl + tot);
+                if (overflow_out && (int64_t)(excl + tot) > capacity) *overflow_out = 1;  // sticky
+            }
+        }
+        __syncwarp();
+        if (l < 8) {  // warp offsets within the block
+            unsigned long long pre = 0;
+            for (int k = 0; k < l; ++k) pre += s_warp[k];
+            s_wpre[l] = pre;
         }
     }
     __syncthreads();
-    unsigned long long run = s_excl + s_warp[w] + incl - sum;
+    unsigned long long run = s_excl + s_wpre[w] + incl - sum;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         uint32_t i = base + k;
@@ -450,6 +457,16 @@ __global__ void __launch_bounds__(256) tile_ranges_kernel(const uint32_t* __rest
     }
 }
 
+__global__ void bin_clear_kernel(uint32_t* ctrl, uint32_t ctrl_words, uint32_t* start,
+                                 uint32_t* end, uint32_t n_tiles) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    for (uint32_t k = i; k < ctrl_words; k += gridDim.x * blockDim.x) ctrl[k] = 0u;
+    for (uint32_t k = i; k < n_tiles; k += gridDim.x * blockDim.x) {
+        start[k] = 0u;
+        end[k] = 0u;
+    }
+}
+
 // Copy a device int64 (clamped) into a u32 count for the pair passes.
 __global__ void clamp_count_kernel(const int64_t* total, int64_t cap, uint32_t* out) {
     int64_t P = *total;
@@ -540,12 +557,11 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
     size_t need = 0;
     BinLayout L = bin_layout(n, cap, n_tiles, ws, &need);
     if (need > ws_bytes) return cudaErrorInvalidValue;
-    cudaError_t e = cudaMemsetAsync(L.ctrl, 0, L.ctrl_bytes, s);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(bins->d_tile_start, 0, sizeof(uint32_t) * n_tiles, s);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(bins->d_tile_end, 0, sizeof(uint32_t) * n_tiles, s);
-    if (e != cudaSuccess) return e;
+    // one launch clears the look-back control words and the tile ranges
+    bin_clear_kernel<<<div_up(n_tiles > 1024 ? n_tiles : 1024, 256), 256, 0, s>>>(
+        reinterpret_cast<uint32_t*>(L.ctrl), (uint32_t)(L.ctrl_bytes / 4), bins->d_tile_start,
+        bins->d_tile_end, (uint32_t)n_tiles);
+    cudaError_t e = cudaSuccess;
     int64_t* P = &st->pair_count;
     if (n > 0) {
         uint32_t nn = (uint32_t)n;
@@ -583,7 +599,8 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
             uint32_t* kdst = (pk == L.pk0) ? L.pk1 : L.pk0;
             if (packed) {
                 rs_pass<kPairItems>(pk, nullptr, kdst, nullptr, L.pcount, 0u, (uint32_t)cap,
-                                    sbits + 8 * p, L.rs_counts, L.rs_totals, s);
+                                    sbits + 8 * p, L.rs_counts, L.rs_totals, s,
+                                    tbits - 8 * p < 8 ? tbits - 8 * p : 8);
             } else {
                 // the last pass lands in d_pair_splat
                 uint32_t* vdst = last ? bins->d_pair_splat : ((pv == L.pv0) ? L.pv1 : L.pv0);

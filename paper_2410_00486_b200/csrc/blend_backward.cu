@@ -235,6 +235,19 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
     }
 }
 
+__global__ void bwd_clear_kernel(float* __restrict__ g2d, int64_t nf, uint8_t* contributed,
+                                 int64_t n, uint32_t* counter) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (i == 0) *counter = 0u;
+    const int64_t nf4 = (reinterpret_cast<uintptr_t>(g2d) & 15) ? 0 : nf / 4;
+    float4* g4 = reinterpret_cast<float4*>(g2d);
+    for (int64_t k = i; k < nf4; k += stride) g4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t k = nf4 * 4 + i; k < nf; k += stride) g2d[k] = 0.f;
+    if (contributed)
+        for (int64_t k = i; k < n; k += stride) contributed[k] = 0;
+}
+
 cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
                                   const ss_splats* sp, const ss_bins* bins, const float* image,
                                   const float* grad_image, const float4* pixgrad,
@@ -246,10 +259,10 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
                                   cudaStream_t s) {
     const bool depthf = o->with_depth != 0;
     const int ncol = depthf ? 10 : 9;
-    cudaError_t e = cudaMemsetAsync(g2d, 0, sizeof(float) * (size_t)n * ncol, s);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(counter, 0, sizeof(uint32_t), s);
-    if (e != cudaSuccess) return e;
+    // one launch clears the gradient rows, the contributed marks and the
+    // work-unit counter
+    bwd_clear_kernel<<<div_up(n * ncol > 4 ? n * ncol / 4 : 1, 256), 256, 0, s>>>(
+        g2d, (int64_t)n * ncol, contributed, n, counter);
     int tx = div_up(cam->width, kTile);
     const int threads = 32 * kBwdWarps;
     const size_t smem = 0;

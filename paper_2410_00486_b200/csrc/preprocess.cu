@@ -194,6 +194,17 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     if (lane_id() == 0 && bal)
         atomicAdd(reinterpret_cast<unsigned long long*>(&status->visible_count),
                   (unsigned long long)__popc(bal));
+    // opacity regulariser value, sum of sigmoid(logit) over ALL Gaussians
+    // with the pre-update logits (losses.py:157-168)
+    __shared__ double s_os[8];
+    double os = warp_sum(i < n ? (double)sigmoid_stable(opl[i]) : 0.0);
+    if (lane_id() == 0) s_os[threadIdx.x >> 5] = os;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) b += s_os[k];
+        atomicAdd(&status->opacity_sum, b);
+    }
 }
 
 void fill_camf(const ss_camera* c, CamF& f) {

@@ -44,17 +44,17 @@ STATUS_LAG = 2
 KERNELS_PER_CALL = {
     # status_begin 1 + preprocess 1 + blend 1 + loss (ssim fwd, ssim bwd,
     # reduce) 3 + backward 1; binning is counted separately (binning_kernels)
-    "step_fb": 1 + 1 + 1 + 3 + 1,
+    "step_fb": 1 + 1 + 1 + 3 + 2,  # backward = clear + splat-wise kernel
     "chain_adam": 1,
-    "opacity_reg": 2,
+    "snapshot": 1,
 }
 
 
 def binning_kernels(n_tiles: int) -> int:
-    """4 depth passes x 3 + scan + emit + clamp + tile passes x 3 + ranges +
-    checkpoint-base scan (binning.cu)."""
+    """clear + 4 depth passes x 3 + scan + emit + clamp + tile passes x 3 +
+    ranges + checkpoint-base scan (binning.cu)."""
     bits = max(1, (n_tiles - 1).bit_length())
-    return 4 * 3 + 1 + 1 + 1 + 3 * ((bits + 7) // 8) + 1 + 1
+    return 1 + 4 * 3 + 1 + 1 + 1 + 3 * ((bits + 7) // 8) + 1 + 1
 
 
 @dataclass
@@ -104,7 +104,8 @@ class MappingEngine:
         self.status = torch.empty(_lib.STATUS_WORDS, dtype=torch.int64, device=self.dev)
         check(lib().ss_status_reset(P(self.status), stream_handle()), "ss_status_reset")
         self._slots = 8
-        self._host = torch.zeros((self._slots, _lib.STATUS_WORDS + 4), dtype=torch.float64,
+        # page-locked snapshot rows written by ss_step_snapshot (one kernel)
+        self._host = torch.zeros((self._slots, _lib.SNAPSHOT_DOUBLES), dtype=torch.float64,
                                  pin_memory=True)
         self._graphs: dict = {}
         self._alloc_map_buffers()
@@ -167,7 +168,6 @@ class MappingEngine:
         self.pixgrad = torch.empty((self.H, self.W, 4), **f32)
         self.k_eff = torch.empty(self.n_tiles, dtype=torch.int32, device=dev)
         self.sums = torch.zeros(_lib.SS_REDUCE_DOUBLES, dtype=torch.float64, device=dev)
-        self.osum = torch.zeros(_lib.SS_REDUCE_DOUBLES, dtype=torch.float64, device=dev)
         self.dsum = torch.zeros(_lib.SS_REDUCE_DOUBLES, dtype=torch.float64, device=dev)
         self.loss_ws = torch.empty(int(lib().ss_loss_workspace_bytes(self.H, self.W)),
                                    dtype=torch.uint8, device=dev)
@@ -229,7 +229,6 @@ class MappingEngine:
             else:
                 self.grad_depth.zero_()
         self._mark("loss")
-        self.contributed.zero_()
         check(L.ss_backward_splat(ctypes.byref(cm), ctypes.byref(op), ctypes.byref(spss),
                                   ctypes.byref(bss), P(self.image), P(self.grad_image),
                                   P(self.pixgrad) if use_pg else None, P(self.depth),
@@ -243,9 +242,8 @@ class MappingEngine:
     def _snapshot(self, rec: StepRecord):
         """Copy the step's status block + loss sums into its pinned slot."""
         row = self._host[rec.slot]
-        row[:_lib.STATUS_WORDS].copy_(self.status.double(), non_blocking=True)
-        row[_lib.STATUS_WORDS:_lib.STATUS_WORDS + 2].copy_(self.sums[:2], non_blocking=True)
-        row[_lib.STATUS_WORDS + 2:_lib.STATUS_WORDS + 3].copy_(self.osum[:1], non_blocking=True)
+        check(lib().ss_step_snapshot(P(self.status), P(self.sums), row.data_ptr(),
+                                     stream_handle()), "ss_step_snapshot")
         rec.event.record()
 
     # ---------------------------------------------------------- main step
@@ -279,8 +277,6 @@ class MappingEngine:
                               ctypes.byref(self.state.planes("v")), ctypes.byref(hp0), d_hp,
                               P(self.status), stream_handle()), "ss_chain_adam")
         self._mark("chain_adam")
-        check(L.ss_opacity_reg(n, P(self.gmap.opacity_logits), 0.0, None, 0, P(self.osum),
-                               stream_handle()), "ss_opacity_reg")
 
     def _run(self, rec: StepRecord):
         self._stage_params(rec)
@@ -302,7 +298,7 @@ class MappingEngine:
 
     def _launches_per_step(self):
         k = (KERNELS_PER_CALL["step_fb"] + binning_kernels(self.n_tiles)
-             + KERNELS_PER_CALL["chain_adam"] + KERNELS_PER_CALL["opacity_reg"])
+             + KERNELS_PER_CALL["chain_adam"] + KERNELS_PER_CALL["snapshot"])
         if self.opts.with_depth and self.cfg.depth_weight:
             k += 3
         return k
@@ -329,11 +325,11 @@ class MappingEngine:
 
     def _log(self, rec, row):
         npx = self.H * self.W * 3
-        l1 = row[_lib.STATUS_WORDS] / npx
-        ssim = row[_lib.STATUS_WORDS + 1] / npx
+        l1 = row[_lib.SN_L1_SUM] / npx
+        ssim = row[_lib.SN_SSIM_SUM] / npx
         lam = self.cfg.lambda_ssim
         rendered = (1 - lam) * l1 + lam * (1 - ssim)
-        reg = row[_lib.STATUS_WORDS + 2] / max(len(self.gmap), 1)
+        reg = row[_lib.SN_OPACITY_SUM] / max(len(self.gmap), 1)
         self._loss_log.append((rec.index, rendered + self.cfg.lambda_o * reg, rendered))
 
     def _recover(self, pairs_seen: int):

@@ -56,7 +56,7 @@ def test_invalid_arguments_rejected_without_launch():
 
 def test_struct_layouts_match_header():
     from paper_2410_00486_b200 import _lib
-    assert ctypes.sizeof(_lib.SSStatus) == 64
+    assert ctypes.sizeof(_lib.SSStatus) == 80
     assert ctypes.sizeof(_lib.SSMap) == 80
     assert ctypes.sizeof(_lib.SSCamera) == 4 * 4 + 8 + 4 * 15
     assert ctypes.sizeof(_lib.SSParamGrads) == 80

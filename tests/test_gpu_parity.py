@@ -261,6 +261,31 @@ def test_engine_graph_replay_matches_stream_launches():
     np.testing.assert_allclose([x[1] for x in la], [x[1] for x in lb], rtol=1e-5)
 
 
+def test_engine_loss_snapshot_uses_pre_step_opacities():
+    """The engine's loss feed (ss_step_snapshot) reports the step's rendered
+    loss and lambda_o * mean sigmoid(logits) of the parameters the step was
+    rendered with (losses.py:157-168,224-228), i.e. before its Adam update."""
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    import oracle as orc
+    d = load("iter_sh0_small")
+    cam = fixture_camera(d)
+    arrs = fixture_scene(d)
+    tgt = torch.as_tensor(d["target"], dtype=torch.float32, device="cuda")
+    g = ss.GaussianMap.from_arrays(*arrs)
+    logits0 = g.opacity_logits.cpu().numpy().astype(np.float64)
+    eng = ss.MappingEngine(g, cam.width, cam.height, ss.RasterOpts(sh_degree=0))
+    eng.step(cam, tgt)
+    (_, total, rendered), = eng.losses()
+    reg = float(np.mean(1.0 / (1.0 + np.exp(-logits0))))
+    assert abs((total - rendered) - eng.cfg.lambda_o * reg) <= 1e-9
+    # rendered loss of the pre-step map, as the oracle computes it
+    om = orc.OMap(*[a.astype(np.float64) if a is not None else None for a in arrs])
+    r = orc.rasterize(om, cam, sh_degree=0, with_checkpoints=False)
+    lb = orc.losses(r.image, d["target"].astype(np.float64), om.opacity_logits)
+    assert abs(rendered - lb.rendered) <= 1e-5 * abs(lb.rendered)
+
+
 def test_engine_recovers_from_pair_overflow():
     _need_gpu()
     import paper_2410_00486_b200 as ss
