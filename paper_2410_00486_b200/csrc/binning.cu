@@ -273,6 +273,7 @@ static void rs_pass(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, ui
 // words (2 flag bits + 62-bit sum).  total_out (u64, optional) and
 // optional capacity check writing the overflow flag.
 constexpr int kScanItems = 16;
+constexpr int kScanItemsTiles = 4;  // checkpoint-base scan (few thousand tiles)
 constexpr unsigned long long kSFlagAgg = 1ull << 62;
 constexpr unsigned long long kSFlagInc = 2ull << 62;
 constexpr unsigned long long kSValMask = (1ull << 62) - 1;
@@ -285,7 +286,8 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t* __restrict__ 
                                                    unsigned long long* status, uint32_t* counter,
                                                    int64_t* total_out, int64_t* overflow_out,
                                                    int64_t capacity) {
-    constexpr int TILE = 256 * kScanItems;
+    constexpr int ITEMS = CEIL_DIV32 ? kScanItemsTiles : kScanItems;
+    constexpr int TILE = 256 * ITEMS;
     __shared__ uint32_t s_bid;
     __shared__ unsigned long long s_warp[8], s_wpre[8];
     __shared__ unsigned long long s_excl;
@@ -293,11 +295,11 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t* __restrict__ 
     if (t == 0) s_bid = atomicAdd(counter, 1u);
     __syncthreads();
     const uint32_t bid = s_bid;
-    const uint32_t base = bid * TILE + t * kScanItems;
-    uint32_t v[kScanItems];
+    const uint32_t base = bid * TILE + t * ITEMS;
+    uint32_t v[ITEMS];
     unsigned long long sum = 0;
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
+    for (int k = 0; k < ITEMS; ++k) {
         uint32_t i = base + k;
         uint32_t x = 0;
         if (i < n) {
@@ -347,7 +349,7 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t* __restrict__ 
     __syncthreads();
     unsigned long long run = s_excl + s_wpre[w] + incl - sum;
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
+    for (int k = 0; k < ITEMS; ++k) {
         uint32_t i = base + k;
         if (i < n) out[i] = (uint32_t)run;
         run += v[k];
@@ -517,7 +519,7 @@ BinLayout bin_layout(int64_t n, int64_t cap, int n_tiles, void* ws, size_t* byte
     (void)n_tiles;
     L.ctrl = w.take<uint32_t>(16);
     L.st_scan1 = w.take<unsigned long long>(div_up(n > 0 ? n : 1, 256 * kScanItems) + 1);
-    L.st_scan2 = w.take<unsigned long long>(div_up(n_tiles + 1, 256 * kScanItems) + 1);
+    L.st_scan2 = w.take<unsigned long long>(div_up(n_tiles + 1, 256 * kScanItemsTiles) + 1);
     w.off = (w.off + 255) & ~size_t(255);
     L.ctrl_bytes = w.off;
     L.kA = w.take<uint32_t>(n);
@@ -619,7 +621,7 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
         if (e != cudaSuccess) return e;
     }
     // checkpoint slot bases: exclusive scan of ceil(len/32), n_tiles+1 entries
-    scan_kernel<true><<<div_up(n_tiles + 1, 256 * kScanItems), 256, 0, s>>>(
+    scan_kernel<true><<<div_up(n_tiles + 1, 256 * kScanItemsTiles), 256, 0, s>>>(
         bins->d_tile_start, nullptr, bins->d_tile_end, (uint32_t)n_tiles + 1, bins->d_ckpt_base,
         L.st_scan2, L.ctrl + 9, nullptr, nullptr, 0);
     return cudaGetLastError();

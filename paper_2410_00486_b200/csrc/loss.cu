@@ -223,8 +223,25 @@ __global__ void __launch_bounds__(256, 3) ssim_bwd_kernel(int H, int W, const fl
                                                        const float* __restrict__ gxx,
                                                        const float* __restrict__ gxy, float lam,
                                                        float* __restrict__ grad,
-                                                       float4* __restrict__ pixgrad) {
+                                                       float4* __restrict__ pixgrad,
+                                                       const double* __restrict__ partials,
+                                                       int n_partials,
+                                                       double* __restrict__ sums) {
     extern __shared__ __align__(16) float smem_b[];
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 32) {
+        // fixed-order reduction of ssim_fwd's per-CTA (|x-y|, SSIM) sums
+        double a = 0.0, b = 0.0;
+        for (int i = threadIdx.x; i < n_partials; i += 32) {
+            a += partials[2 * i];
+            b += partials[2 * i + 1];
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        if (threadIdx.x == 0) {
+            sums[0] = a;
+            sums[1] = b;
+        }
+    }
     float(*sgb)[3][LH][LP] = reinterpret_cast<float(*)[3][LH][LP]>(smem_b);          // [2]
     float(*sh)[LH][LT] = reinterpret_cast<float(*)[LH][LT]>(smem_b + 6 * LH * LP);  // [3]
     const int t = threadIdx.x;
@@ -416,8 +433,8 @@ cudaError_t launch_loss(int H, int W, const float* x, const float* y, float lam,
     if (e != cudaSuccess) return e;
     ssim_fwd_kernel<<<grid, 256, 0, s>>>(H, W, x, y, win, gmu, gxx, gxy, partials);
     ssim_bwd_kernel<<<grid, 256, smem_b, s>>>(H, W, x, y, win, gmu, gxx, gxy, lam, grad,
-                                              reinterpret_cast<float4*>(pixgrad));
-    reduce_pairs_kernel<<<1, 256, 0, s>>>(grid.x * grid.y, partials, sums);
+                                              reinterpret_cast<float4*>(pixgrad), partials,
+                                              (int)(grid.x * grid.y), sums);
     return cudaGetLastError();
 }
 

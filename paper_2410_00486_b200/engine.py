@@ -42,9 +42,10 @@ STATUS_LAG = 2
 
 # kernels each C-ABI call enqueues (counted for bench.py's gpu_launches)
 KERNELS_PER_CALL = {
-    # status_begin 1 + preprocess 1 + blend 1 + loss (ssim fwd, ssim bwd,
-    # reduce) 3 + backward 1; binning is counted separately (binning_kernels)
-    "step_fb": 1 + 1 + 1 + 3 + 2,  # backward = clear + splat-wise kernel
+    # status_begin 1 + preprocess 1 + blend 1 + loss (ssim fwd, ssim bwd with
+    # the partial-sum reduction) 2 + backward (clear, splat-wise) 2; binning
+    # is counted separately (binning_kernels)
+    "step_fb": 1 + 1 + 1 + 2 + 2,
     "chain_adam": 1,
     "snapshot": 1,
 }
