@@ -105,18 +105,23 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ algorithmic bytes
-def algorithmic_bytes(n, m, p, hw, t, c, e, G=14):
+def algorithmic_bytes(n, m, p, hw, t, c, e, u=None, G=14):
     """SURVEY.md 8d per-stage compulsory HBM traffic (float32, int32 ids,
-    u64 keys, sort = one read + one write), bytes per iteration."""
+    u64 keys, sort = one read + one write), bytes per iteration.  c =
+    checkpoint slots (32-position buckets, sum ceil(k_eff/32)): the forward
+    writes a (T, rgb) state and a blend mask per pixel per slot; u = backward
+    work units (64 positions = 2 slots), each reading one state slot and two
+    mask slots."""
+    u = c / 2 if u is None else u
     st = {
         "preprocess": n * G * 4 + n * 48,
         "scan": n * 8,
         "dup": n * 20 + p * 12,
         "sort": p * 24,
         "ranges": p * 8 + t * 8,
-        "blend_forward": p * 4 + m * 36 + hw * 20 + c * 4096 + n,
+        "blend_forward": p * 4 + m * 36 + hw * 20 + c * (4096 + 1024) + n,
         "loss": hw * 36,
-        "backward": e * 4 + m * 36 + c * 4096 + hw * 28 + m * 36,
+        "backward": e * 4 + m * 36 + u * (4096 + 2048) + hw * 28 + m * 36,
         "chain": m * 36 + n * G * 8 + n * 5,
         "adam": n * G * 28,
         "stats": n * 57,
@@ -124,14 +129,19 @@ def algorithmic_bytes(n, m, p, hw, t, c, e, G=14):
     return st
 
 
-def ncu_traffic(kernel):
-    """dram read+write bytes per launch of `kernel` from the committed ncu
-    --set full capture summary (profiles/ncu_traffic.json), else None."""
+def ncu_stats(kernel):
+    """Per-launch figures of `kernel` from the committed ncu --set full
+    capture summary (profiles/ncu_traffic.json), else {}."""
     try:
         with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(kernel)
+            return json.load(f).get(kernel) or {}
     except Exception:
-        return None
+        return {}
+
+
+def ncu_traffic(kernel):
+    """dram read+write bytes per launch of `kernel` (ncu), else None."""
+    return ncu_stats(kernel).get("dram_bytes")
 
 
 def load_peaks():
@@ -305,12 +315,13 @@ def main():
     # ---- workload statistics for the algorithmic-byte model
     st = eng.status.cpu().numpy()
     P = int(st[3])
-    C = int(st[5])
+    U = int(st[5])  # backward work units (64 list positions)
     M = int(st[6])
     E = int(eng.k_eff.sum().item())
+    C = int(((eng.k_eff.long() + 31) // 32).sum().item())  # checkpoint slots
     HW = W * H
     T = eng.n_tiles
-    algo = algorithmic_bytes(N, M, P, HW, T, C, E)
+    algo = algorithmic_bytes(N, M, P, HW, T, C, E, U)
     peak, peak_src = load_peaks()
     per_kernel = {
         "blend_forward": algo["blend_forward"],
@@ -390,13 +401,19 @@ def main():
             "config": {"workload": f"replica-shaped S({N},{W}x{H}) SH0, "
                                    f"{'single view' if world == 1 else '1 view per GPU, NCCL all-reduce'}"
                                    " (BASELINE configs[1])", "gaussians": N, "image": [W, H],
-                       "sh_degree": 0, "pairs": P, "visible": M, "buckets": C,
+                       "sh_degree": 0, "pairs": P, "visible": M, "checkpoint_slots": C,
+                       "backward_units": U,
                        "l2": "256 MB buffer written between timed steps (outside the events)",
                        "parallelism": f"keyframe-sharded x{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
                          "unit": "GB/s", "frac": ach / peak, "traffic": ncu_traffic(dom),
                          "algorithmic_bytes": per_kernel[dom], "avg_ms": stage_ms[dom],
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         "ncu": {k: v for k, v in ncu_stats(dom).items()
+                                 if k in ("issue_slots_pct", "warps_active_pct")},
+                         "note": "FP32 CUDA-core kernel limited by instruction issue "
+                                 "(ncu issue_slots_pct), not by HBM; no tensor-core work "
+                                 "on this path"},
             "iteration_roofline": {"algorithmic_MB": it_bytes / 1e6,
                                    "achieved_GBs": it_bytes * value / views / 1e9,
                                    "frac": it_bytes * value / views / 1e9 / peak},
