@@ -25,6 +25,9 @@
 // scatter writes coalesced runs).  A one-sweep pass with decoupled look-back
 // was measured first and was latency-bound here: with hundreds of CTAs
 // co-resident, each CTA walks back over all its predecessors' aggregates.
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ss {
@@ -475,6 +478,288 @@ __global__ void clamp_count_kernel(const int64_t* total, int64_t cap, uint32_t* 
     *out = (P > cap) ? 0u : (uint32_t)P;
 }
 
+// ------------------------------------------------- persistent front end
+// Depth sort + pair offsets + pair emission in ONE cooperative launch (the
+// per-pass kernels above are latency-bound at N = 300k: 12 launches of
+// 147 CTAs, then a look-back scan and the emission).  One sort tile of
+// kFeTile keys per CTA; no atomics (deterministic); nine grid barriers:
+//   pass p, phase A  load the tile (from the previous pass's output),
+//                    stable warp multi-split ranking, publish the tile's
+//                    digit histogram                                 -> sync
+//   pass p, phase B  digit totals and the column prefix over preceding
+//                    tiles from the published histograms (4 thread groups
+//                    x 256 digits), local reorder, coalesced scatter -> sync
+//   chunk sums       each CTA sums the touched-tile counts of its tile of
+//                    the final order                                 -> sync
+//   emission         tile prefix, block scan -> pair offsets, P, capacity
+//                    check, warp-cooperative emission (as emit_pairs).
+constexpr int kFeThreads = 1024;
+constexpr int kFeWarps = kFeThreads / 32;
+constexpr int kFeColChunks = 5;  // column walk covers n_tiles <= 160 (one CTA per SM)
+// keys per thread: 2, 4 or 8 (2048 / 4096 / 8192-key tiles), the smallest
+// that gives every co-resident CTA at most one tile
+template <int ITEMS>
+constexpr size_t fe_smem_bytes() {
+    return sizeof(uint32_t) * (kFeWarps * 256 + 2 * kFeThreads * ITEMS + 4 * 512);
+}
+inline size_t fe_smem_bytes_rt(int items) {
+    return sizeof(uint32_t) * (kFeWarps * 256 + 2 * kFeThreads * items + 4 * 512);
+}
+
+struct FeArgs {
+    uint32_t n;
+    uint32_t n_tiles;
+    const uint32_t* key_in;
+    uint32_t *kA, *vA, *kB, *vB;
+    uint32_t* counts;      // [2][n_tiles][256] (pass parity)
+    uint32_t* chunk_sum;   // [n_tiles]
+    const uint32_t* tiles;
+    const uint2* rect;
+    int tiles_x;
+    uint32_t* pair_k;
+    uint32_t* pair_v;      // null: packed words
+    int sb;
+    int64_t* total;
+    int64_t* overflow;
+    int64_t cap;
+    uint32_t* pcount;
+};
+
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp) {
+    const int t = threadIdx.x, w = t >> 5, l = t & 31;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += y;
+    }
+    if (l == 31) s_warp[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t x = l < NT / 32 ? s_warp[l] : 0u;
+        uint32_t xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, xi, o);
+            if (l >= o) xi += y;
+        }
+        if (l < NT / 32) s_warp[l] = xi - x;
+    }
+    __syncthreads();
+    const uint32_t r = s_warp[w] + incl - v;
+    __syncthreads();
+    return r;
+}
+
+template <int ITEMS>
+__global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
+    constexpr int kFeTile = kFeThreads * ITEMS;
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ uint32_t fe_smem[];
+    uint32_t(*s_cnt)[256] = reinterpret_cast<uint32_t(*)[256]>(fe_smem);  // [kFeWarps]
+    uint32_t* s_keys = fe_smem + kFeWarps * 256;
+    uint32_t* s_vals = s_keys + kFeTile;
+    uint32_t(*s_part)[512] = reinterpret_cast<uint32_t(*)[512]>(s_vals + kFeTile);  // [4]
+    __shared__ uint32_t s_base[256], s_local[256], s_warp[32];
+    const int t = threadIdx.x, w = t >> 5, l = t & 31;
+    const uint32_t tile = blockIdx.x;    // gridDim.x == n_tiles
+    const uint32_t base = tile * kFeTile;
+    const uint32_t nloc = min((uint32_t)kFeTile, a.n - base);
+    const uint32_t wbase = w * 32 * ITEMS;
+
+#pragma unroll 1
+    for (int p = 0; p < 4; ++p) {
+        const uint32_t* kin = p == 0 ? a.key_in : ((p & 1) ? a.kA : a.kB);
+        const uint32_t* vin = p == 0 ? nullptr : ((p & 1) ? a.vA : a.vB);
+        uint32_t* kout = (p & 1) ? a.kB : a.kA;
+        uint32_t* vout = (p & 1) ? a.vB : a.vA;
+        uint32_t* cnt = a.counts + (size_t)(p & 1) * a.n_tiles * 256;
+        const int shift = 8 * p;
+        // ---- phase A: rank within the tile, publish the digit histogram
+        for (int k = t; k < kFeWarps * 256; k += kFeThreads) (&s_cnt[0][0])[k] = 0u;
+        __syncthreads();
+        uint32_t key[ITEMS], val[ITEMS], rank[ITEMS];
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            const uint32_t li = wbase + r * 32 + l;
+            key[r] = li < nloc ? kin[base + li] : 0u;
+            val[r] = li < nloc ? (vin ? vin[base + li] : base + li) : 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            const uint32_t li = wbase + r * 32 + l;
+            const bool valid = li < nloc;
+            const uint32_t d = (key[r] >> shift) & 255u;
+            const unsigned peers = peers8(d, valid);
+            const uint32_t before = valid ? s_cnt[w][d] : 0u;
+            rank[r] = before + __popc(peers & lanemask_lt());
+            __syncwarp();
+            if (valid && (peers & lanemask_lt()) == 0) s_cnt[w][d] = before + __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        uint32_t run = 0;
+        if (t < 256) {
+#pragma unroll 8
+            for (int k = 0; k < kFeWarps; ++k) {
+                const uint32_t c = s_cnt[k][t];
+                s_cnt[k][t] = run;
+                run += c;
+            }
+            cnt[(size_t)t * a.n_tiles + tile] = run;  // this tile's digit histogram ([d][tile])
+        }
+        const uint32_t loc = block_excl_scan<kFeThreads>(t < 256 ? run : 0u, s_warp);
+        if (t < 256) s_local[t] = loc;
+        grid.sync();
+        // ---- phase B: digit starts = exclusive digit total + column prefix;
+        //      warp w reduces the columns of digits w + 32 k (coalesced rows of
+        //      the [digit][tile] histograms), all loads of a batch in flight
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            uint32_t c[4][kFeColChunks];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int j = 0; j < kFeColChunks; ++j) {
+                    const uint32_t q = l + 32 * j;
+                    const int d = w + kFeWarps * (4 * half + k);
+                    c[k][j] = q < a.n_tiles ? cnt[(size_t)d * a.n_tiles + q] : 0u;
+                }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t before = 0, all = 0;
+#pragma unroll
+                for (int j = 0; j < kFeColChunks; ++j) {
+                    all += c[k][j];
+                    before += (l + 32 * j) < tile ? c[k][j] : 0u;
+                }
+                all = warp_sum(all);
+                before = warp_sum(before);
+                if (l == 0) {
+                    const int d = w + kFeWarps * (4 * half + k);
+                    s_part[0][d] = before;
+                    s_part[0][256 + d] = all;
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t col = t < 256 ? s_part[0][t] : 0u;
+        const uint32_t tot = t < 256 ? s_part[0][256 + t] : 0u;
+        const uint32_t excl = block_excl_scan<kFeThreads>(t < 256 ? tot : 0u, s_warp);
+        if (t < 256) s_base[t] = excl + col;
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            const uint32_t li = wbase + r * 32 + l;
+            if (li < nloc) {
+                const uint32_t d = (key[r] >> shift) & 255u;
+                const uint32_t lp = s_local[d] + s_cnt[w][d] + rank[r];
+                s_keys[lp] = key[r];
+                s_vals[lp] = val[r];
+            }
+        }
+        __syncthreads();
+        for (uint32_t i = t; i < nloc; i += kFeThreads) {
+            const uint32_t k = s_keys[i];
+            const uint32_t d = (k >> shift) & 255u;
+            const uint32_t gp = s_base[d] + (i - s_local[d]);
+            vout[gp] = s_vals[i];
+            if (p < 3) kout[gp] = k;
+        }
+        grid.sync();
+    }
+
+    // ---- chunk sums of the final order (vB: pass 3 wrote the B buffers);
+    //      warp w holds rows of 32 consecutive splats, wbase + 32 r + lane
+    const uint32_t* order = a.vB;
+    uint32_t sidr[ITEMS], cr[ITEMS], ir[ITEMS], rpre[ITEMS];
+    uint32_t wtot = 0;
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+        const uint32_t j = base + wbase + r * 32 + l;
+        sidr[r] = j < a.n ? order[j] : 0u;
+        cr[r] = j < a.n ? a.tiles[sidr[r]] : 0u;
+        uint32_t x = cr[r];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (l >= o) x += y;
+        }
+        ir[r] = x;
+        rpre[r] = wtot;
+        wtot += __shfl_sync(0xffffffffu, x, 31);
+    }
+    const uint32_t wex = block_excl_scan<kFeThreads>(l == 0 ? wtot : 0u, s_warp);
+    const uint32_t wpre = __shfl_sync(0xffffffffu, wex, 0);
+    if (t == kFeThreads - 1) a.chunk_sum[tile] = wpre + wtot;  // last warp: tile total
+    grid.sync();
+    // ---- P, capacity check, tile prefix
+    uint32_t P = 0, pre = 0;
+    for (uint32_t q = l; q < a.n_tiles; q += 32) {
+        const uint32_t c = a.chunk_sum[q];
+        P += c;
+        pre += q < tile ? c : 0u;
+    }
+    P = warp_sum(P);
+    pre = warp_sum(pre);
+    if ((int64_t)P > a.cap) {
+        if (tile == 0 && t == 0) {
+            *a.total = (int64_t)P;
+            *a.overflow = 1;  // sticky; the step is replayed with larger buffers
+            *a.pcount = 0u;
+        }
+        return;
+    }
+    if (tile == 0 && t == 0) {
+        *a.total = (int64_t)P;
+        *a.pcount = P;
+    }
+    // ---- emission, warp-cooperative per row of 32 splats
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+        const uint32_t j = base + wbase + r * 32 + l;
+        const uint32_t cc = cr[r];
+        const uint32_t o = pre + wpre + rpre[r] + ir[r] - cc;
+        uint32_t x0 = 0, y0 = 0, wx = 1;
+        if (j < a.n && cc) {
+            const uint2 rc = a.rect[sidr[r]];
+            x0 = rc.x & 0xffffu;
+            y0 = rc.x >> 16;
+            wx = (rc.y & 0xffffu) - x0 + 1;
+        }
+        const uint32_t b0 = __shfl_sync(0xffffffffu, o, 0);
+        const uint32_t rel = j < a.n ? o - b0 : 0x7fffffffu;
+        uint32_t endw = j < a.n ? rel + cc : 0u;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) endw = max(endw, __shfl_xor_sync(0xffffffffu, endw, d));
+        for (uint32_t e0 = 0; e0 < endw; e0 += 32) {
+            const uint32_t e = e0 + l;
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t rr = __shfl_sync(0xffffffffu, rel, lo + step);
+                if (rr <= e) lo += step;
+            }
+            const uint32_t li = e - __shfl_sync(0xffffffffu, rel, lo);
+            const uint32_t ox = __shfl_sync(0xffffffffu, x0, lo);
+            const uint32_t oy = __shfl_sync(0xffffffffu, y0, lo);
+            const uint32_t ow = __shfl_sync(0xffffffffu, wx, lo);
+            const uint32_t sid = __shfl_sync(0xffffffffu, sidr[r], lo);
+            if (e < endw) {
+                const uint32_t ry = li / ow;
+                const uint32_t tid = (oy + ry) * a.tiles_x + ox + (li - ry * ow);
+                if (a.pair_v) {
+                    a.pair_k[b0 + e] = tid;
+                    a.pair_v[b0 + e] = sid;
+                } else {
+                    a.pair_k[b0 + e] = (tid << a.sb) | sid;
+                }
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------ workspace
 struct BinWorkspace {
     size_t off = 0;
@@ -504,6 +789,9 @@ struct BinLayout {
     uint32_t* pcount;                 // 1
     uint32_t* rs_counts;              // 256 * max blocks
     uint32_t* rs_totals;              // 256
+    // persistent front end (in the zeroed control region)
+    uint32_t* fe_counts;              // 2 * n_fe_tiles * 256
+    uint32_t* fe_chunk;               // n_fe_tiles
 };
 
 inline int tile_passes(int n_tiles) {
@@ -533,6 +821,11 @@ BinLayout bin_layout(int64_t n, int64_t cap, int n_tiles, void* ws, size_t* byte
     L.pv1 = w.take<uint32_t>(cap);
     L.pcount = w.take<uint32_t>(4);
     {
+        const int64_t nft = div_up(n > 0 ? n : 1, 2 * kFeThreads);  // smallest tiles
+        L.fe_counts = w.take<uint32_t>(2 * nft * 256);
+        L.fe_chunk = w.take<uint32_t>(nft);
+    }
+    {
         int64_t mx = cap > n ? cap : n;
         L.rs_counts = w.take<uint32_t>(
             (size_t)256 * (div_up(mx > 0 ? mx : 1, 256 * (kDepthItems < kPairItems ? kDepthItems
@@ -548,6 +841,73 @@ size_t bin_workspace_bytes(int64_t n, int64_t cap, int n_tiles) {
     size_t b = 0;
     bin_layout(n, cap, n_tiles, nullptr, &b);
     return b;
+}
+
+template <int ITEMS>
+static int fe_capacity() {  // co-resident CTAs of bin_front_kernel<ITEMS>, 0 = unusable
+    int dev = 0, coop = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int bytes = (int)fe_smem_bytes<ITEMS>();
+    if (!coop ||
+        cudaFuncSetAttribute(bin_front_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             bytes) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bin_front_kernel<ITEMS>, kFeThreads,
+                                                      bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return sms * occ;
+}
+
+// Cooperative launch of bin_front_kernel (one sort tile per co-resident
+// CTA); false -> use the per-pass kernels (N too large, cooperative launch
+// unavailable, or SS_BIN_FRONT=0 in the environment).
+static bool front_end_launch(int64_t n, const ss_splats* sp, int tiles_x, const BinLayout& L,
+                             bool packed, int sbits, int64_t cap, ss_status* st, cudaStream_t s) {
+    static int cap2 = -1, cap4 = -1, cap8 = -1, enabled = -1;
+    if (enabled < 0) {
+        const char* env = getenv("SS_BIN_FRONT");
+        enabled = !(env && env[0] == '0');
+        cap2 = fe_capacity<2>();
+        cap4 = fe_capacity<4>();
+        cap8 = fe_capacity<8>();
+    }
+    if (!enabled) return false;
+    FeArgs a;
+    a.n = (uint32_t)n;
+    a.key_in = sp->d_depth_key;
+    a.kA = L.kA;
+    a.vA = L.vA;
+    a.kB = L.kB;
+    a.vB = L.vB;
+    a.counts = L.fe_counts;
+    a.chunk_sum = L.fe_chunk;
+    a.tiles = sp->d_tiles;
+    a.rect = reinterpret_cast<const uint2*>(sp->d_rect);
+    a.tiles_x = tiles_x;
+    a.pair_k = L.pk0;
+    a.pair_v = packed ? nullptr : L.pv0;
+    a.sb = sbits;
+    a.total = &st->pair_count;
+    a.overflow = &st->pair_overflow;
+    a.cap = cap;
+    a.pcount = L.pcount;
+    void* args[] = {&a};
+    auto go = [&](auto kern, int items, int capacity) -> bool {
+        const int64_t nft = div_up(n, (int64_t)kFeThreads * items);
+        if (nft > capacity || nft > 32 * kFeColChunks) return false;
+        a.n_tiles = (uint32_t)nft;
+        if (cudaLaunchCooperativeKernel((const void*)kern, (int)nft, kFeThreads, args,
+                                        fe_smem_bytes_rt(items), s) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return true;
+    };
+    return go(bin_front_kernel<2>, 2, cap2) || go(bin_front_kernel<4>, 4, cap4) ||
+           go(bin_front_kernel<8>, 8, cap8);
 }
 
 cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam,
@@ -567,6 +927,13 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
     int64_t* P = &st->pair_count;
     if (n > 0) {
         uint32_t nn = (uint32_t)n;
+        int sbits = 1, tbits = 1;
+        while ((1ll << sbits) < n) ++sbits;
+        while ((1ll << tbits) < n_tiles) ++tbits;
+        const bool packed = sbits + tbits <= 32;
+        if (front_end_launch(n, sp, tiles_x, L, packed, sbits, cap, st, s)) {
+            // depth sort + offsets + emission done by the persistent kernel
+        } else {
         // 1. depth sort of splats (4 stable 8-bit reduce-then-scan passes)
         const uint32_t* kin = sp->d_depth_key;
         const uint32_t* vin = nullptr;
@@ -584,14 +951,11 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
             &st->pair_overflow, cap);
         // 3. emission of (tile, splat) pairs in depth order; one packed
         //    32-bit word per pair when tile and splat ids fit
-        int sbits = 1, tbits = 1;
-        while ((1ll << sbits) < n) ++sbits;
-        while ((1ll << tbits) < n_tiles) ++tbits;
-        const bool packed = sbits + tbits <= 32;
         emit_pairs_kernel<<<div_up(n, 256), 256, 0, s>>>(
             nn, order, sp->d_tiles, reinterpret_cast<const uint2*>(sp->d_rect), L.offsets, tiles_x,
             P, cap, L.pk0, packed ? nullptr : L.pv0, sbits);
         clamp_count_kernel<<<1, 1, 0, s>>>(P, cap, L.pcount);
+        }
         // 4. stable sort of pairs by tile id
         const int np = tile_passes(n_tiles);
         const uint32_t* pk = L.pk0;

@@ -51,11 +51,14 @@ KERNELS_PER_CALL = {
 }
 
 
-def binning_kernels(n_tiles: int) -> int:
-    """clear + 4 depth passes x 3 + scan + emit + clamp + tile passes x 3 +
-    ranges + checkpoint-base scan (binning.cu)."""
+def binning_kernels(n_tiles: int, n: int = 0) -> int:
+    """clear + front end + tile passes x 3 + ranges + checkpoint-base scan
+    (binning.cu).  The front end (depth sort, pair offsets, emission) is one
+    cooperative kernel up to ~300k-1.2M splats, else 4 x 3 radix kernels +
+    scan + emit + clamp."""
     bits = max(1, (n_tiles - 1).bit_length())
-    return 1 + 4 * 3 + 1 + 1 + 1 + 3 * ((bits + 7) // 8) + 1 + 1
+    front = 1 if n <= 148 * 8192 else 4 * 3 + 1 + 1 + 1
+    return 1 + front + 3 * ((bits + 7) // 8) + 1 + 1
 
 
 @dataclass
@@ -298,7 +301,7 @@ class MappingEngine:
         self._snapshot(rec)
 
     def _launches_per_step(self):
-        k = (KERNELS_PER_CALL["step_fb"] + binning_kernels(self.n_tiles)
+        k = (KERNELS_PER_CALL["step_fb"] + binning_kernels(self.n_tiles, len(self.gmap))
              + KERNELS_PER_CALL["chain_adam"] + KERNELS_PER_CALL["snapshot"])
         if self.opts.with_depth and self.cfg.depth_weight:
             k += 3
