@@ -40,12 +40,15 @@ struct SplatAcc {
     float r0, r1, r2, rz, s_da, s_dx, s_dy, s_xx, s_xy, s_yy;
 };
 
-template <bool DEPTH>
+template <bool DEPTH, bool CLAMP>
 __device__ __forceinline__ void bwd_term(bool bit, float px, float py, const float4& pg, float gd,
                                          const float4& A, const float4& B, const float4& C,
                                          float amax, float& T, float& G, SplatAcc& q) {
     float dx, dy;
-    float a = splat_alpha_blended(px, py, A, B, amax, dx, dy);
+    // CLAMP == false: no splat of the unit has sigma >= alpha_max, so
+    // sigma * falloff < alpha_max and the clamp is the identity
+    float a = CLAMP ? splat_alpha_blended(px, py, A, B, amax, dx, dy)
+                    : splat_falloff(splat_power(px, py, A, B, dx, dy), B);
     a = bit ? a : 0.f;
     const float w = __fmul_rn(a, T);
     float grgb = pg.x * C.x + pg.y * C.y + pg.z * C.z;
@@ -61,7 +64,7 @@ __device__ __forceinline__ void bwd_term(bool bit, float px, float py, const flo
     // not blended: a = 0)
     const float om = __fsub_rn(1.0f, a);
     const float dal = T * grgb - (pg.w - Gafter) * rcp_approx(om);
-    const float da = dal * (a != amax ? a : 0.f);
+    const float da = dal * ((!CLAMP || a != amax) ? a : 0.f);
     const float tx = da * dx, ty = da * dy;
     q.s_da += da;
     q.s_dx += tx;
@@ -92,6 +95,43 @@ __device__ __forceinline__ void bwd_commit(const SplatAcc& q, const float4& A, c
 #pragma unroll
     for (int c = 0; c < NC; ++c)
         if (acc[c] != 0.f) atomicAdd(row + c, acc[c]);
+}
+
+// Diagonal wavefront over the warp's compacted pixel list; lane i applies
+// list positions 2i and 2i+1 to each pixel in turn.  Returns the lane's
+// blended-bit summary (bit 0: first splat blended somewhere, bit 1: second).
+template <bool DEPTH, bool CLAMP>
+__device__ __forceinline__ uint32_t bwd_wavefront(
+    int nact, int lane, bool hi, int sh, const float4* __restrict__ sG,
+    const float2* __restrict__ sS, const float2* __restrict__ sXY, const uint2* __restrict__ sM,
+    const float* __restrict__ sD, const float4& A0, const float4& B0, const float4& C0,
+    const float4& A1, const float4& B1, const float4& C1, float amax, SplatAcc& q0,
+    SplatAcc& q1) {
+    float T = 0.f, G = 0.f;
+    uint32_t seen = 0u;
+    const int steps = nact + 31;
+#pragma unroll 1
+    for (int st = 0; st < steps; ++st) {
+        T = __shfl_up_sync(0xffffffffu, T, 1);
+        G = __shfl_up_sync(0xffffffffu, G, 1);
+        const int j = st - lane;
+        if ((unsigned)j >= (unsigned)nact) continue;
+        const uint2 m = sM[j];
+        if (lane == 0) {
+            const float2 s = sS[j];
+            T = s.x;
+            G = s.y;
+        }
+        const uint32_t bits = ((hi ? m.y : m.x) >> sh) & 3u;
+        if (bits == 0u) continue;
+        seen |= bits;
+        const float2 xy = sXY[j];
+        const float4 pg = sG[j];
+        const float gd = DEPTH ? sD[j] : 0.f;
+        bwd_term<DEPTH, CLAMP>(bits & 1u, xy.x, xy.y, pg, gd, A0, B0, C0, amax, T, G, q0);
+        bwd_term<DEPTH, CLAMP>(bits & 2u, xy.x, xy.y, pg, gd, A1, B1, C1, amax, T, G, q1);
+    }
+    return seen;
 }
 
 template <bool DEPTH>
@@ -199,30 +239,18 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
         //   d mean  = (c0 S_dx + c1 S_dy, c1 S_dx + c2 S_dy),  S_d. = sum da d.
         //   d conic = -1/2 (S_dxdx, 2 S_dxdy, S_dydy),        d sigma = S_da / sigma
         SplatAcc q0 = {}, q1 = {};
-        float T = 0.f, G = 0.f;
-        uint32_t seen = 0u;
-        const int steps = nact + 31;
-#pragma unroll 1
-        for (int st = 0; st < steps; ++st) {
-            T = __shfl_up_sync(0xffffffffu, T, 1);
-            G = __shfl_up_sync(0xffffffffu, G, 1);
-            const int j = st - lane;
-            if ((unsigned)j >= (unsigned)nact) continue;
-            const uint2 m = sM[wid][j];
-            if (lane == 0) {
-                const float2 s = sS[wid][j];
-                T = s.x;
-                G = s.y;
-            }
-            const uint32_t bits = ((hi ? m.y : m.x) >> sh) & 3u;
-            if (bits == 0u) continue;
-            seen |= bits;
-            const float2 xy = sXY[wid][j];
-            const float4 pg = sG[wid][j];
-            const float gd = DEPTH ? sD[wid][j] : 0.f;
-            bwd_term<DEPTH>(bits & 1u, xy.x, xy.y, pg, gd, A0, B0, C0, amax, T, G, q0);
-            bwd_term<DEPTH>(bits & 2u, xy.x, xy.y, pg, gd, A1, B1, C1, amax, T, G, q1);
-        }
+        uint32_t seen;
+        // the clamp at alpha_max can only bind for splats with sigma >= alpha_max
+        const bool clamp = __any_sync(0xffffffffu, (k0 < ke && B0.y >= amax * 0.999999f) ||
+                                                       (k1 < ke && B1.y >= amax * 0.999999f));
+        if (clamp)
+            seen = bwd_wavefront<DEPTH, true>(nact, lane, hi, sh, sG[wid], sS[wid], sXY[wid],
+                                              sM[wid], DEPTH ? sD[wid] : nullptr, A0, B0, C0, A1,
+                                              B1, C1, amax, q0, q1);
+        else
+            seen = bwd_wavefront<DEPTH, false>(nact, lane, hi, sh, sG[wid], sS[wid], sXY[wid],
+                                               sM[wid], DEPTH ? sD[wid] : nullptr, A0, B0, C0, A1,
+                                               B1, C1, amax, q0, q1);
         if (k0 < ke) {
             bwd_commit<NC>(q0, A0, B0, g2d + (size_t)s0 * NC);
             if (contributed && (seen & 1u)) contributed[s0] = 1;
