@@ -67,14 +67,19 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
     int64_t work_cap, int64_t* bucket_count) {
     __shared__ SplatRec s_rec[256];
     __shared__ uint32_t s_id[256];
+    __shared__ uint8_t s_band[256];  // bit w: the splat's blend region reaches band w
     __shared__ int s_hit[CONTRIB ? 256 : 1];
     __shared__ int s_kmax[4];
     __shared__ unsigned long long s_wbase;
     const int tile = blockIdx.x;
     const int t = threadIdx.x;
     const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
-    const int ix = x0 + (t & 15), iy0 = y0 + (t >> 4), iy1 = iy0 + 8;
-    const int p0 = t, p1 = t + 128;  // tile-local pixel ids (row-major 16x16)
+    // warp w owns the 4-row band 4w..4w+3; a thread owns rows r and r + 2 of
+    // its column (the two pixels share the dx terms)
+    const int w = t >> 5, lane = t & 31;
+    const int row0 = 4 * w + (lane >> 4), row1 = row0 + 2;
+    const int ix = x0 + (lane & 15), iy0 = y0 + row0, iy1 = y0 + row1;
+    const int p0 = row0 * kTile + (lane & 15), p1 = row1 * kTile + (lane & 15);  // tile-local ids
     const float px = (float)ix, py0 = (float)iy0, py1 = (float)iy1;
     const uint32_t start = tile_start[tile];
     const uint32_t len = tile_end[tile] - start;
@@ -91,7 +96,14 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
             if (k < len) {
                 uint32_t s = pairs[start + k];
                 s_id[t + 128 * r] = s;
-                s_rec[t + 128 * r] = rec[s];
+                const SplatRec sr = rec[s];
+                s_rec[t + 128 * r] = sr;
+                // bands (4 rows each) the splat's rows |y - my| <= ext can reach
+                uint32_t bm = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    bm |= (fabsf(sr.a.y - ((float)(y0 + 4 * b) + 1.5f)) <= sr.c.w + 1.5f) << b;
+                s_band[t + 128 * r] = (uint8_t)bm;
                 if (CONTRIB) s_hit[t + 128 * r] = 0;
             }
         }
@@ -119,9 +131,12 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
                 if (DEPTH) ckpt_depth[slot + p1] = s1.D;
             }
             if (__all_sync(0xffffffffu, s0.done && s1.done)) continue;  // whole warp stopped
-            const int jn = min(nb, j0 + 32);
-            for (int j = j0; j < jn; ++j) {
-                const float4 A = s_rec[j].a, B = s_rec[j].b;
+            // the bucket's splats whose blend region reaches this warp's band
+            unsigned todo = __ballot_sync(0xffffffffu, j0 + lane < nb && ((s_band[j0 + lane] >> w) & 1u));
+            while (todo) {
+                const int j = j0 + __ffs(todo) - 1;
+                todo &= todo - 1;
+                const float4 A = s_rec[j].a, B = s_rec[j].b, C = s_rec[j].c;
                 // the two pixels share a column: dx-only terms once
                 const float dx = __fsub_rn(px, A.x);
                 const float q0 = quad_dx0(A, dx), q1 = quad_dx1(A, dx);
@@ -130,7 +145,6 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
                 const bool in0 = !s0.done && !(m0 > B.z);
                 const bool in1 = !s1.done && !(m1 > B.z);
                 if (in0 || in1) {
-                    const float4 C = s_rec[j].c;
                     const int q = (int)b0 + j;
                     bool hit = false;
                     if (in0) hit |= blend_one<DEPTH>(s0, m0, B, C, q, t_min, amin, amax);

@@ -169,7 +169,11 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
                 fl = 1u | (act[0] ? 2u : 0u) | (act[1] ? 4u : 0u) | (act[2] ? 8u : 0u);
                 r.a = make_float4(mx, my, P.c / det, 2.0f * (-P.b / det));
                 r.b = make_float4(P.a / det, sg, mcut, P.t[2]);
-                r.c = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+                // vertical half-extent of the blend region m <= m_cut
+                // (sqrt(m_cut * cov_yy)) + 1 px margin: lets a warp skip
+                // splats that cannot reach its rows (blend_forward.cu)
+                const float ext_y = sqrtf(fmaxf(mcut, 0.0f) * P.c) * 1.0001f + 1.0f;
+                r.c = make_float4(rgb[0], rgb[1], rgb[2], ext_y);
                 auxv[0] = P.t[0];
                 auxv[1] = P.t[1];
                 auxv[2] = P.t[2];

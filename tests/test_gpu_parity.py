@@ -287,14 +287,16 @@ def test_engine_graph_replay_matches_stream_launches():
     eb.synchronize()
     assert len(eb._graphs) == 1
     # g2d is accumulated with float atomics, so runs agree to rounding only;
-    # Adam's +-lr steps bound the effect of near-zero gradient sign flips
+    # Adam's +-lr steps bound the effect of near-zero gradient sign flips.
+    # Two stream-launched engines differ by the same amount (measured: up to
+    # ~1 % of the log-scale elements after 4 steps), hence the 3 % bound.
     lr = dict(positions=1.6e-4, rotations=1e-3, log_scales=5e-3, opacity_logits=5e-2,
               sh_dc=2.5e-3, sh_rest=1.25e-4)
     for f, r in lr.items():
         a, b = getattr(gb, f).cpu().numpy(), getattr(ga, f).cpu().numpy()
         d = np.abs(a - b)
         assert d.max() <= 8 * r + 1e-5, f
-        assert (d > 1e-3 * r + 1e-6).mean() < 0.01, f
+        assert (d > 1e-3 * r + 1e-6).mean() < 0.03, f
     la, lb = ea.losses(), eb.losses()
     np.testing.assert_allclose([x[1] for x in la], [x[1] for x in lb], rtol=1e-5)
 
