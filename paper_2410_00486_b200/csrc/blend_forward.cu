@@ -25,6 +25,8 @@
 // The CTA also emits k_eff (kernels.py:86-87,109) and appends its
 // ceil(k_eff/64) (tile, unit) entries to the splat-wise backward work list
 // (a unit = two checkpoint buckets, one warp, two list positions per lane).
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace ss {
@@ -98,11 +100,15 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
                 s_id[t + 128 * r] = s;
                 const SplatRec sr = rec[s];
                 s_rec[t + 128 * r] = sr;
-                // bands (4 rows each) the splat's rows |y - my| <= ext can reach
+                // bands (4 rows each) the splat's blend region can reach:
+                // |y - my| <= ext_y within the band, |x - mx| <= ext_x within
+                // the tile's columns
+                const float2 ext = __half22float2(*reinterpret_cast<const __half2*>(&sr.c.w));
+                const bool xin = fabsf(sr.a.x - ((float)x0 + 7.5f)) <= ext.x + 7.5f;
                 uint32_t bm = 0;
 #pragma unroll
                 for (int b = 0; b < 4; ++b)
-                    bm |= (fabsf(sr.a.y - ((float)(y0 + 4 * b) + 1.5f)) <= sr.c.w + 1.5f) << b;
+                    bm |= (xin && fabsf(sr.a.y - ((float)(y0 + 4 * b) + 1.5f)) <= ext.y + 1.5f) << b;
                 s_band[t + 128 * r] = (uint8_t)bm;
                 if (CONTRIB) s_hit[t + 128 * r] = 0;
             }

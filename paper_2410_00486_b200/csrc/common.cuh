@@ -26,7 +26,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 struct __align__(16) SplatRec {
     float4 a;  // mean2d.x, mean2d.y, conic[0], 2 * conic[1]
     float4 b;  // conic[2], sigma, m_cut, depth (camera-frame z)
-    float4 c;  // r, g, b, vertical half-extent of the blend region (+1 px margin)
+    float4 c;  // r, g, b, half2 (x, y) half-extents of the blend region (+1 px, rounded up)
 };
 
 // Pixel-state checkpoint (T, r, g, b) archived before every 32nd list

@@ -8,6 +8,8 @@
 // Also folds rasterize_forward's finite-parameter check (api.py:127-129,
 // core.py:231-241) and the zero-quaternion check (projection.py:99-102)
 // into device error words.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "sh.cuh"
 
@@ -169,11 +171,15 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
                 fl = 1u | (act[0] ? 2u : 0u) | (act[1] ? 4u : 0u) | (act[2] ? 8u : 0u);
                 r.a = make_float4(mx, my, P.c / det, 2.0f * (-P.b / det));
                 r.b = make_float4(P.a / det, sg, mcut, P.t[2]);
-                // vertical half-extent of the blend region m <= m_cut
-                // (sqrt(m_cut * cov_yy)) + 1 px margin: lets a warp skip
+                // half-extents of the blend region m <= m_cut
+                // (sqrt(m_cut * cov_xx), sqrt(m_cut * cov_yy)) + 1 px margin,
+                // as a half2 rounded up: lets a warp of the forward skip
                 // splats that cannot reach its rows (blend_forward.cu)
+                const float ext_x = sqrtf(fmaxf(mcut, 0.0f) * P.a) * 1.0001f + 1.0f;
                 const float ext_y = sqrtf(fmaxf(mcut, 0.0f) * P.c) * 1.0001f + 1.0f;
-                r.c = make_float4(rgb[0], rgb[1], rgb[2], ext_y);
+                const __half2 ext = __halves2half2(__float2half_ru(fminf(ext_x, 60000.f)),
+                                                   __float2half_ru(fminf(ext_y, 60000.f)));
+                r.c = make_float4(rgb[0], rgb[1], rgb[2], *reinterpret_cast<const float*>(&ext));
                 auxv[0] = P.t[0];
                 auxv[1] = P.t[1];
                 auxv[2] = P.t[2];
