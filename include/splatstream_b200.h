@@ -217,6 +217,18 @@ typedef struct ss_param_grads {
 #define SS_CHAIN_ACCUMULATE 2  /* add into grads (multi-view sum) instead of overwriting */
 #define SS_CHAIN_STAT_PLANES 4 /* add statistics increments into grads->d_stat_* */
 
+/* Replaces backward_pixelwise up to g2d (api.py:227-272,
+ * backward_pixel_tile kernels.py:181-268): pixel-parallel, no checkpoints
+ * needed -- every pixel re-runs its forward prefix up to n_contrib; per
+ * splat, the tile's pixel contributions are reduced across each warp and
+ * merged as one row per (tile, list position).  The paper's ablation
+ * baseline for ss_backward_splat (same per-(pixel, splat) terms).  d_g2d
+ * [n * 9] float is zeroed here.  opts->with_depth must be 0. */
+int ss_backward_pixel(const ss_camera *cam, const ss_raster_opts *opts, const ss_splats *splats,
+                      const ss_bins *bins, const float *d_image, const float *d_grad_image,
+                      const int32_t *d_n_contrib, const int32_t *d_k_eff, int64_t n,
+                      float *d_g2d, void *stream);
+
 /* Replaces chain_backward (projection.py:200-299) + _finish_backward
  * (api.py:217-224).  Options: add the opacity regulariser's gradient
  * lambda_o sigma(1-sigma)/n to every Gaussian (trainer.py:206,

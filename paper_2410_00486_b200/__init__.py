@@ -15,7 +15,8 @@ from .engine import EngineConfig, MappingEngine
 from .losses import LossBreakdown, compute_losses, depth_l1, opacity_reg, total_loss
 from .optimizer import AdamState, LearningRates, adam_step, resize_for_densify
 from .rasterizer import (ParamGrads, Projection, RasterOpts, RenderOutput, TileIndex,
-                         backward_splatwise, rasterize_forward, screen_space_grads)
+                         backward_pixelwise, backward_splatwise, rasterize_forward,
+                         screen_space_grads, screen_space_grads_pixelwise)
 from .scene import CONFIGS, survey_camera, survey_scene
 
 __version__ = "0.1.0"
@@ -24,7 +25,7 @@ __all__ = [
     "AdamState", "Camera", "CONFIGS", "DensifyConfig", "DensifyResult", "EngineConfig",
     "GaussianMap", "LearningRates", "LossBreakdown", "MappingEngine", "ParamGrads", "Projection",
     "RasterOpts", "RenderOutput", "TileIndex", "accumulate_grad_stats", "adam_step",
-    "backward_splatwise", "compute_losses", "densify_and_prune", "depth_l1", "logistic", "logit",
+    "backward_pixelwise", "backward_splatwise", "compute_losses", "densify_and_prune", "depth_l1", "logistic", "logit",
     "opacity_reg", "opacity_reset", "rasterize_forward", "resize_for_densify",
-    "screen_space_grads", "survey_camera", "survey_scene", "total_loss",
+    "screen_space_grads", "screen_space_grads_pixelwise", "survey_camera", "survey_scene", "total_loss",
 ]

@@ -22,6 +22,9 @@ cudaError_t launch_backward_splat(const ss_camera*, const ss_raster_opts*, const
                                   const void*, const float*, const uint32_t*, const uint32_t*,
                                   int64_t, int64_t, float*, uint8_t*, const ss_status*, uint32_t*,
                                   cudaStream_t);
+cudaError_t launch_backward_pixel(const ss_camera*, const ss_raster_opts*, const ss_splats*,
+                                  const ss_bins*, const float*, const float*, const int32_t*,
+                                  const int32_t*, int64_t, float*, cudaStream_t);
 size_t loss_workspace_bytes(int, int);
 cudaError_t launch_loss(int, int, const float*, const float*, float, float*, float*, double*,
                         void*, size_t, cudaStream_t);
@@ -211,6 +214,17 @@ int ss_backward_splat(const ss_camera* cam, const ss_raster_opts* opts, const ss
                                     d_grad_depth, d_n_contrib, d_k_eff, d_ckpt, d_ckpt_depth,
                                     d_ckpt_mask, d_work, work_capacity, n, d_g2d, d_contributed,
                                     d_status, counter, S(stream)));
+}
+
+int ss_backward_pixel(const ss_camera* cam, const ss_raster_opts* opts, const ss_splats* splats,
+                      const ss_bins* bins, const float* d_image, const float* d_grad_image,
+                      const int32_t* d_n_contrib, const int32_t* d_k_eff, int64_t n,
+                      float* d_g2d, void* stream) {
+    if (!cam || !opts_ok(opts) || opts->with_depth || !splats || !bins || !d_image ||
+        !d_grad_image || !d_n_contrib || !d_k_eff || !d_g2d || n < 0)
+        return SS_EINVAL;
+    return rc(launch_backward_pixel(cam, opts, splats, bins, d_image, d_grad_image, d_n_contrib,
+                                    d_k_eff, n, d_g2d, S(stream)));
 }
 
 int ss_chain_backward(const ss_map* map, const ss_camera* cam, const ss_raster_opts* opts,

@@ -409,6 +409,33 @@ def backward_splatwise(render: RenderOutput, grad_image, n_workers=None,
     return _finish_backward(render, g2d)
 
 
+def screen_space_grads_pixelwise(render: RenderOutput, grad_image):
+    """F2 (api.py:227-272): the pixel-parallel backward up to the screen-space
+    rows g2d (N, 9), the paper's ablation baseline for the splat-wise K7."""
+    if render.opts.with_depth:
+        raise ValueError("backward_pixelwise does not support the depth extension")
+    dev = render.image.device
+    if tuple(grad_image.shape) != tuple(render.image.shape):
+        raise ValueError(f"grad_image shape {tuple(grad_image.shape)} does not match "
+                         f"rendered image shape {tuple(render.image.shape)}")
+    g = _as_image(grad_image, render.image.shape, dev)
+    n = render.n_primitives
+    g2d = torch.empty((max(n, 1), 9), dtype=torch.float32, device=dev)
+    cm, op = render.camera.to_ss(), render.opts.to_ss()
+    check(lib().ss_backward_pixel(
+        ctypes.byref(cm), ctypes.byref(op), ctypes.byref(render.splats.ss()),
+        ctypes.byref(render.bins.ss()), P(render.image), P(g), P(render.n_contrib),
+        P(render.k_eff_tiles), n, P(g2d), stream_handle()), "ss_backward_pixel")
+    return g2d[:n]
+
+
+def backward_pixelwise(render: RenderOutput, grad_image, n_workers=None) -> ParamGrads:
+    """api.py:227-272: pixel-parallel backward + K8 chain to parameters (the
+    reference's alternative to backward_splatwise; no checkpoints needed)."""
+    g2d = screen_space_grads_pixelwise(render, grad_image)
+    return _finish_backward(render, g2d)
+
+
 def _finish_backward(render: RenderOutput, g2d) -> ParamGrads:
     """api.py:217-224: chain_backward + validate_finite."""
     n = render.n_primitives

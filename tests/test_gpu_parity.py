@@ -179,6 +179,31 @@ def test_backward_g2d_matches_oracle(case):
         assert normwise(a, b) <= 1e-3, cols
 
 
+def test_backward_pixelwise_matches_oracle_and_splatwise(case):
+    """F2 pixel-wise backward (api.py:227-272): g2d vs the oracle's
+    backward_pixel_tile restatement fed the same float32 render, and vs the
+    splat-wise K7 (the same per-(pixel, splat) terms, other summation order)."""
+    if case["opts"].with_depth:
+        pytest.skip("depth extension not in the pixel-wise path")
+    ss, out = case["ss"], case["out"]
+    rng = np.random.default_rng(3)
+    gimg = rng.standard_normal(out.image.shape).astype(np.float32) * 1e-3
+    gt = torch.as_tensor(gimg, device="cuda")
+    px = ss.screen_space_grads_pixelwise(out, gt).cpu().numpy().astype(np.float64)
+    sw = ss.screen_space_grads(out, gt).cpu().numpy().astype(np.float64)
+    r = _oracle_render_on_gpu_inputs(case)
+    ref = orc.backward_pixel(r, gimg.astype(np.float64))
+    mi = out.proj.map_index
+    for cols in ([0, 1, 2], [3, 4], [5, 6, 7], [8]):
+        assert normwise(px[mi][:, cols], ref[:, cols]) <= 1e-3, cols
+        assert normwise(px[:, cols], sw[:, cols]) <= 1e-4, cols
+    grads = ss.backward_pixelwise(out, gt)
+    gs = ss.backward_splatwise(out, gt)
+    for name in ("position", "rotation", "log_scale", "opacity_logit"):
+        assert normwise(getattr(grads, name).cpu().numpy(),
+                        getattr(gs, name).cpu().numpy()) <= 1e-4, name
+
+
 def test_chain_matches_oracle(case):
     """K8 vs chain_backward on the same g2d."""
     ss, out, cam, deg = case["ss"], case["out"], case["cam"], case["deg"]
