@@ -12,11 +12,13 @@ from .core import Camera, GaussianMap, logistic, logit
 from .densify import (DensifyConfig, DensifyResult, accumulate_grad_stats, densify_and_prune,
                       opacity_reset)
 from .engine import EngineConfig, MappingEngine
-from .losses import LossBreakdown, compute_losses, depth_l1, opacity_reg, total_loss
+from .losses import (LossBreakdown, compute_losses, depth_l1, opacity_reg, psnr, ssim_metric,
+                     total_loss)
 from .optimizer import AdamState, LearningRates, adam_step, resize_for_densify
 from .rasterizer import (ParamGrads, Projection, RasterOpts, RenderOutput, TileIndex,
                          backward_pixelwise, backward_splatwise, rasterize_forward,
-                         screen_space_grads, screen_space_grads_pixelwise)
+                         render_trajectory, screen_space_grads, screen_space_grads_pixelwise)
+from .scheduler import KeyframeScheduler, ScheduledMapper
 from .scene import CONFIGS, survey_camera, survey_scene
 
 __version__ = "0.1.0"
@@ -26,6 +28,7 @@ __all__ = [
     "GaussianMap", "LearningRates", "LossBreakdown", "MappingEngine", "ParamGrads", "Projection",
     "RasterOpts", "RenderOutput", "TileIndex", "accumulate_grad_stats", "adam_step",
     "backward_pixelwise", "backward_splatwise", "compute_losses", "densify_and_prune", "depth_l1", "logistic", "logit",
-    "opacity_reg", "opacity_reset", "rasterize_forward", "resize_for_densify",
+    "KeyframeScheduler", "ScheduledMapper", "opacity_reg", "opacity_reset", "psnr",
+    "rasterize_forward", "render_trajectory", "resize_for_densify", "ssim_metric",
     "screen_space_grads", "screen_space_grads_pixelwise", "survey_camera", "survey_scene", "total_loss",
 ]

@@ -55,6 +55,34 @@ def photometric(rendered: torch.Tensor, target: torch.Tensor, lambda_ssim: float
     return ws
 
 
+PSNR_CAP_DB = 100.0
+
+
+def ssim_metric(a, b) -> float:
+    """losses.py:176-182: mean local SSIM over pixels and channels (the K6
+    forward's SSIM sum; images of at least 6 x 6 pixels)."""
+    dev = a.device if isinstance(a, torch.Tensor) else torch.device("cuda")
+    x, y = _img(a, dev), _img(b, dev)
+    if x.shape != y.shape or x.dim() != 3 or x.shape[2] != 3:
+        raise ValueError(f"image shapes {tuple(x.shape)} and {tuple(y.shape)} must match (H,W,3)")
+    sums = torch.zeros(_lib.SS_REDUCE_DOUBLES, dtype=torch.float64, device=dev)
+    photometric(x, y, 1.0, torch.empty_like(x), sums)
+    return float(sums[1].item()) / x.numel()
+
+
+def psnr(a, b) -> float:
+    """losses.py:112-116: PSNR in dB for [0, 1] images, capped at 100 dB
+    (evaluation metric, off the mapping path: a device reduction)."""
+    dev = a.device if isinstance(a, torch.Tensor) else torch.device("cuda")
+    x, y = _img(a, dev), _img(b, dev)
+    if x.shape != y.shape:
+        raise ValueError(f"image shapes {tuple(x.shape)} and {tuple(y.shape)} must match")
+    mse = float(((x.double() - y.double()) ** 2).mean().item())
+    if mse < 1e-10:
+        return PSNR_CAP_DB
+    return min(PSNR_CAP_DB, 10.0 * float(np.log10(1.0 / mse)))
+
+
 def compute_losses(rendered, target, opacity_logits, lambda_ssim: float = 0.2,
                    lambda_o: float = 0.001) -> LossBreakdown:
     """losses.py:198-228."""

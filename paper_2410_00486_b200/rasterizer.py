@@ -12,6 +12,7 @@ C-ABI calls on the current CUDA stream.
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -371,6 +372,13 @@ class ParamGrads:
         if not (bool(torch.isfinite(self.sh_dc).all()) and bool(torch.isfinite(self.sh_rest).all())):
             raise FloatingPointError("non-finite gradient in sh")
         return self
+
+
+def render_trajectory(gmap: GaussianMap, cameras, opts: RasterOpts | None = None):
+    """trainer.py:271-279: one image per camera, forward only (no checkpoints)."""
+    opts = opts if opts is not None else RasterOpts()
+    opts = dataclasses.replace(opts, with_checkpoints=False)
+    return [rasterize_forward(gmap, cam, opts).image for cam in cameras]
 
 
 def screen_space_grads(render: RenderOutput, grad_image, grad_depth=None):

@@ -228,6 +228,43 @@ def capture_loss_odd():
     print("loss_small done")
 
 
+def capture_scheduler_and_metrics():
+    """KeyframeScheduler traces (scheduler.py:22-89) and the eval metrics
+    psnr / ssim_metric (losses.py:112-116,176-182) evaluated by the reference."""
+    from splatstream.scheduler import KeyframeScheduler
+
+    def loss_of(kf, step):
+        return 1.0 / (1.0 + kf) + 0.01 * ((step * 7919) % 13)
+
+    out = {}
+    for d, r0, seed in ((4, 8, 0), (2, 3, 7)):
+        sch = KeyframeScheduler(d=d, r0=r0, seed=seed)
+        picks = []
+        for step in range(240):
+            if step % 10 == 0:
+                sch.add_keyframe(step // 10)
+            kf = sch.select()
+            picks.append(int(kf))
+            sch.record_result(kf, loss_of(kf, step))
+        out[f"select_d{d}_r{r0}_s{seed}"] = picks
+        out[f"remaining_d{d}_r{r0}_s{seed}"] = [int(r) for r in sch.remaining]
+        base = KeyframeScheduler(d=d, r0=r0, seed=seed)
+        for k in range(5):
+            base.add_keyframe(k)
+        out[f"uniform_d{d}_r{r0}_s{seed}"] = [int(base.select_uniform_baseline())
+                                              for _ in range(50)]
+    rng = np.random.default_rng(11)
+    a = rng.random((20, 24, 3))
+    b = np.clip(a + 0.05 * rng.standard_normal(a.shape), 0, 1)
+    out["metrics_a"] = a.tolist()
+    out["metrics_b"] = b.tolist()
+    out["psnr_ab"] = ss.psnr(a, b)
+    out["ssim_metric_ab"] = ss.ssim_metric(a, b)
+    with open(os.path.join(HERE, "scheduler_metrics.json"), "w") as f:
+        json.dump(out, f)
+    print("scheduler/metrics done")
+
+
 if __name__ == "__main__":
     capture_iteration("iter_sh0_small", 800, 64, 48, 0, seed=0)
     capture_iteration("iter_sh3_small", 600, 48, 40, 3, seed=1, view=1, n_views=3)
@@ -236,4 +273,5 @@ if __name__ == "__main__":
     capture_densify()
     capture_loss_odd()
     known_answers()
+    capture_scheduler_and_metrics()
     _ = ref_losses

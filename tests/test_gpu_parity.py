@@ -532,3 +532,31 @@ def test_two_splat_known_answer():
     np.testing.assert_allclose(out.image.cpu().numpy()[8, 8], [0.5, 0.25, 0.0], atol=1e-6)
     assert abs(float(out.final_t[8, 8]) - 0.25) < 1e-6
     assert int(out.n_contrib[8, 8]) == 2
+
+
+def test_eval_metrics_and_trajectory_match_reference():
+    """F4: psnr / ssim_metric (losses.py:112-116,176-182) vs the reference's
+    values (tests/golden/scheduler_metrics.json, known_answers.json), and
+    render_trajectory (trainer.py:271-279) = forward-only renders."""
+    _need_gpu()
+    import json
+    import os
+    import paper_2410_00486_b200 as ss
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    with open(os.path.join(here, "scheduler_metrics.json")) as f:
+        gm = json.load(f)
+    with open(os.path.join(here, "known_answers.json")) as f:
+        ka = json.load(f)
+    a, b = np.array(gm["metrics_a"]), np.array(gm["metrics_b"])
+    assert abs(ss.psnr(a, b) - gm["psnr_ab"]) <= 1e-4
+    assert abs(ss.ssim_metric(a, b) - gm["ssim_metric_ab"]) <= 1e-5
+    z, o = np.zeros((16, 16, 3)), np.ones((16, 16, 3))
+    assert abs(ss.ssim_metric(z, o) - ka["ssim_const_0_1"]) <= 1e-5
+    assert ss.psnr(z, z) == ka["psnr_same"]
+    assert abs(ss.psnr(z, np.full_like(z, 0.1)) - ka["psnr_mse_0.01"]) <= 1e-4
+    d = load("iter_sh0_small")
+    cam = fixture_camera(d)
+    g = ss.GaussianMap.from_arrays(*fixture_scene(d))
+    imgs = ss.render_trajectory(g, [cam, cam], ss.RasterOpts(sh_degree=0))
+    ref = ss.rasterize_forward(g, cam, ss.RasterOpts(sh_degree=0)).image
+    assert len(imgs) == 2 and torch.equal(imgs[0], ref) and torch.equal(imgs[1], ref)
