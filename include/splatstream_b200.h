@@ -285,6 +285,22 @@ int ss_chain_adam(const ss_map *map, const ss_camera *cam, const ss_camera *d_ca
 int ss_accumulate_grad_stats(const ss_map *map, const ss_param_grads *grads,
                              const uint8_t *d_contributed, void *stream);
 
+/* ----------------------------------------------------------- seeding */
+/* Replaces seed_from_points (densify.py:53-83) for a keyframe's point
+ * cloud: d_points / d_colors (n,3) float32; outputs position (n,3),
+ * rotation (n,4) = (1,0,0,0), log_scale (n,3) = log(max(mean distance to the
+ * 3 nearest neighbours within the cloud, 1e-4)) (0.01 * scene_extent for a
+ * lone point), opacity logit (n) = logit(0.1), sh_dc (n,3) = (c - 0.5) /
+ * SH_C0.  Exact kNN (float64 distances) on a uniform cell grid.
+ * *d_nonfinite (device int32) is set to 1 when a point is non-finite
+ * (ValueError("non-finite point in seed cloud") in the reference). */
+size_t ss_seed_workspace_bytes(int64_t n);
+int ss_seed_from_points(int64_t n, const float *d_points, const float *d_colors,
+                        float scene_extent, float *d_positions, float *d_rotations,
+                        float *d_log_scales, float *d_opacity_logits, float *d_sh_dc,
+                        int32_t *d_nonfinite, void *d_workspace, size_t workspace_bytes,
+                        void *stream);
+
 /* ------------------------------------------------------------- densify */
 /* densify_and_prune (densify.py:103-173) as stream compaction, phase 1:
  * masks in float64 from the stored values (densify.py:110-117,148,158) and

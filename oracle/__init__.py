@@ -774,3 +774,39 @@ def multiview_grads(gmap: OMap, cams, targets, sh_degree=0, lambda_ssim=0.2, lam
 
 __all__ = [n for n in dir() if not n.startswith("_")]
 _ = math
+
+
+# ---------------------------------------------------------------- seeding
+
+def seed_from_points(points, colors, scene_extent=1.0):
+    """seed_from_points (densify.py:53-83): one isotropic primitive per point,
+    scale = mean distance to the 3 nearest neighbours within the cloud
+    (brute-force float64 kNN in chunks: the k + 1 smallest distances
+    including the point itself, self dropped, as cKDTree.query(k=4)[:, 1:]),
+    floored at 1e-4 (a lone point: 0.01 * scene_extent); identity rotation,
+    opacity logit(0.1), DC colour (c - 0.5) / SH_C0."""
+    p = np.asarray(points, np.float64).reshape(-1, 3)
+    c = np.asarray(colors, np.float64).reshape(-1, 3)
+    n = p.shape[0]
+    if n == 0:
+        return (np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 3)), np.zeros(0),
+                np.zeros((0, 16, 3)))
+    if not np.isfinite(p).all():
+        raise ValueError("non-finite point in seed cloud")
+    if n == 1:
+        md = np.array([0.01 * scene_extent])
+    else:
+        k = min(3, n - 1)
+        md = np.empty(n)
+        for a in range(0, n, 512):
+            d2 = ((p[a:a + 512, None, :] - p[None, :, :]) ** 2).sum(-1)
+            part = np.sqrt(np.partition(d2, k, axis=1)[:, :k + 1])
+            part.sort(axis=1)
+            md[a:a + 512] = part[:, 1:].mean(axis=1)
+    ls = np.log(np.maximum(md, 1e-4))[:, None].repeat(3, axis=1)
+    rot = np.zeros((n, 4))
+    rot[:, 0] = 1.0
+    op = np.full(n, np.log(0.1 / 0.9))
+    sh = np.zeros((n, 16, 3))
+    sh[:, 0, :] = (c - 0.5) / 0.28209479177387814
+    return p.copy(), rot, ls, op, sh

@@ -10,7 +10,7 @@ the CUDA library or device is missing.
 
 from .core import Camera, GaussianMap, logistic, logit
 from .densify import (DensifyConfig, DensifyResult, accumulate_grad_stats, densify_and_prune,
-                      opacity_reset)
+                      opacity_reset, seed_from_points)
 from .engine import EngineConfig, MappingEngine
 from .losses import (LossBreakdown, compute_losses, depth_l1, opacity_reg, psnr, ssim_metric,
                      total_loss)
@@ -29,6 +29,7 @@ __all__ = [
     "RasterOpts", "RenderOutput", "TileIndex", "accumulate_grad_stats", "adam_step",
     "backward_pixelwise", "backward_splatwise", "compute_losses", "densify_and_prune", "depth_l1", "logistic", "logit",
     "KeyframeScheduler", "ScheduledMapper", "opacity_reg", "opacity_reset", "psnr",
-    "rasterize_forward", "render_trajectory", "resize_for_densify", "ssim_metric",
+    "rasterize_forward", "render_trajectory", "resize_for_densify", "seed_from_points",
+    "ssim_metric",
     "screen_space_grads", "screen_space_grads_pixelwise", "survey_camera", "survey_scene", "total_loss",
 ]

@@ -226,6 +226,23 @@ class GaussianMap:
             setattr(self, f, torch.cat([getattr(self, f), getattr(other, f)]).contiguous())
         return self
 
+    def insert_device(self, positions, rotations, log_scales, opacity_logits, sh_dc,
+                      sh_rest=None):
+        """insert_arrays for float32 device tensors (no host round trip);
+        sh_rest defaults to zeros (seeded primitives, densify.py:79-81)."""
+        n = int(positions.shape[0])
+        if sh_rest is None:
+            sh_rest = torch.zeros((n, 45), dtype=torch.float32, device=self.device)
+        new = dict(positions=positions.reshape(n, 3), rotations=rotations.reshape(n, 4),
+                   log_scales=log_scales.reshape(n, 3), opacity_logits=opacity_logits.reshape(n),
+                   sh_dc=sh_dc.reshape(n, 3), sh_rest=sh_rest.reshape(n, 45),
+                   grad2d_accum=torch.zeros(n, dtype=torch.float32, device=self.device),
+                   grad3d_accum=torch.zeros((n, 3), dtype=torch.float32, device=self.device),
+                   obs_count=torch.zeros(n, dtype=torch.int32, device=self.device))
+        for f in self.FIELDS:
+            setattr(self, f, torch.cat([getattr(self, f), new[f]]).contiguous())
+        return self
+
     def ss(self) -> _lib.SSMap:
         m = _lib.SSMap()
         m.n = len(self)

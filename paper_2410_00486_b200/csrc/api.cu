@@ -25,6 +25,9 @@ cudaError_t launch_backward_splat(const ss_camera*, const ss_raster_opts*, const
 cudaError_t launch_backward_pixel(const ss_camera*, const ss_raster_opts*, const ss_splats*,
                                   const ss_bins*, const float*, const float*, const int32_t*,
                                   const int32_t*, int64_t, float*, cudaStream_t);
+size_t seed_workspace_bytes(int64_t);
+cudaError_t launch_seed(int64_t, const float*, const float*, float, float*, float*, float*,
+                        float*, float*, int32_t*, void*, size_t, cudaStream_t);
 size_t loss_workspace_bytes(int, int);
 cudaError_t launch_loss(int, int, const float*, const float*, float, float*, float*, double*,
                         void*, size_t, cudaStream_t);
@@ -289,3 +292,21 @@ int ss_opacity_reset(const ss_map* map, float ceiling, float* d_m_opacity, float
 }
 
 }  // extern "C"
+
+size_t ss_seed_workspace_bytes(int64_t n) { return n < 0 ? 0 : seed_workspace_bytes(n); }
+
+int ss_seed_from_points(int64_t n, const float* d_points, const float* d_colors,
+                        float scene_extent, float* d_positions, float* d_rotations,
+                        float* d_log_scales, float* d_opacity_logits, float* d_sh_dc,
+                        int32_t* d_nonfinite, void* d_workspace, size_t workspace_bytes,
+                        void* stream) {
+    if (n < 0 || !d_nonfinite || !d_workspace) return SS_EINVAL;
+    if (n > 0 && (!d_points || !d_colors || !d_positions || !d_rotations || !d_log_scales ||
+                  !d_opacity_logits || !d_sh_dc))
+        return SS_EINVAL;
+    if (n >= (int64_t)1 << 31) return SS_EINVAL;
+    if (workspace_bytes < seed_workspace_bytes(n)) return SS_ECAPACITY;
+    return rc(launch_seed(n, d_points, d_colors, scene_extent, d_positions, d_rotations,
+                          d_log_scales, d_opacity_logits, d_sh_dc, d_nonfinite, d_workspace,
+                          workspace_bytes, S(stream)));
+}

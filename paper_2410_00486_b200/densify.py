@@ -50,6 +50,44 @@ class DensifyResult:
     n_pruned: int
 
 
+def seed_from_points(points, colors, scene_extent: float = 1.0, device=None):
+    """densify.py:53-83 on the GPU: one isotropic primitive per point, scale =
+    mean distance to the 3 nearest neighbours in the cloud (exact kNN on a
+    cell grid, ss_seed_from_points).  Returns device float32 tensors
+    (positions (n,3), rotations (n,4), log_scales (n,3), opacity_logits (n,),
+    sh (n,16,3) with only the DC band set)."""
+    dev = torch.device(device) if device is not None else (
+        points.device if isinstance(points, torch.Tensor) else torch.device("cuda"))
+
+    def f32(a):
+        if isinstance(a, torch.Tensor):
+            return a.to(device=dev, dtype=torch.float32).reshape(-1, 3).contiguous()
+        return torch.as_tensor(np.asarray(a, np.float64).reshape(-1, 3),
+                               dtype=torch.float32).to(dev).contiguous()
+
+    pts, col = f32(points), f32(colors)
+    n = int(pts.shape[0])
+    if col.shape[0] != n:
+        raise ValueError("points and colors must have the same length")
+    out = dict(positions=torch.empty((n, 3), dtype=torch.float32, device=dev),
+               rotations=torch.empty((n, 4), dtype=torch.float32, device=dev),
+               log_scales=torch.empty((n, 3), dtype=torch.float32, device=dev),
+               opacity_logits=torch.empty(n, dtype=torch.float32, device=dev),
+               sh_dc=torch.empty((n, 3), dtype=torch.float32, device=dev))
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = torch.empty(int(lib().ss_seed_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+    check(lib().ss_seed_from_points(n, P(pts), P(col), float(scene_extent),
+                                    P(out["positions"]), P(out["rotations"]),
+                                    P(out["log_scales"]), P(out["opacity_logits"]),
+                                    P(out["sh_dc"]), P(bad), P(ws), ws.numel(), stream_handle()),
+          "ss_seed_from_points")
+    if int(bad.item()):
+        raise ValueError("non-finite point in seed cloud")
+    sh = torch.zeros((n, 16, 3), dtype=torch.float32, device=dev)
+    sh[:, 0, :] = out["sh_dc"]
+    return out["positions"], out["rotations"], out["log_scales"], out["opacity_logits"], sh
+
+
 def accumulate_grad_stats(gmap: GaussianMap, grads: ParamGrads) -> GaussianMap:
     """densify.py:86-100."""
     if len(grads) != len(gmap):

@@ -417,6 +417,27 @@ class MappingEngine:
             self._alloc_pair_buffers(max(self._cap * len(self.gmap) // max(n, 1), 4096))
         return res
 
+    def add_points(self, points, colors):
+        """A keyframe's point cloud enters the map (trainer.py:160-174):
+        seed_from_points on the GPU, insert, Adam moments grown with zeros
+        (resize_for_densify with every old primitive surviving)."""
+        from .densify import seed_from_points
+        self.synchronize()
+        pos, rot, ls, opl, sh = seed_from_points(points, colors, self.cfg.scene_extent,
+                                                 self.dev)
+        n_new = int(pos.shape[0])
+        if n_new == 0:
+            return 0
+        n = len(self.gmap)
+        self.gmap.insert_device(pos, rot, ls, opl, sh[:, 0, :])
+        for d in (self.state.m, self.state.v):
+            for k, t in list(d.items()):
+                z = torch.zeros((n_new,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+                d[k] = torch.cat([t, z]).contiguous()
+        self._alloc_map_buffers()
+        self._alloc_pair_buffers(max(self._cap * len(self.gmap) // max(n, 1), 4096))
+        return n_new
+
     # ------------------------------------------------------- multi-view
     def _flat_grads(self):
         n = len(self.gmap)

@@ -265,6 +265,34 @@ def capture_scheduler_and_metrics():
     print("scheduler/metrics done")
 
 
+def capture_seed():
+    """seed_from_points (densify.py:53-83) by the reference on float32-exact
+    clouds: uniform, clustered with duplicates, and the n = 1, 2, 3 cases."""
+    rng = np.random.default_rng(21)
+    clouds = {
+        "uniform": rng.uniform(-1.0, 1.0, (3000, 3)),
+        "clustered": np.concatenate([rng.normal(c, 0.02, (400, 3))
+                                     for c in rng.uniform(-2, 2, (5, 3))]),
+        "n1": rng.uniform(-1, 1, (1, 3)),
+        "n2": rng.uniform(-1, 1, (2, 3)),
+        "n3": rng.uniform(-1, 1, (3, 3)),
+    }
+    clouds["clustered"][:10] = clouds["clustered"][10:20]  # exact duplicates
+    out = {}
+    for name, p in clouds.items():
+        p = p.astype(np.float32).astype(np.float64)
+        c = rng.uniform(0, 1, p.shape).astype(np.float32).astype(np.float64)
+        pos, rot, ls, op, sh = ref_densify.seed_from_points(p, c, scene_extent=2.5)
+        out[f"{name}_points"] = p
+        out[f"{name}_colors"] = c
+        out[f"{name}_log_scales"] = ls
+        out[f"{name}_opacity"] = op
+        out[f"{name}_sh_dc"] = sh[:, 0, :]
+        out[f"{name}_rotations"] = rot
+    np.savez_compressed(os.path.join(HERE, "seed.npz"), **out)
+    print("seed done")
+
+
 if __name__ == "__main__":
     capture_iteration("iter_sh0_small", 800, 64, 48, 0, seed=0)
     capture_iteration("iter_sh3_small", 600, 48, 40, 3, seed=1, view=1, n_views=3)
@@ -274,4 +302,5 @@ if __name__ == "__main__":
     capture_loss_odd()
     known_answers()
     capture_scheduler_and_metrics()
+    capture_seed()
     _ = ref_losses

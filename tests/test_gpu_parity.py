@@ -560,3 +560,53 @@ def test_eval_metrics_and_trajectory_match_reference():
     imgs = ss.render_trajectory(g, [cam, cam], ss.RasterOpts(sh_degree=0))
     ref = ss.rasterize_forward(g, cam, ss.RasterOpts(sh_degree=0)).image
     assert len(imgs) == 2 and torch.equal(imgs[0], ref) and torch.equal(imgs[1], ref)
+
+
+@pytest.mark.parametrize("cloud", ["uniform", "clustered", "n1", "n2", "n3"])
+def test_seed_from_points_matches_reference(cloud):
+    """F3: GPU seeding (exact grid kNN, float64 distances) vs the reference's
+    seed_from_points (tests/golden/seed.npz)."""
+    _need_gpu()
+    import os
+    import paper_2410_00486_b200 as ss
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "seed.npz"))
+    pos, rot, ls, op, sh = ss.seed_from_points(d[f"{cloud}_points"], d[f"{cloud}_colors"], 2.5)
+    np.testing.assert_allclose(ls.cpu().numpy(), d[f"{cloud}_log_scales"], rtol=0, atol=2e-6)
+    np.testing.assert_allclose(op.cpu().numpy(), d[f"{cloud}_opacity"], rtol=1e-6)
+    np.testing.assert_allclose(sh[:, 0, :].cpu().numpy(), d[f"{cloud}_sh_dc"], rtol=1e-6,
+                               atol=1e-6)
+    np.testing.assert_array_equal(rot.cpu().numpy(), d[f"{cloud}_rotations"])
+    np.testing.assert_array_equal(pos.cpu().numpy(), d[f"{cloud}_points"].astype(np.float32))
+
+
+def test_seed_large_cloud_vs_oracle_and_engine_insert():
+    """Grid kNN on a skewed 30k cloud (a dense cluster in a sparse shell) vs
+    the oracle's brute force; non-finite points raise; MappingEngine.add_points
+    grows the map and the Adam moments, and the next step runs."""
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    rng = np.random.default_rng(4)
+    p = np.concatenate([rng.normal(0, 0.01, (20000, 3)), rng.uniform(-3, 3, (10000, 3))])
+    p = p.astype(np.float32).astype(np.float64)
+    c = rng.uniform(0, 1, p.shape)
+    _, _, ls, _, _ = ss.seed_from_points(p, c, 1.0)
+    _, _, ls_ref, _, _ = orc.seed_from_points(p, c, 1.0)
+    np.testing.assert_allclose(ls.cpu().numpy(), ls_ref, rtol=0, atol=2e-6)
+    bad = p.copy()
+    bad[7, 1] = np.nan
+    with pytest.raises(ValueError):
+        ss.seed_from_points(bad, c, 1.0)
+    d = load("iter_sh0_small")
+    cam = fixture_camera(d)
+    tgt = torch.as_tensor(d["target"], dtype=torch.float32, device="cuda")
+    g = ss.GaussianMap.from_arrays(*fixture_scene(d))
+    n0 = len(g)
+    eng = ss.MappingEngine(g, cam.width, cam.height, ss.RasterOpts(sh_degree=0))
+    eng.step(cam, tgt)
+    pts = rng.uniform(-0.3, 0.3, (500, 3))
+    assert eng.add_points(pts, rng.uniform(0, 1, (500, 3))) == 500
+    assert len(eng.gmap) == n0 + 500
+    assert all(t.shape[0] == n0 + 500 for t in eng.state.m.values())
+    eng.step(cam, tgt)
+    eng.synchronize()
+    assert len(eng.losses()) == 2

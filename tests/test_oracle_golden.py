@@ -241,3 +241,15 @@ def test_two_splat_blend_known_answer():
     np.testing.assert_allclose(r.image[0, 0], [0.5, 0.25, 0.0])
     assert r.final_t[0, 0] == 0.25
     assert r.n_contrib[0, 0] == 2
+
+
+@pytest.mark.parametrize("cloud", ["uniform", "clustered", "n1", "n2", "n3"])
+def test_oracle_seed_from_points_matches_reference(cloud):
+    """F3 seeding restatement vs the reference's seed_from_points outputs."""
+    d = np.load(os.path.join(GOLDEN, "seed.npz"))
+    pos, rot, ls, op, sh = orc.seed_from_points(d[f"{cloud}_points"], d[f"{cloud}_colors"],
+                                                scene_extent=2.5)
+    np.testing.assert_allclose(ls, d[f"{cloud}_log_scales"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(op, d[f"{cloud}_opacity"], rtol=1e-15)
+    np.testing.assert_allclose(sh[:, 0, :], d[f"{cloud}_sh_dc"], rtol=1e-14)
+    np.testing.assert_array_equal(rot, d[f"{cloud}_rotations"])
