@@ -18,6 +18,7 @@ from .optimizer import AdamState, LearningRates, adam_step, resize_for_densify
 from .rasterizer import (ParamGrads, Projection, RasterOpts, RenderOutput, TileIndex,
                          backward_pixelwise, backward_splatwise, rasterize_forward,
                          render_trajectory, screen_space_grads, screen_space_grads_pixelwise)
+from .mapio import load_map, save_map
 from .scheduler import KeyframeScheduler, ScheduledMapper
 from .scene import CONFIGS, survey_camera, survey_scene
 
@@ -28,8 +29,9 @@ __all__ = [
     "GaussianMap", "LearningRates", "LossBreakdown", "MappingEngine", "ParamGrads", "Projection",
     "RasterOpts", "RenderOutput", "TileIndex", "accumulate_grad_stats", "adam_step",
     "backward_pixelwise", "backward_splatwise", "compute_losses", "densify_and_prune", "depth_l1", "logistic", "logit",
-    "KeyframeScheduler", "ScheduledMapper", "opacity_reg", "opacity_reset", "psnr",
-    "rasterize_forward", "render_trajectory", "resize_for_densify", "seed_from_points",
+    "KeyframeScheduler", "ScheduledMapper", "load_map", "opacity_reg", "opacity_reset", "psnr",
+    "rasterize_forward", "render_trajectory", "resize_for_densify", "save_map",
+    "seed_from_points",
     "ssim_metric",
     "screen_space_grads", "screen_space_grads_pixelwise", "survey_camera", "survey_scene", "total_loss",
 ]

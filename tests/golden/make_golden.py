@@ -293,6 +293,23 @@ def capture_seed():
     print("seed done")
 
 
+def capture_ply():
+    """save_map (dataio.py:279-305) by the reference, double and float32
+    layouts, of a small float32-exact SH3 map."""
+    from splatstream import dataio as ref_io
+    rng = np.random.default_rng(31)
+    n = 40
+    f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+    rot = rng.standard_normal((n, 4))
+    rot /= np.linalg.norm(rot, axis=1, keepdims=True)
+    g = ss.GaussianMap()
+    g.insert_arrays(f32(rng.uniform(-1, 1, (n, 3))), f32(rot), f32(rng.normal(-3, 0.3, (n, 3))),
+                    f32(rng.normal(0, 1, n)), f32(rng.normal(0, 0.2, (n, 16, 3))))
+    ref_io.save_map(g, os.path.join(HERE, "map_f64.ply"))
+    ref_io.save_map(g, os.path.join(HERE, "map_f32.ply"), float32=True)
+    print("ply done")
+
+
 if __name__ == "__main__":
     capture_iteration("iter_sh0_small", 800, 64, 48, 0, seed=0)
     capture_iteration("iter_sh3_small", 600, 48, 40, 3, seed=1, view=1, n_views=3)
@@ -303,4 +320,5 @@ if __name__ == "__main__":
     known_answers()
     capture_scheduler_and_metrics()
     capture_seed()
+    capture_ply()
     _ = ref_losses
