@@ -88,7 +88,7 @@ __device__ __forceinline__ void chain_one(const float p[3], float4 q4, const flo
                                           const float dc[3], const float* __restrict__ rest,
                                           const CamC& cam, int deg, float dilation,
                                           const float* g, uint8_t flags, GaussGrad& o,
-                                          float* rest_grad) {
+                                          float* rest_grad, float* basis_out = nullptr) {
     // ---- projection context (projection.py:86-121)
     float t[3];
 #pragma unroll
@@ -216,6 +216,12 @@ __device__ __forceinline__ void chain_one(const float p[3], float4 q4, const flo
     float grgb[3] = {(flags & 2) ? g[0] : 0.f, (flags & 4) ? g[1] : 0.f, (flags & 8) ? g[2] : 0.f};
     float bs[16];
     sh_basis16(d, deg, bs);
+    if (basis_out) {  // rest gradient factors: g_rest[k][ch] = bs[k] * grgb[ch]
+#pragma unroll
+        for (int k = 0; k < 16; ++k) basis_out[k] = bs[k];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) basis_out[16 + ch] = grgb[ch];
+    }
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) o.dc[ch] = bs[0] * grgb[ch];
     if (deg > 0) {
@@ -505,6 +511,94 @@ __global__ void __launch_bounds__(256, REST ? 2 : 4) chain_adam_kernel(
                   st);
 }
 
+// ------------------------------------------------ chain+adam, SH rest on
+// sh_rest is (N, 45) per Gaussian: a thread walking its own row strides
+// 180 B between lanes.  Here the CTA's 256 rows (one contiguous span) are
+// staged through shared memory for the chain's direction gradient, each
+// thread exports its 16 basis values and 3 colour gradients, and the CTA
+// then runs Adam over the span's 256 x 45 parameters and moments with
+// consecutive threads on consecutive elements.
+constexpr int kRestCTA = 256;
+constexpr int kRestRow = 45;
+
+template <int NC>
+__global__ void __launch_bounds__(kRestCTA, 2) chain_adam_rest_kernel(
+    int64_t n, float* __restrict__ pos, float4* __restrict__ rot, float* __restrict__ ls,
+    float* __restrict__ opl, float* __restrict__ shdc, float* __restrict__ shrest, CamC cam_v,
+    const ss_camera* __restrict__ d_cam, int deg, float dilation, const float* __restrict__ g2d,
+    const uint8_t* __restrict__ flags, const uint8_t* __restrict__ contributed, float lo_over_n,
+    ss_param_grads M, ss_param_grads V, AdamHP hp_v, const ss_adam_hparams* __restrict__ d_hp,
+    float* __restrict__ grad2d_accum, float* __restrict__ grad3d_accum,
+    int32_t* __restrict__ obs_count, ss_status* st) {
+    extern __shared__ float rs_smem[];
+    float* s_rest = rs_smem;                         // [kRestCTA * 45] parameters
+    float* s_fac = rs_smem + kRestCTA * kRestRow;    // [kRestCTA * 19] basis, colour grad
+    if (st->pair_overflow) return;  // uniform: the step is replayed
+    const int t = threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * kRestCTA;
+    const int cnt = (int)min((int64_t)kRestCTA, n - base);
+    const int span = cnt * kRestRow;
+    const float* rest_g = shrest + base * kRestRow;
+    for (int e = t; e < span; e += kRestCTA) s_rest[e] = rest_g[e];
+    __syncthreads();
+    if (t < cnt) {
+        const int64_t i = base + t;
+        CamC cam = cam_v;
+        AdamHP hp = hp_v;
+        if (d_cam) load_camc(d_cam, cam);
+        if (d_hp) load_hp(d_hp, hp);
+        GaussGrad o = {};
+        const uint8_t fl = flags[i];
+        const float opi = opl[i];
+        float* fac = s_fac + 19 * t;
+        if (fl & 1) {
+            float p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+            float l[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
+            float dc[3] = {shdc[3 * i], shdc[3 * i + 1], shdc[3 * i + 2]};
+            float g[NC];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) g[k] = g2d[NC * i + k];
+            chain_one<NC>(p, rot[i], l, opi, dc, s_rest + kRestRow * t, cam, deg, dilation, g,
+                          fl, o, nullptr, fac);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 19; ++k) fac[k] = 0.f;
+        }
+        if (lo_over_n != 0.f) {
+            float sg = sigm(opi);
+            o.op += lo_over_n * sg * (1.f - sg);
+        }
+        if (!grad_finite(o)) report_first(&st->first_nonfinite_grad, i);
+        if (contributed && contributed[i]) {
+            grad2d_accum[i] += o.n2d;
+            grad3d_accum[3 * i] += o.pos[0];
+            grad3d_accum[3 * i + 1] += o.pos[1];
+            grad3d_accum[3 * i + 2] += o.pos[2];
+            obs_count[i] += 1;
+        }
+        adam_gaussian(i, o, nullptr, pos, rot, ls, opl, shdc, shrest, M, V, hp, false, st);
+    }
+    __syncthreads();
+    // Adam over the CTA's contiguous sh_rest span (bands >= deg + 1 get g = 0)
+    AdamHP hp = hp_v;
+    if (d_hp) load_hp(d_hp, hp);
+    const int nb = (deg + 1) * (deg + 1);
+    float* pm = M.d_sh_rest + base * kRestRow;
+    float* pv = V.d_sh_rest + base * kRestRow;
+    float* pp = shrest + base * kRestRow;
+    for (int e = t; e < span; e += kRestCTA) {
+        const int gi = e / kRestRow, j = e - gi * kRestRow;
+        const int k = j / 3 + 1, ch = j - 3 * (k - 1);
+        const float* fac = s_fac + 19 * gi;
+        const float gr = k < nb ? fac[k] * fac[16 + ch] : 0.f;
+        float p = s_rest[e], m = pm[e], v = pv[e];
+        adam_elem(p, gr, m, v, hp.lr[5], hp);
+        pp[e] = p;
+        pm[e] = m;
+        pv[e] = v;
+    }
+}
+
 // ---------------------------------------------------------------- stats
 __global__ void stats_kernel(int64_t n, const float* __restrict__ gpos,
                              const float* __restrict__ n2d, const uint8_t* __restrict__ contributed,
@@ -609,10 +703,25 @@ cudaError_t launch_chain_adam(const ss_map* mp, const ss_camera* cam, const ss_c
             mp->d_grad3d_accum, mp->d_obs_count, st);
     };
     const bool rest = h->update_sh_rest != 0;
+    if (rest) {
+        const int smem = (int)(sizeof(float) * kRestCTA * (kRestRow + 19));
+        auto gor = [&](auto kern) -> cudaError_t {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 smem);
+            if (e != cudaSuccess) return e;
+            kern<<<div_up(mp->n, kRestCTA), kRestCTA, smem, s>>>(
+                mp->n, mp->d_positions, reinterpret_cast<float4*>(mp->d_rotations),
+                mp->d_log_scales, mp->d_opacity_logits, mp->d_sh_dc, mp->d_sh_rest, cc, d_cam,
+                o->sh_degree, o->dilation, g2d, flags, contributed, lo_over_n, *M, *V, make_hp(h),
+                d_hp, mp->d_grad2d_accum, mp->d_grad3d_accum, mp->d_obs_count, st);
+            return cudaGetLastError();
+        };
+        return o->with_depth ? gor(chain_adam_rest_kernel<10>) : gor(chain_adam_rest_kernel<9>);
+    }
     if (o->with_depth)
-        rest ? go(chain_adam_kernel<10, true>) : go(chain_adam_kernel<10, false>);
+        go(chain_adam_kernel<10, false>);
     else
-        rest ? go(chain_adam_kernel<9, true>) : go(chain_adam_kernel<9, false>);
+        go(chain_adam_kernel<9, false>);
     return cudaGetLastError();
 }
 
