@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
     const float4* __restrict__ ckpt, const float* __restrict__ ckpt_depth,
     const uint32_t* __restrict__ ckpt_mask, const uint2* __restrict__ work,
     const int64_t* __restrict__ work_count, int64_t work_cap, uint32_t* work_counter,
-    float* __restrict__ g2d, uint8_t* __restrict__ contributed) {
+    float* __restrict__ g2d, uint8_t* __restrict__ contributed, int n_tiles) {
     constexpr int NC = DEPTH ? 10 : 9;
     // per-warp compacted pixel list: gradient side (g, g . image), state at
     // the unit start (T0, G0), coordinates, the two buckets' blend masks,
@@ -159,14 +159,33 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
     const bool hi = lane >= 16;            // lane's splats live in the second bucket
     const int sh = (2 * lane) & 31;        // their bit pair in that bucket's mask
     const int64_t count = min(*work_count, work_cap);
+    // schedule built by bwd_schedule_kernel (mode 0: the forward's list)
+    const uint32_t mode = work_counter[1];
+    const uint32_t mu = mode >> 1;
+    const uint32_t* sched_start =
+        reinterpret_cast<const uint32_t*>(work) + (2 * work_cap - (n_tiles + (int64_t)mu + 2));
+    const uint32_t* sched_tiles = sched_start + mu + 1;
 
     for (;;) {
         uint32_t item = 0;
         if (lane == 0) item = atomicAdd(work_counter, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if ((int64_t)item >= count) break;
-        const uint2 wk = work[item];
-        const int tile = (int)wk.x, u = (int)wk.y;
+        int tile, u;
+        if (mode & 1u) {
+            uint32_t lo = 0, hi_ = mu;  // largest u with start[u] <= item
+            while (hi_ - lo > 1) {
+                const uint32_t mid = (lo + hi_) >> 1;
+                if (sched_start[mid] <= item) lo = mid;
+                else hi_ = mid;
+            }
+            u = (int)lo;
+            tile = (int)sched_tiles[item - sched_start[lo]];
+        } else {
+            const uint2 wk = work[item];
+            tile = (int)wk.x;
+            u = (int)wk.y;
+        }
         const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
         const uint32_t start = tile_start[tile];
         const int ke = k_eff[tile];
@@ -263,6 +282,82 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
     }
 }
 
+// Longest-units-first schedule.  A unit's size is roughly the number of
+// pixels still blending at its first bucket, so earlier units of a tile are
+// larger, and tiles with more units are the deeper ones.  Handing units out
+// unit-index-major with the tiles of each index in descending unit count
+// approximates longest-processing-time-first and shortens the tail of the
+// persistent backward.  One CTA builds it from k_eff: tiles counting-sorted
+// by unit count, descending (S), and start[u] = sum over u' < u of #tiles
+// with more than u' units; item c is unit u (largest u with start[u] <= c)
+// of tile S[c - start[u]].  Written at the end of the work buffer (past the
+// forward's list); the mode word (high half of the status block's counter
+// word) = 1 | max_units << 1, or 0 to keep the forward's list (more than
+// kMaxUnits units in a tile, too many tiles, or no room).
+constexpr int kMaxUnits = 1024;
+constexpr int kSchedTiles = 16384;  // 4K frames at 16 px tiles fit
+
+__global__ void __launch_bounds__(1024) bwd_schedule_kernel(uint32_t* counter,
+                                                            const int32_t* __restrict__ k_eff,
+                                                            int n_tiles, uint32_t* __restrict__ wl,
+                                                            int64_t wl_cap,
+                                                            const int64_t* __restrict__ total) {
+    __shared__ uint32_t h[kMaxUnits + 1];
+    __shared__ uint16_t s_nb[kSchedTiles];
+    __shared__ uint32_t s_max;
+    const int t = threadIdx.x;
+    if (n_tiles > kSchedTiles) {
+        if (t == 0) counter[1] = 0u;
+        return;
+    }
+    for (int v = t; v <= kMaxUnits; v += blockDim.x) h[v] = 0u;
+    if (t == 0) s_max = 0u;
+#pragma unroll 8
+    for (int q = t; q < n_tiles; q += blockDim.x)  // independent loads, all in flight
+        s_nb[q] = (uint16_t)min((k_eff[q] + kUnit - 1) / kUnit, 65535);
+    __syncthreads();
+    uint32_t m = 0;
+    for (int q = t; q < n_tiles; q += blockDim.x) {
+        const uint32_t nb = s_nb[q];
+        m = max(m, nb);
+        if (nb <= kMaxUnits) atomicAdd(&h[nb], 1u);
+    }
+    atomicMax(&s_max, m);
+    __syncthreads();
+    const uint32_t mu = s_max;
+    const int64_t off = wl_cap - ((int64_t)n_tiles + mu + 2);
+    if (mu > (uint32_t)kMaxUnits || off < 2 * min(*total, wl_cap / 2)) {
+        if (t == 0) counter[1] = 0u;  // keep the forward's list
+        return;
+    }
+    uint32_t* start = wl + off;    // [mu + 1]
+    uint32_t* S = start + mu + 1;  // [n_tiles]
+    if (t == 0) {
+        uint32_t above = 0;
+        for (int v = (int)mu; v >= 0; --v) {  // h[v] -> #tiles with more than v units
+            const uint32_t c = h[v];           //         = first position of bucket v in S
+            h[v] = above;
+            above += c;
+        }
+        uint32_t pre = 0;
+        for (uint32_t u = 0; u < mu; ++u) {
+            start[u] = pre;
+            pre += h[u];
+        }
+        start[mu] = pre;
+    }
+    __syncthreads();
+    for (int q = t; q < n_tiles; q += blockDim.x) {
+        const uint32_t nb = s_nb[q];
+        if (nb != 0) S[atomicAdd(&h[nb], 1u)] = (uint32_t)q;
+    }
+    __syncthreads();
+    if (t == 0) {
+        __threadfence();
+        counter[1] = 1u | (mu << 1);
+    }
+}
+
 __global__ void bwd_clear_kernel(float* __restrict__ g2d, int64_t nf, uint8_t* contributed,
                                  int64_t n, uint32_t* counter) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -289,9 +384,11 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
     const int ncol = depthf ? 10 : 9;
     // one launch clears the gradient rows, the contributed marks and the
     // work-unit counter
+    int tx = div_up(cam->width, kTile), ty = div_up(cam->height, kTile);
     bwd_clear_kernel<<<div_up(n * ncol > 4 ? n * ncol / 4 : 1, 256), 256, 0, s>>>(
         g2d, (int64_t)n * ncol, contributed, n, counter);
-    int tx = div_up(cam->width, kTile);
+    bwd_schedule_kernel<<<1, 1024, 0, s>>>(counter, k_eff, tx * ty, const_cast<uint32_t*>(work),
+                                          2 * work_cap, &st->bucket_count);
     const int threads = 32 * kBwdWarps;
     const size_t smem = 0;
     int dev = 0, sms = 148, per_sm = 1;
@@ -306,7 +403,7 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
             grad_image, pixgrad, depth, grad_depth, n_contrib,
             reinterpret_cast<const float4*>(ckpt), ckpt_depth, ckpt_mask,
             reinterpret_cast<const uint2*>(work), &st->bucket_count, work_cap, counter, g2d,
-            contributed);
+            contributed, tx * ty);
         return cudaGetLastError();
     };
     return depthf ? go(backward_splat_kernel<true>) : go(backward_splat_kernel<false>);

@@ -43,9 +43,9 @@ STATUS_LAG = 2
 # kernels each C-ABI call enqueues (counted for bench.py's gpu_launches)
 KERNELS_PER_CALL = {
     # status_begin 1 + preprocess 1 + blend 1 + loss (ssim fwd, ssim bwd with
-    # the partial-sum reduction) 2 + backward (clear, splat-wise) 2; binning
-    # is counted separately (binning_kernels)
-    "step_fb": 1 + 1 + 1 + 2 + 2,
+    # the partial-sum reduction) 2 + backward (clear, schedule, splat-wise) 3;
+    # binning is counted separately (binning_kernels)
+    "step_fb": 1 + 1 + 1 + 2 + 3,
     "chain_adam": 1,
     "snapshot": 1,
 }
