@@ -180,6 +180,15 @@ int ss_depth_l1(int32_t height, int32_t width, const float *d_depth, const float
                 float weight, float *d_grad_depth, double *d_sums, void *stream);
 
 /* --------------------------------------------------------- backward */
+/* Longest-units-first schedule of the splat-wise backward's work units,
+ * built from the forward's d_k_eff by one CTA (tiles counting-sorted by
+ * unit count; units handed out unit-index-major) into the tail of d_work;
+ * ss_backward_splat uses it when present in d_status (reset by
+ * ss_status_reset / ss_status_begin_step), else the forward's list.  May run
+ * concurrently with the loss kernels (it reads only d_k_eff). */
+int ss_backward_schedule(const ss_camera *cam, const int32_t *d_k_eff, uint32_t *d_work,
+                         int64_t work_capacity, ss_status *d_status, void *stream);
+
 /* Replaces backward_splatwise up to the screen-space rows g2d
  * (api.py:275-336; backward_splat_tile / _splat_bucket_inner
  * kernels.py:271-373).  d_pixgrad (optional, from ss_loss_l1_ssim; its .w

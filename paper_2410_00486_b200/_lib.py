@@ -106,6 +106,7 @@ _SIGS = {
     "ss_backward_pixel": (I32, [VP, VP, VP, VP, VP, VP, VP, VP, I64, VP, VP]),
     "ss_seed_workspace_bytes": (SZ, [I64]),
     "ss_seed_from_points": (I32, [I64, VP, VP, F32, VP, VP, VP, VP, VP, VP, VP, SZ, VP]),
+    "ss_backward_schedule": (I32, [VP, VP, VP, I64, VP, VP]),
     "ss_chain_backward": (I32, [P(SSMap), P(SSCamera), P(SSRasterOpts), VP, VP, VP, F32, I32,
                                 P(SSParamGrads), VP, VP]),
     "ss_adam_step": (I32, [P(SSMap), P(SSParamGrads), P(SSParamGrads), P(SSParamGrads),

@@ -28,6 +28,8 @@ cudaError_t launch_backward_pixel(const ss_camera*, const ss_raster_opts*, const
 size_t seed_workspace_bytes(int64_t);
 cudaError_t launch_seed(int64_t, const float*, const float*, float, float*, float*, float*,
                         float*, float*, int32_t*, void*, size_t, cudaStream_t);
+cudaError_t launch_backward_schedule(const ss_camera*, const int32_t*, uint32_t*, int64_t,
+                                     ss_status*, cudaStream_t);
 size_t loss_workspace_bytes(int, int);
 cudaError_t launch_loss(int, int, const float*, const float*, float, float*, float*, double*,
                         void*, size_t, cudaStream_t);
@@ -196,6 +198,13 @@ int ss_depth_l1(int32_t height, int32_t width, const float* d_depth, const float
     if (!d_depth || !d_target || !d_grad_depth || !d_sums) return SS_EINVAL;
     return rc(launch_depth_l1(height, width, d_depth, d_target, weight, d_grad_depth, d_sums,
                               d_sums + 2, S(stream)));
+}
+
+int ss_backward_schedule(const ss_camera* cam, const int32_t* d_k_eff, uint32_t* d_work,
+                         int64_t work_capacity, ss_status* d_status, void* stream) {
+    if (!cam || !d_k_eff || !d_work || work_capacity <= 0 || !d_status) return SS_EINVAL;
+    return rc(launch_backward_schedule(cam, d_k_eff, d_work, work_capacity, d_status,
+                                       S(stream)));
 }
 
 int ss_backward_splat(const ss_camera* cam, const ss_raster_opts* opts, const ss_splats* splats,

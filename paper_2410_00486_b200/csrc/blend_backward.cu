@@ -371,6 +371,15 @@ __global__ void bwd_clear_kernel(float* __restrict__ g2d, int64_t nf, uint8_t* c
         for (int64_t k = i; k < n; k += stride) contributed[k] = 0;
 }
 
+cudaError_t launch_backward_schedule(const ss_camera* cam, const int32_t* k_eff, uint32_t* work,
+                                     int64_t work_cap, ss_status* st, cudaStream_t s) {
+    const int tx = div_up(cam->width, kTile), ty = div_up(cam->height, kTile);
+    uint32_t* counter = reinterpret_cast<uint32_t*>(&st->reserved);
+    bwd_schedule_kernel<<<1, 1024, 0, s>>>(counter, k_eff, tx * ty, work, 2 * work_cap,
+                                          &st->bucket_count);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
                                   const ss_splats* sp, const ss_bins* bins, const float* image,
                                   const float* grad_image, const float4* pixgrad,
@@ -387,8 +396,6 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
     int tx = div_up(cam->width, kTile), ty = div_up(cam->height, kTile);
     bwd_clear_kernel<<<div_up(n * ncol > 4 ? n * ncol / 4 : 1, 256), 256, 0, s>>>(
         g2d, (int64_t)n * ncol, contributed, n, counter);
-    bwd_schedule_kernel<<<1, 1024, 0, s>>>(counter, k_eff, tx * ty, const_cast<uint32_t*>(work),
-                                          2 * work_cap, &st->bucket_count);
     const int threads = 32 * kBwdWarps;
     const size_t smem = 0;
     int dev = 0, sms = 148, per_sm = 1;

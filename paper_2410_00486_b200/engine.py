@@ -220,6 +220,9 @@ class MappingEngine:
                                  P(self.work), self.work_cap, P(self.status), s),
               "ss_blend_forward")
         self._mark("blend_forward")
+        # the backward's longest-units-first schedule (needs only k_eff)
+        check(L.ss_backward_schedule(ctypes.byref(cm), P(self.k_eff), P(self.work), self.work_cap,
+                                     P(self.status), s), "ss_backward_schedule")
         use_pg = self.cfg.lambda_ssim != 0.0 and not self.opts.with_depth
         check(L.ss_loss_l1_ssim(self.H, self.W, P(self.image), P(target),
                                 float(self.cfg.lambda_ssim), P(self.grad_image),

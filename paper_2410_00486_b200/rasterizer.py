@@ -400,6 +400,9 @@ def screen_space_grads(render: RenderOutput, grad_image, grad_depth=None):
     n = render.n_primitives
     g2d = torch.empty((max(n, 1), ncol), dtype=torch.float32, device=dev)
     cm, op = render.camera.to_ss(), render.opts.to_ss()
+    check(lib().ss_backward_schedule(ctypes.byref(cm), P(render.k_eff_tiles), P(render.work),
+                                     render.work_capacity, P(render.status), stream_handle()),
+          "ss_backward_schedule")
     check(lib().ss_backward_splat(
         ctypes.byref(cm), ctypes.byref(op), ctypes.byref(render.splats.ss()),
         ctypes.byref(render.bins.ss()), P(render.image), P(g), None, P(render.depth), P(gd),
