@@ -269,6 +269,16 @@ def main():
         one_step()
     eng.synchronize() if world == 1 else torch.cuda.synchronize()
 
+    # parameters + Adam state after warm-up: the e2e run below restores them
+    # in place (graph pointers stay valid) so it times the same iterations
+    # as the device-timed run -- the per-iteration cost drifts as training
+    # lowers opacities (profiles/r01_training_drift.txt)
+    snap = None
+    if world == 1:
+        snap = ([getattr(eng.gmap, f).clone() for f in eng.gmap.FIELDS],
+                {k: t.clone() for k, t in eng.state.m.items()},
+                {k: t.clone() for k, t in eng.state.v.items()}, eng.state.step_count)
+
     # ---- timed region: per-step CUDA events, L2 flushed between steps
     sampler = ClockSampler(local)
     if dist is not None:
@@ -341,6 +351,14 @@ def main():
     # the step's loss/status snapshot comes back to the host
     e2e = None
     if world == 1 and not args.no_e2e:
+        eng.synchronize()
+        for f, t in zip(eng.gmap.FIELDS, snap[0]):
+            getattr(eng.gmap, f).copy_(t)
+        for k, t in snap[1].items():
+            eng.state.m[k].copy_(t)
+        for k, t in snap[2].items():
+            eng.state.v[k].copy_(t)
+        eng.state.step_count = snap[3]
         host_tgt = my_tgt.cpu().pin_memory()
         bufs = [torch.empty_like(my_tgt), torch.empty_like(my_tgt)]
         copy_stream = torch.cuda.Stream()
@@ -370,16 +388,20 @@ def main():
             e2e_step(k)
         eng.synchronize()
         torch.cuda.synchronize()
+        # the same number of iterations as the device-timed run, from the
+        # same state (the 2 graph-capture steps above are not timed)
+        n_e2e = args.steps
         t0 = time.perf_counter()
-        for k in range(2, 2 + args.steps):
+        for k in range(2, 2 + n_e2e):
             e2e_step(k)
         eng.synchronize()  # every step's loss is on the host
         wall = time.perf_counter() - t0
-        e2e = {"value": args.steps / wall, "unit": "it/s",
+        e2e = {"value": n_e2e / wall, "unit": "it/s", "steps": n_e2e,
                "h2d_bytes_per_step": int(host_tgt.numel() * 4),
                "d2h_bytes_per_step": int(eng._host.shape[1] * 8),
-               "timing": "wall clock, host pinned target upload per step (copy stream, "
-                         "double-buffered) + per-step loss/status read back"}
+               "timing": "wall clock over the same iterations as `value` (state restored), "
+                         "host pinned target upload per step (copy stream, double-buffered) "
+                         "+ per-step loss/status read back"}
 
     # ---- CPU baseline (rank 0, N = 1): bounded oracle sample
     cpu = None
@@ -404,6 +426,10 @@ def main():
                        "sh_degree": 0, "pairs": P, "visible": M, "checkpoint_slots": C,
                        "backward_units": U,
                        "l2": "256 MB buffer written between timed steps (outside the events)",
+                       "phase": f"iterations {max(args.warmup, 3) + 1}-"
+                                f"{max(args.warmup, 3) + args.steps} from the survey "
+                                "initialisation (the cost per iteration rises ~2x by "
+                                "iteration 150 as training lowers opacities)",
                        "parallelism": f"keyframe-sharded x{world}" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
                          "unit": "GB/s", "frac": ach / peak, "traffic": ncu_traffic(dom),
