@@ -38,25 +38,6 @@ struct PixState {
     bool done, live;
 };
 
-// Blend splat q into one pixel whose quadratic form m passed m <= m_cut.
-template <bool DEPTH>
-__device__ __forceinline__ bool blend_one(PixState& s, float m, const float4& B, const float4& C,
-                                          int q, float t_min, float amin, float amax) {
-    float a = splat_falloff(m, B);
-    if (a < amin) return false;
-    a = fminf(a, amax);
-    const float w = __fmul_rn(a, s.T);
-    s.c0 = __fmaf_rn(C.x, w, s.c0);
-    s.c1 = __fmaf_rn(C.y, w, s.c1);
-    s.c2 = __fmaf_rn(C.z, w, s.c2);
-    if (DEPTH) s.D = __fmaf_rn(B.w, w, s.D);
-    s.T = __fmul_rn(s.T, __fsub_rn(1.0f, a));
-    s.last = q + 1;
-    s.bm |= 1u << (q & 31);
-    if (s.T < t_min) s.done = true;
-    return true;
-}
-
 template <bool DEPTH, bool CONTRIB>
 __global__ void __launch_bounds__(128) blend_forward_kernel(
     int W, int H, int tiles_x, const uint32_t* __restrict__ tile_start,
@@ -87,8 +68,21 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
     const uint32_t len = tile_end[tile] - start;
     const uint32_t cbase = ckpt_base[tile];
 
+    // the thread's two pixels as the (lo, hi) lanes of packed f32x2 state:
+    // transmittance, colour (and depth); FADD2/FMUL2/FFMA2 give per lane the
+    // scalar IEEE results, so everything the backward replays is unchanged
+    f32x2 T2 = pk2(1.f, 1.f), R2 = pk2(0.f, 0.f), G2 = R2, B2 = R2, D2 = R2;
+    const f32x2 PY2 = pk2(py0, py1), KE2 = pk2(-0.5f * kLog2e, -0.5f * kLog2e),
+                ONE2 = pk2(1.f, 1.f);
     PixState s0 = {1.f, 0.f, 0.f, 0.f, 0.f, 0, 0u, !(ix < W && iy0 < H), false};
     PixState s1 = {1.f, 0.f, 0.f, 0.f, 0.f, 0, 0u, !(ix < W && iy1 < H), false};
+    auto sync_state = [&]() {  // packed -> scalar (checkpoints, outputs)
+        upk2(T2, s0.T, s1.T);
+        upk2(R2, s0.c0, s1.c0);
+        upk2(G2, s0.c1, s1.c1);
+        upk2(B2, s0.c2, s1.c2);
+        if (DEPTH) upk2(D2, s0.D, s1.D);
+    };
     int open_bucket = -1;
     for (uint32_t b0 = 0; b0 < len; b0 += 256) {
         if (__syncthreads_count(!(s0.done && s1.done)) == 0) break;
@@ -127,6 +121,7 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
             s0.live = !s0.done;
             s1.live = !s1.done;
             s0.bm = s1.bm = 0u;
+            sync_state();
             const size_t slot = (size_t)(cbase + bucket) * kTilePx;
             if (s0.live) {
                 ckpt[slot + p0] = make_float4(s0.T, s0.c0, s0.c1, s0.c2);
@@ -143,19 +138,44 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
                 const int j = j0 + __ffs(todo) - 1;
                 todo &= todo - 1;
                 const float4 A = s_rec[j].a, B = s_rec[j].b, C = s_rec[j].c;
-                // the two pixels share a column: dx-only terms once
+                // the two pixels share a column: dx-only terms once; then the
+                // quad_finish / splat_falloff operations of both pixels packed
                 const float dx = __fsub_rn(px, A.x);
                 const float q0 = quad_dx0(A, dx), q1 = quad_dx1(A, dx);
-                const float m0 = quad_finish(q0, q1, B, __fsub_rn(py0, A.y));
-                const float m1 = quad_finish(q0, q1, B, __fsub_rn(py1, A.y));
+                const f32x2 dy2 = sub2(PY2, pk2(A.y, A.y));
+                const f32x2 m2 = fma2(mul2(pk2(B.x, B.x), dy2), dy2,
+                                      fma2(pk2(q1, q1), dy2, pk2(q0, q0)));
+                float m0, m1;
+                upk2(m2, m0, m1);
                 const bool in0 = !s0.done && !(m0 > B.z);
                 const bool in1 = !s1.done && !(m1 > B.z);
                 if (in0 || in1) {
+                    float e0, e1, a0, a1;
+                    upk2(mul2(m2, KE2), e0, e1);
+                    upk2(mul2(pk2(B.y, B.y), pk2(ex2_approx(e0), ex2_approx(e1))), a0, a1);
+                    const bool ok0 = in0 && !(a0 < amin), ok1 = in1 && !(a1 < amin);
+                    // a pixel that does not blend gets a = 0: its state is unchanged
+                    const f32x2 a2 = pk2(ok0 ? fminf(a0, amax) : 0.f, ok1 ? fminf(a1, amax) : 0.f);
+                    const f32x2 w2 = mul2(a2, T2);
+                    R2 = fma2(pk2(C.x, C.x), w2, R2);
+                    G2 = fma2(pk2(C.y, C.y), w2, G2);
+                    B2 = fma2(pk2(C.z, C.z), w2, B2);
+                    if (DEPTH) D2 = fma2(pk2(B.w, B.w), w2, D2);
+                    T2 = mul2(T2, sub2(ONE2, a2));
+                    float T0, T1;
+                    upk2(T2, T0, T1);
                     const int q = (int)b0 + j;
-                    bool hit = false;
-                    if (in0) hit |= blend_one<DEPTH>(s0, m0, B, C, q, t_min, amin, amax);
-                    if (in1) hit |= blend_one<DEPTH>(s1, m1, B, C, q, t_min, amin, amax);
-                    if (CONTRIB && hit) s_hit[j] = 1;
+                    if (ok0) {
+                        s0.last = q + 1;
+                        s0.bm |= 1u << (q & 31);
+                        if (T0 < t_min) s0.done = true;
+                    }
+                    if (ok1) {
+                        s1.last = q + 1;
+                        s1.bm |= 1u << (q & 31);
+                        if (T1 < t_min) s1.done = true;
+                    }
+                    if (CONTRIB && (ok0 || ok1)) s_hit[j] = 1;
                 }
             }
         }
@@ -173,6 +193,7 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
         if (s0.live) ckpt_mask[prev + p0] = s0.bm;
         if (s1.live) ckpt_mask[prev + p1] = s1.bm;
     }
+    sync_state();
     if (ix < W) {
         if (iy0 < H) {
             const size_t o = (size_t)iy0 * W + ix;
