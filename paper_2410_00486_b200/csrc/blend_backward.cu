@@ -114,20 +114,25 @@ __device__ __forceinline__ uint32_t bwd_wavefront(
     for (int st = 0; st < steps; ++st) {
         T = __shfl_up_sync(0xffffffffu, T, 1);
         G = __shfl_up_sync(0xffffffffu, G, 1);
+        // lanes outside the diagonal run with bits = 0 on pixel 0 (a = 0:
+        // nothing changes, T and G stay finite), so the only branch is
+        // warp-uniform -- no divergence bookkeeping per step
         const int j = st - lane;
-        if ((unsigned)j >= (unsigned)nact) continue;
-        const uint2 m = sM[j];
-        if (lane == 0) {
-            const float2 s = sS[j];
+        const bool inr = (unsigned)j < (unsigned)nact;
+        const int jj = inr ? j : 0;
+        const uint2 m = sM[jj];
+        if (lane == 0 && inr) {
+            const float2 s = sS[jj];
             T = s.x;
             G = s.y;
         }
-        const uint32_t bits = ((hi ? m.y : m.x) >> sh) & 3u;
-        if (bits == 0u) continue;
+        const uint32_t bits = inr ? ((hi ? m.y : m.x) >> sh) & 3u : 0u;
+        if (!__any_sync(0xffffffffu, bits != 0u)) continue;
         seen |= bits;
-        const float2 xy = sXY[j];
-        const float4 pg = sG[j];
-        const float gd = DEPTH ? sD[j] : 0.f;
+        const int j_ = jj;
+        const float2 xy = sXY[j_];
+        const float4 pg = sG[j_];
+        const float gd = DEPTH ? sD[j_] : 0.f;
         bwd_term<DEPTH, CLAMP>(bits & 1u, xy.x, xy.y, pg, gd, A0, B0, C0, amax, T, G, q0);
         bwd_term<DEPTH, CLAMP>(bits & 2u, xy.x, xy.y, pg, gd, A1, B1, C1, amax, T, G, q1);
     }
