@@ -45,6 +45,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--configs", default="replica,tum")
+    ap.add_argument("--train-steps", type=int, default=0,
+                    help="fused training steps on the target before timing (converged regime)")
     args = ap.parse_args()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     opts = ss.RasterOpts(sh_degree=0)
@@ -54,6 +56,14 @@ def main():
         gmap = ss.GaussianMap.from_scene(survey_scene(n, 0))
         tgt = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(n, 100)), cam,
                                    opts).image.clone()
+        if args.train_steps:
+            trainer = ss.MappingEngine(gmap, w, h, opts)
+            trainer.fit_capacity(cam)
+            trainer.enable_graph()
+            for _ in range(args.train_steps):
+                trainer.step(cam, tgt)
+            trainer.synchronize()
+            gmap = trainer.gmap
         out = ss.rasterize_forward(gmap, cam, opts)
         lb = ss.compute_losses(out.image, tgt, gmap.opacity_logits)
         g = lb.grad_image
@@ -63,14 +73,16 @@ def main():
         b = ss.screen_space_grads_pixelwise(out, g).double()
         agree = float((a - b).norm() / a.norm())
         # whole fused iteration (CUDA graph), and with the pixel-wise kernel swapped in
-        eng = ss.MappingEngine(ss.GaussianMap.from_scene(survey_scene(n, 0)), w, h, opts)
+        eng = ss.MappingEngine(gmap.clone(), w, h, opts)
         eng.fit_capacity(cam)
         eng.enable_graph()
         it_ms = timed(lambda: eng.step(cam, tgt), args.reps, flush)
         eng.synchronize()
         line = {
-            "config": {"workload": f"S({n},{w}x{h}) SH0, one view", "gaussians": n,
-                       "image": [w, h], "pairs": out.pair_count},
+            "config": {"workload": f"S({n},{w}x{h}) SH0, one view"
+                                   + (f", after {args.train_steps} training steps"
+                                      if args.train_steps else ""),
+                       "gaussians": n, "image": [w, h], "pairs": out.pair_count},
             "backward_splatwise_ms": splat_ms,
             "backward_pixelwise_ms": pixel_ms,
             "speedup_splat_over_pixel": pixel_ms / splat_ms,
