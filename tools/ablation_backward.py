@@ -8,7 +8,7 @@ each is timed alone with CUDA events on the launching stream, L2 flushed
 between repetitions.  Also reports the whole fused iteration time and the
 iteration time with the pixel-wise kernel substituted.
 
-    python ablation_backward.py [--reps 20] > profiles/r01_ablation_backward.jsonl
+    python tools/ablation_backward.py [--reps 20] > profiles/r01_ablation_backward.jsonl
 """
 
 import argparse
@@ -16,7 +16,7 @@ import json
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2410_00486_b200 as ss  # noqa: E402

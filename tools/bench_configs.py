@@ -3,14 +3,14 @@
 S(1M, 1200x680) per view, and SH3 S(500k, 1200x680).  Device time of K
 CUDA-graph steps bracketed by events, L2 flushed between steps.
 
-    python bench_configs.py > profiles/r01_configs.jsonl
+    python tools/bench_configs.py > profiles/r01_configs.jsonl
 """
 
 import json
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2410_00486_b200 as ss  # noqa: E402

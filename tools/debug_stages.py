@@ -1,6 +1,6 @@
 """Stage-by-stage timing/debug run at increasing map sizes (GPU)."""
 import sys, time, os
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2410_00486_b200 as ss
 from paper_2410_00486_b200 import _lib

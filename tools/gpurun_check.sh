@@ -2,7 +2,7 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 timeout 400 python -m pytest tests -m gpu -q -x --timeout 120 > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
-timeout 200 python profile_kernels.py > gpurun_out/kernels.txt 2>&1
+timeout 200 python tools/profile_kernels.py > gpurun_out/kernels.txt 2>&1
 timeout 200 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench.log 2>&1
 echo "bench exit $?" >> gpurun_out/bench.log
 tail -2 gpurun_out/pytest_gpu.log; grep -v Warn gpurun_out/kernels.txt | head -24; tail -2 gpurun_out/bench.log | cut -c1-200

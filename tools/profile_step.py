@@ -3,7 +3,7 @@ cudaProfilerStart/Stop window (for `ncu --profile-from-start off`)."""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2410_00486_b200 as ss  # noqa: E402
