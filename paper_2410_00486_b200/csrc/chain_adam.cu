@@ -522,7 +522,7 @@ constexpr int kRestCTA = 256;
 constexpr int kRestRow = 45;
 
 template <int NC>
-__global__ void __launch_bounds__(kRestCTA, 2) chain_adam_rest_kernel(
+__global__ void __launch_bounds__(kRestCTA, 3) chain_adam_rest_kernel(
     int64_t n, float* __restrict__ pos, float4* __restrict__ rot, float* __restrict__ ls,
     float* __restrict__ opl, float* __restrict__ shdc, float* __restrict__ shrest, CamC cam_v,
     const ss_camera* __restrict__ d_cam, int deg, float dilation, const float* __restrict__ g2d,
