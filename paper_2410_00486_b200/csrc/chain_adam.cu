@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t n, float* pos, float4
     bool fin = grad_finite(o);
     const float* rg = (upd_rest && Gr.d_sh_rest) ? Gr.d_sh_rest + 45 * i : nullptr;
     if (rg)
-        for (int k = 0; k < 45; ++k) fin = fin && finitef(rg[k]);
+        for (int k = 0; k < 45; ++k) fin &= finitef(rg[k]);  // loads in flight together
     if (!fin) report_first(&st->first_nonfinite_grad, i);
     adam_gaussian(i, o, rg, pos, rot, ls, opl, shdc, shrest, M, V, hp, upd_rest != 0, st);
 }

@@ -117,7 +117,11 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         if (sh_degree > 0) {
             // sh_rest only changes when it is optimised (sh_degree > 0); at
             // degree 0 the host validates it once on upload.
-            for (int k = 0; k < 45; ++k) fin = fin && finitef(sh_rest[45 * i + k]);
+            // non-short-circuit: all 45 loads in flight (a && chain waits on each)
+            bool rf = true;
+#pragma unroll 15
+            for (int k = 0; k < 45; ++k) rf &= finitef(sh_rest[45 * i + k]);
+            fin = fin && rf;
         }
         if (!fin) report_first(&status->first_nonfinite_param, i);
 
