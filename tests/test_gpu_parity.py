@@ -432,6 +432,62 @@ def test_densify_masks_and_indices_bit_exact():
     np.testing.assert_array_equal(res.survivors.cpu().numpy(), d["survivors"])
 
 
+def test_engine_densify_equals_api_densify_plus_resize():
+    """MappingEngine.densify (compaction with the Adam moments riding along as
+    extra planes, trainer.py:187-193) == densify_and_prune + resize_for_densify
+    (densify.py:103-173, optimizer.py:136-146) on identical inputs."""
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    d = load("densify")
+
+    def make():
+        g = ss.GaussianMap.from_arrays(d["pre_positions"], d["pre_rotations"],
+                                       d["pre_log_scales"], d["pre_opacity_logits"], d["pre_sh"])
+        g.grad2d_accum = torch.as_tensor(d["pre_grad2d_accum"], dtype=torch.float32,
+                                         device="cuda")
+        g.grad3d_accum = torch.as_tensor(d["pre_grad3d_accum"], dtype=torch.float32,
+                                         device="cuda")
+        g.obs_count = torch.as_tensor(d["pre_obs_count"], dtype=torch.int32, device="cuda")
+        return g
+
+    ext = float(d["extent"])
+    cfg = ss.DensifyConfig()
+    ga, gb = make(), make()
+    h = ga.to_numpy()
+    om = orc.OMap(h["positions"], h["rotations"], h["log_scales"], h["opacity_logits"], h["sh"],
+                  h["grad2d_accum"], h["grad3d_accum"], h["obs_count"])
+    _, large, _ = orc.densify_masks(om, scene_extent=ext)
+    normals = np.random.default_rng(11).standard_normal((2 * int(large.sum()), 3))
+    eng = ss.MappingEngine(ga, 64, 48, ss.RasterOpts(sh_degree=3),
+                           ss.EngineConfig(densify=cfg, scene_extent=ext))
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    for dct in (eng.state.m, eng.state.v):
+        for t in dct.values():
+            t.copy_(torch.rand(t.shape, device="cuda", generator=gen))
+    st = ss.AdamState.for_map(gb)
+    for src, dst in ((eng.state.m, st.m), (eng.state.v, st.v)):
+        for k, t in src.items():
+            dst[k] = t.clone()
+    ra = eng.densify(normals=normals)
+    rb = ss.densify_and_prune(gb, cfg, ext, normals=normals)
+    st = ss.resize_for_densify(st, rb.survivors, rb.n_new)
+    assert len(ga) == len(gb) and ra.n_new == rb.n_new
+    np.testing.assert_array_equal(ra.survivors.cpu().numpy(), rb.survivors.cpu().numpy())
+    a, b = ga.to_numpy(), gb.to_numpy()
+    for f in ("positions", "rotations", "log_scales", "opacity_logits", "sh"):
+        np.testing.assert_array_equal(a[f], b[f])
+    for src, dst in ((eng.state.m, st.m), (eng.state.v, st.v)):
+        for k in src:
+            np.testing.assert_array_equal(src[k].cpu().numpy(), dst[k].cpu().numpy())
+    # the engine's buffers follow the new size and the next step runs
+    tgt = torch.zeros((48, 64, 3), device="cuda")
+    cam = ss.Camera.looking_at(60.0, 60.0, 32.0, 24.0, 64, 48, eye=(0.0, 0.3, 1.5),
+                               target=(0.0, 0.0, 0.0))
+    eng.step(cam, tgt)
+    eng.synchronize()
+    assert np.isfinite(eng.losses()[-1][1])
+
+
 def test_opacity_reset():
     _need_gpu()
     import paper_2410_00486_b200 as ss
