@@ -39,7 +39,7 @@ extern "C" {
 #define SS_ECUDA (-2)
 #define SS_ECAPACITY (-3)
 
-#define SS_ABI_VERSION 1
+#define SS_ABI_VERSION 2
 
 /* Device status block, zeroed/initialised by ss_status_reset.  Index words
  * hold INT64_MAX when no failure was seen. */
@@ -113,7 +113,16 @@ typedef struct ss_bins {
     uint32_t *d_tile_start;  /* [n_tiles] */
     uint32_t *d_tile_end;    /* [n_tiles] */
     uint32_t *d_ckpt_base;   /* [n_tiles+1] exclusive scan of ceil(len/32) */
+    /* Optional forward schedule (both or neither; n_tiles <= SS_ORDER_MAX_TILES):
+     * d_tile_cost receives each tile's blend cost from ss_blend_forward
+     * (SM cycles), ss_bin_sort turns the last costs into d_tile_order (the
+     * permutation of tiles the forward's CTAs take, costliest first).  The
+     * caller initialises d_tile_order to the identity and d_tile_cost to 0.
+     * Results do not depend on the order; only the kernel's tail does. */
+    uint32_t *d_tile_order;  /* [n_tiles] */
+    uint32_t *d_tile_cost;   /* [n_tiles] */
 } ss_bins;
+#define SS_ORDER_MAX_TILES 16384
 
 /* ---------------------------------------------------------------- status */
 int ss_abi_version(void);

@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 
 SS_OK, SS_EINVAL, SS_ECUDA, SS_ECAPACITY = 0, -1, -2, -3
 SS_REDUCE_DOUBLES = 2 + 2 * 592
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 VP = ctypes.c_void_p
 I32 = ctypes.c_int32
@@ -34,6 +34,7 @@ class SSStatus(ctypes.Structure):
                 ("opacity_sum", F64), ("reserved2", I64)]
 
 
+ORDER_MAX_TILES = 16384  # SS_ORDER_MAX_TILES
 STATUS_WORDS = 10  # 80-byte ss_status as int64 words (word 8 holds a double)
 SNAPSHOT_DOUBLES = 11  # ss_step_snapshot row: 8 status words, opacity sum, 2 loss sums
 SN_OPACITY_SUM, SN_L1_SUM, SN_SSIM_SUM = 8, 9, 10
@@ -65,7 +66,8 @@ class SSSplats(ctypes.Structure):
 
 class SSBins(ctypes.Structure):
     _fields_ = [("pair_capacity", I64), ("d_pair_splat", VP), ("d_tile_start", VP),
-                ("d_tile_end", VP), ("d_ckpt_base", VP)]
+                ("d_tile_end", VP), ("d_ckpt_base", VP), ("d_tile_order", VP),
+                ("d_tile_cost", VP)]
 
 
 class SSParamGrads(ctypes.Structure):

@@ -359,6 +359,91 @@ __global__ void __launch_bounds__(256) scan_kernel(const uint32_t* __restrict__ 
     }
 }
 
+// 1-CTA tile metadata (n_tiles <= SS_ORDER_MAX_TILES): the checkpoint slot
+// bases -- exclusive scan of ceil(len/32) over n_tiles + 1 entries, as
+// scan_kernel<true> -- and the forward's tile order for this call, costliest
+// first by the previous forward's per-tile cost (64 linear buckets of
+// cost / max cost; order within a bucket is arbitrary).  The forward's
+// per-tile durations vary 70x and follow the previous iteration's closely;
+// a raster-order grid leaves the longest tiles to start last.
+constexpr int kOrderBuckets = 64;
+
+__global__ void __launch_bounds__(1024) tile_meta_kernel(const uint32_t* __restrict__ tstart,
+                                                         const uint32_t* __restrict__ tend,
+                                                         int n_tiles,
+                                                         uint32_t* __restrict__ ckpt_base,
+                                                         const uint32_t* __restrict__ cost,
+                                                         uint32_t* __restrict__ order) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_max;
+    __shared__ uint32_t s_h[kOrderBuckets];
+    const int t = threadIdx.x, w = t >> 5, l = t & 31;
+    const int n = n_tiles + 1;
+    const int per = (n + 1023) / 1024;  // <= 17
+    const int i0 = t * per;
+    uint32_t sum = 0, cmax = 0;
+    for (int k = 0; k < per; ++k) {
+        const int i = i0 + k;
+        if (i < n_tiles) {
+            sum += (tend[i] - tstart[i] + 31u) >> 5;
+            cmax = max(cmax, cost[i]);
+        }
+    }
+    if (t < kOrderBuckets) s_h[t] = 0u;
+    if (t == 0) s_max = 0u;
+    // block exclusive scan of the per-thread sums
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += y;
+    }
+    if (l == 31) s_warp[w] = incl;
+    cmax = __reduce_max_sync(0xffffffffu, cmax);
+    __syncthreads();
+    if (l == 0) atomicMax(&s_max, cmax);
+    if (w == 0) {
+        uint32_t v = s_warp[l], vi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, vi, o);
+            if (l >= o) vi += y;
+        }
+        s_warp[l] = vi - v;
+    }
+    __syncthreads();
+    uint32_t run = s_warp[w] + incl - sum;
+    for (int k = 0; k < per; ++k) {
+        const int i = i0 + k;
+        if (i < n) ckpt_base[i] = run;
+        if (i < n_tiles) run += (tend[i] - tstart[i] + 31u) >> 5;
+    }
+    // counting sort by cost bucket, descending
+    const unsigned long long mx = (unsigned long long)s_max + 1ull;
+    for (int i = t; i < n_tiles; i += 1024) {
+        const uint32_t b = (uint32_t)(((unsigned long long)cost[i] * kOrderBuckets) / mx);
+        atomicAdd(&s_h[kOrderBuckets - 1 - b], 1u);
+    }
+    __syncthreads();
+    if (w == 0) {
+        uint32_t a = s_h[l], b = s_h[l + 32], ai = a, bi = b;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ya = __shfl_up_sync(0xffffffffu, ai, o);
+            const uint32_t yb = __shfl_up_sync(0xffffffffu, bi, o);
+            if (l >= o) ai += ya, bi += yb;
+        }
+        const uint32_t atot = __shfl_sync(0xffffffffu, ai, 31);
+        s_h[l] = ai - a;
+        s_h[l + 32] = atot + bi - b;
+    }
+    __syncthreads();
+    for (int i = t; i < n_tiles; i += 1024) {
+        const uint32_t b = (uint32_t)(((unsigned long long)cost[i] * kOrderBuckets) / mx);
+        order[atomicAdd(&s_h[kOrderBuckets - 1 - b], 1u)] = (uint32_t)i;
+    }
+}
+
 // ------------------------------------------------------------------- emit
 // One warp per 32 consecutive splats in (depth, index) order: the warp's
 // pairs form one contiguous output range, written lane-strided (coalesced);
@@ -985,9 +1070,16 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
         if (e != cudaSuccess) return e;
     }
     // checkpoint slot bases: exclusive scan of ceil(len/32), n_tiles+1 entries
-    scan_kernel<true><<<div_up(n_tiles + 1, 256 * kScanItemsTiles), 256, 0, s>>>(
-        bins->d_tile_start, nullptr, bins->d_tile_end, (uint32_t)n_tiles + 1, bins->d_ckpt_base,
-        L.st_scan2, L.ctrl + 9, nullptr, nullptr, 0);
+    // (+ the forward's tile order when the caller keeps one)
+    if (bins->d_tile_order && bins->d_tile_cost && n_tiles <= SS_ORDER_MAX_TILES) {
+        tile_meta_kernel<<<1, 1024, 0, s>>>(bins->d_tile_start, bins->d_tile_end, n_tiles,
+                                            bins->d_ckpt_base, bins->d_tile_cost,
+                                            bins->d_tile_order);
+    } else {
+        scan_kernel<true><<<div_up(n_tiles + 1, 256 * kScanItemsTiles), 256, 0, s>>>(
+            bins->d_tile_start, nullptr, bins->d_tile_end, (uint32_t)n_tiles + 1,
+            bins->d_ckpt_base, L.st_scan2, L.ctrl + 9, nullptr, nullptr, 0);
+    }
     return cudaGetLastError();
 }
 

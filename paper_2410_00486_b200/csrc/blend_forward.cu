@@ -31,6 +31,12 @@
 
 namespace ss {
 
+#ifdef SS_FWD_TRACE
+// diagnostics build only (tools/trace_forward.py): per-CTA (tile, smid,
+// start, end) from the global timer
+__device__ unsigned long long g_fwd_trace[4 * 65536];
+#endif
+
 struct PixState {
     float T, c0, c1, c2, D;
     int last;
@@ -47,15 +53,24 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
     float* __restrict__ final_t, int32_t* __restrict__ n_contrib, float* __restrict__ depth_img,
     int32_t* __restrict__ k_eff, uint8_t* __restrict__ contributed, float4* __restrict__ ckpt,
     float* __restrict__ ckpt_depth, uint32_t* __restrict__ ckpt_mask, uint2* __restrict__ work,
-    int64_t work_cap, int64_t* bucket_count) {
+    int64_t work_cap, int64_t* bucket_count, const uint32_t* __restrict__ tile_order,
+    uint32_t* __restrict__ tile_cost) {
     __shared__ SplatRec s_rec[256];
     __shared__ uint32_t s_id[256];
     __shared__ uint8_t s_band[256];  // bit w: the splat's blend region reaches band w
     __shared__ int s_hit[CONTRIB ? 256 : 1];
     __shared__ int s_kmax[4];
     __shared__ unsigned long long s_wbase;
-    const int tile = blockIdx.x;
+    // CTA -> tile through the costliest-first order of ss_bin_sort (the
+    // tiles' results do not depend on it); the CTA's cycles feed the next one
+    const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
+    const long long clk0 = clock64();
     const int t = threadIdx.x;
+#ifdef SS_FWD_TRACE
+    unsigned long long tr0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
+    uint32_t tr_iters = 0;
+#endif
     const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
     // warp w owns the 4-row band 4w..4w+3; a thread owns rows r and r + 2 of
     // its column (the two pixels share the dx terms)
@@ -137,6 +152,9 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
             while (todo) {
                 const int j = j0 + __ffs(todo) - 1;
                 todo &= todo - 1;
+#ifdef SS_FWD_TRACE
+                ++tr_iters;
+#endif
                 const float4 A = s_rec[j].a, B = s_rec[j].b, C = s_rec[j].c;
                 // the two pixels share a column: dx-only terms once; then the
                 // quad_finish / splat_falloff operations of both pixels packed
@@ -218,7 +236,27 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
     if ((t & 31) == 0) s_kmax[t >> 5] = km;
     __syncthreads();
     const int kmax = max(max(s_kmax[0], s_kmax[1]), max(s_kmax[2], s_kmax[3]));
-    if (t == 0) k_eff[tile] = kmax;
+    if (t == 0) {
+        k_eff[tile] = kmax;
+        if (tile_cost) tile_cost[tile] = (uint32_t)min(clock64() - clk0, 0xffffffffll);
+    }
+#ifdef SS_FWD_TRACE
+    __shared__ uint32_t s_iters;
+    if (t == 0) s_iters = 0;
+    __syncthreads();
+    if ((t & 31) == 0) atomicAdd(&s_iters, tr_iters);
+    __syncthreads();
+    if (t == 0 && tile < 65536) {
+        unsigned long long tr1;
+        uint32_t smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_fwd_trace[4 * tile] = s_iters;
+        g_fwd_trace[4 * tile + 1] = smid;
+        g_fwd_trace[4 * tile + 2] = tr0;
+        g_fwd_trace[4 * tile + 3] = tr1;
+    }
+#endif
     const int nbk = (kmax + kUnit - 1) / kUnit;  // backward units of 64 list positions
     if (nbk > 0 && work) {
         if (t == 0)
@@ -242,13 +280,15 @@ cudaError_t launch_blend_forward(const ss_camera* cam, const ss_raster_opts* o,
     int n_tiles = tx * ty;
     const bool depthf = o->with_depth != 0;
     const bool contribf = contributed != nullptr;
+    const bool ordered = bins->d_tile_order && bins->d_tile_cost && n_tiles <= SS_ORDER_MAX_TILES;
     auto args = [&](auto kern) {
         kern<<<n_tiles, 128, 0, s>>>(
             cam->width, cam->height, tx, bins->d_tile_start, bins->d_tile_end, bins->d_ckpt_base,
             bins->d_pair_splat, reinterpret_cast<const SplatRec*>(sp->d_rec), o->t_min,
             o->alpha_min, o->alpha_max, o->background[0], o->background[1], o->background[2],
             image, final_t, n_contrib, depth, k_eff, contributed, reinterpret_cast<float4*>(ckpt),
-            ckpt_depth, ckpt_mask, reinterpret_cast<uint2*>(work), work_cap, &st->bucket_count);
+            ckpt_depth, ckpt_mask, reinterpret_cast<uint2*>(work), work_cap, &st->bucket_count,
+            ordered ? bins->d_tile_order : nullptr, ordered ? bins->d_tile_cost : nullptr);
     };
     if (depthf && contribf)
         args(blend_forward_kernel<true, true>);
@@ -262,3 +302,10 @@ cudaError_t launch_blend_forward(const ss_camera* cam, const ss_raster_opts* o,
 }
 
 }  // namespace ss
+
+#ifdef SS_FWD_TRACE
+extern "C" int ss_debug_fwd_trace(void* host, size_t bytes) {
+    if (bytes > sizeof(ss::g_fwd_trace)) bytes = sizeof(ss::g_fwd_trace);
+    return (int)cudaMemcpyFromSymbol(host, ss::g_fwd_trace, bytes);
+}
+#endif

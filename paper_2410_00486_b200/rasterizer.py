@@ -105,18 +105,23 @@ class BinBuffers:
     tile_start: torch.Tensor  # (T,)
     tile_end: torch.Tensor    # (T,)
     ckpt_base: torch.Tensor   # (T+1,)
+    tile_order: torch.Tensor  # (T,) forward CTA -> tile, costliest first (identity at start)
+    tile_cost: torch.Tensor   # (T,) last forward's per-tile cost (SM cycles)
 
     @classmethod
     def alloc(cls, cap, n_tiles, dev):
         i32 = dict(dtype=torch.int32, device=dev)
         return cls(cap, torch.empty(max(cap, 1), **i32), torch.empty(n_tiles, **i32),
-                   torch.empty(n_tiles, **i32), torch.empty(n_tiles + 1, **i32))
+                   torch.empty(n_tiles, **i32), torch.empty(n_tiles + 1, **i32),
+                   torch.arange(n_tiles, **i32), torch.zeros(n_tiles, **i32))
 
     def ss(self):
         b = _lib.SSBins()
         b.pair_capacity = self.capacity
         b.d_pair_splat, b.d_tile_start = P(self.pairs), P(self.tile_start)
         b.d_tile_end, b.d_ckpt_base = P(self.tile_end), P(self.ckpt_base)
+        if self.tile_order is not None and self.tile_order.numel() <= _lib.ORDER_MAX_TILES:
+            b.d_tile_order, b.d_tile_cost = P(self.tile_order), P(self.tile_cost)
         return b
 
 
