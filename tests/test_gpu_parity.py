@@ -87,6 +87,55 @@ def test_binning_bit_exact(case):
     np.testing.assert_array_equal(g.active_tiles, ti.active_tiles)
 
 
+def test_tile_meta_ckpt_bases_and_forward_order(case):
+    """tile_meta_kernel: checkpoint bases == exclusive scan of ceil(len/32);
+    after a forward has written the per-tile costs, a second ss_bin_sort
+    orders the tiles costliest first (64 cost buckets), and a forward run
+    in that order reproduces the raster-order results bit for bit."""
+    import ctypes
+    from paper_2410_00486_b200 import _lib
+    from paper_2410_00486_b200.rasterizer import P, bin_workspace, stream_handle
+    ss, out, cam = case["ss"], case["out"], case["cam"]
+    b = out.bins
+    T = b.tile_start.numel()
+    lens = (b.tile_end.cpu().numpy().astype(np.int64) - b.tile_start.cpu().numpy().astype(np.int64))
+    lens[lens < 0] = 0
+    ref = np.concatenate([[0], np.cumsum((lens + 31) // 32)])
+    np.testing.assert_array_equal(b.ckpt_base.cpu().numpy().astype(np.int64), ref)
+    cost = b.tile_cost.cpu().numpy().astype(np.uint64)
+    assert cost[lens > 0].min() > 0  # every non-empty tile's CTA recorded its cycles
+    # re-bin: the order now follows those costs
+    L = _lib.lib()
+    n = len(case["g"])
+    ws = bin_workspace(n, b.capacity, T, b.pairs.device)
+    st = torch.zeros(_lib.STATUS_WORDS, dtype=torch.int64, device=b.pairs.device)
+    assert L.ss_status_reset(P(st), stream_handle()) == 0
+    cm = cam.to_ss() if hasattr(cam, "to_ss") else ss.Camera.of(cam).to_ss()
+    assert L.ss_bin_sort(n, ctypes.byref(out.splats.ss()), ctypes.byref(cm),
+                         ctypes.byref(b.ss()), P(ws), ws.numel(), P(st), stream_handle()) == 0
+    order = b.tile_order.cpu().numpy().astype(np.int64)
+    assert sorted(order.tolist()) == list(range(T))
+    bucket = (cost * 64) // (cost.max() + 1)
+    assert np.all(np.diff(bucket[order].astype(np.int64)) <= 0)
+    np.testing.assert_array_equal(b.ckpt_base.cpu().numpy().astype(np.int64), ref)
+    # forward in the new order == the first (arbitrary-order) forward
+    dev = b.pairs.device
+    img, ft = torch.empty_like(out.image), torch.empty_like(out.final_t)
+    nc, ke = torch.empty_like(out.n_contrib), torch.empty_like(out.k_eff_tiles)
+    contrib = torch.zeros(n, dtype=torch.uint8, device=dev)
+    ck, cmask = torch.empty_like(out.ckpt), torch.empty_like(out.ckpt_mask)
+    work = torch.empty_like(out.work)
+    op = case["opts"].to_ss()
+    assert L.ss_blend_forward(ctypes.byref(cm), ctypes.byref(op), ctypes.byref(out.splats.ss()),
+                              ctypes.byref(b.ss()), P(img), P(ft), P(nc), None, P(ke),
+                              P(contrib), P(ck), None, P(cmask), P(work), out.work_capacity,
+                              P(st), stream_handle()) == 0
+    torch.cuda.synchronize()
+    for a_, b_ in ((img, out.image), (ft, out.final_t), (nc, out.n_contrib),
+                   (ke, out.k_eff_tiles), (contrib.bool(), out.contributed)):
+        np.testing.assert_array_equal(a_.cpu().numpy(), b_.cpu().numpy())
+
+
 _LEGACY_BINNING = r"""
 import sys, numpy as np
 sys.path.insert(0, {repo!r}); sys.path.insert(0, {tests!r})
