@@ -26,6 +26,32 @@ constexpr int LT = 32;                // output tile side
 constexpr int LH = LT + 2 * LR;       // 42: halo side
 constexpr int LP = 44;                // padded row pitch (float4 rows)
 
+#ifdef SS_FWD_TRACE
+// diagnostics build only: per-CTA (smid, start, end) of ssim_fwd [0] and ssim_bwd [1]
+__device__ unsigned long long g_ssim_trace[2][4 * 4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+}
+#define SSIM_TRACE_BEGIN const unsigned long long tr0 = gtimer();
+#define SSIM_TRACE_END(K)                                                          \
+    if (threadIdx.x == 0) {                                                        \
+        uint32_t smid;                                                             \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));                          \
+        const int b = blockIdx.y * gridDim.x + blockIdx.x;                         \
+        if (b < 4096) {                                                            \
+            g_ssim_trace[K][4 * b] = b;                                            \
+            g_ssim_trace[K][4 * b + 1] = smid;                                     \
+            g_ssim_trace[K][4 * b + 2] = tr0;                                      \
+            g_ssim_trace[K][4 * b + 3] = gtimer();                                 \
+        }                                                                          \
+    }
+#else
+#define SSIM_TRACE_BEGIN
+#define SSIM_TRACE_END(K)
+#endif
+
 struct SsimWindow {
     float w[11];
 };
@@ -76,6 +102,7 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
     __shared__ __align__(16) float sy[LH][LP];
     __shared__ __align__(16) float sh[5][LH][LT];
     __shared__ double red[2][8];
+    SSIM_TRACE_BEGIN
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * LT, y0 = blockIdx.y * LT;
     const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
@@ -191,6 +218,7 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
         partials[2 * bid] = a;
         partials[2 * bid + 1] = b;
     }
+    SSIM_TRACE_END(0)
 }
 
 // gp(u) = sum_m w[m] g[u - 5 + m] over a zero-extended shared line; lc is
@@ -228,6 +256,7 @@ __global__ void __launch_bounds__(256, 3) ssim_bwd_kernel(int H, int W, const fl
                                                        int n_partials,
                                                        double* __restrict__ sums) {
     extern __shared__ __align__(16) float smem_b[];
+    SSIM_TRACE_BEGIN
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 32) {
         // fixed-order reduction of ssim_fwd's per-CTA (|x-y|, SSIM) sums
         double a = 0.0, b = 0.0;
@@ -289,17 +318,23 @@ __global__ void __launch_bounds__(256, 3) ssim_bwd_kernel(int H, int W, const fl
                 }
                 float o4[4];
                 taps4(v, win, o4);
-                if (xborder) {
-#pragma unroll
-                    for (int o = 0; o < 4; ++o) {
-                        const int j = x0 + c0 + o;
-                        o4[o] += fold_extra(j, W, x0, win, [&](int k) { return sg[f][r][k]; });
-                    }
-                }
                 *reinterpret_cast<float4*>(&sh[f][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
             }
         }
         __syncthreads();
+        if (xborder) {
+            // mirror folds of the <= 10 columns next to the image borders as
+            // their own (column, row, map) tasks: inside the row pass every
+            // warp held a folding lane and ran the fold for all of them
+            for (int task = t; task < 2 * LR * LH * 3; task += 256) {
+                const int idx = task % (2 * LR), rest = task / (2 * LR);
+                const int r = rest % LH, f = rest / LH;
+                const int j = idx < LR ? 1 + idx : W - 6 + (idx - LR);
+                if (j < x0 || j >= x0 + LT || (idx >= LR && j <= LR)) continue;
+                sh[f][r][j - x0] += fold_extra(j, W, x0, win, [&](int k) { return sg[f][r][k]; });
+            }
+            __syncthreads();
+        }
         // axis 0 (rows): column q, 4 consecutive rows; combine
         float adj[3][4];
 #pragma unroll
@@ -311,8 +346,9 @@ __global__ void __launch_bounds__(256, 3) ssim_bwd_kernel(int H, int W, const fl
             if (yborder) {
 #pragma unroll
                 for (int o = 0; o < 4; ++o) {
-                    const int i = y0 + 4 * rg + o;
-                    adj[f][o] += fold_extra(i, H, y0, win, [&](int k) { return sh[f][k][q]; });
+                    const int i = y0 + 4 * rg + o;  // warp-uniform
+                    if ((i >= 1 && i <= LR) || (i >= H - 6 && i <= H - 2))
+                        adj[f][o] += fold_extra(i, H, y0, win, [&](int k) { return sh[f][k][q]; });
                 }
             }
         }
@@ -340,6 +376,7 @@ __global__ void __launch_bounds__(256, 3) ssim_bwd_kernel(int H, int W, const fl
             if (oy < H) pg[4 * ((size_t)oy * W + ox) + 3] = gdot[o];
         }
     }
+    SSIM_TRACE_END(1)
 }
 
 // L1-only variant (lambda_ssim == 0): losses.py:147-153
@@ -528,3 +565,11 @@ cudaError_t launch_depth_l1(int H, int W, const float* d, const float* tgt, floa
 }
 
 }  // namespace ss
+
+#ifdef SS_FWD_TRACE
+extern "C" int ss_debug_ssim_trace(int kind, void* host, size_t bytes) {
+    if (bytes > sizeof(ss::g_ssim_trace[0])) bytes = sizeof(ss::g_ssim_trace[0]);
+    return (int)cudaMemcpyFromSymbol(host, ss::g_ssim_trace, bytes,
+                                     (size_t)kind * sizeof(ss::g_ssim_trace[0]));
+}
+#endif

@@ -100,3 +100,22 @@ for name, seq in (("raster", np.arange(T)), ("prev dur", np.argsort(-dur)),
         v = heapq.heappop(h)
         heapq.heappush(h, v + dur2[i] * 1.0)
     print(f"next iteration, order {name:10s}: makespan {max(h) / 1e3:.1f} us")
+# SSIM kernels (same diagnostics build)
+if hasattr(L, "ss_debug_ssim_trace"):
+    f2 = L.ss_debug_ssim_trace
+    f2.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
+    nb = ((W + 31) // 32) * ((H + 31) // 32)
+    for kind, name in ((0, "ssim_fwd"), (1, "ssim_bwd")):
+        b3 = np.zeros(4 * nb, np.uint64)
+        assert f2(kind, b3.ctypes.data, b3.nbytes) == 0
+        t3 = b3.reshape(nb, 4).astype(np.int64)
+        s3, a3, e3 = t3[:, 1], t3[:, 2] - t3[:, 2].min(), t3[:, 3] - t3[:, 2].min()
+        d3 = e3 - a3
+        lastend = np.array([e3[s3 == k].max() for k in np.unique(s3)])
+        nper = np.bincount(s3)
+        print(f"{name}: CTAs {nb} elapsed {e3.max() / 1e3:.1f} us, CTA dur mean "
+              f"{d3.mean() / 1e3:.2f} min {d3.min() / 1e3:.2f} max {d3.max() / 1e3:.2f} us, "
+              f"SM last-end min {lastend.min() / 1e3:.1f} median {np.median(lastend) / 1e3:.1f}, "
+              f"CTAs/SM {nper[nper > 0].min()}..{nper.max()}, start of last CTA "
+              f"{a3.max() / 1e3:.1f} us")
+        np.save(f"gpurun_out/{name}_trace.npy", t3)
