@@ -32,109 +32,181 @@ namespace ss {
 
 constexpr int kBwdWarps = 2;
 
-// One (pixel, splat) term of the wavefront.  `bit` is the forward's blend
-// mask bit; a pair that was not blended gets a = 0, which leaves T and G
-// bit-exactly unchanged and contributes nothing, so a lane's two terms run
-// branch-free.
-struct SplatAcc {
-    float r0, r1, r2, rz, s_da, s_dx, s_dy, s_xx, s_xy, s_yy;
+// The wavefront carries TWO pixels per lane and step, as the (lo, hi) lanes
+// of packed f32x2 values (FADD2/FMUL2/FFMA2: per lane the scalar IEEE
+// result, so alpha is recomputed with exactly the forward's operations).
+// The two pixel chains are independent, which doubles the work between the
+// shuffles and halves the number of wavefront steps.
+struct SplatAcc2 {  // one splat's partial sums, (pixel a, pixel b) lanes
+    f32x2 r0, r1, r2, rz, s_da, s_dx, s_dy, s_xx, s_xy, s_yy;
+};
+struct SplatP2 {  // one splat's record fields, duplicated into both lanes
+    f32x2 mx, my, c0, c1x2, c2, sig, cr, cg, cb, z;
 };
 
+__device__ __forceinline__ SplatP2 splat_p2(const float4& A, const float4& B, const float4& C) {
+    SplatP2 p;
+    p.mx = pk2(A.x, A.x);
+    p.my = pk2(A.y, A.y);
+    p.c0 = pk2(A.z, A.z);
+    p.c1x2 = pk2(A.w, A.w);
+    p.c2 = pk2(B.x, B.x);
+    p.sig = pk2(B.y, B.y);
+    p.cr = pk2(C.x, C.x);
+    p.cg = pk2(C.y, C.y);
+    p.cb = pk2(C.z, C.z);
+    p.z = pk2(B.w, B.w);
+    return p;
+}
+
+// One splat applied to a pixel pair.  `ba` / `bb` are the forward's blend
+// mask bits of the two pixels; a pair that was not blended gets a = 0, which
+// leaves T and G bit-exactly unchanged and contributes nothing, so the term
+// runs branch-free.
 template <bool DEPTH, bool CLAMP>
-__device__ __forceinline__ void bwd_term(bool bit, float px, float py, const float4& pg, float gd,
-                                         const float4& A, const float4& B, const float4& C,
-                                         float amax, float& T, float& G, SplatAcc& q) {
-    float dx, dy;
-    // CLAMP == false: no splat of the unit has sigma >= alpha_max, so
-    // sigma * falloff < alpha_max and the clamp is the identity
-    float a = CLAMP ? splat_alpha_blended(px, py, A, B, amax, dx, dy)
-                    : splat_falloff(splat_power(px, py, A, B, dx, dy), B);
-    a = bit ? a : 0.f;
-    const float w = __fmul_rn(a, T);
-    float grgb = pg.x * C.x + pg.y * C.y + pg.z * C.z;
-    if (DEPTH) {
-        grgb += gd * B.w;
-        q.rz += w * gd;
+__device__ __forceinline__ void bwd_term2(uint32_t ba, uint32_t bb, f32x2 px, f32x2 py, f32x2 gx,
+                                          f32x2 gy, f32x2 gz, f32x2 gw, f32x2 gd,
+                                          const SplatP2& S, float amax, f32x2& T, f32x2& G,
+                                          SplatAcc2& q) {
+    // splat_power / splat_falloff (common.cuh) per lane: same operations,
+    // same rounding as the forward's blend decision
+    const f32x2 dx = sub2(px, S.mx), dy = sub2(py, S.my);
+    const f32x2 m = fma2(mul2(S.c2, dy), dy, fma2(mul2(S.c1x2, dx), dy, mul2(mul2(S.c0, dx), dx)));
+    float e0, e1;
+    upk2(mul2(m, pk2(-0.5f * kLog2e, -0.5f * kLog2e)), e0, e1);
+    float a0, a1;
+    upk2(mul2(S.sig, pk2(ex2_approx(e0), ex2_approx(e1))), a0, a1);
+    // CLAMP == false: no splat of the unit has sigma >= alpha_max, so the
+    // clamp is the identity
+    if (CLAMP) {
+        a0 = fminf(a0, amax);
+        a1 = fminf(a1, amax);
     }
-    const float Gafter = G + grgb * w;
-    q.r0 += w * pg.x;
-    q.r1 += w * pg.y;
-    q.r2 += w * pg.z;
-    // alpha-path gradient (kernels.py:342-364); zero when clamped (and when
-    // not blended: a = 0)
-    const float om = __fsub_rn(1.0f, a);
-    const float dal = T * grgb - (pg.w - Gafter) * rcp_approx(om);
-    const float da = dal * ((!CLAMP || a != amax) ? a : 0.f);
-    const float tx = da * dx, ty = da * dy;
-    q.s_da += da;
-    q.s_dx += tx;
-    q.s_dy += ty;
-    q.s_xx += tx * dx;
-    q.s_xy += tx * dy;
-    q.s_yy += ty * dy;
-    T = __fmul_rn(T, om);
+    a0 = ba ? a0 : 0.f;
+    a1 = bb ? a1 : 0.f;
+    const f32x2 a = pk2(a0, a1);
+    const f32x2 w = mul2(a, T);
+    f32x2 grgb = fma2(gz, S.cb, fma2(gy, S.cg, mul2(gx, S.cr)));
+    if (DEPTH) {
+        grgb = fma2(gd, S.z, grgb);
+        q.rz = fma2(w, gd, q.rz);
+    }
+    const f32x2 Gafter = fma2(grgb, w, G);
+    q.r0 = fma2(w, gx, q.r0);
+    q.r1 = fma2(w, gy, q.r1);
+    q.r2 = fma2(w, gz, q.r2);
+    // alpha-path gradient (kernels.py:342-364):
+    //   dL/da = T (g . rgb) - (g . image - G_after) / (1 - a)
+    // zero when clamped (and when not blended: a = 0)
+    const f32x2 om = sub2(pk2(1.f, 1.f), a);
+    float o0, o1;
+    upk2(om, o0, o1);
+    const f32x2 dal = fma2(T, grgb, mul2(sub2(Gafter, gw), pk2(rcp_approx(o0), rcp_approx(o1))));
+    const f32x2 da =
+        mul2(dal, CLAMP ? pk2(a0 != amax ? a0 : 0.f, a1 != amax ? a1 : 0.f) : a);
+    const f32x2 tx = mul2(da, dx), ty = mul2(da, dy);
+    q.s_da = add2(q.s_da, da);
+    q.s_dx = add2(q.s_dx, tx);
+    q.s_dy = add2(q.s_dy, ty);
+    q.s_xx = fma2(tx, dx, q.s_xx);
+    q.s_xy = fma2(tx, dy, q.s_xy);
+    q.s_yy = fma2(ty, dy, q.s_yy);
+    T = mul2(T, om);
     G = Gafter;
+}
+
+__device__ __forceinline__ float hsum(f32x2 v) {
+    float lo, hi;
+    upk2(v, lo, hi);
+    return lo + hi;
 }
 
 // Commit one splat's sums as its 9 (10) screen-space gradients.
 template <int NC>
-__device__ __forceinline__ void bwd_commit(const SplatAcc& q, const float4& A, const float4& B,
+__device__ __forceinline__ void bwd_commit(const SplatAcc2& q, const float4& A, const float4& B,
                                            float* __restrict__ row) {
     const float c1 = 0.5f * A.w;
+    const float s_dx = hsum(q.s_dx), s_dy = hsum(q.s_dy);
     float acc[NC];
-    acc[0] = q.r0;
-    acc[1] = q.r1;
-    acc[2] = q.r2;
-    acc[3] = A.z * q.s_dx + c1 * q.s_dy;
-    acc[4] = c1 * q.s_dx + B.x * q.s_dy;
-    acc[5] = -0.5f * q.s_xx;
-    acc[6] = -q.s_xy;
-    acc[7] = -0.5f * q.s_yy;
-    acc[8] = q.s_da / B.y;
-    if (NC == 10) acc[NC - 1] = q.rz;
+    acc[0] = hsum(q.r0);
+    acc[1] = hsum(q.r1);
+    acc[2] = hsum(q.r2);
+    acc[3] = A.z * s_dx + c1 * s_dy;
+    acc[4] = c1 * s_dx + B.x * s_dy;
+    acc[5] = -0.5f * hsum(q.s_xx);
+    acc[6] = -hsum(q.s_xy);
+    acc[7] = -0.5f * hsum(q.s_yy);
+    acc[8] = hsum(q.s_da) / B.y;
+    if (NC == 10) acc[NC - 1] = hsum(q.rz);
 #pragma unroll
     for (int c = 0; c < NC; ++c)
         if (acc[c] != 0.f) atomicAdd(row + c, acc[c]);
 }
 
-// Diagonal wavefront over the warp's compacted pixel list; lane i applies
-// list positions 2i and 2i+1 to each pixel in turn.  Returns the lane's
+__device__ __forceinline__ f32x2 shfl_up2(f32x2 v) {
+    float lo, hi;
+    upk2(v, lo, hi);
+    return pk2(__shfl_up_sync(0xffffffffu, lo, 1), __shfl_up_sync(0xffffffffu, hi, 1));
+}
+
+// Per-warp compacted pixel list, pair-interleaved so that one pair's values
+// load as ready-made f32x2 operands: pixel j of pair jp = j >> 1 sits in lane
+// (j & 1) of each packed field.
+struct BwdList {
+    float x[kTilePx], y[kTilePx];  // coordinates (pair jp = float2 at 2 jp)
+    float g[4 * kTilePx];          // per pair: gx, gx', gy, gy', gz, gz', gw, gw'
+    float s[kTilePx * 2];          // per pair: T0, T0', G0, G0' (state at the unit start)
+    uint2 m[kTilePx];              // the two buckets' blend masks (pair = uint4)
+};
+
+// Diagonal wavefront over the warp's compacted pixel pairs; lane i applies
+// list positions 2i and 2i+1 to each pixel pair in turn.  Returns the lane's
 // blended-bit summary (bit 0: first splat blended somewhere, bit 1: second).
 template <bool DEPTH, bool CLAMP>
-__device__ __forceinline__ uint32_t bwd_wavefront(
-    int nact, int lane, bool hi, int sh, const float4* __restrict__ sG,
-    const float2* __restrict__ sS, const float2* __restrict__ sXY, const uint2* __restrict__ sM,
-    const float* __restrict__ sD, const float4& A0, const float4& B0, const float4& C0,
-    const float4& A1, const float4& B1, const float4& C1, float amax, SplatAcc& q0,
-    SplatAcc& q1) {
-    float T = 0.f, G = 0.f;
+__device__ __forceinline__ uint32_t bwd_wavefront(int npair, int lane, bool hi, int sh,
+                                                  const BwdList& L, const float* __restrict__ sD,
+                                                  const SplatP2& S0, const SplatP2& S1,
+                                                  float amax, SplatAcc2& q0, SplatAcc2& q1) {
+    f32x2 T = pk2(0.f, 0.f), G = T;
     uint32_t seen = 0u;
-    const int steps = nact + 31;
+    const int steps = npair + 31;
+    const uint4* M4 = reinterpret_cast<const uint4*>(L.m);
+    const float4* S4 = reinterpret_cast<const float4*>(L.s);
+    const float4* G4 = reinterpret_cast<const float4*>(L.g);
+    const float2* X2 = reinterpret_cast<const float2*>(L.x);
+    const float2* Y2 = reinterpret_cast<const float2*>(L.y);
 #pragma unroll 1
     for (int st = 0; st < steps; ++st) {
-        T = __shfl_up_sync(0xffffffffu, T, 1);
-        G = __shfl_up_sync(0xffffffffu, G, 1);
-        // lanes outside the diagonal run with bits = 0 on pixel 0 (a = 0:
+        T = shfl_up2(T);
+        G = shfl_up2(G);
+        // lanes outside the diagonal run with bits = 0 on pair 0 (a = 0:
         // nothing changes, T and G stay finite), so the only branch is
         // warp-uniform -- no divergence bookkeeping per step
         const int j = st - lane;
-        const bool inr = (unsigned)j < (unsigned)nact;
+        const bool inr = (unsigned)j < (unsigned)npair;
         const int jj = inr ? j : 0;
-        const uint2 m = sM[jj];
+        const uint4 m = M4[jj];
         if (lane == 0 && inr) {
-            const float2 s = sS[jj];
-            T = s.x;
-            G = s.y;
+            const float4 s = S4[jj];
+            T = pk2(s.x, s.y);
+            G = pk2(s.z, s.w);
         }
-        const uint32_t bits = inr ? ((hi ? m.y : m.x) >> sh) & 3u : 0u;
-        if (!__any_sync(0xffffffffu, bits != 0u)) continue;
-        seen |= bits;
-        const int j_ = jj;
-        const float2 xy = sXY[j_];
-        const float4 pg = sG[j_];
-        const float gd = DEPTH ? sD[j_] : 0.f;
-        bwd_term<DEPTH, CLAMP>(bits & 1u, xy.x, xy.y, pg, gd, A0, B0, C0, amax, T, G, q0);
-        bwd_term<DEPTH, CLAMP>(bits & 2u, xy.x, xy.y, pg, gd, A1, B1, C1, amax, T, G, q1);
+        const uint32_t ba = inr ? ((hi ? m.y : m.x) >> sh) & 3u : 0u;
+        const uint32_t bb = inr ? ((hi ? m.w : m.z) >> sh) & 3u : 0u;
+        if (!__any_sync(0xffffffffu, (ba | bb) != 0u)) continue;
+        seen |= ba | bb;
+        const float2 x = X2[jj], y = Y2[jj];
+        const float4 g0 = G4[2 * jj], g1 = G4[2 * jj + 1];
+        const f32x2 px = pk2(x.x, x.y), py = pk2(y.x, y.y);
+        const f32x2 gx = pk2(g0.x, g0.y), gy = pk2(g0.z, g0.w), gz = pk2(g1.x, g1.y),
+                    gw = pk2(g1.z, g1.w);
+        f32x2 gd = pk2(0.f, 0.f);
+        if (DEPTH) {
+            const float2 d = reinterpret_cast<const float2*>(sD)[jj];
+            gd = pk2(d.x, d.y);
+        }
+        bwd_term2<DEPTH, CLAMP>(ba & 1u, bb & 1u, px, py, gx, gy, gz, gw, gd, S0, amax, T, G, q0);
+        bwd_term2<DEPTH, CLAMP>(ba & 2u, bb & 2u, px, py, gx, gy, gz, gw, gd, S1, amax, T, G, q1);
     }
     return seen;
 }
@@ -155,10 +227,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
     // per-warp compacted pixel list: gradient side (g, g . image), state at
     // the unit start (T0, G0), coordinates, the two buckets' blend masks,
     // depth gradient
-    __shared__ float4 sG[kBwdWarps][kTilePx];
-    __shared__ float2 sS[kBwdWarps][kTilePx];
-    __shared__ float2 sXY[kBwdWarps][kTilePx];
-    __shared__ uint2 sM[kBwdWarps][kTilePx];
+    __shared__ BwdList sL[kBwdWarps];
     __shared__ float sD[DEPTH ? kBwdWarps : 1][DEPTH ? kTilePx : 1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const bool hi = lane >= 16;            // lane's splats live in the second bucket
@@ -248,33 +317,54 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
                     G0 += gd * ckpt_depth[slot0 + p];
                     sD[wid][pos] = gd;
                 }
-                sG[wid][pos] = pg;
-                sS[wid][pos] = make_float2(ck.x, G0);
-                sM[wid][pos] = make_uint2(m0, m1);
-                sXY[wid][pos] = make_float2((float)ix, (float)iy);
+                BwdList& L = sL[wid];
+                const int pb = (pos >> 1) * 8 + (pos & 1);  // pair-interleaved slots
+                L.g[pb] = pg.x;
+                L.g[pb + 2] = pg.y;
+                L.g[pb + 4] = pg.z;
+                L.g[pb + 6] = pg.w;
+                const int ps = (pos >> 1) * 4 + (pos & 1);
+                L.s[ps] = ck.x;
+                L.s[ps + 2] = G0;
+                L.m[pos] = make_uint2(m0, m1);
+                L.x[pos] = (float)ix;
+                L.y[pos] = (float)iy;
             }
             nact += __popc(bal);
         }
+        // odd count: pad the last pair with an inert pixel (no blend bits,
+        // zero gradient, finite state)
+        if ((nact & 1) && lane == 0) {
+            BwdList& L = sL[wid];
+            const int pb = (nact >> 1) * 8 + 1, ps = (nact >> 1) * 4 + 1;
+            L.g[pb] = L.g[pb + 2] = L.g[pb + 4] = L.g[pb + 6] = 0.f;
+            L.s[ps] = 1.f;
+            L.s[ps + 2] = 0.f;
+            L.m[nact] = make_uint2(0u, 0u);
+            L.x[nact] = L.y[nact] = 0.f;
+            if (DEPTH) sD[wid][nact] = 0.f;
+        }
         __syncwarp();
-        // ---- diagonal wavefront over the active pixels; lane i applies
-        // list positions 2i and 2i+1 to each pixel in turn.
+        // ---- diagonal wavefront over the active pixel pairs; lane i applies
+        // list positions 2i and 2i+1 to each pair in turn.
         // Per-splat sums; the splat-constant factors (conic, 1/sigma, -1/2)
         // are applied once at the end:
         //   d mean  = (c0 S_dx + c1 S_dy, c1 S_dx + c2 S_dy),  S_d. = sum da d.
         //   d conic = -1/2 (S_dxdx, 2 S_dxdy, S_dydy),        d sigma = S_da / sigma
-        SplatAcc q0 = {}, q1 = {};
+        const f32x2 z2 = pk2(0.f, 0.f);
+        SplatAcc2 q0 = {z2, z2, z2, z2, z2, z2, z2, z2, z2, z2}, q1 = q0;
+        const SplatP2 S0 = splat_p2(A0, B0, C0), S1 = splat_p2(A1, B1, C1);
+        const int npair = (nact + 1) >> 1;
         uint32_t seen;
         // the clamp at alpha_max can only bind for splats with sigma >= alpha_max
         const bool clamp = __any_sync(0xffffffffu, (k0 < ke && B0.y >= amax * 0.999999f) ||
                                                        (k1 < ke && B1.y >= amax * 0.999999f));
         if (clamp)
-            seen = bwd_wavefront<DEPTH, true>(nact, lane, hi, sh, sG[wid], sS[wid], sXY[wid],
-                                              sM[wid], DEPTH ? sD[wid] : nullptr, A0, B0, C0, A1,
-                                              B1, C1, amax, q0, q1);
+            seen = bwd_wavefront<DEPTH, true>(npair, lane, hi, sh, sL[wid],
+                                              DEPTH ? sD[wid] : nullptr, S0, S1, amax, q0, q1);
         else
-            seen = bwd_wavefront<DEPTH, false>(nact, lane, hi, sh, sG[wid], sS[wid], sXY[wid],
-                                               sM[wid], DEPTH ? sD[wid] : nullptr, A0, B0, C0, A1,
-                                               B1, C1, amax, q0, q1);
+            seen = bwd_wavefront<DEPTH, false>(npair, lane, hi, sh, sL[wid],
+                                               DEPTH ? sD[wid] : nullptr, S0, S1, amax, q0, q1);
         if (k0 < ke) {
             bwd_commit<NC>(q0, A0, B0, g2d + (size_t)s0 * NC);
             if (contributed && (seen & 1u)) contributed[s0] = 1;
