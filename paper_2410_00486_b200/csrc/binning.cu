@@ -608,6 +608,16 @@ struct FeArgs {
     int64_t* overflow;
     int64_t cap;
     uint32_t* pcount;
+    // direct tile emission (fe_direct); direct == 0 -> depth-order emission
+    int direct;
+    uint32_t n_img_tiles;
+    uint32_t* col;         // [n_img_tiles][gridDim.x] per-CTA tile counts -> column prefixes
+    uint32_t* col_tot;     // [n_img_tiles] tile totals
+    uint32_t* out_splat;   // pair list (Gaussian ids) in (tile, depth, id) order
+    uint32_t* tile_start;
+    uint32_t* tile_end;
+    uint4* drec;           // [n] depth-order splat records (fe_direct)
+    uint32_t* keyred;      // [2 n_tiles] per-CTA AND / OR of the keys with pairs
 };
 
 template <int NT>
@@ -637,6 +647,414 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
     return r;
 }
 
+
+#ifdef SS_FE_TRACE
+// diagnostics build only (tools/trace_front.py): per CTA, globaltimer stamps
+// at the phase boundaries of bin_front_kernel
+constexpr int kFeTraceSlots = 24;
+__device__ unsigned long long g_fe_trace[160 * kFeTraceSlots];
+__device__ __forceinline__ void fe_stamp(int slot) {
+    if (threadIdx.x == 0 && slot < kFeTraceSlots) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_fe_trace[blockIdx.x * kFeTraceSlots + slot] = t;
+    }
+}
+#define FE_STAMP(k) fe_stamp(k)
+#else
+#define FE_STAMP(k)
+#endif
+
+// ------------------------------------------------- direct tile emission
+// After the depth sort every pair goes straight to its final slot in
+// (tile, depth, id) order -- no emission in depth order followed by radix
+// passes over all P pairs:
+//   slot = start[tile] + (pairs of that tile earlier in depth order).
+// The P pairs, in depth order, are split evenly over the CTAs (pair-balanced:
+// near splats cover many more tiles than far ones), and each CTA's range over
+// G "placer" warps.  A placer warp walks its contiguous range 32 pairs per
+// step and ranks each pair among the step's pairs of the same tile with a
+// ballot multi-split; a per-(warp, tile) counter in shared memory carries the
+// running count, so the order inside the warp's range is exactly the depth
+// order.  Pass 1 counts; per-tile totals per CTA -> grid barrier -> prefix
+// over the CTAs per tile -> grid barrier -> tile starts (every CTA scans the
+// totals) -> pass 2 repeats the walk with the counters preset to each warp's
+// first slot per tile and writes the Gaussian ids.  Deterministic, atomic-
+// free.
+constexpr int kDirMaxTiles = 8192;  // image tiles handled by the direct path
+constexpr int kDirSmemBytes = 200 * 1024;
+constexpr uint32_t kDirPiece = 65535;  // pairs per piece (16-bit counters)
+// placer warps: 16-bit counters per (warp, tile) + a 32-bit base per tile
+__host__ __device__ inline int fe_direct_warps(int n_img_tiles) {
+    const int nt = n_img_tiles > 0 ? n_img_tiles : 1;
+    const int g = (kDirSmemBytes - 4 * nt) / (2 * (nt + 1));
+    return g > 32 ? 32 : g;
+}
+inline size_t fe_direct_smem_bytes(int n_img_tiles) {
+    const size_t g = (size_t)fe_direct_warps(n_img_tiles);
+    return 2 * g * (size_t)((n_img_tiles + 1) & ~1) + 4 * (size_t)n_img_tiles;
+}
+
+// Block-wide exclusive scan of s[0..n) in place (n <= 8 * kFeThreads);
+// returns the total.
+__device__ __forceinline__ uint32_t fe_scan_smem(uint32_t* s, uint32_t n, uint32_t* s_warp) {
+    const int t = threadIdx.x;
+    const uint32_t per = (n + kFeThreads - 1) / kFeThreads;
+    const uint32_t q0 = t * per;
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        v[k] = (k < (int)per && q0 + k < n) ? s[q0 + k] : 0u;
+        sum += v[k];
+    }
+    __shared__ uint32_t s_total;
+    const uint32_t ex = block_excl_scan<kFeThreads>(sum, s_warp);
+    if (t == kFeThreads - 1) s_total = ex + sum;
+    uint32_t run = ex;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (k < (int)per && q0 + k < n) {
+            s[q0 + k] = run;
+            run += v[k];
+        }
+    __syncthreads();
+    return s_total;
+}
+
+// One warp's walk over the depth-order pairs [q0, q1), 32 consecutive pairs
+// per step (lane = pair; its splat = owner lane of the current row of 32
+// splats, found by a shuffle binary search).  drec[j] = depth-order record of
+// splat j: (first pair, Gaussian id, x0 | y0 << 16, wx | wy << 16).  Counters
+// are 16-bit, packed two per word: c16w = the word array, index = tile.
+// MODE 1: count (red.add, order-free).  MODE 0: rank = counter value before
+// the step + number of earlier lanes of the step with the same tile, then
+// fn(tile, rank, Gaussian id); the earlier same-tile lanes can only belong
+// to earlier splats of the step (a splat's tiles are distinct), so each lane
+// tests, for every earlier splat of the step, whether its rect holds the
+// lane's tile at a pair index inside this step -- no MATCH.ANY.
+template <int MODE, typename F>
+__device__ __forceinline__ void fe_walk(const uint4* __restrict__ drec,
+                                        const uint32_t* __restrict__ cb, int cshift, uint32_t n,
+                                        uint32_t q0, uint32_t q1, int tiles_x,
+                                        uint32_t* __restrict__ c16w, F&& fn) {
+    const int l = threadIdx.x & 31;
+    if (q0 >= q1) return;
+    // owner of pair q0 = largest j with first[j] <= q0 (zero-count splats
+    // share their successor's first pair, so the owner has pairs); the warp
+    // narrows [lo, hi) 32-fold per round
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t j = lo + l * step;
+        const bool le = j < hi && drec[j].x + cb[j >> cshift] <= q0;
+        const unsigned m = __ballot_sync(0xffffffffu, le);  // lanes 0..k set (monotone)
+        const int k = 31 - __clz(m);                           // m has bit 0: drec[lo].x <= q0
+        lo = lo + k * step;
+        hi = min(hi, lo + step);
+    }
+    const uint4 kEnd = make_uint4(0xffffffffu, 0u, 0u, 0u);
+    uint32_t js = lo;
+    uint4 cur = js + l < n ? drec[js + l] : kEnd;
+    uint32_t q = q0;
+    while (q < q1) {
+        const uint4 nxt = js + 32 + l < n ? drec[js + 32 + l] : kEnd;  // prefetch
+        if (cur.x != 0xffffffffu) cur.x += cb[(js + l) >> cshift];
+        const bool valid = cur.x != 0xffffffffu;
+        const uint32_t wx = max(cur.w & 0xffffu, 1u), wy = cur.w >> 16;
+        const uint32_t c = valid ? wx * wy : 0u;
+        const uint32_t rlo = __shfl_sync(0xffffffffu, cur.x, 0);
+        const uint32_t rel = valid ? cur.x - rlo : 0x7fffffffu;
+        uint32_t endw = valid ? rel + c : 0u;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) endw = max(endw, __shfl_xor_sync(0xffffffffu, endw, d));
+        const uint32_t a1 = min(rlo + endw, q1);
+        const uint32_t pw = wx | (wy << 16);
+        for (uint32_t e0 = q - rlo; e0 < a1 - rlo; e0 += 32) {
+            const uint32_t e = e0 + l;
+            const bool in = e < a1 - rlo;
+            int o = 0;  // owner lane = largest lane with rel <= e
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const uint32_t r = __shfl_sync(0xffffffffu, rel, o + st);
+                if (r <= e) o += st;
+            }
+            const uint32_t li = e - __shfl_sync(0xffffffffu, rel, o);
+            const uint32_t oxy = __shfl_sync(0xffffffffu, cur.z, o);
+            const uint32_t ow = __shfl_sync(0xffffffffu, wx, o);
+            uint32_t tx = 0, ty = 0;
+            if (in) {
+                // li / ow through a float quotient, corrected to the exact one
+                uint32_t ry = __float2uint_rz(__fdividef((float)li, (float)ow));
+                if (ry * ow > li) --ry;
+                if ((ry + 1) * ow <= li) ++ry;
+                tx = (oxy & 0xffffu) + (li - ry * ow);
+                ty = (oxy >> 16) + ry;
+            }
+            const uint32_t tile = ty * (uint32_t)tiles_x + tx;
+            uint32_t* word = c16w + (tile >> 1);
+            const uint32_t sh = 16 * (tile & 1);
+            if (MODE == 2) {  // 32-bit counters
+                if (in) atomicAdd(c16w + tile, 1u);
+            } else if (MODE == 1) {
+                if (in) atomicAdd(word, 1u << sh);
+            } else {
+                const uint32_t gid = __shfl_sync(0xffffffffu, cur.y, o);
+                // earlier lanes of the step with the same tile
+                const int o_first = __shfl_sync(0xffffffffu, o, 0);
+                const int o_last = __shfl_sync(0xffffffffu, in ? o : 0, 31 - __clz(__ballot_sync(0xffffffffu, in)));
+                uint32_t inrank = 0;
+#pragma unroll 1
+                for (int o2 = o_first; o2 < o_last; ++o2) {
+                    const uint32_t r2 = __shfl_sync(0xffffffffu, rel, o2);
+                    const uint32_t xy2 = __shfl_sync(0xffffffffu, cur.z, o2);
+                    const uint32_t p2 = __shfl_sync(0xffffffffu, pw, o2);
+                    const uint32_t dx = tx - (xy2 & 0xffffu), dy = ty - (xy2 >> 16);
+                    const uint32_t w2 = p2 & 0xffffu;
+                    if (in && o2 < o && dx < w2 && dy < (p2 >> 16) && r2 + dy * w2 + dx >= e0)
+                        ++inrank;
+                }
+                uint32_t before = 0;
+                if (in) before = (*word >> sh) & 0xffffu;
+                __syncwarp();
+                if (in) {
+                    atomicAdd(word, 1u << sh);
+                    fn(tile, before + inrank, gid);
+                }
+            }
+            __syncwarp();
+        }
+        q = a1;
+        js += 32;
+        cur = nxt;
+    }
+}
+
+__device__ __forceinline__ uint32_t wq_span(uint32_t p0, uint32_t p1, uint32_t g, uint32_t G) {
+    return (uint32_t)(((uint64_t)(p1 - p0) * (g + 1)) / G) - (uint32_t)(((uint64_t)(p1 - p0) * g) / G);
+}
+
+template <int ITEMS>
+__device__ void fe_direct(const FeArgs& a, cooperative_groups::grid_group& grid, uint32_t* sm,
+                          uint32_t* s_warp, const uint32_t* order) {
+    constexpr int kFeTile = kFeThreads * ITEMS;
+    const int t = threadIdx.x, w = t >> 5, l = t & 31;
+    const uint32_t cta = blockIdx.x, nc = gridDim.x;
+    const uint32_t base = cta * kFeTile;
+    const uint32_t wbase = w * 32 * ITEMS;
+    const uint32_t NT = a.n_img_tiles;
+    const uint32_t G = (uint32_t)fe_direct_warps((int)NT);
+    const uint32_t NT2 = (NT + 1) & ~1u;  // counter row stride (whole words)
+    uint16_t* s_c16 = reinterpret_cast<uint16_t*>(sm);  // [G][NT2] placer-warp counters
+    uint32_t* s_base = sm + (size_t)G * NT2 / 2;       // [NT] 32-bit per tile
+
+    // ---- this CTA's depth-sort chunk: pair counts, chunk total
+    uint32_t sid[ITEMS], cnt[ITEMS], off[ITEMS];
+    uint32_t wtot = 0;
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+        const uint32_t j = base + wbase + r * 32 + l;
+        sid[r] = j < a.n ? order[j] : 0u;
+        cnt[r] = j < a.n ? a.tiles[sid[r]] : 0u;
+        uint32_t x = cnt[r];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (l >= o) x += y;
+        }
+        off[r] = wtot + x - cnt[r];
+        wtot += __shfl_sync(0xffffffffu, x, 31);
+    }
+    const uint32_t wex = block_excl_scan<kFeThreads>(l == 0 ? wtot : 0u, s_warp);
+    const uint32_t wpre = __shfl_sync(0xffffffffu, wex, 0);
+    if (t == kFeThreads - 1) a.chunk_sum[cta] = wpre + wtot;
+    // depth-order records with chunk-local first pairs (the walks add the
+    // chunk's base from s_cb)
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+        const uint32_t j = base + wbase + r * 32 + l;
+        if (j < a.n) {
+            uint4 d = make_uint4(wpre + off[r], sid[r], 0u, 0u);
+            if (cnt[r]) {
+                const uint2 rc = a.rect[sid[r]];
+                d.z = rc.x;
+                d.w = ((rc.y & 0xffffu) - (rc.x & 0xffffu) + 1) |
+                      (((rc.y >> 16) - (rc.x >> 16) + 1) << 16);
+            }
+            a.drec[j] = d;
+        }
+    }
+    for (uint32_t q = t; q < (uint32_t)G * NT2 / 2; q += kFeThreads) sm[q] = 0u;
+    for (uint32_t q = t; q < NT; q += kFeThreads) s_base[q] = 0u;
+    FE_STAMP(10);
+    grid.sync();
+    FE_STAMP(11);
+    // ---- chunk bases (exclusive prefix of the chunk sums), P, capacity
+    __shared__ uint32_t s_cb[32 * kFeColChunks + 1];
+    if (w == 0) {
+        uint32_t c[kFeColChunks], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kFeColChunks; ++k) {
+            const uint32_t i = l * kFeColChunks + k;
+            c[k] = i < nc ? a.chunk_sum[i] : 0u;
+            sum += c[k];
+        }
+        uint32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (l >= o) x += y;
+        }
+        uint32_t run = x - sum;
+#pragma unroll
+        for (int k = 0; k < kFeColChunks; ++k) {
+            const uint32_t i = l * kFeColChunks + k;
+            if (i < nc) s_cb[i] = run;
+            run += c[k];
+        }
+        if (l == 31) s_cb[nc] = x;
+    }
+    __syncthreads();
+    const uint32_t P = s_cb[nc];
+    if ((int64_t)P > a.cap) {
+        if (cta == 0 && t == 0) {
+            *a.total = (int64_t)P;
+            *a.overflow = 1;  // sticky; the step is replayed with larger buffers
+            *a.pcount = 0u;
+        }
+        return;
+    }
+    if (cta == 0 && t == 0) {
+        *a.total = (int64_t)P;
+        *a.pcount = P;
+    }
+    const int cshift = 31 - __clz(kFeTile);
+    // the CTA's pair range (pair-balanced), processed in pieces of at most
+    // kDirPiece pairs so the per-(warp, tile) counters fit 16 bits
+    const uint32_t p0 = (uint32_t)(((uint64_t)P * cta) / nc);
+    const uint32_t p1 = (uint32_t)(((uint64_t)P * (cta + 1)) / nc);
+    const uint32_t npieces = (p1 - p0 + kDirPiece - 1) / kDirPiece;
+    // count walk over [c0, c1): placer warp g counts its own share into its
+    // private row (the same split as the rank walk)
+    auto count_piece = [&](uint32_t c0, uint32_t c1) {
+        if (w < (int)G) {
+            const uint32_t span = c1 - c0;
+            const uint32_t g0 = c0 + (uint32_t)(((uint64_t)span * w) / G);
+            const uint32_t g1 = c0 + (uint32_t)(((uint64_t)span * (w + 1)) / G);
+            fe_walk<1>(a.drec, s_cb, cshift, a.n, g0, g1, a.tiles_x, sm + (size_t)w * (NT2 / 2),
+                       [](uint32_t, uint32_t, uint32_t) {});
+        }
+    };
+    // placer-warp counters -> exclusive prefix over the warps (per tile);
+    // returns nothing, totals land in tot (may alias nothing)
+    auto prefix_warps = [&](uint32_t* tot) {
+        for (uint32_t q = t; q < NT; q += kFeThreads) {
+            uint32_t run = 0;
+            for (uint32_t g = 0; g < G; ++g) {
+                const uint32_t c = s_c16[(size_t)g * NT2 + q];
+                s_c16[(size_t)g * NT2 + q] = (uint16_t)run;
+                run += c;
+            }
+            if (tot) tot[q] = run;
+        }
+    };
+    auto zero_c16 = [&]() {
+        for (uint32_t q = t; q < (uint32_t)G * NT2 / 2; q += kFeThreads) sm[q] = 0u;
+    };
+    // ---- count: per-tile totals of the CTA's range -> col[cta][tile]
+    if (npieces <= 1) {
+        count_piece(p0, p1);
+        __syncthreads();
+        prefix_warps(s_base);
+    } else {
+        for (uint32_t q0 = p0 + w * 32 * 64; q0 < p1; q0 += kFeWarps * 32 * 64)
+            fe_walk<2>(a.drec, s_cb, cshift, a.n, q0, min(p1, q0 + 32 * 64), a.tiles_x, s_base,
+                       [](uint32_t, uint32_t, uint32_t) {});
+    }
+    __syncthreads();
+    for (uint32_t q = t; q < NT; q += kFeThreads) a.col[(size_t)cta * NT + q] = s_base[q];
+    FE_STAMP(14);
+    grid.sync();
+    FE_STAMP(15);
+    // ---- per tile: exclusive prefix over the CTAs (in place), tile total;
+    //      a warp per tile (tiles spread over the CTAs), lane l holds CTAs
+    //      5 l .. 5 l + 4
+    for (uint32_t q = w * nc + cta; q < NT; q += nc * kFeWarps) {
+        uint32_t c[kFeColChunks], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kFeColChunks; ++k) {
+            const uint32_t i = l * kFeColChunks + k;
+            c[k] = i < nc ? a.col[(size_t)i * NT + q] : 0u;
+            sum += c[k];
+        }
+        uint32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (l >= o) x += y;
+        }
+        uint32_t run = x - sum;
+#pragma unroll
+        for (int k = 0; k < kFeColChunks; ++k) {
+            const uint32_t i = l * kFeColChunks + k;
+            if (i < nc) a.col[(size_t)i * NT + q] = run;
+            run += c[k];
+        }
+        if (l == 31) a.col_tot[q] = x;
+    }
+    FE_STAMP(16);
+    grid.sync();
+    FE_STAMP(17);
+    // ---- tile starts (every CTA scans the totals); the CTA's first slot per
+    //      tile -> s_base
+    for (uint32_t q = t; q < NT; q += kFeThreads) s_base[q] = a.col_tot[q];
+    __syncthreads();
+    fe_scan_smem(s_base, NT, s_warp);
+    for (uint32_t q = t; q < NT; q += kFeThreads) {
+        const uint32_t st = s_base[q];
+        if (cta == 0) {
+            a.tile_start[q] = st;
+            a.tile_end[q] = st + a.col_tot[q];
+        }
+        s_base[q] = st + a.col[(size_t)cta * NT + q];
+    }
+    __syncthreads();
+    FE_STAMP(18);
+    // ---- rank + write, piece by piece: placer warp g walks its share of the
+    //      piece in depth order; slot = CTA base + earlier pieces + earlier
+    //      placer warps + rank in the warp's walk
+    uint32_t* out = a.out_splat;
+#pragma unroll 1
+    for (uint32_t pc = 0; pc < max(npieces, 1u); ++pc) {
+        const uint32_t c0 = p0 + pc * kDirPiece, c1 = min(p1, c0 + kDirPiece);
+        if (npieces > 1) {
+            zero_c16();
+            __syncthreads();
+            count_piece(c0, c1);
+            __syncthreads();
+            prefix_warps(nullptr);
+            __syncthreads();
+        }
+        if (w < (int)G) {
+            const uint32_t span = c1 - c0;
+            const uint32_t g0 = c0 + (uint32_t)(((uint64_t)span * w) / G);
+            const uint32_t g1 = c0 + (uint32_t)(((uint64_t)span * (w + 1)) / G);
+            const uint32_t* sb = s_base;
+            fe_walk<0>(a.drec, s_cb, cshift, a.n, g0, g1, a.tiles_x, sm + (size_t)w * (NT2 / 2),
+                       [out, sb](uint32_t tile, uint32_t r, uint32_t gid) {
+                           out[sb[tile] + r] = gid;
+                       });
+        }
+        __syncthreads();
+        if (pc + 1 < npieces) {
+            // the last placer warp's counters ended at the piece totals
+            for (uint32_t q = t; q < NT; q += kFeThreads)
+                s_base[q] += s_c16[(size_t)(G - 1) * NT2 + q];
+            __syncthreads();
+        }
+    }
+    FE_STAMP(19);
+}
+
 template <int ITEMS>
 __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
     constexpr int kFeTile = kFeThreads * ITEMS;
@@ -654,13 +1072,26 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
     const uint32_t nloc = min((uint32_t)kFeTile, a.n - base);
     const uint32_t wbase = w * 32 * ITEMS;
 
+    FE_STAMP(0);
+    // Direct mode skips the passes whose digit is the same for every splat
+    // that has pairs (e.g. the exponent byte when all depths lie in one
+    // binade pair): splats without pairs never reach the pair list, so their
+    // relative order is irrelevant, and a stable pass over a constant digit
+    // is the identity on the others.  The AND / OR of those keys is reduced
+    // in pass 0; the mask is known after its first barrier.
+    __shared__ uint32_t s_red[2][kFeWarps], s_skip;
+    const uint32_t* ksrc = a.key_in;
+    const uint32_t* vsrc = nullptr;
+    int par = 0, lastp = 3;
+    uint32_t skipmask = 0;
 #pragma unroll 1
     for (int p = 0; p < 4; ++p) {
-        const uint32_t* kin = p == 0 ? a.key_in : ((p & 1) ? a.kA : a.kB);
-        const uint32_t* vin = p == 0 ? nullptr : ((p & 1) ? a.vA : a.vB);
-        uint32_t* kout = (p & 1) ? a.kB : a.kA;
-        uint32_t* vout = (p & 1) ? a.vB : a.vA;
-        uint32_t* cnt = a.counts + (size_t)(p & 1) * a.n_tiles * 256;
+        if ((skipmask >> p) & 1u) continue;  // block- and grid-uniform
+        const uint32_t* kin = ksrc;
+        const uint32_t* vin = vsrc;
+        uint32_t* kout = par ? a.kB : a.kA;
+        uint32_t* vout = par ? a.vB : a.vA;
+        uint32_t* cnt = a.counts + (size_t)par * a.n_tiles * 256;
         const int shift = 8 * p;
         // ---- phase A: rank within the tile, publish the digit histogram
         for (int k = t; k < kFeWarps * 256; k += kFeThreads) (&s_cnt[0][0])[k] = 0u;
@@ -697,7 +1128,54 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
         }
         const uint32_t loc = block_excl_scan<kFeThreads>(t < 256 ? run : 0u, s_warp);
         if (t < 256) s_local[t] = loc;
+        if (p == 0 && a.direct) {
+            uint32_t kand = 0xffffffffu, kor = 0u;
+#pragma unroll
+            for (int r = 0; r < ITEMS; ++r) {
+                const uint32_t li = wbase + r * 32 + l;
+                if (li < nloc && a.tiles[base + li] != 0u) {
+                    kand &= key[r];
+                    kor |= key[r];
+                }
+            }
+            kand = __reduce_and_sync(0xffffffffu, kand);
+            kor = __reduce_or_sync(0xffffffffu, kor);
+            if (l == 0) {
+                s_red[0][w] = kand;
+                s_red[1][w] = kor;
+            }
+            __syncthreads();
+            if (t == 0) {
+                for (int k = 1; k < kFeWarps; ++k) {
+                    kand &= s_red[0][k];
+                    kor |= s_red[1][k];
+                }
+                a.keyred[2 * tile] = s_red[0][0] & kand;
+                a.keyred[2 * tile + 1] = s_red[1][0] | kor;
+            }
+        }
+        FE_STAMP(1 + 2 * p);
         grid.sync();
+        if (p == 0 && a.direct) {
+            if (w == 0) {
+                uint32_t kand = 0xffffffffu, kor = 0u;
+                for (uint32_t q = l; q < a.n_tiles; q += 32) {
+                    kand &= a.keyred[2 * q];
+                    kor |= a.keyred[2 * q + 1];
+                }
+                kand = __reduce_and_sync(0xffffffffu, kand);
+                kor = __reduce_or_sync(0xffffffffu, kor);
+                const uint32_t diff = kand ^ kor;
+                uint32_t m = 0;
+                for (int q = 1; q < 4; ++q)
+                    if (((diff >> (8 * q)) & 255u) == 0u) m |= 1u << q;
+                if (l == 0) s_skip = m;
+            }
+            __syncthreads();
+            skipmask = s_skip;
+            lastp = 3;
+            while (lastp > 0 && ((skipmask >> lastp) & 1u)) --lastp;
+        }
         // ---- phase B: digit starts = exclusive digit total + column prefix;
         //      warp w reduces the columns of digits w + 32 k (coalesced rows of
         //      the [digit][tile] histograms), all loads of a batch in flight
@@ -750,11 +1228,19 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
             const uint32_t d = (k >> shift) & 255u;
             const uint32_t gp = s_base[d] + (i - s_local[d]);
             vout[gp] = s_vals[i];
-            if (p < 3) kout[gp] = k;
+            if (p < lastp) kout[gp] = k;
         }
         grid.sync();
+        FE_STAMP(2 + 2 * p);
+        ksrc = kout;
+        vsrc = vout;
+        par ^= 1;
     }
 
+    if (a.direct) {
+        fe_direct<ITEMS>(a, grid, fe_smem, s_warp, vsrc);
+        return;
+    }
     // ---- chunk sums of the final order (vB: pass 3 wrote the B buffers);
     //      warp w holds rows of 32 consecutive splats, wbase + 32 r + lane
     const uint32_t* order = a.vB;
@@ -877,6 +1363,10 @@ struct BinLayout {
     // persistent front end (in the zeroed control region)
     uint32_t* fe_counts;              // 2 * n_fe_tiles * 256
     uint32_t* fe_chunk;               // n_fe_tiles
+    uint32_t* fe_col;                 // 32 * kFeColChunks * n_tiles (direct emission)
+    uint32_t* fe_col_tot;             // n_tiles
+    uint4* fe_drec;                   // n (direct emission)
+    uint32_t* fe_keyred;              // 2 * n_fe_tiles
 };
 
 inline int tile_passes(int n_tiles) {
@@ -889,7 +1379,6 @@ BinLayout bin_layout(int64_t n, int64_t cap, int n_tiles, void* ws, size_t* byte
     BinWorkspace w;
     w.base = reinterpret_cast<char*>(ws);
     BinLayout L;
-    (void)n_tiles;
     L.ctrl = w.take<uint32_t>(16);
     L.st_scan1 = w.take<unsigned long long>(div_up(n > 0 ? n : 1, 256 * kScanItems) + 1);
     L.st_scan2 = w.take<unsigned long long>(div_up(n_tiles + 1, 256 * kScanItemsTiles) + 1);
@@ -909,6 +1398,10 @@ BinLayout bin_layout(int64_t n, int64_t cap, int n_tiles, void* ws, size_t* byte
         const int64_t nft = div_up(n > 0 ? n : 1, 2 * kFeThreads);  // smallest tiles
         L.fe_counts = w.take<uint32_t>(2 * nft * 256);
         L.fe_chunk = w.take<uint32_t>(nft);
+        L.fe_col = w.take<uint32_t>((size_t)32 * kFeColChunks * (n_tiles > 0 ? n_tiles : 1));
+        L.fe_col_tot = w.take<uint32_t>(n_tiles > 0 ? n_tiles : 1);
+        L.fe_drec = w.take<uint4>(n > 0 ? n : 1);
+        L.fe_keyred = w.take<uint32_t>(2 * nft);
     }
     {
         int64_t mx = cap > n ? cap : n;
@@ -929,15 +1422,14 @@ size_t bin_workspace_bytes(int64_t n, int64_t cap, int n_tiles) {
 }
 
 template <int ITEMS>
-static int fe_capacity() {  // co-resident CTAs of bin_front_kernel<ITEMS>, 0 = unusable
+static int fe_capacity(size_t bytes) {  // co-resident CTAs of bin_front_kernel<ITEMS>, 0 = unusable
     int dev = 0, coop = 0, sms = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int bytes = (int)fe_smem_bytes<ITEMS>();
     if (!coop ||
         cudaFuncSetAttribute(bin_front_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             bytes) != cudaSuccess ||
+                             (int)bytes) != cudaSuccess ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bin_front_kernel<ITEMS>, kFeThreads,
                                                       bytes) != cudaSuccess) {
         cudaGetLastError();
@@ -948,18 +1440,22 @@ static int fe_capacity() {  // co-resident CTAs of bin_front_kernel<ITEMS>, 0 = 
 
 // Cooperative launch of bin_front_kernel (one sort tile per co-resident
 // CTA); false -> use the per-pass kernels (N too large, cooperative launch
-// unavailable, or SS_BIN_FRONT=0 in the environment).
-static bool front_end_launch(int64_t n, const ss_splats* sp, int tiles_x, const BinLayout& L,
-                             bool packed, int sbits, int64_t cap, ss_status* st, cudaStream_t s) {
-    static int cap2 = -1, cap4 = -1, cap8 = -1, enabled = -1;
+// unavailable, or SS_BIN_FRONT=0 in the environment).  *direct: the kernel
+// also wrote the final pair list and the tile ranges (fe_direct; off with
+// SS_BIN_DIRECT=0 or more than kDirMaxTiles image tiles).
+static bool front_end_launch(int64_t n, const ss_splats* sp, const ss_bins* bins, int tiles_x,
+                             int n_tiles, const BinLayout& L, bool packed, int sbits, int64_t cap,
+                             ss_status* st, cudaStream_t s, bool* direct) {
+    static int enabled = -1, direct_ok = -1;
     if (enabled < 0) {
         const char* env = getenv("SS_BIN_FRONT");
         enabled = !(env && env[0] == '0');
-        cap2 = fe_capacity<2>();
-        cap4 = fe_capacity<4>();
-        cap8 = fe_capacity<8>();
+        const char* env2 = getenv("SS_BIN_DIRECT");
+        direct_ok = !(env2 && env2[0] == '0');
     }
+    *direct = false;
     if (!enabled) return false;
+    const bool dir = direct_ok && n_tiles <= kDirMaxTiles && n_tiles > 0;
     FeArgs a;
     a.n = (uint32_t)n;
     a.key_in = sp->d_depth_key;
@@ -979,20 +1475,44 @@ static bool front_end_launch(int64_t n, const ss_splats* sp, int tiles_x, const 
     a.overflow = &st->pair_overflow;
     a.cap = cap;
     a.pcount = L.pcount;
+    a.direct = dir ? 1 : 0;
+    a.n_img_tiles = (uint32_t)n_tiles;
+    a.col = L.fe_col;
+    a.col_tot = L.fe_col_tot;
+    a.out_splat = bins->d_pair_splat;
+    a.tile_start = bins->d_tile_start;
+    a.tile_end = bins->d_tile_end;
+    a.drec = L.fe_drec;
+    a.keyred = L.fe_keyred;
     void* args[] = {&a};
     auto go = [&](auto kern, int items, int capacity) -> bool {
         const int64_t nft = div_up(n, (int64_t)kFeThreads * items);
         if (nft > capacity || nft > 32 * kFeColChunks) return false;
         a.n_tiles = (uint32_t)nft;
-        if (cudaLaunchCooperativeKernel((const void*)kern, (int)nft, kFeThreads, args,
-                                        fe_smem_bytes_rt(items), s) != cudaSuccess) {
+        size_t bytes = fe_smem_bytes_rt(items);
+        if (dir && fe_direct_smem_bytes(n_tiles) > bytes) bytes = fe_direct_smem_bytes(n_tiles);
+        if (cudaLaunchCooperativeKernel((const void*)kern, (int)nft, kFeThreads, args, bytes,
+                                        s) != cudaSuccess) {
             cudaGetLastError();
             return false;
         }
         return true;
     };
-    return go(bin_front_kernel<2>, 2, cap2) || go(bin_front_kernel<4>, 4, cap4) ||
-           go(bin_front_kernel<8>, 8, cap8);
+    // capacities for the largest shared-memory footprint this launch may use
+    static int cap2 = -1, cap4 = -1, cap8 = -1;
+    static size_t cap_bytes = 0;
+    const size_t want = (size_t)kDirSmemBytes + 16 > fe_smem_bytes<8>() ? (size_t)kDirSmemBytes + 16
+                                                                        : fe_smem_bytes<8>();
+    if (cap_bytes != want) {
+        cap_bytes = want;
+        cap2 = fe_capacity<2>(want);
+        cap4 = fe_capacity<4>(want);
+        cap8 = fe_capacity<8>(want);
+    }
+    const bool ok = go(bin_front_kernel<2>, 2, cap2) || go(bin_front_kernel<4>, 4, cap4) ||
+                    go(bin_front_kernel<8>, 8, cap8);
+    *direct = ok && dir;
+    return ok;
 }
 
 cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam,
@@ -1016,7 +1536,9 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
         while ((1ll << sbits) < n) ++sbits;
         while ((1ll << tbits) < n_tiles) ++tbits;
         const bool packed = sbits + tbits <= 32;
-        if (front_end_launch(n, sp, tiles_x, L, packed, sbits, cap, st, s)) {
+        bool direct = false;
+        if (front_end_launch(n, sp, bins, tiles_x, n_tiles, L, packed, sbits, cap, st, s,
+                             &direct)) {
             // depth sort + offsets + emission done by the persistent kernel
         } else {
         // 1. depth sort of splats (4 stable 8-bit reduce-then-scan passes)
@@ -1041,8 +1563,9 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
             P, cap, L.pk0, packed ? nullptr : L.pv0, sbits);
         clamp_count_kernel<<<1, 1, 0, s>>>(P, cap, L.pcount);
         }
-        // 4. stable sort of pairs by tile id
-        const int np = tile_passes(n_tiles);
+        // 4. stable sort of pairs by tile id (the direct front end already
+        //    wrote the final list and the ranges)
+        const int np = direct ? 0 : tile_passes(n_tiles);
         const uint32_t* pk = L.pk0;
         const uint32_t* pv = L.pv0;
         for (int p = 0; p < np; ++p) {
@@ -1062,9 +1585,10 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
             pk = kdst;
         }
         // 5. ranges by boundary detection on the sorted tile ids (+ unpack)
-        tile_ranges_kernel<<<div_up(cap > 0 ? cap : 1, 4 * 256), 256, 0, s>>>(
-            pk, P, cap, packed ? sbits : 0, bins->d_tile_start, bins->d_tile_end,
-            bins->d_pair_splat);
+        if (!direct)
+            tile_ranges_kernel<<<div_up(cap > 0 ? cap : 1, 4 * 256), 256, 0, s>>>(
+                pk, P, cap, packed ? sbits : 0, bins->d_tile_start, bins->d_tile_end,
+                bins->d_pair_splat);
     } else {
         e = cudaMemsetAsync(P, 0, sizeof(int64_t) * 2, s);
         if (e != cudaSuccess) return e;
@@ -1104,3 +1628,10 @@ cudaError_t launch_scan_u32(const uint32_t* in, int64_t n, uint32_t* out, int64_
     return cudaGetLastError();
 }
 }  // namespace ss
+
+#ifdef SS_FE_TRACE
+extern "C" int ss_debug_fe_trace(void* host, size_t bytes) {
+    if (bytes > sizeof(ss::g_fe_trace)) bytes = sizeof(ss::g_fe_trace);
+    return (int)cudaMemcpyFromSymbol(host, ss::g_fe_trace, bytes);
+}
+#endif

@@ -149,11 +149,14 @@ np.savez({path!r}, pair_splat=ti.pair_splat, tile_range=ti.tile_range)
 """
 
 
-@pytest.mark.parametrize("n,w,h", [(3000, 96, 80), (300000, 1200, 680)])
-def test_binning_front_end_equals_per_pass_kernels(tmp_path, n, w, h):
-    """The cooperative front end (depth sort + offsets + emission in one
-    kernel) and the per-pass radix kernels (SS_BIN_FRONT=0) produce the
-    same pair list and tile ranges, bit for bit."""
+@pytest.mark.parametrize("legacy", ["SS_BIN_FRONT", "SS_BIN_DIRECT"])
+@pytest.mark.parametrize("n,w,h", [(3000, 96, 80), (300000, 1200, 680), (1000000, 1200, 680)])
+def test_binning_front_end_equals_per_pass_kernels(tmp_path, n, w, h, legacy):
+    """The default binning (cooperative front end: depth sort, then every
+    pair written straight to its (tile, depth, id) slot) equals, bit for
+    bit, the per-pass radix kernels (SS_BIN_FRONT=0) and the front end with
+    depth-order emission + tile radix passes (SS_BIN_DIRECT=0): same pair
+    list and tile ranges."""
     _need_gpu()
     import os
     import subprocess
@@ -164,7 +167,7 @@ def test_binning_front_end_equals_per_pass_kernels(tmp_path, n, w, h):
     path = str(tmp_path / "legacy.npz")
     code = _LEGACY_BINNING.format(repo=repo, tests=os.path.join(repo, "tests"), n=n, w=w, h=h,
                                   path=path)
-    env = dict(os.environ, SS_BIN_FRONT="0")
+    env = dict(os.environ, **{legacy: "0"})
     subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
     ref = np.load(path)
     out = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(n, 7)),
