@@ -153,8 +153,9 @@ __device__ __forceinline__ f32x2 shfl_up2(f32x2 v) {
 // load as ready-made f32x2 operands: pixel j of pair jp = j >> 1 sits in lane
 // (j & 1) of each packed field.
 struct BwdList {
-    float x[kTilePx], y[kTilePx];  // coordinates (pair jp = float2 at 2 jp)
-    float g[4 * kTilePx];          // per pair: gx, gx', gy, gy', gz, gz', gw, gw'
+    float xy[2 * kTilePx];         // per pair: x, x', y, y'
+    float ga[2 * kTilePx];         // per pair: gx, gx', gy, gy'  (16 B per pair: the
+    float gb[2 * kTilePx];         // per pair: gz, gz', gw, gw'   step's loads are contiguous)
     float s[kTilePx * 2];          // per pair: T0, T0', G0, G0' (state at the unit start)
     uint2 m[kTilePx];              // the two buckets' blend masks (pair = uint4)
 };
@@ -172,9 +173,9 @@ __device__ __forceinline__ uint32_t bwd_wavefront(int npair, int lane, bool hi, 
     const int steps = npair + 31;
     const uint4* M4 = reinterpret_cast<const uint4*>(L.m);
     const float4* S4 = reinterpret_cast<const float4*>(L.s);
-    const float4* G4 = reinterpret_cast<const float4*>(L.g);
-    const float2* X2 = reinterpret_cast<const float2*>(L.x);
-    const float2* Y2 = reinterpret_cast<const float2*>(L.y);
+    const float4* GA = reinterpret_cast<const float4*>(L.ga);
+    const float4* GB = reinterpret_cast<const float4*>(L.gb);
+    const float4* XY = reinterpret_cast<const float4*>(L.xy);
 #pragma unroll 1
     for (int st = 0; st < steps; ++st) {
         T = shfl_up2(T);
@@ -195,9 +196,9 @@ __device__ __forceinline__ uint32_t bwd_wavefront(int npair, int lane, bool hi, 
         const uint32_t bb = inr ? ((hi ? m.w : m.z) >> sh) & 3u : 0u;
         if (!__any_sync(0xffffffffu, (ba | bb) != 0u)) continue;
         seen |= ba | bb;
-        const float2 x = X2[jj], y = Y2[jj];
-        const float4 g0 = G4[2 * jj], g1 = G4[2 * jj + 1];
-        const f32x2 px = pk2(x.x, x.y), py = pk2(y.x, y.y);
+        const float4 xy = XY[jj];
+        const float4 g0 = GA[jj], g1 = GB[jj];
+        const f32x2 px = pk2(xy.x, xy.y), py = pk2(xy.z, xy.w);
         const f32x2 gx = pk2(g0.x, g0.y), gy = pk2(g0.z, g0.w), gz = pk2(g1.x, g1.y),
                     gw = pk2(g1.z, g1.w);
         f32x2 gd = pk2(0.f, 0.f);
@@ -318,17 +319,16 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
                     sD[wid][pos] = gd;
                 }
                 BwdList& L = sL[wid];
-                const int pb = (pos >> 1) * 8 + (pos & 1);  // pair-interleaved slots
-                L.g[pb] = pg.x;
-                L.g[pb + 2] = pg.y;
-                L.g[pb + 4] = pg.z;
-                L.g[pb + 6] = pg.w;
-                const int ps = (pos >> 1) * 4 + (pos & 1);
+                const int ps = (pos >> 1) * 4 + (pos & 1);  // pair-interleaved slots
+                L.ga[ps] = pg.x;
+                L.ga[ps + 2] = pg.y;
+                L.gb[ps] = pg.z;
+                L.gb[ps + 2] = pg.w;
                 L.s[ps] = ck.x;
                 L.s[ps + 2] = G0;
                 L.m[pos] = make_uint2(m0, m1);
-                L.x[pos] = (float)ix;
-                L.y[pos] = (float)iy;
+                L.xy[ps] = (float)ix;
+                L.xy[ps + 2] = (float)iy;
             }
             nact += __popc(bal);
         }
@@ -336,12 +336,12 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
         // zero gradient, finite state)
         if ((nact & 1) && lane == 0) {
             BwdList& L = sL[wid];
-            const int pb = (nact >> 1) * 8 + 1, ps = (nact >> 1) * 4 + 1;
-            L.g[pb] = L.g[pb + 2] = L.g[pb + 4] = L.g[pb + 6] = 0.f;
+            const int ps = (nact >> 1) * 4 + 1;
+            L.ga[ps] = L.ga[ps + 2] = L.gb[ps] = L.gb[ps + 2] = 0.f;
             L.s[ps] = 1.f;
             L.s[ps + 2] = 0.f;
             L.m[nact] = make_uint2(0u, 0u);
-            L.x[nact] = L.y[nact] = 0.f;
+            L.xy[ps] = L.xy[ps + 2] = 0.f;
             if (DEPTH) sD[wid][nact] = 0.f;
         }
         __syncwarp();
