@@ -143,10 +143,11 @@ __device__ __forceinline__ void bwd_commit(const SplatAcc2& q, const float4& A, 
         if (acc[c] != 0.f) atomicAdd(row + c, acc[c]);
 }
 
+// shfl.up by one lane inside each half-warp (the two buckets' chains)
 __device__ __forceinline__ f32x2 shfl_up2(f32x2 v) {
     float lo, hi;
     upk2(v, lo, hi);
-    return pk2(__shfl_up_sync(0xffffffffu, lo, 1), __shfl_up_sync(0xffffffffu, hi, 1));
+    return pk2(__shfl_up_sync(0xffffffffu, lo, 1, 16), __shfl_up_sync(0xffffffffu, hi, 1, 16));
 }
 
 // Per-warp compacted pixel list, pair-interleaved so that one pair's values
@@ -157,12 +158,16 @@ struct BwdList {
     float ga[2 * kTilePx];         // per pair: gx, gx', gy, gy'  (16 B per pair: the
     float gb[2 * kTilePx];         // per pair: gz, gz', gw, gw'   step's loads are contiguous)
     float s[kTilePx * 2];          // per pair: T0, T0', G0, G0' (state at the unit start)
+    float s2[kTilePx * 2];         // the same at the second bucket's start
     uint2 m[kTilePx];              // the two buckets' blend masks (pair = uint4)
 };
 
-// Diagonal wavefront over the warp's compacted pixel pairs; lane i applies
-// list positions 2i and 2i+1 to each pixel pair in turn.  Returns the lane's
-// blended-bit summary (bit 0: first splat blended somewhere, bit 1: second).
+// Diagonal wavefronts over the warp's compacted pixel pairs, one per half-
+// warp: lanes 0-15 carry the unit's first bucket, lanes 16-31 the second,
+// each chain starting from its own bucket's checkpoint, so the ramp is 15
+// steps instead of 31.  Lane i applies list positions 2i and 2i+1 to each
+// pixel pair in turn.  Returns the lane's blended-bit summary (bit 0: first
+// splat blended somewhere, bit 1: second).
 template <bool DEPTH, bool CLAMP>
 __device__ __forceinline__ uint32_t bwd_wavefront(int npair, int lane, bool hi, int sh,
                                                   const BwdList& L, const float* __restrict__ sD,
@@ -170,9 +175,10 @@ __device__ __forceinline__ uint32_t bwd_wavefront(int npair, int lane, bool hi, 
                                                   float amax, SplatAcc2& q0, SplatAcc2& q1) {
     f32x2 T = pk2(0.f, 0.f), G = T;
     uint32_t seen = 0u;
-    const int steps = npair + 31;
+    const int steps = npair + 15;
+    const int hl = lane & 15;
     const uint4* M4 = reinterpret_cast<const uint4*>(L.m);
-    const float4* S4 = reinterpret_cast<const float4*>(L.s);
+    const float4* S4 = reinterpret_cast<const float4*>(hi ? L.s2 : L.s);
     const float4* GA = reinterpret_cast<const float4*>(L.ga);
     const float4* GB = reinterpret_cast<const float4*>(L.gb);
     const float4* XY = reinterpret_cast<const float4*>(L.xy);
@@ -183,11 +189,11 @@ __device__ __forceinline__ uint32_t bwd_wavefront(int npair, int lane, bool hi, 
         // lanes outside the diagonal run with bits = 0 on pair 0 (a = 0:
         // nothing changes, T and G stay finite), so the only branch is
         // warp-uniform -- no divergence bookkeeping per step
-        const int j = st - lane;
+        const int j = st - hl;
         const bool inr = (unsigned)j < (unsigned)npair;
         const int jj = inr ? j : 0;
         const uint4 m = M4[jj];
-        if (lane == 0 && inr) {
+        if (hl == 0 && inr) {
             const float4 s = S4[jj];
             T = pk2(s.x, s.y);
             G = pk2(s.z, s.w);
@@ -318,6 +324,17 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
                     G0 += gd * ckpt_depth[slot0 + p];
                     sD[wid][pos] = gd;
                 }
+                // state at the second bucket's start (only pixels still
+                // blending there have that checkpoint; the others get an
+                // inert finite state: their second-bucket bits are 0)
+                float T1 = 0.f, G1 = 0.f;
+                if (m1 != 0u) {
+                    const float4 c2 = ckpt[slot0 + kTilePx + p];
+                    T1 = c2.x;
+                    G1 = pg.x * c2.y + pg.y * c2.z + pg.z * c2.w;
+                    if (DEPTH)
+                        G1 += (grad_depth ? grad_depth[o] : 0.f) * ckpt_depth[slot0 + kTilePx + p];
+                }
                 BwdList& L = sL[wid];
                 const int ps = (pos >> 1) * 4 + (pos & 1);  // pair-interleaved slots
                 L.ga[ps] = pg.x;
@@ -326,6 +343,8 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
                 L.gb[ps + 2] = pg.w;
                 L.s[ps] = ck.x;
                 L.s[ps + 2] = G0;
+                L.s2[ps] = T1;
+                L.s2[ps + 2] = G1;
                 L.m[pos] = make_uint2(m0, m1);
                 L.xy[ps] = (float)ix;
                 L.xy[ps + 2] = (float)iy;
@@ -340,6 +359,8 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
             L.ga[ps] = L.ga[ps + 2] = L.gb[ps] = L.gb[ps + 2] = 0.f;
             L.s[ps] = 1.f;
             L.s[ps + 2] = 0.f;
+            L.s2[ps] = 1.f;
+            L.s2[ps + 2] = 0.f;
             L.m[nact] = make_uint2(0u, 0u);
             L.xy[ps] = L.xy[ps + 2] = 0.f;
             if (DEPTH) sD[wid][nact] = 0.f;
