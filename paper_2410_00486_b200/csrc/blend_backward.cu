@@ -292,17 +292,32 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
         }
         // ---- compact the pixels that blended any splat of this unit
         const size_t slot0 = (size_t)(ckpt_base[tile] + 2 * u) * kTilePx;
+        // the lane's 8 pixels' n_contrib and masks, all loads in flight
+        // together (the records of the active ones follow per pixel)
+        uint32_t mk0[kTilePx / 32], mk1[kTilePx / 32];
+        {
+            int nct[kTilePx / 32];
+#pragma unroll
+            for (int c = 0; c < kTilePx / 32; ++c) {
+                const int p = c * 32 + lane;
+                const int ix = x0 + (p & 15), iy = y0 + (p >> 4);
+                nct[c] = (ix < W && iy < H) ? n_contrib[(size_t)iy * W + ix] : 0;
+            }
+#pragma unroll
+            for (int c = 0; c < kTilePx / 32; ++c) {
+                const int p = c * 32 + lane;
+                // a bucket's mask exists for pixels still blending at its start
+                mk0[c] = nct[c] > kbase ? ckpt_mask[slot0 + p] : 0u;
+                mk1[c] = nct[c] > kbase + kBucket ? ckpt_mask[slot0 + kTilePx + p] : 0u;
+            }
+        }
         int nact = 0;
-#pragma unroll 1
+#pragma unroll
         for (int c = 0; c < kTilePx / 32; ++c) {
             const int p = c * 32 + lane;
             const int ix = x0 + (p & 15), iy = y0 + (p >> 4);
-            const bool inside = ix < W && iy < H;
             const size_t o = (size_t)iy * W + ix;
-            const int nc = inside ? n_contrib[o] : 0;
-            // a bucket's mask exists for pixels still blending at its start
-            const uint32_t m0 = nc > kbase ? ckpt_mask[slot0 + p] : 0u;
-            const uint32_t m1 = nc > kbase + kBucket ? ckpt_mask[slot0 + kTilePx + p] : 0u;
+            const uint32_t m0 = mk0[c], m1 = mk1[c];
             const bool act = (m0 | m1) != 0u;
             const unsigned bal = __ballot_sync(0xffffffffu, act);
             if (act) {
