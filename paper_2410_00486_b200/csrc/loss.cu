@@ -89,18 +89,33 @@ __device__ __forceinline__ void taps4(const float* v, const SsimWindow& win, flo
     }
 }
 
+// 11-tap correlation of 4 consecutive outputs of a packed (lo, hi) pair of
+// quantities: FFMA2 with the tap weight broadcast to both lanes.
+__device__ __forceinline__ void taps4x2(const f32x2* v, const SsimWindow& win, f32x2 out[4]) {
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+        f32x2 a = pk2(0.f, 0.f);
+#pragma unroll
+        for (int m = 0; m < 11; ++m) a = fma2(pk2(win.w[m], win.w[m]), v[o + m], a);
+        out[o] = a;
+    }
+}
+
 // Tiles of 32x32 output pixels, one channel at a time; both separable
 // passes give every thread 4 consecutive outputs from one register window
-// (14 loads per 4 outputs instead of 11 per output).
+// (14 loads per 4 outputs instead of 11 per output).  The five moments run
+// as two packed pairs, (x, y) and (x^2, y^2), plus xy: FFMA2 halves the
+// issue slots of four of them.
 __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const float* __restrict__ x,
                                                        const float* __restrict__ y,
                                                        SsimWindow win, float* __restrict__ gmu,
                                                        float* __restrict__ gxx,
                                                        float* __restrict__ gxy,
                                                        double* __restrict__ partials) {
-    __shared__ __align__(16) float sx[LH][LP];
-    __shared__ __align__(16) float sy[LH][LP];
-    __shared__ __align__(16) float sh[5][LH][LT];
+    __shared__ __align__(16) float2 s_xy[LH][LP];   // (x, y) halo
+    __shared__ __align__(16) float2 shp[LH][LT];   // horizontal pass: (x, y)
+    __shared__ __align__(16) float2 shq[LH][LT];   //                  (x^2, y^2)
+    __shared__ __align__(16) float shm[LH][LT];    //                  xy
     __shared__ double red[2][8];
     SSIM_TRACE_BEGIN
     const int t = threadIdx.x;
@@ -129,8 +144,7 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
                 const int k = t + 256 * i;
                 if (k < LH * LH) {
                     const int r = k / LH, cc = k - r * LH;
-                    sx[r][cc] = vx[i];
-                    sy[r][cc] = vy[i];
+                    s_xy[r][cc] = make_float2(vx[i], vy[i]);
                 }
             }
         }
@@ -138,42 +152,54 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
         // horizontal (axis 1): 42 rows x 8 groups of 4 columns
         for (int task = t; task < LH * 8; task += 256) {
             const int r = task >> 3, c0 = (task & 7) * 4;
-            float xv[16], yv[16];
+            f32x2 pv[14], qv[14];
+            float mv[14];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float4 a = *reinterpret_cast<const float4*>(&sx[r][c0 + 4 * k]);
-                const float4 b = *reinterpret_cast<const float4*>(&sy[r][c0 + 4 * k]);
-                xv[4 * k] = a.x, xv[4 * k + 1] = a.y, xv[4 * k + 2] = a.z, xv[4 * k + 3] = a.w;
-                yv[4 * k] = b.x, yv[4 * k + 1] = b.y, yv[4 * k + 2] = b.z, yv[4 * k + 3] = b.w;
+            for (int k = 0; k < 7; ++k) {
+                const float4 a = *reinterpret_cast<const float4*>(&s_xy[r][c0 + 2 * k]);
+                pv[2 * k] = pk2(a.x, a.y);
+                pv[2 * k + 1] = pk2(a.z, a.w);
+                mv[2 * k] = a.x * a.y;
+                mv[2 * k + 1] = a.z * a.w;
             }
-            // one quantity at a time (x, y, x^2, y^2, xy), stored before the next
-            float o4[4], pv[14];
-            taps4(xv, win, o4);
-            *reinterpret_cast<float4*>(&sh[0][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
-            taps4(yv, win, o4);
-            *reinterpret_cast<float4*>(&sh[1][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
 #pragma unroll
-            for (int k = 0; k < 14; ++k) pv[k] = xv[k] * xv[k];
-            taps4(pv, win, o4);
-            *reinterpret_cast<float4*>(&sh[2][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
-#pragma unroll
-            for (int k = 0; k < 14; ++k) pv[k] = yv[k] * yv[k];
-            taps4(pv, win, o4);
-            *reinterpret_cast<float4*>(&sh[3][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
-#pragma unroll
-            for (int k = 0; k < 14; ++k) pv[k] = xv[k] * yv[k];
-            taps4(pv, win, o4);
-            *reinterpret_cast<float4*>(&sh[4][r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+            for (int k = 0; k < 14; ++k) qv[k] = mul2(pv[k], pv[k]);
+            f32x2 o2[4];
+            float o4[4];
+            taps4x2(pv, win, o2);
+            *reinterpret_cast<float4*>(&shp[r][c0]) = *reinterpret_cast<const float4*>(&o2[0]);
+            *reinterpret_cast<float4*>(&shp[r][c0 + 2]) = *reinterpret_cast<const float4*>(&o2[2]);
+            taps4x2(qv, win, o2);
+            *reinterpret_cast<float4*>(&shq[r][c0]) = *reinterpret_cast<const float4*>(&o2[0]);
+            *reinterpret_cast<float4*>(&shq[r][c0 + 2]) = *reinterpret_cast<const float4*>(&o2[2]);
+            taps4(mv, win, o4);
+            *reinterpret_cast<float4*>(&shm[r][c0]) = make_float4(o4[0], o4[1], o4[2], o4[3]);
         }
         __syncthreads();
         // vertical (axis 0): column q, 4 consecutive rows
         float mom[5][4];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
+        {
+            f32x2 v2[14], o2[4];
             float v[14];
 #pragma unroll
-            for (int i = 0; i < 14; ++i) v[i] = sh[k][4 * rg + i][q];
-            taps4(v, win, mom[k]);
+            for (int i = 0; i < 14; ++i) {
+                const float2 e = shp[4 * rg + i][q];
+                v2[i] = pk2(e.x, e.y);
+            }
+            taps4x2(v2, win, o2);
+#pragma unroll
+            for (int o = 0; o < 4; ++o) upk2(o2[o], mom[0][o], mom[1][o]);
+#pragma unroll
+            for (int i = 0; i < 14; ++i) {
+                const float2 e = shq[4 * rg + i][q];
+                v2[i] = pk2(e.x, e.y);
+            }
+            taps4x2(v2, win, o2);
+#pragma unroll
+            for (int o = 0; o < 4; ++o) upk2(o2[o], mom[2][o], mom[3][o]);
+#pragma unroll
+            for (int i = 0; i < 14; ++i) v[i] = shm[4 * rg + i][q];
+            taps4(v, win, mom[4]);
         }
         const int ox = x0 + q;
 #pragma unroll
@@ -196,7 +222,8 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
                 gxx[go] = gb2;
                 gxy[go] = 2.f * ga2;
                 ssum += (double)ss;
-                l1 += (double)fabsf(sx[LR + 4 * rg + o][LR + q] - sy[LR + 4 * rg + o][LR + q]);
+                const float2 e = s_xy[LR + 4 * rg + o][LR + q];
+                l1 += (double)fabsf(e.x - e.y);
             }
         }
         __syncthreads();
