@@ -142,6 +142,7 @@ sys.path.insert(0, {repo!r}); sys.path.insert(0, {tests!r})
 import paper_2410_00486_b200 as ss
 from paper_2410_00486_b200.scene import survey_camera, survey_scene
 sc = survey_scene({n}, 7)
+sc.positions = sc.positions * {spread}
 cam = survey_camera({w}, {h})
 out = ss.rasterize_forward(ss.GaussianMap.from_scene(sc), cam, ss.RasterOpts(sh_degree=0))
 ti = out.tile_index
@@ -150,8 +151,13 @@ np.savez({path!r}, pair_splat=ti.pair_splat, tile_range=ti.tile_range)
 
 
 @pytest.mark.parametrize("legacy", ["SS_BIN_FRONT", "SS_BIN_DIRECT"])
-@pytest.mark.parametrize("n,w,h", [(3000, 96, 80), (300000, 1200, 680), (1000000, 1200, 680)])
-def test_binning_front_end_equals_per_pass_kernels(tmp_path, n, w, h, legacy):
+@pytest.mark.parametrize("n,w,h,spread", [(3000, 96, 80, 1.0), (300000, 1200, 680, 1.0),
+                                          (1000000, 1200, 680, 1.0),
+                                          # depths over many binades: no depth pass skipped
+                                          (300000, 1200, 680, 3.0),
+                                          # > 8192 tiles: depth-order emission + tile passes
+                                          (200000, 2400, 1088, 1.0)])
+def test_binning_front_end_equals_per_pass_kernels(tmp_path, n, w, h, spread, legacy):
     """The default binning (cooperative front end: depth sort, then every
     pair written straight to its (tile, depth, id) slot) equals, bit for
     bit, the per-pass radix kernels (SS_BIN_FRONT=0) and the front end with
@@ -166,13 +172,16 @@ def test_binning_front_end_equals_per_pass_kernels(tmp_path, n, w, h, legacy):
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     path = str(tmp_path / "legacy.npz")
     code = _LEGACY_BINNING.format(repo=repo, tests=os.path.join(repo, "tests"), n=n, w=w, h=h,
-                                  path=path)
+                                  spread=spread, path=path)
     env = dict(os.environ, **{legacy: "0"})
     subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
     ref = np.load(path)
-    out = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(n, 7)),
-                               survey_camera(w, h), ss.RasterOpts(sh_degree=0))
+    sc = survey_scene(n, 7)
+    sc.positions = sc.positions * spread
+    out = ss.rasterize_forward(ss.GaussianMap.from_scene(sc), survey_camera(w, h),
+                               ss.RasterOpts(sh_degree=0))
     ti = out.tile_index
+    assert len(ti.pair_splat) > 0
     np.testing.assert_array_equal(ti.pair_splat, ref["pair_splat"])
     np.testing.assert_array_equal(ti.tile_range, ref["tile_range"])
 
