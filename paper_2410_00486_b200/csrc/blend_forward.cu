@@ -131,6 +131,9 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
                 const size_t prev = (size_t)(cbase + open_bucket) * kTilePx;
                 if (s0.live) ckpt_mask[prev + p0] = s0.bm;
                 if (s1.live) ckpt_mask[prev + p1] = s1.bm;
+                // n_contrib = last blended position + 1, from the closed mask
+                if (s0.bm) s0.last = 32 * open_bucket + 32 - __clz(s0.bm);
+                if (s1.bm) s1.last = 32 * open_bucket + 32 - __clz(s1.bm);
             }
             open_bucket = bucket;
             s0.live = !s0.done;
@@ -184,12 +187,10 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
                     upk2(T2, T0, T1);
                     const int q = (int)b0 + j;
                     if (ok0) {
-                        s0.last = q + 1;
                         s0.bm |= 1u << (q & 31);
                         if (T0 < t_min) s0.done = true;
                     }
                     if (ok1) {
-                        s1.last = q + 1;
                         s1.bm |= 1u << (q & 31);
                         if (T1 < t_min) s1.done = true;
                     }
@@ -210,6 +211,8 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
         const size_t prev = (size_t)(cbase + open_bucket) * kTilePx;
         if (s0.live) ckpt_mask[prev + p0] = s0.bm;
         if (s1.live) ckpt_mask[prev + p1] = s1.bm;
+        if (s0.bm) s0.last = 32 * open_bucket + 32 - __clz(s0.bm);
+        if (s1.bm) s1.last = 32 * open_bucket + 32 - __clz(s1.bm);
     }
     sync_state();
     if (ix < W) {
