@@ -220,9 +220,15 @@ class MappingEngine:
                                  P(self.work), self.work_cap, P(self.status), s),
               "ss_blend_forward")
         self._mark("blend_forward")
-        # the backward's longest-units-first schedule (needs only k_eff)
-        check(L.ss_backward_schedule(ctypes.byref(cm), P(self.k_eff), P(self.work), self.work_cap,
-                                     P(self.status), s), "ss_backward_schedule")
+        # the backward's longest-units-first schedule (needs only k_eff): on a
+        # side stream, concurrent with the loss kernels (fork / join by events,
+        # captured into the step's graph like the main stream)
+        side = self._side_stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            check(L.ss_backward_schedule(ctypes.byref(cm), P(self.k_eff), P(self.work),
+                                         self.work_cap, P(self.status), stream_handle()),
+                  "ss_backward_schedule")
         use_pg = self.cfg.lambda_ssim != 0.0 and not self.opts.with_depth
         check(L.ss_loss_l1_ssim(self.H, self.W, P(self.image), P(target),
                                 float(self.cfg.lambda_ssim), P(self.grad_image),
@@ -236,6 +242,7 @@ class MappingEngine:
             else:
                 self.grad_depth.zero_()
         self._mark("loss")
+        torch.cuda.current_stream().wait_stream(side)
         check(L.ss_backward_splat(ctypes.byref(cm), ctypes.byref(op), ctypes.byref(spss),
                                   ctypes.byref(bss), P(self.image), P(self.grad_image),
                                   P(self.pixgrad) if use_pg else None, P(self.depth),
@@ -245,6 +252,11 @@ class MappingEngine:
                                   P(self.contributed), P(self.status), s), "ss_backward_splat")
         self._mark("backward")
         return mp, cm, op
+
+    def _side_stream(self):
+        if getattr(self, "_side", None) is None or self._side.device != self.dev:
+            self._side = torch.cuda.Stream(device=self.dev)
+        return self._side
 
     def _snapshot(self, rec: StepRecord):
         """Copy the step's status block + loss sums into its pinned slot."""
