@@ -117,7 +117,10 @@ __device__ __forceinline__ void sh_color(const float d[3], int degree, const flo
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
         float raw = b[0] * dc[ch];
-        for (int k = 1; k < nb; ++k) raw += b[k] * rest[3 * (k - 1) + ch];
+        // static indices (b stays in registers), same summation order
+#pragma unroll
+        for (int k = 1; k < 16; ++k)
+            if (k < nb) raw += b[k] * rest[3 * (k - 1) + ch];
         raw += 0.5f;
         act[ch] = raw > 0.f;
         rgb[ch] = fmaxf(raw, 0.f);
