@@ -9,16 +9,21 @@
 // half of a pair's key is a function of its splat alone, those passes are
 // run here over the N splats instead of the P ~ 12 N pairs:
 //
-//   1. LSD sort of the N depth keys (4 x 8-bit passes), stable, values =
-//      splat index                               -> splats in (depth, index) order
-//   2. exclusive scan of touched-tile counts in that order  -> pair offsets, P
-//   3. coalesced emission of (tile, splat) pairs in that order
-//   4. LSD sort of the pair tile ids (ceil(log2 T / 8) passes), stable
-//                                                -> (tile, depth, index) order
-//   5. tile ranges by boundary detection; checkpoint slot bases by scan.
+//   1. LSD sort of the N depth keys (8-bit passes), stable, values = splat
+//      index                                    -> splats in (depth, index) order
+//   2. default (bin_front_kernel + fe_direct): every pair is written
+//      straight to its final slot, start[tile] + (pairs of that tile earlier
+//      in depth order), counted per (CTA, placer warp) and prefixed across
+//      them; tile ranges come out of the same scan.
+//      fallback (SS_BIN_DIRECT=0, > 8192 tiles, or the per-pass path):
+//      exclusive scan of touched-tile counts, coalesced emission of
+//      (tile, splat) pairs in depth order, LSD sort of the pair tile ids
+//      (ceil(log2 T / 8) passes), tile ranges by boundary detection;
+//   3. checkpoint slot bases by scan.
 //
 // The result is bit-identical to the reference order (tests/test_gpu_parity.py
-// compares it with the oracle's build_tile_index fed this projection).
+// compares it with the oracle's build_tile_index fed this projection, and
+// the default path with both fallbacks).
 //
 // Each radix pass is reduce-then-scan (upsweep counts, per-digit scan,
 // downsweep with warp ballot ranking and a shared-memory reorder so the
@@ -829,9 +834,6 @@ __device__ __forceinline__ void fe_walk(const uint4* __restrict__ drec,
     }
 }
 
-__device__ __forceinline__ uint32_t wq_span(uint32_t p0, uint32_t p1, uint32_t g, uint32_t G) {
-    return (uint32_t)(((uint64_t)(p1 - p0) * (g + 1)) / G) - (uint32_t)(((uint64_t)(p1 - p0) * g) / G);
-}
 
 template <int ITEMS>
 __device__ void fe_direct(const FeArgs& a, cooperative_groups::grid_group& grid, uint32_t* sm,
