@@ -583,19 +583,37 @@ __global__ void __launch_bounds__(kRestCTA, 3) chain_adam_rest_kernel(
     AdamHP hp = hp_v;
     if (d_hp) load_hp(d_hp, hp);
     const int nb = (deg + 1) * (deg + 1);
-    float* pm = M.d_sh_rest + base * kRestRow;
-    float* pv = V.d_sh_rest + base * kRestRow;
-    float* pp = shrest + base * kRestRow;
-    for (int e = t; e < span; e += kRestCTA) {
-        const int gi = e / kRestRow, j = e - gi * kRestRow;
-        const int k = j / 3 + 1, ch = j - 3 * (k - 1);
-        const float* fac = s_fac + 19 * gi;
-        const float gr = k < nb ? fac[k] * fac[16 + ch] : 0.f;
-        float p = s_rest[e], m = pm[e], v = pv[e];
-        adam_elem(p, gr, m, v, hp.lr[5], hp);
-        pp[e] = p;
-        pm[e] = m;
-        pv[e] = v;
+    float* __restrict__ pm = M.d_sh_rest + base * kRestRow;
+    float* __restrict__ pv = V.d_sh_rest + base * kRestRow;
+    float* __restrict__ pp = shrest + base * kRestRow;
+    // 9 elements per thread and round, all 18 moment loads in flight before
+    // the updates (the span is 45 rows of kRestCTA: latency, not bandwidth,
+    // bounded this loop with one element per round)
+    constexpr int U = 9;
+#pragma unroll 1
+    for (int e0 = t; e0 < span; e0 += kRestCTA * U) {
+        float m[U], v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * kRestCTA;
+            m[u] = e < span ? pm[e] : 0.f;
+            v[u] = e < span ? pv[e] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * kRestCTA;
+            if (e < span) {
+                const int gi = e / kRestRow, j = e - gi * kRestRow;
+                const int k = j / 3 + 1, ch = j - 3 * (k - 1);
+                const float* fac = s_fac + 19 * gi;
+                const float gr = k < nb ? fac[k] * fac[16 + ch] : 0.f;
+                float p = s_rest[e];
+                adam_elem(p, gr, m[u], v[u], hp.lr[5], hp);
+                pp[e] = p;
+                pm[e] = m[u];
+                pv[e] = v[u];
+            }
+        }
     }
 }
 
