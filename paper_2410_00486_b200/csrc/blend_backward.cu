@@ -159,7 +159,8 @@ struct BwdList {
     float gb[2 * kTilePx];         // per pair: gz, gz', gw, gw'   step's loads are contiguous)
     float s[kTilePx * 2];          // per pair: T0, T0', G0, G0' (state at the unit start)
     float s2[kTilePx * 2];         // the same at the second bucket's start
-    uint2 m[kTilePx];              // the two buckets' blend masks (pair = uint4)
+    uint32_t ma[kTilePx];          // first bucket's blend masks (pair = uint2)
+    uint32_t mb[kTilePx];          // second bucket's (each half-warp loads only its own)
 };
 
 // Diagonal wavefronts over the warp's compacted pixel pairs, one per half-
@@ -177,7 +178,7 @@ __device__ __forceinline__ uint32_t bwd_wavefront(int npair, int lane, bool hi, 
     uint32_t seen = 0u;
     const int steps = npair + 15;
     const int hl = lane & 15;
-    const uint4* M4 = reinterpret_cast<const uint4*>(L.m);
+    const uint2* M2 = reinterpret_cast<const uint2*>(hi ? L.mb : L.ma);
     const float4* S4 = reinterpret_cast<const float4*>(hi ? L.s2 : L.s);
     const float4* GA = reinterpret_cast<const float4*>(L.ga);
     const float4* GB = reinterpret_cast<const float4*>(L.gb);
@@ -192,14 +193,14 @@ __device__ __forceinline__ uint32_t bwd_wavefront(int npair, int lane, bool hi, 
         const int j = st - hl;
         const bool inr = (unsigned)j < (unsigned)npair;
         const int jj = inr ? j : 0;
-        const uint4 m = M4[jj];
+        const uint2 m = M2[jj];
         if (hl == 0 && inr) {
             const float4 s = S4[jj];
             T = pk2(s.x, s.y);
             G = pk2(s.z, s.w);
         }
-        const uint32_t ba = inr ? ((hi ? m.y : m.x) >> sh) & 3u : 0u;
-        const uint32_t bb = inr ? ((hi ? m.w : m.z) >> sh) & 3u : 0u;
+        const uint32_t ba = inr ? (m.x >> sh) & 3u : 0u;
+        const uint32_t bb = inr ? (m.y >> sh) & 3u : 0u;
         if (!__any_sync(0xffffffffu, (ba | bb) != 0u)) continue;
         seen |= ba | bb;
         const float4 xy = XY[jj];
@@ -360,7 +361,8 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
                 L.s[ps + 2] = G0;
                 L.s2[ps] = T1;
                 L.s2[ps + 2] = G1;
-                L.m[pos] = make_uint2(m0, m1);
+                L.ma[pos] = m0;
+                L.mb[pos] = m1;
                 L.xy[ps] = (float)ix;
                 L.xy[ps + 2] = (float)iy;
             }
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
             L.s[ps + 2] = 0.f;
             L.s2[ps] = 1.f;
             L.s2[ps + 2] = 0.f;
-            L.m[nact] = make_uint2(0u, 0u);
+            L.ma[nact] = L.mb[nact] = 0u;
             L.xy[ps] = L.xy[ps + 2] = 0.f;
             if (DEPTH) sD[wid][nact] = 0.f;
         }
