@@ -156,7 +156,10 @@ np.savez({path!r}, pair_splat=ti.pair_splat, tile_range=ti.tile_range)
                                           # depths over many binades: no depth pass skipped
                                           (300000, 1200, 680, 3.0),
                                           # > 8192 tiles: depth-order emission + tile passes
-                                          (200000, 2400, 1088, 1.0)])
+                                          (200000, 2400, 1088, 1.0),
+                                          # few large splats: > 65535 pairs per CTA, the
+                                          # placement runs in 16-bit-counter pieces
+                                          (3000, 1200, 680, 1.0)])
 def test_binning_front_end_equals_per_pass_kernels(tmp_path, n, w, h, spread, legacy):
     """The default binning (cooperative front end: depth sort, then every
     pair written straight to its (tile, depth, id) slot) equals, bit for
@@ -182,6 +185,8 @@ def test_binning_front_end_equals_per_pass_kernels(tmp_path, n, w, h, spread, le
                                ss.RasterOpts(sh_degree=0))
     ti = out.tile_index
     assert len(ti.pair_splat) > 0
+    if n == 3000 and w == 1200:
+        assert len(ti.pair_splat) > 2 * 65535  # more than one piece per CTA
     np.testing.assert_array_equal(ti.pair_splat, ref["pair_splat"])
     np.testing.assert_array_equal(ti.tile_range, ref["tile_range"])
 
