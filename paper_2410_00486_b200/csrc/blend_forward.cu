@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
             unsigned todo = __ballot_sync(0xffffffffu, j0 + lane < nb && ((s_band[j0 + lane] >> w) & 1u));
             while (todo) {
                 const int j = j0 + __ffs(todo) - 1;
+                const uint32_t qb = todo & (0u - todo);  // bit (b0 + j) & 31 of the masks
                 todo &= todo - 1;
 #ifdef SS_FWD_TRACE
                 ++tr_iters;
@@ -185,13 +186,12 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
                     T2 = mul2(T2, sub2(ONE2, a2));
                     float T0, T1;
                     upk2(T2, T0, T1);
-                    const int q = (int)b0 + j;
                     if (ok0) {
-                        s0.bm |= 1u << (q & 31);
+                        s0.bm |= qb;
                         if (T0 < t_min) s0.done = true;
                     }
                     if (ok1) {
-                        s1.bm |= 1u << (q & 31);
+                        s1.bm |= qb;
                         if (T1 < t_min) s1.done = true;
                     }
                     if (CONTRIB && (ok0 || ok1)) s_hit[j] = 1;
