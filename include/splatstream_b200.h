@@ -147,6 +147,12 @@ int ss_preprocess(const ss_map *map, const ss_camera *cam, const ss_camera *d_ca
 size_t ss_bin_workspace_bytes(int64_t n, int64_t pair_capacity, int32_t n_tiles);
 int ss_bin_sort(int64_t n, const ss_splats *splats, const ss_camera *cam, const ss_bins *bins,
                 void *d_workspace, size_t workspace_bytes, ss_status *d_status, void *stream);
+/* The forward's tile order alone (d_tile_cost -> d_tile_order, costliest
+ * first), so a caller can compute it off the critical path -- e.g. on a
+ * side stream during ss_preprocess -- and pass ss_bin_sort a ss_bins with
+ * d_tile_cost = NULL (ss_bin_sort then leaves d_tile_order as it is).
+ * Needs both pointers and n_tiles <= SS_ORDER_MAX_TILES. */
+int ss_tile_order(const ss_camera *cam, const ss_bins *bins, void *stream);
 
 /* ------------------------------------------------------------ blend fwd */
 /* Replaces rasterize_forward's blend (api.py:135-206; forward_tile

@@ -97,6 +97,7 @@ _SIGS = {
     "ss_preprocess": (I32, [P(SSMap), P(SSCamera), VP, P(SSRasterOpts), P(SSSplats), VP, VP]),
     "ss_bin_workspace_bytes": (SZ, [I64, I64, I32]),
     "ss_bin_sort": (I32, [I64, P(SSSplats), P(SSCamera), P(SSBins), VP, SZ, VP, VP]),
+    "ss_tile_order": (I32, [P(SSCamera), P(SSBins), VP]),
     "ss_blend_forward": (I32, [P(SSCamera), P(SSRasterOpts), P(SSSplats), P(SSBins), VP, VP, VP,
                                VP, VP, VP, VP, VP, VP, VP, I64, VP, VP]),
     "ss_loss_workspace_bytes": (SZ, [I32, I32]),

@@ -10,6 +10,7 @@ namespace ss {
 cudaError_t launch_preprocess(const ss_map*, const ss_camera*, const ss_camera*,
                               const ss_raster_opts*, const ss_splats*, ss_status*, cudaStream_t);
 size_t bin_workspace_bytes(int64_t, int64_t, int);
+cudaError_t launch_tile_order(const ss_camera*, const ss_bins*, cudaStream_t);
 cudaError_t launch_bin_sort(int64_t, const ss_splats*, const ss_camera*, const ss_bins*, void*,
                             size_t, ss_status*, cudaStream_t);
 cudaError_t launch_blend_forward(const ss_camera*, const ss_raster_opts*, const ss_splats*,
@@ -142,6 +143,11 @@ int ss_preprocess(const ss_map* map, const ss_camera* cam, const ss_camera* d_ca
 
 size_t ss_bin_workspace_bytes(int64_t n, int64_t pair_capacity, int32_t n_tiles) {
     return bin_workspace_bytes(n, pair_capacity, n_tiles);
+}
+
+int ss_tile_order(const ss_camera* cam, const ss_bins* bins, void* stream) {
+    if (!cam || !bins) return SS_EINVAL;
+    return rc(launch_tile_order(cam, bins, S(stream)));
 }
 
 int ss_bin_sort(int64_t n, const ss_splats* splats, const ss_camera* cam, const ss_bins* bins,

@@ -376,7 +376,7 @@ constexpr int kOrderBuckets = 64;
 __global__ void __launch_bounds__(1024) tile_meta_kernel(const uint32_t* __restrict__ tstart,
                                                          const uint32_t* __restrict__ tend,
                                                          int n_tiles,
-                                                         uint32_t* __restrict__ ckpt_base,
+                                                         uint32_t* __restrict__ ckpt_base,  // null: order only
                                                          const uint32_t* __restrict__ cost,
                                                          uint32_t* __restrict__ order) {
     __shared__ uint32_t s_warp[32];
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(1024) tile_meta_kernel(const uint32_t* __restr
     for (int k = 0; k < per; ++k) {
         const int i = i0 + k;
         if (i < n_tiles) {
-            sum += (tend[i] - tstart[i] + 31u) >> 5;
+            if (ckpt_base) sum += (tend[i] - tstart[i] + 31u) >> 5;
             cmax = max(cmax, cost[i]);
         }
     }
@@ -418,11 +418,12 @@ __global__ void __launch_bounds__(1024) tile_meta_kernel(const uint32_t* __restr
     }
     __syncthreads();
     uint32_t run = s_warp[w] + incl - sum;
-    for (int k = 0; k < per; ++k) {
-        const int i = i0 + k;
-        if (i < n) ckpt_base[i] = run;
-        if (i < n_tiles) run += (tend[i] - tstart[i] + 31u) >> 5;
-    }
+    if (ckpt_base)
+        for (int k = 0; k < per; ++k) {
+            const int i = i0 + k;
+            if (i < n) ckpt_base[i] = run;
+            if (i < n_tiles) run += (tend[i] - tstart[i] + 31u) >> 5;
+        }
     // counting sort by cost bucket, descending
     const unsigned long long mx = (unsigned long long)s_max + 1ull;
     for (int i = t; i < n_tiles; i += 1024) {
@@ -623,6 +624,7 @@ struct FeArgs {
     uint32_t* tile_end;
     uint4* drec;           // [n] depth-order splat records (fe_direct)
     uint32_t* keyred;      // [2 n_tiles] per-CTA AND / OR of the keys with pairs
+    uint32_t* ckpt_base;   // [n_img_tiles + 1] checkpoint slot bases (written by CTA 0)
 };
 
 template <int NT>
@@ -1018,6 +1020,22 @@ __device__ void fe_direct(const FeArgs& a, cooperative_groups::grid_group& grid,
             a.tile_end[q] = st + a.col_tot[q];
         }
         s_base[q] = st + a.col[(size_t)cta * NT + q];
+    }
+    if (cta == 0) {
+        // checkpoint slot bases: exclusive scan of ceil(len / 32) over the
+        // tiles, n_tiles + 1 entries (thread t: tiles t per .. t per + per - 1)
+        const uint32_t per = (NT + kFeThreads - 1) / kFeThreads;
+        const uint32_t q0 = t * per;
+        uint32_t sum = 0;
+        for (uint32_t k = 0; k < per; ++k)
+            if (q0 + k < NT) sum += (a.col_tot[q0 + k] + 31u) >> 5;
+        uint32_t run = block_excl_scan<kFeThreads>(sum, s_warp);
+        for (uint32_t k = 0; k < per; ++k)
+            if (q0 + k < NT) {
+                a.ckpt_base[q0 + k] = run;
+                run += (a.col_tot[q0 + k] + 31u) >> 5;
+            }
+        if (q0 < NT && q0 + per >= NT) a.ckpt_base[NT] = run;  // the thread holding the last tile
     }
     __syncthreads();
     FE_STAMP(18);
@@ -1486,6 +1504,7 @@ static bool front_end_launch(int64_t n, const ss_splats* sp, const ss_bins* bins
     a.tile_end = bins->d_tile_end;
     a.drec = L.fe_drec;
     a.keyred = L.fe_keyred;
+    a.ckpt_base = bins->d_ckpt_base;
     void* args[] = {&a};
     auto go = [&](auto kern, int items, int capacity) -> bool {
         const int64_t nft = div_up(n, (int64_t)kFeThreads * items);
@@ -1517,6 +1536,17 @@ static bool front_end_launch(int64_t n, const ss_splats* sp, const ss_bins* bins
     return ok;
 }
 
+// The forward's tile order alone (costliest first by d_tile_cost), e.g. on
+// a side stream while the next step's projection runs.
+cudaError_t launch_tile_order(const ss_camera* cam, const ss_bins* bins, cudaStream_t s) {
+    const int n_tiles = div_up(cam->width, kTile) * div_up(cam->height, kTile);
+    if (!bins->d_tile_order || !bins->d_tile_cost || n_tiles > SS_ORDER_MAX_TILES)
+        return cudaErrorInvalidValue;
+    tile_meta_kernel<<<1, 1024, 0, s>>>(bins->d_tile_start, bins->d_tile_end, n_tiles, nullptr,
+                                        bins->d_tile_cost, bins->d_tile_order);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam,
                             const ss_bins* bins, void* ws, size_t ws_bytes, ss_status* st,
                             cudaStream_t s) {
@@ -1532,6 +1562,7 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
         bins->d_tile_end, (uint32_t)n_tiles);
     cudaError_t e = cudaSuccess;
     int64_t* P = &st->pair_count;
+    bool direct_done = false;  // the direct front end also wrote the checkpoint bases
     if (n > 0) {
         uint32_t nn = (uint32_t)n;
         int sbits = 1, tbits = 1;
@@ -1539,8 +1570,10 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
         while ((1ll << tbits) < n_tiles) ++tbits;
         const bool packed = sbits + tbits <= 32;
         bool direct = false;
-        if (front_end_launch(n, sp, bins, tiles_x, n_tiles, L, packed, sbits, cap, st, s,
-                             &direct)) {
+        const bool fe = front_end_launch(n, sp, bins, tiles_x, n_tiles, L, packed, sbits, cap,
+                                         st, s, &direct);
+        direct_done = direct;
+        if (fe) {
             // depth sort + offsets + emission done by the persistent kernel
         } else {
         // 1. depth sort of splats (4 stable 8-bit reduce-then-scan passes)
@@ -1597,7 +1630,13 @@ cudaError_t launch_bin_sort(int64_t n, const ss_splats* sp, const ss_camera* cam
     }
     // checkpoint slot bases: exclusive scan of ceil(len/32), n_tiles+1 entries
     // (+ the forward's tile order when the caller keeps one)
-    if (bins->d_tile_order && bins->d_tile_cost && n_tiles <= SS_ORDER_MAX_TILES) {
+    const bool order = bins->d_tile_order && bins->d_tile_cost && n_tiles <= SS_ORDER_MAX_TILES;
+    if (direct_done) {
+        // the front end wrote the checkpoint bases; the order alone remains
+        if (order)
+            tile_meta_kernel<<<1, 1024, 0, s>>>(bins->d_tile_start, bins->d_tile_end, n_tiles,
+                                                nullptr, bins->d_tile_cost, bins->d_tile_order);
+    } else if (order) {
         tile_meta_kernel<<<1, 1024, 0, s>>>(bins->d_tile_start, bins->d_tile_end, n_tiles,
                                             bins->d_ckpt_base, bins->d_tile_cost,
                                             bins->d_tile_order);

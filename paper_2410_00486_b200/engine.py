@@ -204,12 +204,26 @@ class MappingEngine:
         spss, bss = self.splats.ss(), self.bins.ss()
         n = len(self.gmap)
         self._mark("begin")
+        # the forward's tile order (costliest first, from the last forward's
+        # per-tile costs) on a side stream, overlapping the projection; joined
+        # before the cooperative binning launch, which then leaves the order
+        # alone (its ss_bins copy has no cost array)
+        side = self._side_stream()
+        bss_sort = bss
+        if bss.d_tile_order and bss.d_tile_cost:
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                check(L.ss_tile_order(ctypes.byref(cm), ctypes.byref(bss), stream_handle()),
+                      "ss_tile_order")
+            bss_sort = self.bins.ss()
+            bss_sort.d_tile_cost = None
         check(L.ss_status_begin_step(P(self.status), s), "ss_status_begin_step")
         d_cam = self._params_ptrs()[0] if view_mode is None else None
         check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), d_cam, ctypes.byref(op),
                               ctypes.byref(spss), P(self.status), s), "ss_preprocess")
         self._mark("preprocess")
-        check(L.ss_bin_sort(n, ctypes.byref(spss), ctypes.byref(cm), ctypes.byref(bss),
+        torch.cuda.current_stream().wait_stream(side)
+        check(L.ss_bin_sort(n, ctypes.byref(spss), ctypes.byref(cm), ctypes.byref(bss_sort),
                             P(self.bin_ws), self.bin_ws.numel(), P(self.status), s),
               "ss_bin_sort")
         self._mark("binning")
