@@ -118,6 +118,19 @@ def test_tile_meta_ckpt_bases_and_forward_order(case):
     bucket = (cost * 64) // (cost.max() + 1)
     assert np.all(np.diff(bucket[order].astype(np.int64)) <= 0)
     np.testing.assert_array_equal(b.ckpt_base.cpu().numpy().astype(np.int64), ref)
+    # ss_tile_order alone (the engine's side-stream call) gives an order of the
+    # same cost buckets; ss_bin_sort without a cost array leaves the order as is
+    b.tile_order.copy_(torch.arange(T, dtype=torch.int32, device=b.tile_order.device))
+    assert L.ss_tile_order(ctypes.byref(cm), ctypes.byref(b.ss()), stream_handle()) == 0
+    o2 = b.tile_order.cpu().numpy().astype(np.int64)
+    assert sorted(o2.tolist()) == list(range(T))
+    np.testing.assert_array_equal(bucket[o2], bucket[order])
+    bs = b.ss()
+    bs.d_tile_cost = None
+    assert L.ss_bin_sort(n, ctypes.byref(out.splats.ss()), ctypes.byref(cm), ctypes.byref(bs),
+                         P(ws), ws.numel(), P(st), stream_handle()) == 0
+    np.testing.assert_array_equal(b.tile_order.cpu().numpy().astype(np.int64), o2)
+    np.testing.assert_array_equal(b.ckpt_base.cpu().numpy().astype(np.int64), ref)
     # forward in the new order == the first (arbitrary-order) forward
     dev = b.pairs.device
     img, ft = torch.empty_like(out.image), torch.empty_like(out.final_t)
