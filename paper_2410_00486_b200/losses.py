@@ -102,12 +102,12 @@ def compute_losses(rendered, target, opacity_logits, lambda_ssim: float = 0.2,
     g_logit = torch.empty(n, dtype=torch.float32, device=dev)
     check(lib().ss_opacity_reg(n, P(logits), float(lambda_o), P(g_logit), 0, P(osum),
                                stream_handle()), "ss_opacity_reg")
-    sh = sums[:2].cpu().numpy()
+    sh = torch.cat((sums[:2], osum[:1])).cpu().numpy()  # one host read
     npx = H * W * 3
     l1 = float(sh[0] / npx)
     ssim_loss = 1.0 - float(sh[1] / npx) if lambda_ssim != 0.0 else 0.0
     rendered_val = (1.0 - lambda_ssim) * l1 + lambda_ssim * ssim_loss
-    reg = float(osum[0].item() / n) if n else 0.0
+    reg = float(sh[2] / n) if n else 0.0
     return LossBreakdown(l1=l1, ssim_loss=ssim_loss, rendered=rendered_val, opacity_reg=reg,
                          total=rendered_val + lambda_o * reg, grad_image=grad,
                          grad_opacity_logit=g_logit)

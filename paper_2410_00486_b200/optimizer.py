@@ -16,7 +16,7 @@ import torch
 from . import _lib
 from ._lib import check, lib
 from .core import GaussianMap
-from .rasterizer import ParamGrads, P, stream_handle
+from .rasterizer import P, ParamGrads, finite_flags, stream_handle
 
 PARAM_SHAPES = {
     "position": (3,),
@@ -110,12 +110,16 @@ def adam_step(gmap: GaussianMap, grads: ParamGrads, state: AdamState, sh_degree:
     if len(grads) != len(gmap):
         raise ValueError(
             f"gradient length {len(grads)} does not match map length {len(gmap)}")
-    for name, t in (("position", grads.position), ("rotation", grads.rotation),
-                    ("log_scale", grads.log_scale), ("opacity_logit", grads.opacity_logit),
-                    ("sh_dc", grads.sh_dc), ("sh_rest", grads.sh_rest)):
-        if not bool(torch.isfinite(t).all()):
+    named = (("position", grads.position), ("rotation", grads.rotation),
+             ("log_scale", grads.log_scale), ("opacity_logit", grads.opacity_logit),
+             ("sh_dc", grads.sh_dc), ("sh_rest", grads.sh_rest))
+    # the finite checks and the "sh_rest in use" test as one host read
+    extra = () if state.sh_rest_active else ((grads.sh_rest != 0).any(),)
+    host = finite_flags([t for _, t in named], extra)
+    for (name, _), good in zip(named, host):
+        if not good:
             raise FloatingPointError(f"non-finite gradient for parameter '{name}'")
-    upd_rest = state.sh_rest_active or bool((grads.sh_rest != 0).any())
+    upd_rest = state.sh_rest_active or bool(host[len(named)])
     state.sh_rest_active = upd_rest
     state.step_count += 1
     st = torch.empty(_lib.STATUS_WORDS, dtype=torch.int64, device=gmap.device)

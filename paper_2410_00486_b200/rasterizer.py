@@ -134,6 +134,20 @@ def new_status(dev):
     return st
 
 
+def finite_flags(tensors, extra=()):
+    """[all(isfinite(t)) for t in tensors] + [bool(e) for e in extra] with one
+    fused max-|x| reduction over the tensors (torch._foreach_norm, inf-norm:
+    NaN and inf propagate, finite values cannot overflow) and ONE host read.
+    `extra`: 0-d device tensors read back in the same transfer."""
+    nonempty = [t for t in tensors if t.numel()]
+    vals = list(torch._foreach_norm(nonempty, float("inf"))) if nonempty else []
+    host = torch.stack([torch.isfinite(v) for v in vals] + [e.bool() for e in extra]).cpu() \
+        if (vals or extra) else torch.zeros(0, dtype=torch.bool)
+    it = iter(host.tolist())
+    flags = [bool(next(it)) if t.numel() else True for t in tensors]
+    return flags + [bool(v) for v in it]
+
+
 def raise_param_errors(st_host):
     bad = int(st_host[_lib.ST_BAD_PARAM])
     if bad != _lib.INT64_MAX:
@@ -300,15 +314,16 @@ def rasterize_forward(gmap: GaussianMap, camera, opts: RasterOpts | None = None)
         ws = bin_workspace(n, cap, n_tiles, dev)
         check(L.ss_bin_sort(n, ctypes.byref(sp.ss()), ctypes.byref(cm), ctypes.byref(bins.ss()),
                             P(ws), ws.numel(), P(st), s), "ss_bin_sort")
-        sh = st.cpu()
-        raise_param_errors(sh)
+        # status words + the checkpoint slot total in one host read
+        sh = torch.cat((st, bins.ckpt_base[n_tiles:n_tiles + 1].to(torch.int64))).cpu()
+        raise_param_errors(sh[:-1])
         pcount = int(sh[_lib.ST_PAIRS])
         if not int(sh[_lib.ST_OVERFLOW]):
             break
         st[_lib.ST_OVERFLOW] = 0  # the overflow word is sticky; clear it for the retry
         cap = int(pcount * 1.25) + 1024
     _CAP_HINT[key] = cap
-    n_slots = int(bins.ckpt_base[n_tiles].item())
+    n_slots = int(sh[-1])
     f32 = dict(dtype=torch.float32, device=dev)
     ckpt = torch.empty((max(n_slots, 1) * 256, 4), **f32)
     ckpt_depth = torch.empty(max(n_slots, 1) * 256, **f32) if opts.with_depth else None
@@ -370,12 +385,12 @@ class ParamGrads:
         return g
 
     def validate_finite(self):
-        """api.py:74-79."""
-        for name in ("position", "rotation", "log_scale", "opacity_logit"):
-            if not bool(torch.isfinite(getattr(self, name)).all()):
-                raise FloatingPointError(f"non-finite gradient in {name}")
-        if not (bool(torch.isfinite(self.sh_dc).all()) and bool(torch.isfinite(self.sh_rest).all())):
-            raise FloatingPointError("non-finite gradient in sh")
+        """api.py:74-79 (one fused reduction, one host read)."""
+        names = ("position", "rotation", "log_scale", "opacity_logit", "sh_dc", "sh_rest")
+        for k, good in zip(names, finite_flags([getattr(self, k) for k in names])):
+            if not good:
+                raise FloatingPointError(
+                    f"non-finite gradient in {'sh' if k.startswith('sh') else k}")
         return self
 
 

@@ -1,0 +1,32 @@
+"""Per-iteration time of the reference-shaped Python API path (rasterize_forward +
+compute_losses + backward_splatwise + adam_step + accumulate_grad_stats) at the bench
+workload, and a torch.profiler table of one iteration (host syncs, launches)."""
+import sys, os, time
+sys.path.insert(0, os.getcwd())
+import torch
+import paper_2410_00486_b200 as ss
+from paper_2410_00486_b200.scene import survey_camera, survey_scene
+n, W, H = 300000, 1200, 680
+g = ss.GaussianMap.from_scene(survey_scene(n, 0))
+cam = survey_camera(W, H)
+opts = ss.RasterOpts(sh_degree=0)
+tgt = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(n, 100)), cam, opts).image
+st = ss.AdamState.for_map(g)
+def it():
+    out = ss.rasterize_forward(g, cam, opts)
+    lb = ss.compute_losses(out.image, tgt, g.opacity_logits)
+    gr = ss.backward_splatwise(out, lb.grad_image)
+    gr.opacity_logit += lb.grad_opacity_logit
+    ss.adam_step(g, gr, st)
+    ss.accumulate_grad_stats(g, gr)
+for _ in range(3): it()
+torch.cuda.synchronize()
+t = time.perf_counter()
+K = 20
+for _ in range(K): it()
+torch.cuda.synchronize()
+dt = (time.perf_counter() - t) / K
+print(f"API path (rasterize_forward + compute_losses + backward_splatwise + adam_step + stats): {dt*1e3:.3f} ms/it, {1/dt:.0f} it/s")
+with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU, torch.profiler.ProfilerActivity.CUDA]) as p:
+    it(); torch.cuda.synchronize()
+print(p.key_averages().table(sort_by="self_cpu_time_total", row_limit=12))
