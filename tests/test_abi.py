@@ -70,3 +70,16 @@ def test_product_raises_without_gpu():
     import paper_2410_00486_b200 as ss
     with pytest.raises(RuntimeError, match="CUDA device"):
         ss.GaussianMap(10)
+
+
+def test_finite_flags_host_logic():
+    """finite_flags: one fused inf-norm reduction per call, empty tensors
+    count as finite, extra 0-d flags appended in order (CPU tensors here)."""
+    import torch
+    from paper_2410_00486_b200.rasterizer import finite_flags
+    nan, inf = float("nan"), float("inf")
+    got = finite_flags([torch.ones(3), torch.tensor([nan, 1.0]), torch.zeros(0),
+                        torch.tensor([3e38, -3e38]), torch.tensor([-inf])],
+                       (torch.tensor(True), torch.tensor(False)))
+    assert got == [True, False, True, True, False, True, False]
+    assert finite_flags([]) == []
