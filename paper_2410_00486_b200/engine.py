@@ -48,15 +48,21 @@ KERNELS_PER_CALL = {
     "step_fb": 1 + 1 + 1 + 2 + 3,
     "chain_adam": 1,
     "snapshot": 1,
+    "tile_order": 1,  # ss_tile_order on the side stream
 }
 
 
 def binning_kernels(n_tiles: int, n: int = 0) -> int:
-    """clear + front end + tile passes x 3 + ranges + checkpoint-base scan
-    (binning.cu).  The front end (depth sort, pair offsets, emission) is one
-    cooperative kernel up to ~300k-1.2M splats, else 4 x 3 radix kernels +
-    scan + emit + clamp."""
+    """Kernels of one ss_bin_sort (binning.cu) as the engine calls it (no
+    tile order: that is ss_tile_order on the side stream).  Up to ~1.2M
+    splats the front end is one cooperative kernel; with <= 8192 tiles it also
+    places the pairs and writes the checkpoint bases (clear + front end),
+    else clear + front end + tile passes x 3 + ranges + checkpoint-base scan;
+    beyond ~1.2M splats the front end is 4 x 3 radix kernels + scan + emit +
+    clamp."""
     bits = max(1, (n_tiles - 1).bit_length())
+    if n <= 148 * 8192 and n_tiles <= 8192:
+        return 1 + 1
     front = 1 if n <= 148 * 8192 else 4 * 3 + 1 + 1 + 1
     return 1 + front + 3 * ((bits + 7) // 8) + 1 + 1
 
@@ -332,6 +338,8 @@ class MappingEngine:
     def _launches_per_step(self):
         k = (KERNELS_PER_CALL["step_fb"] + binning_kernels(self.n_tiles, len(self.gmap))
              + KERNELS_PER_CALL["chain_adam"] + KERNELS_PER_CALL["snapshot"])
+        if self.n_tiles <= _lib.ORDER_MAX_TILES:
+            k += KERNELS_PER_CALL["tile_order"]
         if self.opts.with_depth and self.cfg.depth_weight:
             k += 3
         return k
