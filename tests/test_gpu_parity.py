@@ -772,3 +772,33 @@ def test_seed_large_cloud_vs_oracle_and_engine_insert():
     eng.step(cam, tgt)
     eng.synchronize()
     assert len(eng.losses()) == 2
+
+
+def test_engine_launch_count_matches_profiler():
+    """MappingEngine.launches (bench.py's gpu_launches) equals the library
+    kernels CUPTI sees in graph-replayed steps, side-stream kernels included."""
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    from paper_2410_00486_b200.scene import survey_camera, survey_scene
+    n, w, h = 20000, 320, 240
+    g = ss.GaussianMap.from_scene(survey_scene(n, 0))
+    cam = survey_camera(w, h)
+    opts = ss.RasterOpts(sh_degree=0)
+    tgt = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(n, 100)), cam,
+                               opts).image.clone()
+    eng = ss.MappingEngine(g, w, h, opts)
+    eng.fit_capacity(cam)
+    eng.enable_graph()
+    for _ in range(3):
+        eng.step(cam, tgt)
+    eng.synchronize()
+    steps = 4
+    l0 = eng.launches
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        for _ in range(steps):
+            eng.step(cam, tgt)
+        eng.synchronize()
+    ours = sum(e.count for e in prof.key_averages() if e.key.startswith("ss::")
+               or "ss::" in e.key.split("(")[0])
+    assert eng.launches - l0 == ours
+    assert ours == steps * eng._launches_per_step()
