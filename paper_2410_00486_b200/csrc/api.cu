@@ -80,6 +80,7 @@ __global__ void status_begin_step_kernel(ss_status* st) {
 }
 
 __global__ void step_snapshot_kernel(const ss_status* st, const double* sums, double* row) {
+    PDL_WAIT();
     const int t = threadIdx.x;
     const int64_t* w = reinterpret_cast<const int64_t*>(st);
     if (t < 8) row[t] = (double)w[t];
@@ -122,8 +123,8 @@ int ss_step_snapshot(const ss_status* d_status, const double* d_loss_sums, doubl
         cudaGetLastError();
         return SS_EINVAL;  // not page-locked / mapped host memory
     }
-    step_snapshot_kernel<<<1, 32, 0, S(stream)>>>(d_status, d_loss_sums,
-                                                  reinterpret_cast<double*>(dev_row));
+    launch_pdl(step_snapshot_kernel, dim3(1), dim3(32), 0, S(stream), d_status, d_loss_sums,
+               reinterpret_cast<double*>(dev_row));
     return rc(cudaGetLastError());
 }
 

@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
     // depth gradient
     __shared__ BwdList sL[kBwdWarps];
     __shared__ float sD[DEPTH ? kBwdWarps : 1][DEPTH ? kTilePx : 1];
+    PDL_WAIT();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const bool hi = lane >= 16;            // lane's splats live in the second bucket
     const int sh = (2 * lane) & 31;        // their bit pair in that bucket's mask
@@ -493,6 +494,7 @@ __global__ void __launch_bounds__(1024) bwd_schedule_kernel(uint32_t* counter,
 
 __global__ void bwd_clear_kernel(float* __restrict__ g2d, int64_t nf, uint8_t* contributed,
                                  int64_t n, uint32_t* counter) {
+    PDL_WAIT();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if (i == 0) *counter = 0u;
@@ -527,8 +529,8 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
     // one launch clears the gradient rows, the contributed marks and the
     // work-unit counter
     int tx = div_up(cam->width, kTile), ty = div_up(cam->height, kTile);
-    bwd_clear_kernel<<<div_up(n * ncol > 4 ? n * ncol / 4 : 1, 256), 256, 0, s>>>(
-        g2d, (int64_t)n * ncol, contributed, n, counter);
+    launch_pdl(bwd_clear_kernel, dim3(div_up(n * ncol > 4 ? n * ncol / 4 : 1, 256)), dim3(256),
+               0, s, g2d, (int64_t)n * ncol, contributed, n, counter);
     const int threads = 32 * kBwdWarps;
     const size_t smem = 0;
     int dev = 0, sms = 148, per_sm = 1;
@@ -537,7 +539,7 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
     auto go = [&](auto kern) -> cudaError_t {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
         if (per_sm < 1) per_sm = 1;
-        kern<<<sms * per_sm, threads, smem, s>>>(
+        launch_pdl(kern, dim3(sms * per_sm), dim3(threads), smem, s,
             cam->width, cam->height, tx, bins->d_tile_start, bins->d_ckpt_base, k_eff,
             bins->d_pair_splat, reinterpret_cast<const SplatRec*>(sp->d_rec), o->alpha_max, image,
             grad_image, pixgrad, depth, grad_depth, n_contrib,

@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
     __shared__ unsigned long long s_wbase;
     // CTA -> tile through the costliest-first order of ss_bin_sort (the
     // tiles' results do not depend on it); the CTA's cycles feed the next one
+    PDL_WAIT();
     const int tile = tile_order ? (int)tile_order[blockIdx.x] : (int)blockIdx.x;
     const long long clk0 = clock64();
     const int t = threadIdx.x;
@@ -285,7 +286,7 @@ cudaError_t launch_blend_forward(const ss_camera* cam, const ss_raster_opts* o,
     const bool contribf = contributed != nullptr;
     const bool ordered = bins->d_tile_order && bins->d_tile_cost && n_tiles <= SS_ORDER_MAX_TILES;
     auto args = [&](auto kern) {
-        kern<<<n_tiles, 128, 0, s>>>(
+        launch_pdl(kern, dim3(n_tiles), dim3(128), 0, s,
             cam->width, cam->height, tx, bins->d_tile_start, bins->d_tile_end, bins->d_ckpt_base,
             bins->d_pair_splat, reinterpret_cast<const SplatRec*>(sp->d_rec), o->t_min,
             o->alpha_min, o->alpha_max, o->background[0], o->background[1], o->background[2],

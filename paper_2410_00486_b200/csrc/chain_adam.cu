@@ -472,6 +472,7 @@ __global__ void __launch_bounds__(256, REST ? 2 : 4) chain_adam_kernel(
     ss_param_grads M, ss_param_grads V, AdamHP hp_v, const ss_adam_hparams* __restrict__ d_hp,
     float* __restrict__ grad2d_accum, float* __restrict__ grad3d_accum,
     int32_t* __restrict__ obs_count, ss_status* st) {
+    PDL_WAIT();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n || st->pair_overflow) return;
     CamC cam = cam_v;
@@ -714,7 +715,7 @@ cudaError_t launch_chain_adam(const ss_map* mp, const ss_camera* cam, const ss_c
     CamC cc;
     fill_camc(cam, cc);
     auto go = [&](auto kern) {
-        kern<<<div_up(mp->n, 256), 256, 0, s>>>(
+        launch_pdl(kern, dim3(div_up(mp->n, 256)), dim3(256), 0, s,
             mp->n, mp->d_positions, reinterpret_cast<float4*>(mp->d_rotations), mp->d_log_scales,
             mp->d_opacity_logits, mp->d_sh_dc, mp->d_sh_rest, cc, d_cam, o->sh_degree, o->dilation,
             g2d, flags, contributed, lo_over_n, *M, *V, make_hp(h), d_hp, mp->d_grad2d_accum,

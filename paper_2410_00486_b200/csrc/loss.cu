@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
     __shared__ __align__(16) float2 shq[LH][LT];   //                  (x^2, y^2)
     __shared__ __align__(16) float shm[LH][LT];    //                  xy
     __shared__ double red[2][8];
+    PDL_WAIT();
     SSIM_TRACE_BEGIN
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * LT, y0 = blockIdx.y * LT;
@@ -283,6 +284,7 @@ __global__ void __launch_bounds__(256, 3) ssim_bwd_kernel(int H, int W, const fl
                                                        int n_partials,
                                                        double* __restrict__ sums) {
     extern __shared__ __align__(16) float smem_b[];
+    PDL_WAIT();
     SSIM_TRACE_BEGIN
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 32) {
         // fixed-order reduction of ssim_fwd's per-CTA (|x-y|, SSIM) sums
@@ -495,8 +497,8 @@ cudaError_t launch_loss(int H, int W, const float* x, const float* y, float lam,
     cudaError_t e =
         cudaFuncSetAttribute(ssim_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_b);
     if (e != cudaSuccess) return e;
-    ssim_fwd_kernel<<<grid, 256, 0, s>>>(H, W, x, y, win, gmu, gxx, gxy, partials);
-    ssim_bwd_kernel<<<grid, 256, smem_b, s>>>(H, W, x, y, win, gmu, gxx, gxy, lam, grad,
+    launch_pdl(ssim_fwd_kernel, grid, dim3(256), 0, s, H, W, x, y, win, gmu, gxx, gxy, partials);
+    launch_pdl(ssim_bwd_kernel, grid, dim3(256), (size_t)smem_b, s, H, W, x, y, win, gmu, gxx, gxy, lam, grad,
                                               reinterpret_cast<float4*>(pixgrad), partials,
                                               (int)(grid.x * grid.y), sums);
     return cudaGetLastError();
