@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     SplatRec* __restrict__ rec,
     uint32_t* __restrict__ depth_key, uint32_t* __restrict__ tiles, uint2* __restrict__ rect,
     uint8_t* __restrict__ flags, float* __restrict__ aux, ss_status* status) {
+    PDL_WAIT();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     CamF cam = cam_v;
     if (d_cam) load_camf(d_cam, cam);  // graph replay: camera from device memory
@@ -244,7 +245,7 @@ cudaError_t launch_preprocess(const ss_map* map, const ss_camera* cam, const ss_
     int tx = div_up(cam->width, kTile), ty = div_up(cam->height, kTile);
     int threads = 256;
     int blocks = div_up(map->n, threads);
-    preprocess_kernel<<<blocks, threads, 0, s>>>(
+    launch_pdl(preprocess_kernel, dim3(blocks), dim3(threads), 0, s,
         map->n, map->d_positions, reinterpret_cast<const float4*>(map->d_rotations),
         map->d_log_scales, map->d_opacity_logits, map->d_sh_dc, map->d_sh_rest, cf, d_cam,
         o->sh_degree, o->near_plane, o->dilation, logf(o->alpha_min), tx, ty,
