@@ -183,7 +183,7 @@ __device__ __forceinline__ uint32_t bwd_wavefront(int npair, int lane, bool hi, 
     const float4* GA = reinterpret_cast<const float4*>(L.ga);
     const float4* GB = reinterpret_cast<const float4*>(L.gb);
     const float4* XY = reinterpret_cast<const float4*>(L.xy);
-#pragma unroll 1
+#pragma unroll 2
     for (int st = 0; st < steps; ++st) {
         T = shfl_up2(T);
         G = shfl_up2(G);
