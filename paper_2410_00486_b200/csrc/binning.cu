@@ -776,6 +776,7 @@ __device__ __forceinline__ void fe_walk(const uint4* __restrict__ drec,
         for (int d = 16; d > 0; d >>= 1) endw = max(endw, __shfl_xor_sync(0xffffffffu, endw, d));
         const uint32_t a1 = min(rlo + endw, q1);
         const uint32_t pw = wx | (wy << 16);
+#pragma unroll 2
         for (uint32_t e0 = q - rlo; e0 < a1 - rlo; e0 += 32) {
             const uint32_t e = e0 + l;
             const bool in = e < a1 - rlo;
