@@ -201,7 +201,7 @@ __device__ __forceinline__ uint32_t bwd_wavefront(int npair, int lane, bool hi, 
         }
         const uint32_t ba = inr ? (m.x >> sh) & 3u : 0u;
         const uint32_t bb = inr ? (m.y >> sh) & 3u : 0u;
-        if (!__any_sync(0xffffffffu, (ba | bb) != 0u)) continue;
+        // (no warp-uniform skip: a branch here would split the unrolled steps)
         seen |= ba | bb;
         const float4 xy = XY[jj];
         const float4 g0 = GA[jj], g1 = GB[jj];
