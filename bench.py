@@ -437,9 +437,10 @@ def main():
                          "peak_source": peak_src,
                          "ncu": {k: v for k, v in ncu_stats(dom).items()
                                  if k in ("issue_slots_pct", "warps_active_pct")},
-                         "note": "FP32 CUDA-core kernel limited by instruction issue "
-                                 "(ncu issue_slots_pct), not by HBM; no tensor-core work "
-                                 "on this path"},
+                         "note": "FP32 CUDA-core kernel bound by instruction issue, "
+                                 "FMA-pipe occupancy and dependent latency (ncu: issue "
+                                 "slots ~55 %, FMA pipe ~56 %, 4 warps/SMSP at 128 regs), "
+                                 "not by HBM; no tensor-core work on this path"},
             "iteration_roofline": {"algorithmic_MB": it_bytes / 1e6,
                                    "achieved_GBs": it_bytes * value / views / 1e9,
                                    "frac": it_bytes * value / views / 1e9 / peak},
