@@ -505,31 +505,53 @@ class MappingEngine:
                        add_reg: bool = True):
         """Keyframe batch: sum of per-view gradients (+ the opacity-reg
         gradient once), optional all-reduce of the flat buffer, then Adam and
-        the statistics update.  Synchronous on the status (overflow check)."""
+        the statistics update.  Reads the overflow status once per step on one
+        GPU (once per view when an all-reduce follows: every rank must redo a
+        view before the collective)."""
         self._maybe_densify()
         L = lib()
         s = stream_handle()
         n = len(self.gmap)
         flat, fss = self._flat_grads()
-        flat.zero_()
         lon = float(self.cfg.lambda_o / n) if (n and add_reg) else 0.0
-        losses = []
-        for v, (cam, tgt) in enumerate(zip(cameras, targets)):
-            cam = Camera.of(cam)
-            td = target_depths[v] if target_depths is not None else None
-            while True:
-                mp, cm, op = self._forward_backward(cam, tgt, td, v)
-                sh = self.status.cpu()
-                if not int(sh[_lib.ST_OVERFLOW]):
-                    break
-                self._alloc_pair_buffers(int(int(sh[_lib.ST_PAIRS]) * self.cfg.pair_margin) + 4096)
-                check(L.ss_status_reset(P(self.status), s), "ss_status_reset")
+
+        def chain(v, mp, cm, op):
             check(L.ss_chain_backward(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op),
                                       P(self.g2d), P(self.splats.flags), P(self.contributed),
                                       lon if v == 0 else 0.0,
                                       _lib.SS_CHAIN_ACCUMULATE | _lib.SS_CHAIN_STAT_PLANES,
                                       ctypes.byref(fss), P(self.status), s), "ss_chain_backward")
-            losses.append(self.sums[:2].clone())
+
+        views = [(Camera.of(c), t, target_depths[v] if target_depths is not None else None)
+                 for v, (c, t) in enumerate(zip(cameras, targets))]
+        losses = None
+        if allreduce is None:
+            # one GPU: every view enqueued without a host sync, then one read
+            # of the (sticky) overflow word; on overflow the step is redone
+            # view by view below (nothing has been applied yet)
+            flat.zero_()
+            losses = []
+            for v, (cam, tgt, td) in enumerate(views):
+                mp, cm, op = self._forward_backward(cam, tgt, td, v)
+                chain(v, mp, cm, op)
+                losses.append(self.sums[:2].clone())
+            if int(self.status[_lib.ST_OVERFLOW].item()):
+                check(L.ss_status_reset(P(self.status), s), "ss_status_reset")
+                losses = None
+        if losses is None:
+            flat.zero_()
+            losses = []
+            for v, (cam, tgt, td) in enumerate(views):
+                while True:
+                    mp, cm, op = self._forward_backward(cam, tgt, td, v)
+                    sh = self.status.cpu()
+                    if not int(sh[_lib.ST_OVERFLOW]):
+                        break
+                    self._alloc_pair_buffers(
+                        int(int(sh[_lib.ST_PAIRS]) * self.cfg.pair_margin) + 4096)
+                    check(L.ss_status_reset(P(self.status), s), "ss_status_reset")
+                chain(v, mp, cm, op)
+                losses.append(self.sums[:2].clone())
         if allreduce is not None:
             allreduce(flat)
         self.state.step_count += 1

@@ -802,3 +802,30 @@ def test_engine_launch_count_matches_profiler():
                or "ss::" in e.key.split("(")[0])
     assert eng.launches - l0 == ours
     assert ours == steps * eng._launches_per_step()
+
+
+def test_multiview_step_recovers_from_pair_overflow():
+    """One-GPU keyframe batch: the views are enqueued without host syncs and
+    the sticky overflow word is read once; an overflowing step is redone view
+    by view with grown buffers -- same result as an engine sized up front."""
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    from paper_2410_00486_b200.scene import survey_camera, survey_scene
+    n, w, h, V = 4000, 96, 80, 3
+    sc, tsc = survey_scene(n, 3), survey_scene(n, 103)
+    opts = ss.RasterOpts(sh_degree=0)
+    cams = [survey_camera(w, h, v, V) for v in range(V)]
+    tm = ss.GaussianMap.from_scene(tsc)
+    tg = [ss.rasterize_forward(tm, c, opts).image.clone() for c in cams]
+    ga, gb = ss.GaussianMap.from_scene(sc), ss.GaussianMap.from_scene(sc)
+    ea = ss.MappingEngine(ga, w, h, opts, pair_capacity=64)
+    eb = ss.MappingEngine(gb, w, h, opts)
+    for c in cams:
+        eb.fit_capacity(c)
+    for _ in range(2):
+        ea.multiview_step(cams, tg)
+        eb.multiview_step(cams, tg)
+    torch.cuda.synchronize()
+    assert ea.pair_capacity > 64
+    np.testing.assert_allclose(ga.positions.cpu().numpy(), gb.positions.cpu().numpy(),
+                               rtol=0, atol=1e-6)
