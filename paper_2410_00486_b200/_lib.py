@@ -92,6 +92,7 @@ _SIGS = {
     "ss_abi_version": (I32, []),
     "ss_status_reset": (I32, [VP, VP]),
     "ss_status_begin_step": (I32, [VP, VP]),
+    "ss_status_flags": (I32, [VP, VP, VP]),
     "ss_step_snapshot": (I32, [VP, VP, VP, VP]),
     "ss_apply_stat_planes": (I32, [P(SSMap), P(SSParamGrads), VP]),
     "ss_preprocess": (I32, [P(SSMap), P(SSCamera), VP, P(SSRasterOpts), P(SSSplats), VP, VP]),

@@ -79,6 +79,12 @@ __global__ void status_begin_step_kernel(ss_status* st) {
     st->opacity_sum = 0.0;
 }
 
+__global__ void status_flags_kernel(const ss_status* st, float* flags) {
+    flags[0] = st->pair_overflow ? 1.f : 0.f;
+    flags[1] = (st->first_nonfinite_param != LLONG_MAX || st->first_zero_quat != LLONG_MAX ||
+                st->first_nonfinite_grad != LLONG_MAX) ? 1.f : 0.f;
+}
+
 __global__ void step_snapshot_kernel(const ss_status* st, const double* sums, double* row) {
     PDL_WAIT();
     const int t = threadIdx.x;
@@ -112,6 +118,12 @@ int ss_status_reset(ss_status* d_status, void* stream) {
 int ss_status_begin_step(ss_status* d_status, void* stream) {
     if (!d_status) return SS_EINVAL;
     status_begin_step_kernel<<<1, 1, 0, S(stream)>>>(d_status);
+    return rc(cudaGetLastError());
+}
+
+int ss_status_flags(const ss_status* d_status, float* d_flags, void* stream) {
+    if (!d_status || !d_flags) return SS_EINVAL;
+    status_flags_kernel<<<1, 1, 0, S(stream)>>>(d_status, d_flags);
     return rc(cudaGetLastError());
 }
 

@@ -458,7 +458,10 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t n, float* pos, float4
     const float* rg = (upd_rest && Gr.d_sh_rest) ? Gr.d_sh_rest + 45 * i : nullptr;
     if (rg)
         for (int k = 0; k < 45; ++k) fin &= finitef(rg[k]);  // loads in flight together
-    if (!fin) report_first(&st->first_nonfinite_grad, i);
+    if (!fin) {  // optimizer.py:111-113 raises before touching the map: leave this one as is
+        report_first(&st->first_nonfinite_grad, i);
+        return;
+    }
     adam_gaussian(i, o, rg, pos, rot, ls, opl, shdc, shrest, M, V, hp, upd_rest != 0, st);
 }
 
@@ -500,7 +503,12 @@ __global__ void __launch_bounds__(256, REST ? 2 : 4) chain_adam_kernel(
         float sg = sigm(opi);
         o.op += lo_over_n * sg * (1.f - sg);
     }
-    if (!grad_finite(o)) report_first(&st->first_nonfinite_grad, i);
+    if (!grad_finite(o)) {
+        // the reference raises before any update (api.py:74-79, optimizer.py:111-113): this
+        // Gaussian's parameters, moments and statistics stay as they were
+        report_first(&st->first_nonfinite_grad, i);
+        return;
+    }
     if (contributed && contributed[i]) {
         grad2d_accum[i] += o.n2d;
         grad3d_accum[3 * i] += o.pos[0];
@@ -532,6 +540,7 @@ __global__ void __launch_bounds__(kRestCTA, 3) chain_adam_rest_kernel(
     float* __restrict__ grad2d_accum, float* __restrict__ grad3d_accum,
     int32_t* __restrict__ obs_count, ss_status* st) {
     extern __shared__ float rs_smem[];
+    __shared__ uint8_t s_ok[kRestCTA];               // gradient finite: update this row
     float* s_rest = rs_smem;                         // [kRestCTA * 45] parameters
     float* s_fac = rs_smem + kRestCTA * kRestRow;    // [kRestCTA * 19] basis, colour grad
     if (st->pair_overflow) return;  // uniform: the step is replayed
@@ -569,15 +578,20 @@ __global__ void __launch_bounds__(kRestCTA, 3) chain_adam_rest_kernel(
             float sg = sigm(opi);
             o.op += lo_over_n * sg * (1.f - sg);
         }
-        if (!grad_finite(o)) report_first(&st->first_nonfinite_grad, i);
-        if (contributed && contributed[i]) {
-            grad2d_accum[i] += o.n2d;
-            grad3d_accum[3 * i] += o.pos[0];
-            grad3d_accum[3 * i + 1] += o.pos[1];
-            grad3d_accum[3 * i + 2] += o.pos[2];
-            obs_count[i] += 1;
+        const bool fin = grad_finite(o);
+        s_ok[t] = fin;
+        if (!fin) {
+            report_first(&st->first_nonfinite_grad, i);  // row left unchanged (see above)
+        } else {
+            if (contributed && contributed[i]) {
+                grad2d_accum[i] += o.n2d;
+                grad3d_accum[3 * i] += o.pos[0];
+                grad3d_accum[3 * i + 1] += o.pos[1];
+                grad3d_accum[3 * i + 2] += o.pos[2];
+                obs_count[i] += 1;
+            }
+            adam_gaussian(i, o, nullptr, pos, rot, ls, opl, shdc, shrest, M, V, hp, false, st);
         }
-        adam_gaussian(i, o, nullptr, pos, rot, ls, opl, shdc, shrest, M, V, hp, false, st);
     }
     __syncthreads();
     // Adam over the CTA's contiguous sh_rest span (bands >= deg + 1 get g = 0)
@@ -603,8 +617,9 @@ __global__ void __launch_bounds__(kRestCTA, 3) chain_adam_rest_kernel(
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int e = e0 + u * kRestCTA;
-            if (e < span) {
-                const int gi = e / kRestRow, j = e - gi * kRestRow;
+            const int gi = e / kRestRow;
+            if (e < span && s_ok[gi]) {
+                const int j = e - gi * kRestRow;
                 const int k = j / 3 + 1, ch = j - 3 * (k - 1);
                 const float* fac = s_fac + 19 * gi;
                 const float gr = k < nb ? fac[k] * fac[16 + ch] : 0.f;

@@ -20,6 +20,30 @@ import torch
 import torch.distributed as dist
 
 
+# The flat per-Gaussian buffer one keyframe-batch step sums over views and
+# ranks (SURVEY 8e): plane name -> floats per Gaussian, planes stored one
+# after another (plane-major, each N x k), then FLAT_TAIL floats written by
+# ss_status_flags (any pair overflow, any error) so the gradient all-reduce
+# also tells every rank whether some rank has to redo the step or raise.
+FLAT_PLANES = (("position", 3), ("rotation", 4), ("log_scale", 3), ("opacity", 1),
+               ("sh_dc", 3), ("sh_rest", 45), ("pos2d", 1), ("stat_g2d", 1), ("stat_g3d", 3),
+               ("stat_cnt", 1))
+FLAT_TAIL = 2
+
+
+def flat_layout(n: int, sh_degree: int):
+    """[(plane, floats per Gaussian, offset in floats)] of the flat buffer
+    for a map of n Gaussians, and its total length in floats (tail
+    included).  sh_rest is absent (0 floats) at SH degree 0."""
+    out, off = [], 0
+    for name, k in FLAT_PLANES:
+        if name == "sh_rest" and sh_degree == 0:
+            k = 0
+        out.append((name, k, off))
+        off += k * n
+    return out, off + FLAT_TAIL
+
+
 def shard_views(n_views: int, rank: int, world: int) -> list[int]:
     """Round-robin view assignment: rank r gets r, r + world, ..."""
     return list(range(rank, n_views, world))

@@ -131,11 +131,13 @@ class MappingEngine:
                                   pin_memory=True)
         self._pdev = torch.zeros(self._pbytes, dtype=torch.uint8, device=self.dev)
         self.use_graph = False
+        self._mv_unchecked = False
 
     def enable_graph(self, on: bool = True):
-        """Replay the iteration body from a captured CUDA graph (one per
-        target buffer); buffers reallocated by densify or capacity growth
-        drop the captures."""
+        """Replay the iteration body from ONE captured CUDA graph (the step's
+        target is copied into target_buffer(), the camera and Adam values
+        into a device parameter block); buffers reallocated by densify or
+        capacity growth drop the capture."""
         self.use_graph = on
         self._graphs.clear()
 
@@ -181,6 +183,9 @@ class MappingEngine:
         self.dsum = torch.zeros(_lib.SS_REDUCE_DOUBLES, dtype=torch.float64, device=dev)
         self.loss_ws = torch.empty(int(lib().ss_loss_workspace_bytes(self.H, self.W)),
                                    dtype=torch.uint8, device=dev)
+        if getattr(self, "_tgt_buf", None) is None:
+            self._tgt_buf = torch.zeros((self.H, self.W, 3), **f32)
+            self._tdep_buf = None
         self._flat = None
 
     def _alloc_pair_buffers(self, cap):
@@ -317,17 +322,40 @@ class MappingEngine:
                               P(self.status), stream_handle()), "ss_chain_adam")
         self._mark("chain_adam")
 
+    def target_buffer(self, depth: bool = False) -> torch.Tensor:
+        """The engine's fixed keyframe-target buffer ((H, W, 3), or (H, W)
+        for the depth target) that the captured graph reads.  step() copies
+        its target here (stream-ordered, device to device) unless the caller
+        passes this buffer itself, so every keyframe shares ONE graph."""
+        if depth:
+            if self._tdep_buf is None:
+                self._tdep_buf = torch.zeros((self.H, self.W), dtype=torch.float32,
+                                             device=self.dev)
+            return self._tdep_buf
+        return self._tgt_buf
+
+    def _stage_target(self, rec: StepRecord):
+        tgt = self.target_buffer()
+        if rec.target.data_ptr() != tgt.data_ptr():
+            tgt.copy_(rec.target.reshape(tgt.shape), non_blocking=True)
+        tdep = None
+        if rec.target_depth is not None:
+            tdep = self.target_buffer(depth=True)
+            if rec.target_depth.data_ptr() != tdep.data_ptr():
+                tdep.copy_(rec.target_depth.reshape(tdep.shape), non_blocking=True)
+        return tgt, tdep
+
     def _run(self, rec: StepRecord):
         self._stage_params(rec)
         if self.use_graph and self.profile is None:
-            key = (rec.target.data_ptr(),
-                   rec.target_depth.data_ptr() if rec.target_depth is not None else 0)
+            tgt, tdep = self._stage_target(rec)
+            key = tdep is not None
             g = self._graphs.get(key)
             if g is None:
                 torch.cuda.synchronize()
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
-                    self._body(rec.camera, rec.target, rec.target_depth)
+                    self._body(rec.camera, tgt, tdep)
                 self._graphs[key] = g
             g.replay()
         else:
@@ -358,8 +386,12 @@ class MappingEngine:
             self._records.pop(0)
 
     def _check_errors(self, row):
-        if int(row[_lib.ST_BAD_PARAM]) < len(self.gmap) and row[_lib.ST_BAD_PARAM] < 2 ** 62:
+        """Raise the reference's error for a status row (api.py:127-129,
+        core.py:225-229, optimizer.py:111-113)."""
+        if row[_lib.ST_BAD_PARAM] < 2 ** 62:
             raise ValueError(f"non-finite parameter in primitive {int(row[_lib.ST_BAD_PARAM])}")
+        if row[_lib.ST_ZERO_QUAT] < 2 ** 62:
+            raise ValueError("zero-norm quaternion in map")
         if row[_lib.ST_BAD_GRAD] < 2 ** 62:
             raise FloatingPointError("non-finite gradient (primitive "
                                      f"{int(row[_lib.ST_BAD_GRAD])})")
@@ -389,6 +421,10 @@ class MappingEngine:
 
     def synchronize(self):
         self._drain(0)
+        if self._mv_unchecked:
+            # the last keyframe-batch step's Adam may have reported errors
+            self._mv_unchecked = False
+            self._check_errors(self.status.cpu().numpy())
 
     def losses(self):
         """(iteration, total loss, rendered loss) of every consumed step."""
@@ -398,23 +434,31 @@ class MappingEngine:
     def last_pair_count(self) -> int:
         return int(self.status[_lib.ST_PAIRS].item())
 
-    def fit_capacity(self, camera, margin: float | None = None):
-        """Size the pair buffers for `camera` (one binning + sync, no update)."""
-        cam = Camera.of(camera)
+    def fit_capacity(self, cameras, margin: float | None = None):
+        """Size the pair buffers for a camera or a list of cameras (one
+        binning per camera + one sync, no update).  Only grows the buffers;
+        returns the largest pair count seen."""
+        cams = cameras if isinstance(cameras, (list, tuple)) else [cameras]
         L = lib()
         s = stream_handle()
-        mp, cm, op = self.gmap.ss(), cam.to_ss(), self.opts.to_ss()
-        st = torch.empty(_lib.STATUS_WORDS, dtype=torch.int64, device=self.dev)
-        check(L.ss_status_reset(P(st), s), "ss_status_reset")
-        check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), None, ctypes.byref(op),
-                              ctypes.byref(self.splats.ss()), P(st), s), "ss_preprocess")
+        mp, op = self.gmap.ss(), self.opts.to_ss()
         tiny = BinBuffers.alloc(0, self.n_tiles, self.dev)
         ws = bin_workspace(len(self.gmap), 0, self.n_tiles, self.dev)
-        check(L.ss_bin_sort(len(self.gmap), ctypes.byref(self.splats.ss()), ctypes.byref(cm),
-                            ctypes.byref(tiny.ss()), P(ws), ws.numel(), P(st), s), "ss_bin_sort")
-        p = int(st[_lib.ST_PAIRS].item())
+        sts = torch.empty((len(cams), _lib.STATUS_WORDS), dtype=torch.int64, device=self.dev)
+        for k, camera in enumerate(cams):
+            cm = Camera.of(camera).to_ss()
+            st = sts[k]
+            check(L.ss_status_reset(P(st), s), "ss_status_reset")
+            check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), None, ctypes.byref(op),
+                                  ctypes.byref(self.splats.ss()), P(st), s), "ss_preprocess")
+            check(L.ss_bin_sort(len(self.gmap), ctypes.byref(self.splats.ss()),
+                                ctypes.byref(cm), ctypes.byref(tiny.ss()), P(ws), ws.numel(),
+                                P(st), s), "ss_bin_sort")
+        p = int(sts[:, _lib.ST_PAIRS].max().item()) if cams else 0
         m = self.cfg.pair_margin if margin is None else margin
-        self._alloc_pair_buffers(int(p * m) + 4096)
+        want = int(p * m) + 4096
+        if want > self._cap:
+            self._alloc_pair_buffers(want)
         return p
 
     # ------------------------------------------------- densify / reset (K10)
@@ -449,6 +493,9 @@ class MappingEngine:
                                 extra_planes=planes)
         self.state.m, self.state.v = new_m, new_v
         self.since_densify = 0
+        # the map planes and the Adam moments are new tensors whatever the
+        # count: captured graphs would replay into freed memory
+        self._graphs.clear()
         if len(self.gmap) != n:
             self._alloc_map_buffers()
             self._alloc_pair_buffers(max(self._cap * len(self.gmap) // max(n, 1), 4096))
@@ -477,19 +524,17 @@ class MappingEngine:
 
     # ------------------------------------------------------- multi-view
     def _flat_grads(self):
+        """The flat per-Gaussian buffer of a keyframe-batch step (layout:
+        distributed.flat_layout) and its ss_param_grads view."""
+        from .distributed import flat_layout
         n = len(self.gmap)
-        rest = 45 if self.opts.sh_degree > 0 else 0
         if self._flat is None or self._flat_n != n:
-            per = 3 + 4 + 3 + 1 + 3 + rest + 1 + 1 + 3 + 1
-            self._flat = torch.zeros(per * max(n, 1), dtype=torch.float32, device=self.dev)
+            layout, total = flat_layout(max(n, 1), self.opts.sh_degree)
+            self._flat = torch.zeros(total, dtype=torch.float32, device=self.dev)
             self._flat_n = n
-            views, off = {}, 0
-            for name, k in (("position", 3), ("rotation", 4), ("log_scale", 3), ("opacity", 1),
-                            ("sh_dc", 3), ("sh_rest", rest), ("pos2d", 1), ("stat_g2d", 1),
-                            ("stat_g3d", 3), ("stat_cnt", 1)):
-                views[name] = self._flat[off * n:(off + k) * n]
-                off += k
+            views = {name: self._flat[off:off + k * max(n, 1)] for name, k, off in layout}
             self._fv = views
+            self._flat_tail = self._flat[total - 2:]
             g = _lib.SSParamGrads()
             g.d_position, g.d_rotation = P(views["position"]), P(views["rotation"])
             g.d_log_scale, g.d_opacity = P(views["log_scale"]), P(views["opacity"])
@@ -499,61 +544,78 @@ class MappingEngine:
                                                         P(views["stat_g3d"]),
                                                         P(views["stat_cnt"]))
             self._fss = g
+            self._mv_host = torch.zeros(_lib.STATUS_WORDS + 1, dtype=torch.int64,
+                                        pin_memory=True)
         return self._flat, self._fss
 
     def multiview_step(self, cameras, targets, target_depths=None, allreduce=None,
                        add_reg: bool = True):
-        """Keyframe batch: sum of per-view gradients (+ the opacity-reg
-        gradient once), optional all-reduce of the flat buffer, then Adam and
-        the statistics update.  Reads the overflow status once per step on one
-        GPU (once per view when an all-reduce follows: every rank must redo a
-        view before the collective)."""
+        """Keyframe batch: the sum of per-view gradients
+        (+ the opacity-reg gradient once, add_reg on one rank), an optional
+        all-reduce of the flat buffer, then Adam and the statistics update.
+
+        Every view is enqueued without a host sync.  ss_status_flags writes
+        this rank's overflow / error flags into the buffer's tail, so after
+        the (optional) all-reduce ONE host read tells every rank whether any
+        rank overflowed its pair buffers -- then all ranks redo the step
+        together with grown buffers (nothing was applied yet) -- or hit an
+        error -- then every rank raises before Adam touches the map."""
         self._maybe_densify()
+        # pending single-view steps apply first, in order (errors of the last
+        # batch step's Adam are sticky: this step's status read raises them)
+        self._drain(0)
         L = lib()
         s = stream_handle()
         n = len(self.gmap)
         flat, fss = self._flat_grads()
         lon = float(self.cfg.lambda_o / n) if (n and add_reg) else 0.0
-
-        def chain(v, mp, cm, op):
-            check(L.ss_chain_backward(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op),
-                                      P(self.g2d), P(self.splats.flags), P(self.contributed),
-                                      lon if v == 0 else 0.0,
-                                      _lib.SS_CHAIN_ACCUMULATE | _lib.SS_CHAIN_STAT_PLANES,
-                                      ctypes.byref(fss), P(self.status), s), "ss_chain_backward")
-
         views = [(Camera.of(c), t, target_depths[v] if target_depths is not None else None)
                  for v, (c, t) in enumerate(zip(cameras, targets))]
-        losses = None
-        if allreduce is None:
-            # one GPU: every view enqueued without a host sync, then one read
-            # of the (sticky) overflow word; on overflow the step is redone
-            # view by view below (nothing has been applied yet)
-            flat.zero_()
-            losses = []
-            for v, (cam, tgt, td) in enumerate(views):
-                mp, cm, op = self._forward_backward(cam, tgt, td, v)
-                chain(v, mp, cm, op)
-                losses.append(self.sums[:2].clone())
-            if int(self.status[_lib.ST_OVERFLOW].item()):
-                check(L.ss_status_reset(P(self.status), s), "ss_status_reset")
-                losses = None
-        if losses is None:
+
+        def run_views(sync_each: bool):
             flat.zero_()
             losses = []
             for v, (cam, tgt, td) in enumerate(views):
                 while True:
                     mp, cm, op = self._forward_backward(cam, tgt, td, v)
-                    sh = self.status.cpu()
-                    if not int(sh[_lib.ST_OVERFLOW]):
+                    if not sync_each:
                         break
-                    self._alloc_pair_buffers(
-                        int(int(sh[_lib.ST_PAIRS]) * self.cfg.pair_margin) + 4096)
+                    row = self.status.cpu().numpy()
+                    if not int(row[_lib.ST_OVERFLOW]):
+                        break
+                    # redo path: grow to this view's pair count, run it again
+                    self._alloc_pair_buffers(max(
+                        self._cap, int(int(row[_lib.ST_PAIRS]) * self.cfg.pair_margin) + 4096))
                     check(L.ss_status_reset(P(self.status), s), "ss_status_reset")
-                chain(v, mp, cm, op)
+                check(L.ss_chain_backward(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op),
+                                          P(self.g2d), P(self.splats.flags),
+                                          P(self.contributed), lon if v == 0 else 0.0,
+                                          _lib.SS_CHAIN_ACCUMULATE | _lib.SS_CHAIN_STAT_PLANES,
+                                          ctypes.byref(fss), P(self.status), s),
+                      "ss_chain_backward")
                 losses.append(self.sums[:2].clone())
-        if allreduce is not None:
-            allreduce(flat)
+            check(L.ss_status_flags(P(self.status), P(self._flat_tail), s), "ss_status_flags")
+            if allreduce is not None:
+                allreduce(flat)
+            # one host read: this rank's status row + the (reduced) flags
+            h = self._mv_host
+            h[:_lib.STATUS_WORDS].copy_(self.status, non_blocking=True)
+            h[_lib.STATUS_WORDS:].view(torch.float32).copy_(self._flat_tail, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            row = h[:_lib.STATUS_WORDS].numpy().copy()
+            flags = h[_lib.STATUS_WORDS:].view(torch.float32).numpy().copy()
+            return losses, row, flags
+
+        losses, row, flags = run_views(sync_each=False)
+        if flags[0] > 0:
+            # some rank overflowed: every rank redoes the step, view by view
+            # with a read per view (the rare path), so the collectives match
+            check(L.ss_status_reset(P(self.status), s), "ss_status_reset")
+            losses, row, flags = run_views(sync_each=True)
+        if flags[1] > 0:
+            self._check_errors(row)
+            raise FloatingPointError("non-finite value reported by another rank of the "
+                                     "keyframe-sharded step")
         self.state.step_count += 1
         hp = self.state.hparams(self.opts.sh_degree > 0)
         mp = self.gmap.ss()
@@ -563,6 +625,7 @@ class MappingEngine:
                              P(self.status), s), "ss_adam_step")
         check(L.ss_apply_stat_planes(ctypes.byref(mp), ctypes.byref(fss), s),
               "ss_apply_stat_planes")
+        self._mv_unchecked = True
         self.iteration += 1
         self.since_densify += 1
         return losses

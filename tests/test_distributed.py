@@ -1,10 +1,14 @@
 """Keyframe-sharded step on CPU: world_size 2 over gloo.
 
-Each rank computes the oracle gradients of its shard of the views into the
-engine's flat layout, the buffers are all-reduced, and every rank applies
-the same Adam step.  Checks: the reduced buffer equals the single-process
-sum over all views (the builder-defined batch oracle, A17), and the
-replicas are byte-identical after the update.
+The product's ShardedMapper drives an oracle-backed engine double through
+one keyframe-batch step: each rank sums the oracle gradients of its shard
+of the views into the product's flat layout (distributed.flat_layout), the
+buffers are all-reduced, and every rank applies the same Adam step.
+Checks: the reduced buffer equals the single-process sum over all views
+(the builder-defined batch oracle, A17), the update equals one oracle
+adam_step on that sum, and the replicas are byte-identical afterwards.
+The CUDA engine's own multi-rank step is covered on the GPU
+(tests/test_gpu_engine.py, world 2 over gloo).
 """
 
 import os
@@ -28,15 +32,36 @@ def _free_port():
     return p
 
 
-def _flat(g, contributed_views):
-    """Oracle grads of one view -> the engine's flat layout (SH degree 0):
-    position 3N | rotation 4N | log_scale 3N | opacity N | sh_dc 3N |
-    pos2d N | stat_g2d N | stat_g3d 3N | stat_cnt N."""
-    seen = contributed_views.astype(np.float64)
-    parts = [g.position.reshape(-1), g.rotation.reshape(-1), g.log_scale.reshape(-1),
-             g.opacity_logit.reshape(-1), g.sh[:, 0, :].reshape(-1), g.pos2d_grad_norm,
-             g.pos2d_grad_norm * seen, (g.position * seen[:, None]).reshape(-1), seen]
-    return np.concatenate(parts)
+def _flat(g, seen_mask, sh_degree=0):
+    """Oracle grads of one view -> the engine's flat buffer, laid out by the
+    product's own distributed.flat_layout (the layout MappingEngine uses)."""
+    from paper_2410_00486_b200.distributed import flat_layout
+    n = len(g)
+    seen = seen_mask.astype(np.float64)
+    planes = {"position": g.position, "rotation": g.rotation, "log_scale": g.log_scale,
+              "opacity": g.opacity_logit, "sh_dc": g.sh[:, 0, :], "sh_rest": g.sh[:, 1:, :],
+              "pos2d": g.pos2d_grad_norm, "stat_g2d": g.pos2d_grad_norm * seen,
+              "stat_g3d": g.position * seen[:, None], "stat_cnt": seen}
+    layout, total = flat_layout(n, sh_degree)
+    out = np.zeros(total)
+    for name, k, off in layout:
+        if k:
+            out[off:off + k * n] = np.asarray(planes[name], np.float64).reshape(-1)
+    return out
+
+
+def _unflat(orc, buf, n, sh_degree=0):
+    from paper_2410_00486_b200.distributed import flat_layout
+    layout, _ = flat_layout(n, sh_degree)
+    v = {name: buf[off:off + k * n] for name, k, off in layout}
+    sh = np.zeros((n, 16, 3))
+    sh[:, 0, :] = v["sh_dc"].reshape(n, 3)
+    if sh_degree:
+        sh[:, 1:, :] = v["sh_rest"].reshape(n, 15, 3)
+    g = orc.OGrads(v["position"].reshape(n, 3), v["rotation"].reshape(n, 4),
+                   v["log_scale"].reshape(n, 3), v["opacity"].copy(), sh, v["pos2d"].copy(),
+                   v["stat_cnt"] > 0)
+    return g, v
 
 
 def _scene():
@@ -60,39 +85,78 @@ def _view_flat(orc, om, cam, tgt, add_reg):
     return _flat(g, r.contributed), g
 
 
+class OracleEngine:
+    """Test double with MappingEngine.multiview_step's contract, computing
+    with the CPU oracle (no GPU here): per-view grads summed into the flat
+    buffer (the product's layout), the tail flags, the all-reduce hook, then
+    Adam and the statistics update from the reduced buffer -- so the real
+    ShardedMapper drives it exactly as it drives the CUDA engine."""
+
+    def __init__(self, orc, om):
+        self.orc, self.gmap = orc, om
+        self.state = orc.OAdam.for_map(om)
+        self.reduced = None
+
+    def multiview_step(self, cams, tgts, tds=None, allreduce=None, add_reg=True):
+        orc, om = self.orc, self.gmap
+        n = len(om)
+        local = _flat(orc.OGrads(np.zeros((n, 3)), np.zeros((n, 4)), np.zeros((n, 3)),
+                                 np.zeros(n), np.zeros((n, 16, 3)), np.zeros(n),
+                                 np.zeros(n, bool)), np.zeros(n, bool))
+        for v, (c, t) in enumerate(zip(cams, tgts)):
+            local += _view_flat(orc, om, c, t, add_reg=(add_reg and v == 0))[0]
+        buf = torch.from_numpy(local).double()
+        if allreduce is not None:
+            allreduce(buf)
+        self.reduced = buf.numpy().copy()
+        assert self.reduced[-2:].tolist() == [0.0, 0.0]  # no rank overflowed or failed
+        g, v = _unflat(orc, self.reduced, n)
+        orc.adam(om, g, self.state)
+        seen = v["stat_cnt"] > 0
+        om.grad2d_accum += v["stat_g2d"]
+        om.grad3d_accum += v["stat_g3d"].reshape(n, 3)
+        om.obs_count += v["stat_cnt"].astype(np.int64)
+        assert np.all(v["stat_cnt"][~seen] == 0)
+        return []
+
+
 def _worker(rank, port, out_q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
-    from paper_2410_00486_b200.distributed import (allreduce_sum, checksums_agree,
-                                                   shard_views)
+    from paper_2410_00486_b200.distributed import ShardedMapper, checksums_agree, shard_views
     orc, om, cams, targets = _scene()
-    n = len(om)
-    mine = shard_views(N_VIEWS, rank, WORLD)
-    local = None
-    for v in mine:
-        f, _ = _view_flat(orc, om, cams[v], targets[v], add_reg=(v == 0))
-        local = f if local is None else local + f
-    buf = torch.from_numpy(local if local is not None else np.zeros(21 * n)).double()
-    allreduce_sum(buf)
-    reduced = buf.numpy()
-    # single-process oracle of the batch: sum of all views, reg added once
-    full = sum(_view_flat(orc, om, cams[v], targets[v], add_reg=(v == 0))[0]
-               for v in range(N_VIEWS))
-    err = float(np.abs(reduced - full).max() / max(np.abs(full).max(), 1e-30))
-    # identical Adam step on every rank from the reduced gradients
-    g = orc.OGrads(reduced[:3 * n].reshape(n, 3), reduced[3 * n:7 * n].reshape(n, 4),
-                   reduced[7 * n:10 * n].reshape(n, 3), reduced[10 * n:11 * n],
-                   np.concatenate([reduced[11 * n:14 * n].reshape(n, 1, 3),
-                                   np.zeros((n, 15, 3))], axis=1),
-                   reduced[14 * n:15 * n], reduced[20 * n:21 * n] > 0)
-    st = orc.OAdam.for_map(om)
-    orc.adam(om, g, st)
-    same = checksums_agree([om.positions, om.rotations, om.log_scales, om.opacity_logits, om.sh])
-    out_q.put((rank, err, same, mine))
+    eng = OracleEngine(orc, om.copy())
+    sm = ShardedMapper(eng)
+    assert (sm.rank, sm.world) == (rank, WORLD)
+    sm.step(cams, targets)
+    # single-process oracle of the batch (A17): every view's grads summed, the
+    # opacity-regulariser gradient once, one adam_step on the sum, and
+    # accumulate_grad_stats once per view (densify.py:86-100)
+    per_view = [_view_flat(orc, om, cams[v], targets[v], add_reg=(v == 0))
+                for v in range(N_VIEWS)]
+    full = sum(f for f, _ in per_view)
+    err = float(np.abs(eng.reduced - full).max() / max(np.abs(full).max(), 1e-30))
+    ref = om.copy()
+    g, _ = _unflat(orc, full, len(ref))
+    orc.adam(ref, g, orc.OAdam.for_map(ref))
+    for _, gv in per_view:
+        orc.accumulate_grad_stats(ref, gv)
+    post = eng.gmap
+    same_as_oracle = all(np.allclose(getattr(post, f), getattr(ref, f), rtol=0, atol=1e-12)
+                         for f in ("positions", "rotations", "log_scales", "opacity_logits",
+                                   "sh", "grad2d_accum", "grad3d_accum"))
+    same_as_oracle &= bool(np.array_equal(post.obs_count, ref.obs_count))
+    same = checksums_agree([post.positions, post.rotations, post.log_scales,
+                            post.opacity_logits, post.sh, post.grad2d_accum, post.obs_count])
+    out_q.put((rank, err, same, shard_views(N_VIEWS, rank, WORLD), same_as_oracle))
     dist.destroy_process_group()
 
 
-def test_sharded_allreduce_equals_batch_oracle_and_replicas_agree():
+def test_sharded_mapper_equals_batch_oracle_and_replicas_agree():
+    """ShardedMapper over gloo (world 2) with the product's flat layout: the
+    reduced buffer equals the single-process sum over all views, the update
+    equals one oracle adam_step + accumulate_grad_stats on that sum, and the
+    two replicas are byte-identical afterwards."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -105,9 +169,22 @@ def test_sharded_allreduce_equals_batch_oracle_and_replicas_agree():
         assert p.exitcode == 0
     res.sort()
     assert [r[3] for r in res] == [[0, 2], [1]]
-    for rank, err, same, _ in res:
+    for rank, err, same, _, ok in res:
         assert err < 1e-12, (rank, err)
         assert same, rank
+        assert ok, rank
+
+
+def test_flat_layout_matches_engine_planes():
+    """The layout is plane-major with the 2-float flag tail; SH rest only
+    above degree 0."""
+    from paper_2410_00486_b200.distributed import FLAT_TAIL, flat_layout
+    lay0, t0 = flat_layout(10, 0)
+    lay3, t3 = flat_layout(10, 3)
+    assert t0 == 10 * 20 + FLAT_TAIL and t3 == 10 * 65 + FLAT_TAIL
+    offs = [off for _, _, off in lay3]
+    assert offs == sorted(offs) and offs[0] == 0
+    assert dict((nm, k) for nm, k, _ in lay0)["sh_rest"] == 0
 
 
 @pytest.mark.parametrize("n_views,world", [(8, 1), (8, 2), (8, 4), (8, 8), (3, 4)])
