@@ -3,12 +3,22 @@
 
     python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
 
-One process per GPU (torchrun for N > 1, NCCL).  N = 1: the fused single-
-view iteration (MappingEngine.step).  N > 1: keyframe sharding -- every
-rank renders and back-propagates its own view of the replicated map, the
-flat per-Gaussian gradient buffer is summed with one NCCL all-reduce, and
-every rank applies the identical Adam step (weak scaling: one view per
-GPU per step; value = views * steps / time, all ranks).
+One process per GPU.  ``--gpus N`` with N > 1 starts the N ranks itself
+(an exec of torch.distributed.run, 127.0.0.1 rendezvous) unless it already
+runs under torchrun; ranks talk over NCCL (NCCL_DEBUG=INFO init lines go to
+stderr, so the communicator's nranks can be checked).
+
+* N = 1: BASELINE configs[1], S(300k), 1200x680, SH0, one view per step,
+  the fused single-view iteration (MappingEngine.step, one CUDA graph).
+  The line also carries a ``converged`` block (iterations 251-270 of the
+  same training run, device-timed and end to end) and a ``config4`` block
+  (BASELINE configs[3] on this one GPU: S(1M), a fixed batch of 8 views
+  per step), the N = 1 point of the scaling curve below.
+* N > 1: BASELINE configs[3], S(1M), 1200x680, a FIXED keyframe batch of
+  8 views per step sharded over the N ranks (rank r renders views r, r+N,
+  ...), the flat per-Gaussian gradient buffer summed with one NCCL
+  all-reduce, the identical Adam step on every rank (strong scaling;
+  value = batch steps/s of the whole job, time = max over ranks).
 
 ``--impl reference`` times the reference's CPU implementation of the path
 as restated in oracle/ (float64, all host threads; the reference itself is
@@ -20,6 +30,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -31,6 +42,7 @@ sys.path.insert(0, REPO)
 
 METRIC = "mapping iters/sec (fwd+bwd+Adam) at 1200×680, 300k Gaussians; HBM GB/s"
 WORKLOAD = dict(n=300_000, width=1200, height=680, sh_degree=0)
+BATCH = dict(n=1_000_000, width=1200, height=680, sh_degree=0, views=8)
 
 
 def _args():
@@ -44,8 +56,40 @@ def _args():
     ap.add_argument("--height", type=int, default=WORKLOAD["height"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-converged", action="store_true")
+    ap.add_argument("--no-config4", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)
     return ap.parse_args()
+
+
+def single_workload(args):
+    return (f"replica-shaped S({args.n}, {args.width}x{args.height}) SH0, single view "
+            "(BASELINE configs[1])")
+
+
+def batch_workload(world):
+    return (f"large map S({BATCH['n']}, {BATCH['width']}x{BATCH['height']}) SH0, fixed "
+            f"keyframe batch of {BATCH['views']} views per step sharded over {world} GPU(s), "
+            "NCCL all-reduce of the per-Gaussian gradients (BASELINE configs[3])")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(args):
+    """--gpus N outside torchrun: become torch.distributed.run with N ranks."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execvpe(sys.executable, cmd, env)
 
 
 # ------------------------------------------------------------------ clocks
@@ -139,11 +183,6 @@ def ncu_stats(kernel):
         return {}
 
 
-def ncu_traffic(kernel):
-    """dram read+write bytes per launch of `kernel` (ncu), else None."""
-    return ncu_stats(kernel).get("dram_bytes")
-
-
 def load_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -153,31 +192,37 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.lower().startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or platform.machine()
+
+
 # --------------------------------------------------------------- CPU oracle
-def cpu_iteration_setup(args):
-    import numpy as np
-
+def _oracle_scene(n, seed):
     import oracle as orc
-    from paper_2410_00486_b200.scene import survey_camera, survey_scene
-    sc = survey_scene(args.n, 0)
-    cam = survey_camera(args.width, args.height)
-    om = orc.OMap(sc.positions, sc.rotations, sc.log_scales, sc.opacity_logits, sc.sh)
-    return orc, om, cam, np
-
-
-def cpu_target(args, orc, cam):
     from paper_2410_00486_b200.scene import survey_scene
-    tsc = survey_scene(args.n, 100)
-    tm = orc.OMap(tsc.positions, tsc.rotations, tsc.log_scales, tsc.opacity_logits, tsc.sh)
-    return orc.rasterize(tm, cam, sh_degree=0, with_checkpoints=False).image
+    sc = survey_scene(n, seed)
+    return orc.OMap(sc.positions, sc.rotations, sc.log_scales, sc.opacity_logits, sc.sh)
 
 
-def run_cpu_iterations(args, max_iters, budget_s):
-    """Oracle train_one sequence (trainer.py:199-208) in float64, all threads."""
-    orc, om, cam, np = cpu_iteration_setup(args)
-    threads = os.cpu_count() or 1
+def run_cpu_iterations(args, max_iters, budget_s, threads=None):
+    """Oracle train_one sequence (trainer.py:199-208) in float64 on the
+    single-view workload."""
+    import oracle as orc
+    from paper_2410_00486_b200.scene import survey_camera
+    threads = threads or os.cpu_count() or 1
     orc.set_threads(threads)
-    target = cpu_target(args, orc, cam)
+    cam = survey_camera(args.width, args.height)
+    om = _oracle_scene(args.n, 0)
+    target = orc.rasterize(_oracle_scene(args.n, 100), cam, sh_degree=0,
+                           with_checkpoints=False).image
     st = orc.OAdam.for_map(om)
     times = []
     t_all = time.perf_counter()
@@ -190,152 +235,185 @@ def run_cpu_iterations(args, max_iters, budget_s):
     return times, threads
 
 
+def run_cpu_batch_steps(max_steps, budget_s):
+    """Oracle keyframe-batch step (A17): sum over the 8 views of the
+    per-view train_one gradients, one adam_step, per-view grad stats."""
+    import oracle as orc
+    from paper_2410_00486_b200.scene import survey_camera
+    threads = os.cpu_count() or 1
+    orc.set_threads(threads)
+    V = BATCH["views"]
+    cams = [survey_camera(BATCH["width"], BATCH["height"], v, V) for v in range(V)]
+    om = _oracle_scene(BATCH["n"], 0)
+    tm = _oracle_scene(BATCH["n"], 100)
+    targets = [orc.rasterize(tm, c, sh_degree=0, with_checkpoints=False).image for c in cams]
+    st = orc.OAdam.for_map(om)
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < max_steps:
+        t0 = time.perf_counter()
+        total = None
+        per = []
+        for v, (c, t) in enumerate(zip(cams, targets)):
+            r = orc.rasterize(om, c, sh_degree=0)
+            lb = orc.losses(r.image, t, om.opacity_logits)
+            g = orc.chain(om, c, r.proj, orc.backward_splat(r, lb.grad_image), r.contributed)
+            per.append(g)
+            if v == 0:
+                g.opacity_logit = g.opacity_logit + lb.grad_opacity_logit
+            total = g if total is None else total + g
+        orc.adam(om, total, st)
+        for g in per:
+            orc.accumulate_grad_stats(om, g)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > budget_s:
+            break
+    return times, threads
+
+
 def reference_arm(args, rank, world):
     if rank != 0:
         return 0
-    import platform
-    warm = min(args.warmup, 1)
-    times, threads = run_cpu_iterations(args, warm + args.steps, budget_s=150.0)
+    # the GPU arm's warm-up count (one batch step at N > 1: ~30 s each on the CPU)
+    warm = max(args.warmup, 3) if world == 1 else 1
+    if world > 1:
+        times, threads = run_cpu_batch_steps(warm + args.steps, budget_s=170.0)
+        workload, unit = batch_workload(world), "it/s"
+        sample = "oracle keyframe-batch steps (8 views of S(1M) each, float64)"
+    else:
+        times, threads = run_cpu_iterations(args, warm + args.steps, budget_s=150.0)
+        workload, unit = single_workload(args), "it/s"
+        sample = "full float64 train_one iterations of the oracle restatement (oracle/)"
     timed = times[warm:] if len(times) > warm else times
     it_s = len(timed) / sum(timed)
     line = {
-        "impl": "reference", "metric": METRIC, "value": it_s, "unit": "it/s",
-        "n_gpus": args.gpus, "steps": len(timed), "warmup": warm,
+        "impl": "reference", "metric": METRIC, "value": it_s, "unit": unit,
+        "n_gpus": world, "steps": len(timed), "warmup": len(times) - len(timed),
         "ms_per_step": 1000.0 * sum(timed) / len(timed), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"replica-shaped S({args.n},{args.width}x{args.height}) SH0 "
-                               "single view (BASELINE configs[1])", "gaussians": args.n,
-                   "image": [args.width, args.height], "sh_degree": 0},
-        "cpu_baseline": {"value": it_s, "unit": "it/s", "cores": threads, "kind": "port",
-                         "sample": f"{len(timed)} full float64 iterations of the oracle "
-                                   f"restatement (oracle/, {threads} OpenMP threads, "
-                                   f"host {platform.processor() or platform.machine()}); "
-                                   f"requested {args.steps}, capped at 150 s"},
-        "e2e": {"value": it_s, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": workload},
+        "cpu_baseline": {"value": it_s, "unit": unit, "cores": threads, "kind": "port",
+                         "sample": f"{len(timed)} timed {sample}, {threads} OpenMP threads on "
+                                   f"'{cpu_model()}' ({len(times) - len(timed)} untimed "
+                                   f"warm-up); requested {args.steps}, capped by a time "
+                                   "budget"},
+        "e2e": {"value": it_s, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
 # --------------------------------------------------------------- GPU arm
-def main():
-    args = _args()
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        return reference_arm(args, rank, world)
+class Timer:
+    """Device time of each step (CUDA events on the launching stream), L2
+    flushed between steps by a 256 MB write outside the events."""
 
-    import numpy as np
-    import torch
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    def __init__(self, torch):
+        self.torch = torch
+        self.flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    import paper_2410_00486_b200 as ss
-    from paper_2410_00486_b200.scene import survey_camera, survey_scene
+    def run(self, step, k):
+        torch = self.torch
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        for i in range(k):
+            self.flush.fill_(float(i))
+            starts[i].record()
+            step()
+            ends[i].record()
+        torch.cuda.synchronize()
+        return [s.elapsed_time(e) for s, e in zip(starts, ends)]
 
-    W, H, N = args.width, args.height, args.n
-    sc = survey_scene(N, 0)
-    opts = ss.RasterOpts(sh_degree=0)
-    gmap = ss.GaussianMap.from_scene(sc)
-    views = max(world, 1)
-    cams = [survey_camera(W, H, v, views) for v in range(views)]
-    # targets: render of S(N, seed+100) from each view (rendered
-    # on the GPU here -- the oracle takes seconds per 300k render)
-    tmap = ss.GaussianMap.from_scene(survey_scene(N, 100))
-    targets = [ss.rasterize_forward(tmap, c, opts).image.clone() for c in cams]
-    del tmap
-    eng = ss.MappingEngine(gmap, W, H, opts)
-    pcount = eng.fit_capacity(cams[rank % views])
-    if world == 1:
-        eng.enable_graph()  # the whole iteration is replayed as one CUDA graph
-    my_cam, my_tgt = cams[rank % views], targets[rank % views]
-    # the device-timed steps read the target from the engine's own buffer (the
-    # one its captured graph reads); the e2e run below passes host-uploaded
-    # buffers, which step() copies there
-    eng.target_buffer().copy_(my_tgt)
 
-    from paper_2410_00486_b200.distributed import ShardedMapper
-    sharded = ShardedMapper(eng, rank, world) if world > 1 else None
+def snapshot_state(eng):
+    return ([getattr(eng.gmap, f).clone() for f in eng.gmap.FIELDS],
+            {k: t.clone() for k, t in eng.state.m.items()},
+            {k: t.clone() for k, t in eng.state.v.items()}, eng.state.step_count, eng.iteration)
 
-    def one_step():
-        if sharded is not None:
-            sharded.step(cams, targets)  # one view per rank, one NCCL all-reduce
-        else:
-            eng.step(my_cam, eng.target_buffer())
 
-    # L2 flush buffer (> 126 MB L2), written between timed steps
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    for _ in range(max(args.warmup, 3)):
-        one_step()
-    eng.synchronize() if world == 1 else torch.cuda.synchronize()
+def restore_state(eng, snap):
+    """In place, so captured graph pointers stay valid."""
+    eng.synchronize()
+    for f, t in zip(eng.gmap.FIELDS, snap[0]):
+        getattr(eng.gmap, f).copy_(t)
+    for k, t in snap[1].items():
+        eng.state.m[k].copy_(t)
+    for k, t in snap[2].items():
+        eng.state.v[k].copy_(t)
+    eng.state.step_count = snap[3]
+    eng.iteration = snap[4]
 
-    # parameters + Adam state after warm-up: the e2e run below restores them
-    # in place (graph pointers stay valid) so it times the same iterations
-    # as the device-timed run -- the per-iteration cost drifts as training
-    # lowers opacities (profiles/r01_training_drift.txt)
-    snap = None
-    if world == 1:
-        snap = ([getattr(eng.gmap, f).clone() for f in eng.gmap.FIELDS],
-                {k: t.clone() for k, t in eng.state.m.items()},
-                {k: t.clone() for k, t in eng.state.v.items()}, eng.state.step_count)
 
-    # ---- timed region: per-step CUDA events, L2 flushed between steps
-    sampler = ClockSampler(local)
-    if dist is not None:
-        dist.barrier()
+def e2e_single(torch, eng, cam, tgt, steps):
+    """The public API call a user makes per keyframe iteration, with host
+    buffers: the target uploaded from pinned host memory each step (copy
+    stream, double-buffered so the upload of step k+1 overlaps step k) and
+    the step's loss/status snapshot read back (wall clock)."""
+    host_tgt = tgt.cpu().pin_memory()
+    bufs = [torch.empty_like(tgt), torch.empty_like(tgt)]
+    copy_stream = torch.cuda.Stream()
+    uploaded = [torch.cuda.Event(), torch.cuda.Event()]
+    consumed = [torch.cuda.Event(), torch.cuda.Event()]
+    main = torch.cuda.current_stream()
+
+    def upload(k):
+        b = k % 2
+        with torch.cuda.stream(copy_stream):
+            copy_stream.wait_event(consumed[b])
+            bufs[b].copy_(host_tgt, non_blocking=True)
+            uploaded[b].record(copy_stream)
+
+    def step(k):
+        b = k % 2
+        main.wait_event(uploaded[b])
+        eng.step(cam, bufs[b])
+        consumed[b].record(main)
+        upload(k + 2)
+
+    for b in range(2):
+        consumed[b].record(main)
+    upload(0)
+    upload(1)
+    eng.synchronize()
     torch.cuda.synchronize()
-    sampler.start()
-    launches0 = eng.launches
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    for k in range(args.steps):
-        flush.fill_(float(k))
-        starts[k].record()
-        one_step()
-        ends[k].record()
-    torch.cuda.synchronize()
-    clocks = sampler.stop()
-    if world == 1:
-        eng.synchronize()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = sum(step_ms)
-    launches = eng.launches - launches0
-    if dist is not None:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    value = views * args.steps / (total_ms / 1000.0)
+    t0 = time.perf_counter()
+    for k in range(steps):
+        step(k)
+    eng.synchronize()  # every step's loss is on the host
+    wall = time.perf_counter() - t0
+    copy_stream.synchronize()
+    return {"value": steps / wall, "unit": "it/s", "steps": steps,
+            "h2d_bytes_per_step": int(host_tgt.numel() * 4),
+            "d2h_bytes_per_step": int(eng._host.shape[1] * 8),
+            "timing": "wall clock over the same iterations as the device-timed value (state "
+                      "restored), pinned host target upload per step (copy stream, "
+                      "double-buffered) + per-step loss/status read back"}
 
-    # ---- per-kernel timing (instrumented steps, outside the timed region)
+
+def stage_times(torch, eng, step, k=5):
+    """Per-stage device times from instrumented (event-bracketed, non-graph)
+    steps, outside any timed region."""
     eng.profile = []
-    prof_steps = 5
-    for _ in range(prof_steps):
-        one_step()
+    for _ in range(k):
+        step()
     torch.cuda.synchronize()
+    prof, eng.profile = eng.profile, None
     stages = {}
-    prof = eng.profile
-    eng.profile = None
     for (a, ea), (b, eb) in zip(prof[:-1], prof[1:]):
         if b == "begin":
             continue
         stages.setdefault(b, []).append(ea.elapsed_time(eb))
-    stage_ms = {k: sum(v) / len(v) for k, v in stages.items()}
+    return {k: sum(v) / len(v) for k, v in stages.items()}
 
-    # ---- workload statistics for the algorithmic-byte model
+
+def roofline(torch, eng, stage_ms, n):
     st = eng.status.cpu().numpy()
-    P = int(st[3])
-    U = int(st[5])  # backward work units (64 list positions)
-    M = int(st[6])
+    P, U, M = int(st[3]), int(st[5]), int(st[6])
     E = int(eng.k_eff.sum().item())
     C = int(((eng.k_eff.long() + 31) // 32).sum().item())  # checkpoint slots
-    HW = W * H
-    T = eng.n_tiles
-    algo = algorithmic_bytes(N, M, P, HW, T, C, E, U)
+    HW, T = eng.W * eng.H, eng.n_tiles
+    algo = algorithmic_bytes(n, M, P, HW, T, C, E, U)
     peak, peak_src = load_peaks()
     per_kernel = {
         "blend_forward": algo["blend_forward"],
@@ -347,118 +425,246 @@ def main():
     }
     dom = max((k for k in stage_ms if k in per_kernel), key=lambda k: stage_ms[k])
     ach = per_kernel[dom] / (stage_ms[dom] / 1000.0) / 1e9
-    it_bytes = sum(algo.values())
+    ncu = ncu_stats(dom)
+    return dict(P=P, U=U, M=M, E=E, C=C, algo=algo, peak=peak, roof={
+        "bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+        "frac": ach / peak, "traffic": ncu.get("dram_bytes"),
+        "algorithmic_bytes": per_kernel[dom], "avg_ms": stage_ms[dom], "peak_source": peak_src,
+        "ncu": {k: v for k, v in ncu.items() if k in ("issue_slots_pct", "warps_active_pct")},
+        "note": "FP32 CUDA-core kernel bound by instruction issue, FMA-pipe occupancy and "
+                "dependent latency, not by HBM; no tensor-core work on this path"})
 
-    # ---- end to end through the public API with host buffers (N=1): every
-    # step uploads its keyframe target from pinned host memory (on a copy
-    # stream, double-buffered so the upload of step k+1 overlaps step k) and
-    # the step's loss/status snapshot comes back to the host
-    e2e = None
-    if world == 1 and not args.no_e2e:
-        eng.synchronize()
-        for f, t in zip(eng.gmap.FIELDS, snap[0]):
-            getattr(eng.gmap, f).copy_(t)
-        for k, t in snap[1].items():
-            eng.state.m[k].copy_(t)
-        for k, t in snap[2].items():
-            eng.state.v[k].copy_(t)
-        eng.state.step_count = snap[3]
-        host_tgt = my_tgt.cpu().pin_memory()
-        bufs = [torch.empty_like(my_tgt), torch.empty_like(my_tgt)]
-        copy_stream = torch.cuda.Stream()
-        uploaded = [torch.cuda.Event(), torch.cuda.Event()]
-        consumed = [torch.cuda.Event(), torch.cuda.Event()]
-        main = torch.cuda.current_stream()
 
-        def upload(k):
-            b = k % 2
-            with torch.cuda.stream(copy_stream):
-                copy_stream.wait_event(consumed[b])
-                bufs[b].copy_(host_tgt, non_blocking=True)
-                uploaded[b].record(copy_stream)
-
-        def e2e_step(k):
-            b = k % 2
-            main.wait_event(uploaded[b])
-            eng.step(my_cam, bufs[b])
-            consumed[b].record(main)
-            upload(k + 2)
-
-        for b in range(2):
-            consumed[b].record(main)
-        upload(0)
-        upload(1)
-        for k in range(2):  # capture the graphs of both input buffers
-            e2e_step(k)
-        eng.synchronize()
+def batch_arm(torch, args, rank, world, dist, timer, steps, warmup, with_e2e):
+    """BASELINE configs[3]: S(1M), a fixed batch of 8 views per step sharded
+    over the ranks, one all-reduce of the flat gradient buffer per step."""
+    import paper_2410_00486_b200 as ss
+    from paper_2410_00486_b200.distributed import ShardedMapper, shard_views
+    from paper_2410_00486_b200.scene import survey_camera, survey_scene
+    V, N, W, H = BATCH["views"], BATCH["n"], BATCH["width"], BATCH["height"]
+    opts = ss.RasterOpts(sh_degree=0)
+    cams = [survey_camera(W, H, v, V) for v in range(V)]
+    mine = shard_views(V, rank, world)
+    tmap = ss.GaussianMap.from_scene(survey_scene(N, 100))
+    targets = [ss.rasterize_forward(tmap, cams[v], opts).image.clone() if v in mine else None
+               for v in range(V)]
+    del tmap
+    eng = ss.MappingEngine(ss.GaussianMap.from_scene(survey_scene(N, 0)), W, H, opts)
+    eng.fit_capacity([cams[v] for v in mine])
+    sm = ShardedMapper(eng, rank, world)
+    for _ in range(warmup):
+        sm.step(cams, targets)
+    torch.cuda.synchronize()
+    launches0 = eng.launches
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = timer.run(lambda: sm.step(cams, targets), steps)
+    launches = eng.launches - launches0
+    total_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    out = {"value": steps / (total_ms / 1000.0), "unit": "it/s",
+           "views_per_s": V * steps / (total_ms / 1000.0), "ms_per_step": total_ms / steps,
+           "steps": steps, "warmup": warmup, "views_per_step": V, "gaussians": N,
+           "views_per_rank": len(mine), "pairs_capacity": eng.pair_capacity,
+           "gpu_launches": launches}
+    if with_e2e:
+        # every step: this rank's targets uploaded from pinned host memory, the
+        # per-view loss sums read back (wall clock, max over ranks)
+        hosts = {v: targets[v].cpu().pin_memory() for v in mine}
+        bufs = {v: torch.empty_like(targets[v]) for v in mine}
+        tg = [bufs.get(v) for v in range(V)]
+        if dist is not None:
+            dist.barrier()
         torch.cuda.synchronize()
-        # the same number of iterations as the device-timed run, from the
-        # same state (the 2 graph-capture steps above are not timed)
-        n_e2e = args.steps
         t0 = time.perf_counter()
-        for k in range(2, 2 + n_e2e):
-            e2e_step(k)
-        eng.synchronize()  # every step's loss is on the host
+        for _ in range(steps):
+            for v in mine:
+                bufs[v].copy_(hosts[v], non_blocking=True)
+            losses = sm.step(cams, tg)
+            torch.stack(losses).cpu()
+        torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        e2e = {"value": n_e2e / wall, "unit": "it/s", "steps": n_e2e,
-               "h2d_bytes_per_step": int(host_tgt.numel() * 4),
-               "d2h_bytes_per_step": int(eng._host.shape[1] * 8),
-               "timing": "wall clock over the same iterations as `value` (state restored), "
-                         "host pinned target upload per step (copy stream, double-buffered) "
-                         "+ per-step loss/status read back"}
+        if dist is not None:
+            t = torch.tensor([wall], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall = float(t.item())
+        out["e2e"] = {"value": steps / wall, "unit": "it/s", "steps": steps,
+                      "h2d_bytes_per_step": int(sum(hosts[v].numel() * 4 for v in mine)),
+                      "d2h_bytes_per_step": int(len(mine) * 16),
+                      "timing": "wall clock, max over ranks; each rank uploads its views' "
+                                "targets from pinned host memory and reads back their loss "
+                                "sums every step"}
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    args = _args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    warmup = max(args.warmup, 3)
+    timer = Timer(torch)
+
+    if world > 1:
+        sampler = ClockSampler(local)
+        sampler.start()
+        res = batch_arm(torch, args, rank, world, dist, timer, args.steps, warmup,
+                        not args.no_e2e)
+        clocks = sampler.stop()
+        if rank == 0:
+            line = {
+                "metric": METRIC, "value": res["value"], "unit": "it/s", "n_gpus": world,
+                "steps": args.steps, "warmup": warmup, "ms_per_step": res["ms_per_step"],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": batch_workload(world), "gaussians": BATCH["n"],
+                           "image": [BATCH["width"], BATCH["height"]], "sh_degree": 0,
+                           "views_per_step": BATCH["views"],
+                           "parallelism": f"keyframe-sharded x{world} (NCCL all-reduce)",
+                           "l2": "256 MB buffer written between timed steps (outside the "
+                                 "events)"},
+                "views_per_s": res["views_per_s"], "clocks": clocks, "e2e": res.get("e2e"),
+                "gpu_launches": res["gpu_launches"], "cpu_baseline": None,
+            }
+            print(json.dumps(line), flush=True)
+        dist.barrier()
+        dist.destroy_process_group()
+        return 0
+
+    import paper_2410_00486_b200 as ss
+    from paper_2410_00486_b200.scene import survey_camera, survey_scene
+
+    W, H, N = args.width, args.height, args.n
+    opts = ss.RasterOpts(sh_degree=0)
+    cam = survey_camera(W, H)
+    # target: render of S(N, seed + 100) (SURVEY 8d; rendered on the GPU here --
+    # the oracle takes seconds per 300k render)
+    tgt = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(N, 100)), cam,
+                               opts).image.clone()
+    eng = ss.MappingEngine(ss.GaussianMap.from_scene(survey_scene(N, 0)), W, H, opts)
+    eng.fit_capacity(cam)
+    eng.enable_graph()  # the whole iteration is replayed as one CUDA graph
+    # the device-timed steps read the target from the engine's own buffer (the
+    # one its captured graph reads); the e2e runs pass host-uploaded buffers,
+    # which step() copies there
+    eng.target_buffer().copy_(tgt)
+
+    def one_step():
+        eng.step(cam, eng.target_buffer())
+
+    for _ in range(warmup):
+        one_step()
+    eng.synchronize()
+    snap = snapshot_state(eng)
+
+    # ---- timed region: per-step CUDA events, L2 flushed between steps
+    sampler = ClockSampler(local)
+    torch.cuda.synchronize()
+    sampler.start()
+    launches0 = eng.launches
+    step_ms = timer.run(one_step, args.steps)
+    clocks = sampler.stop()
+    eng.synchronize()
+    launches = eng.launches - launches0
+    total_ms = sum(step_ms)
+    ms_per_step = total_ms / args.steps
+    value = args.steps / (total_ms / 1000.0)
+
+    stage_ms = stage_times(torch, eng, one_step)
+    rf = roofline(torch, eng, stage_ms, N)
+    it_bytes = sum(rf["algo"].values())
+
+    e2e = None
+    if not args.no_e2e:
+        restore_state(eng, snap)
+        e2e = e2e_single(torch, eng, cam, tgt, args.steps)
+
+    # ---- converged regime: iterations 251-270 of the same training run
+    converged = None
+    if not args.no_converged:
+        restore_state(eng, snap)
+        eng.target_buffer().copy_(tgt)
+        while eng.iteration < 250:
+            one_step()
+        eng.synchronize()
+        csnap = snapshot_state(eng)
+        c_ms = timer.run(one_step, args.steps)
+        eng.synchronize()
+        c_stage = stage_times(torch, eng, one_step)
+        c_rf = roofline(torch, eng, c_stage, N)
+        converged = {"value": args.steps / (sum(c_ms) / 1000.0), "unit": "it/s",
+                     "ms_per_step": sum(c_ms) / args.steps,
+                     "iterations": f"{csnap[4] + 1}-{csnap[4] + args.steps}",
+                     "pairs": c_rf["P"], "checkpoint_slots": c_rf["C"],
+                     "backward_units": c_rf["U"], "stage_ms": c_stage,
+                     "roofline": c_rf["roof"]}
+        if not args.no_e2e:
+            restore_state(eng, csnap)
+            converged["e2e"] = e2e_single(torch, eng, cam, tgt, args.steps)
+    del eng
+    torch.cuda.empty_cache()
+
+    # ---- configs[3] on this GPU: the N = 1 point of the scaling curve
+    config4 = None
+    if not args.no_config4:
+        config4 = batch_arm(torch, args, 0, 1, None, timer, max(args.steps // 2, 5), 3,
+                            not args.no_e2e)
+        config4["workload"] = batch_workload(1)
 
     # ---- CPU baseline (rank 0, N = 1): bounded oracle sample
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import platform
-        times, threads = run_cpu_iterations(args, 3, args.cpu_budget_s)
+    if not args.no_cpu_baseline:
+        times, threads = run_cpu_iterations(args, 8, args.cpu_budget_s)
+        t1, _ = run_cpu_iterations(args, 1, 0.0, threads=1)
         cpu = {"value": len(times) / sum(times), "unit": "it/s", "cores": threads,
-               "kind": "port", "sample": f"{len(times)} full float64 iterations of the oracle "
-                                        f"restatement of the reference path (oracle/), same "
-                                        f"scene/camera, {threads} OpenMP threads on "
-                                        f"{platform.machine()}"}
+               "kind": "port", "single_thread_it_s": 1.0 / t1[0],
+               "sample": f"{len(times)} full float64 iterations of the oracle restatement of "
+                         f"the reference path (oracle/), same scene/camera, {threads} OpenMP "
+                         f"threads (n_workers={threads}) on '{cpu_model()}'; "
+                         f"single_thread_it_s: 1 iteration at n_workers=1"}
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
-            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": f"replica-shaped S({N},{W}x{H}) SH0, "
-                                   f"{'single view' if world == 1 else '1 view per GPU, NCCL all-reduce'}"
-                                   " (BASELINE configs[1])", "gaussians": N, "image": [W, H],
-                       "sh_degree": 0, "pairs": P, "visible": M, "checkpoint_slots": C,
-                       "backward_units": U,
-                       "l2": "256 MB buffer written between timed steps (outside the events)",
-                       "phase": f"iterations {max(args.warmup, 3) + 1}-"
-                                f"{max(args.warmup, 3) + args.steps} from the survey "
-                                "initialisation (the cost per iteration rises ~2x by "
-                                "iteration 150 as training lowers opacities)",
-                       "parallelism": f"keyframe-sharded x{world}" if world > 1 else "single GPU"},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak,
-                         "unit": "GB/s", "frac": ach / peak, "traffic": ncu_traffic(dom),
-                         "algorithmic_bytes": per_kernel[dom], "avg_ms": stage_ms[dom],
-                         "peak_source": peak_src,
-                         "ncu": {k: v for k, v in ncu_stats(dom).items()
-                                 if k in ("issue_slots_pct", "warps_active_pct")},
-                         "note": "FP32 CUDA-core kernel bound by instruction issue, "
-                                 "FMA-pipe occupancy and dependent latency (ncu: issue "
-                                 "slots ~55 %, FMA pipe ~56 %, 4 warps/SMSP at 128 regs), "
-                                 "not by HBM; no tensor-core work on this path"},
-            "iteration_roofline": {"algorithmic_MB": it_bytes / 1e6,
-                                   "achieved_GBs": it_bytes * value / views / 1e9,
-                                   "frac": it_bytes * value / views / 1e9 / peak},
-            "stage_ms": stage_ms,
-            "clocks": clocks,
-            "e2e": e2e,
-            "gpu_launches": launches,
-            "cpu_baseline": cpu,
-        }
-        print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.barrier()
-        dist.destroy_process_group()
-    _ = (np, pcount)
+    line = {
+        "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": single_workload(args), "gaussians": N, "image": [W, H],
+                   "sh_degree": 0, "pairs": rf["P"], "visible": rf["M"],
+                   "checkpoint_slots": rf["C"], "backward_units": rf["U"],
+                   "l2": "256 MB buffer written between timed steps (outside the events)",
+                   "phase": f"iterations {warmup + 1}-{warmup + args.steps} from the survey "
+                            "initialisation; `converged` = iterations 251-270",
+                   "parallelism": "single GPU"},
+        "roofline": rf["roof"],
+        "iteration_roofline": {"algorithmic_MB": it_bytes / 1e6,
+                               "achieved_GBs": it_bytes * value / 1e9,
+                               "frac": it_bytes * value / 1e9 / rf["peak"]},
+        "stage_ms": stage_ms,
+        "clocks": clocks,
+        "e2e": e2e,
+        "converged": converged,
+        "config4": config4,
+        "gpu_launches": launches,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
     return 0
 
 

@@ -87,7 +87,7 @@ def lib():
         L.orc_tile_sort.argtypes = [I64, VP, VP, I64, I64, I64, VP, VP]
         L.orc_forward.restype = None
         L.orc_forward.argtypes = [VP, VP, I64, VP, VP, VP, VP, VP, VP, VP, INT, INT, INT, INT,
-                                  DBL, DBL, DBL, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP]
+                                  DBL, DBL, DBL, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, DBL, VP]
         L.orc_replay.restype = None
         L.orc_replay.argtypes = [VP, I64, I64, I64, VP, VP, VP, VP, VP, INT, INT, INT, INT,
                                  DBL, DBL, DBL, VP]
@@ -374,8 +374,14 @@ def tile_index(mean2d, radius, depth, width, height, tile=16) -> OTileIndex:
 
 def forward(proj: OProjection, ti: OTileIndex, width, height, n_primitives, bucket=32,
             t_min=1e-4, alpha_min=1.0 / 255.0, alpha_max=0.99, background=(0.0, 0.0, 0.0),
-            with_depth=False, m_cut=None, with_checkpoints=True) -> ORender:
-    """rasterize_forward's blend stage (api.py:135-206) over forward_tile."""
+            with_depth=False, m_cut=None, with_checkpoints=True,
+            threshold_band=None) -> ORender:
+    """rasterize_forward's blend stage (api.py:135-206) over forward_tile.
+
+    ``threshold_band`` (parity support): also flag, per pixel, whether any
+    of its (pixel, splat) evaluations lies within that relative band of the
+    m_cut / alpha_min / t_min decisions (``extra["threshold_px"]``), i.e.
+    where a float32 evaluation of the same inputs may decide differently."""
     W, H, ts = int(width), int(height), ti.tile_size
     bg = _f64(background).reshape(3)
     image = np.empty((H, W, 3))
@@ -402,20 +408,24 @@ def forward(proj: OProjection, ti: OTileIndex, width, height, n_primitives, buck
     k_eff = np.zeros(A, dtype=np.int64)
     depth = _f64(proj.depth) if with_depth else None
     dimg = np.zeros((H, W)) if with_depth else None
+    thr = np.zeros((H, W), dtype=np.uint8) if threshold_band is not None else None
     lib().orc_forward(_p(np.ascontiguousarray(ti.pair_splat, np.int32)), _p(ti.tile_range), A,
                       _p(active), _p(_f64(proj.mean2d)), _p(_f64(proj.conic)), _p(_f64(proj.rgb)),
                       _p(_f64(proj.sigma)), _p(m_cut), _p(depth), W, H, ts, bucket, t_min,
                       alpha_min, alpha_max, _p(bg), _p(image), _p(acc), _p(final_t),
                       _p(n_contrib), _p(k_eff), _p(contributed_proj), _p(ckpt), _p(ckpt_off),
-                      _p(dimg))
+                      _p(dimg), float(threshold_band or 0.0), _p(thr))
     contributed = np.zeros(n_primitives, dtype=bool)
     if m:
         contributed[proj.map_index[contributed_proj[:m].astype(bool)]] = True
-    return ORender(image=image, acc_rgb=acc, final_t=final_t, n_contrib=n_contrib, proj=proj,
-                   tile_index=ti, k_eff=k_eff, ckpt_flat=ckpt, ckpt_off=ckpt_off,
-                   contributed=contributed, m_cut=m_cut, width=W, height=H, bucket=bucket,
-                   t_min=t_min, alpha_min=alpha_min, alpha_max=alpha_max,
-                   n_primitives=n_primitives, depth=dimg)
+    r = ORender(image=image, acc_rgb=acc, final_t=final_t, n_contrib=n_contrib, proj=proj,
+                tile_index=ti, k_eff=k_eff, ckpt_flat=ckpt, ckpt_off=ckpt_off,
+                contributed=contributed, m_cut=m_cut, width=W, height=H, bucket=bucket,
+                t_min=t_min, alpha_min=alpha_min, alpha_max=alpha_max,
+                n_primitives=n_primitives, depth=dimg)
+    if thr is not None:
+        r.extra["threshold_px"] = thr.astype(bool)
+    return r
 
 
 def rasterize(gmap: OMap, cam, sh_degree=3, tile=16, bucket=32, t_min=1e-4,

@@ -391,6 +391,29 @@ static inline double alpha_at(const splat_set *S, int32_t s, double px, double p
     return a;
 }
 
+/* Parity support (test infrastructure, not in the reference): 1 when this
+ * (pixel, splat) evaluation sits within a relative `band` of one of the
+ * blend's discrete decisions -- the m_cut cull, the alpha_min skip
+ * (kernels.py:14-31) or the t_min termination (kernels.py:93-99) -- so a
+ * float32 evaluation of the same inputs may decide it the other way.
+ * "n_contrib equal except flagged threshold pixels". */
+static inline int near_threshold(const splat_set *S, int32_t s, double px, double py, double T,
+                                 double band) {
+    double dx = px - S->mean2d[2 * s];
+    double dy = py - S->mean2d[2 * s + 1];
+    const double *c = S->conic + 3 * s;
+    double m = c[0] * dx * dx + 2.0 * c[1] * dx * dy + c[2] * dy * dy;
+    double mc = S->mcut[s];
+    if (fabs(m - mc) <= band * (fabs(mc) > 1.0 ? fabs(mc) : 1.0)) return 1;
+    if (m > mc) return 0;
+    double a = S->sigma[s] * exp(-0.5 * m);
+    if (fabs(a - S->amin) <= band * S->amin) return 1;
+    if (a < S->amin) return 0;
+    if (a > S->amax) a = S->amax;
+    double Tn = T * (1.0 - a);
+    return fabs(Tn - S->tmin) <= band * S->tmin;
+}
+
 static inline void tile_geom(int64_t tile_id, int tile, int64_t tx, int W, int H,
                              int *x0, int *y0, int *tw, int *th) {
     *y0 = (int)(tile_id / tx) * tile;
@@ -416,7 +439,7 @@ void orc_forward(const int32_t *order, const int64_t *tile_range, int64_t n_acti
                  int W, int H, int tile, int bucket, double tmin, double amin, double amax,
                  const double *bg, double *image, double *acc, double *final_t,
                  int32_t *n_contrib, int64_t *k_eff, uint8_t *contributed, double *ckpt,
-                 const int64_t *ckpt_off, double *out_depth) {
+                 const int64_t *ckpt_off, double *out_depth, double band, uint8_t *thr_px) {
     splat_set S = {order, mean2d, conic, rgb, sigma, mcut, depth, amin, amax, tmin};
     int64_t tx = (W + tile - 1) / tile;
     int npx_max = tile * tile;
@@ -459,6 +482,8 @@ void orc_forward(const int32_t *order, const int64_t *tile_range, int64_t n_acti
                     int64_t p = alive[ii];
                     double px = (double)(x0 + p % tw), py = (double)(y0 + p / tw);
                     double a = alpha_at(&S, s, px, py);
+                    if (thr_px && near_threshold(&S, s, px, py, st[p], band))
+                        thr_px[(int64_t)(y0 + p / tw) * W + x0 + p % tw] = 1;
                     if (a < 0.0) {
                         ++ii;
                         continue;

@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
     __shared__ __align__(16) float2 shq[LH][LT];   //                  (x^2, y^2)
     __shared__ __align__(16) float shm[LH][LT];    //                  xy
     __shared__ double red[2][8];
+    __shared__ float s_shift[2][8];
     PDL_WAIT();
     SSIM_TRACE_BEGIN
     const int t = threadIdx.x;
@@ -140,16 +141,38 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
                 vx[i] = k < LH * LH ? x[o] : 0.f;
                 vy[i] = k < LH * LH ? y[o] : 0.f;
             }
+            float hx = 0.f, hy = 0.f;
 #pragma unroll
             for (int i = 0; i < NL; ++i) {
                 const int k = t + 256 * i;
                 if (k < LH * LH) {
                     const int r = k / LH, cc = k - r * LH;
                     s_xy[r][cc] = make_float2(vx[i], vy[i]);
+                    hx += vx[i];
+                    hy += vy[i];
                 }
+            }
+            hx = warp_sum(hx);
+            hy = warp_sum(hy);
+            if ((t & 31) == 0) {
+                s_shift[0][t >> 5] = hx;
+                s_shift[1][t >> 5] = hy;
             }
         }
         __syncthreads();
+        // The CTA's moments are taken about its halo means (cx, cy): every
+        // output's window lies inside this halo, so sxx = F((x-cx)^2) -
+        // (F(x)-cx)^2 holds exactly, and centring removes most of the float32
+        // cancellation of F(x^2) - F(x)^2 (grad_image vs the float64 oracle at
+        // configs[1]: 1.1e-5 -> ~5e-6 norm-wise).
+        float cx = 0.f, cy = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            cx += s_shift[0][k];
+            cy += s_shift[1][k];
+        }
+        cx *= 1.f / (LH * LH);
+        cy *= 1.f / (LH * LH);
         // horizontal (axis 1): 42 rows x 8 groups of 4 columns
         for (int task = t; task < LH * 8; task += 256) {
             const int r = task >> 3, c0 = (task & 7) * 4;
@@ -158,10 +181,11 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
 #pragma unroll
             for (int k = 0; k < 7; ++k) {
                 const float4 a = *reinterpret_cast<const float4*>(&s_xy[r][c0 + 2 * k]);
-                pv[2 * k] = pk2(a.x, a.y);
-                pv[2 * k + 1] = pk2(a.z, a.w);
-                mv[2 * k] = a.x * a.y;
-                mv[2 * k + 1] = a.z * a.w;
+                const float ax = a.x - cx, ay = a.y - cy, az = a.z - cx, aw = a.w - cy;
+                pv[2 * k] = pk2(ax, ay);
+                pv[2 * k + 1] = pk2(az, aw);
+                mv[2 * k] = ax * ay;
+                mv[2 * k + 1] = az * aw;
             }
 #pragma unroll
             for (int k = 0; k < 14; ++k) qv[k] = mul2(pv[k], pv[k]);
@@ -207,9 +231,10 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
         for (int o = 0; o < 4; ++o) {
             const int oy = y0 + 4 * rg + o;
             if (ox < W && oy < H) {
-                const float mx = mom[0][o], my = mom[1][o];
-                const float sxx = mom[2][o] - mx * mx, syy = mom[3][o] - my * my;
-                const float sxy = mom[4][o] - mx * my;
+                const float mxs = mom[0][o], mys = mom[1][o];  // means about (cx, cy)
+                const float sxx = mom[2][o] - mxs * mxs, syy = mom[3][o] - mys * mys;
+                const float sxy = mom[4][o] - mxs * mys;
+                const float mx = mxs + cx, my = mys + cy;
                 const float a1 = 2.f * mx * my + C1, a2 = 2.f * sxy + C2;
                 const float b1 = mx * mx + my * my + C1, b2 = sxx + syy + C2;
                 const float ibb = rcp_approx(b1 * b2);  // 1/b1 = b2/bb, 1/b2 = b1/bb

@@ -19,16 +19,20 @@ the GPU's), and compared with the oracle (oracle/, float64) stage by stage:
   radius flips counted (float32 rounding at the ceil boundary);
 * K2-K4b binning (tiles.py:29-65): pair list, tile ranges and active tiles
   BIT-EXACT;
-* K5 blend (kernels.py:34-109): image and final_T <= 1e-4 absolute,
-  n_contrib flips counted and bounded, k_eff equal outside flipped tiles;
+* K5 blend (kernels.py:34-109): image and final_T <= 1e-4 absolute at
+  every pixel clear of the blend's discrete decisions (the oracle flags
+  pixels with an evaluation within BAND of m_cut / alpha_min / t_min);
+  n_contrib flips only at flagged pixels, k_eff equal outside their tiles;
 * K6 loss (losses.py:198-228): scalars <= 1e-6 rel, grad_image <= 1e-5
   norm-wise and max-abs;
 * K7 splat-wise backward (kernels.py:271-373) and K8 chain
   (projection.py:200-325): <= 1e-3 norm-wise AND <= 1e-3 elementwise on
-  entries above 1e-3 x max (SURVEY 8c);
+  entries above 1e-3 x max (for K7 over the rows not blended at
+  a flagged threshold pixel);
 * K9 Adam (optimizer.py:101-133), all six groups incl. the quaternion
   renorm and sh_rest, from non-zero moments: each parameter's step within
-  1e-3 of the oracle's step (plus two float32 ulps of the parameter);
+  1e-3 of the oracle's step (plus two float32 ulps of the parameter, four
+  for the renormalised quaternions);
 * fused K8+K9 (the engine's chain_adam kernel) over one engine step vs the
   oracle chain + regulariser + Adam on the engine's own g2d;
 * K10 densify (densify.py:103-173): survivors, counts bit-exact.
@@ -49,6 +53,12 @@ pytestmark = pytest.mark.gpu
 
 import oracle as orc  # noqa: E402
 from helpers import floored_rel, normwise  # noqa: E402
+
+# relative band around the blend's discrete decisions (m_cut, alpha_min,
+# t_min) inside which float32 and float64 may decide differently; the GPU's
+# alpha is within ~5e-7 relative of the exact value (ex2.approx), its
+# quadratic form within ~1e-6
+BAND = 5e-6
 
 CONFIGS = {
     "replica": (300_000, 1200, 680, 0),
@@ -114,8 +124,25 @@ def _oracle_forward(fs):
         oti = orc.OTileIndex(16, ti.tiles_x, ti.tiles_y, ti.pair_splat, ti.tile_range,
                              ti.active_tiles)
         fs["r"] = orc.forward(po, oti, cam.width, cam.height, out.n_primitives,
-                              m_cut=p.m_cut.astype(np.float64))
+                              m_cut=p.m_cut.astype(np.float64), threshold_band=BAND)
     return fs["r"]
+
+
+def _threshold_rows(fs):
+    """Projection rows blended (by the GPU or the oracle) at a flagged
+    threshold pixel: their g2d rows get that pixel's terms, which a float32
+    threshold decision may legitimately change."""
+    if "thr_rows" not in fs:
+        out, r = fs["out"], _oracle_forward(fs)
+        ti = out.tile_index
+        nc = np.maximum(out.n_contrib.cpu().numpy(), r.n_contrib)
+        rows = set()
+        for y, x in zip(*np.nonzero(r.extra["threshold_px"])):
+            tid = (y // 16) * ti.tiles_x + x // 16
+            a = int(ti.tile_range[tid])
+            rows.update(ti.pair_splat[a:a + int(nc[y, x])].tolist())
+        fs["thr_rows"] = np.array(sorted(rows), dtype=np.int64)
+    return fs["thr_rows"]
 
 
 def _loss(fs):
@@ -171,30 +198,42 @@ def test_binning_bit_exact_vs_oracle(fs):
 
 
 def test_forward_vs_oracle(fs):
+    """K5 on the GPU's list: colour / final_T within 1e-4 absolute at every
+    pixel whose evaluations all lie clear of the blend's discrete decisions
+    ("n_contrib equal except flagged threshold pixels"); the
+    flagged pixels are counted, every n_contrib flip must be one of them,
+    and there the difference is bounded by the few splats a flipped
+    decision can add or drop (alpha_min = 1/255 each)."""
     out = fs["out"]
     r = _oracle_forward(fs)
+    thr = r.extra["threshold_px"]
     img = out.image.cpu().numpy()
     ft = out.final_t.cpu().numpy()
     nc = out.n_contrib.cpu().numpy()
-    e_img = float(np.abs(img - r.image).max())
-    e_t = float(np.abs(ft - r.final_t).max())
+    d_img = np.abs(img - r.image).max(axis=2)
+    d_t = np.abs(ft - r.final_t)
+    e_img = float(d_img[~thr].max())
+    e_t = float(d_t[~thr].max())
+    e_img_thr = float(d_img[thr].max()) if thr.any() else 0.0
     flipped = nc != r.n_contrib
     flips = int(flipped.sum())
     ti = out.tile_index
     ke = out.k_eff
     H, W = nc.shape
-    # tiles holding a flipped pixel may change k_eff; every other tile equal
-    fl_tiles = set()
-    for y, x in zip(*np.nonzero(flipped)):
-        fl_tiles.add((y // 16) * ti.tiles_x + x // 16)
+    # tiles holding a flagged pixel may change k_eff; every other tile equal
+    fl_tiles = set(((y // 16) * ti.tiles_x + x // 16) for y, x in zip(*np.nonzero(thr)))
     ok = np.array([t not in fl_tiles for t in ti.active_tiles])
     ke_mis = int((ke[ok] != r.k_eff[ok]).sum())
     contrib_mis = int((out.contributed.cpu().numpy() != r.contributed).sum())
-    report(fs["name"], "K5_blend", image_abs=e_img, final_t_abs=e_t, n_contrib_flips=flips,
-           pixels=H * W, k_eff_mismatch_outside_flipped=ke_mis, contributed_mismatch=contrib_mis)
+    report(fs["name"], "K5_blend", image_abs=e_img, final_t_abs=e_t,
+           image_abs_all_pixels=float(d_img.max()), threshold_pixels=int(thr.sum()),
+           image_abs_threshold_pixels=e_img_thr, n_contrib_flips=flips,
+           n_contrib_flips_unflagged=int((flipped & ~thr).sum()), pixels=H * W,
+           k_eff_mismatch_outside_flagged_tiles=ke_mis, contributed_mismatch=contrib_mis)
     assert e_img <= 1e-4 and e_t <= 1e-4
-    # SURVEY 8c calibration: 0-1 flips at 150k/300k between f32 and f64 on the same list
-    assert flips <= max(4, H * W // 100_000)
+    assert int((flipped & ~thr).sum()) == 0
+    assert thr.sum() <= H * W // 1000
+    assert e_img_thr <= 0.05
     assert ke_mis == 0
     assert contrib_mis <= 4 * flips + 2
 
@@ -225,13 +264,17 @@ def test_backward_g2d_vs_oracle(fs):
     r = _oracle_forward(fs)
     ref = orc.backward_splat(r, G.cpu().numpy().astype(np.float64))
     fs["g2d_ref"] = ref
+    # elementwise: rows not blended at a flagged threshold pixel (norm-wise: all rows)
+    keep = np.ones(len(ref), bool)
+    keep[_threshold_rows(fs)] = False
     res = {}
     for nm, cols in (("rgb", slice(0, 3)), ("mean2d", slice(3, 5)), ("conic", slice(5, 8)),
                      ("sigma", slice(8, 9))):
         res[nm] = (normwise(mine[:, cols], ref[:, cols]),
-                   floored_rel(mine[:, cols], ref[:, cols], 1e-3))
+                   floored_rel(mine[keep, cols], ref[keep, cols], 1e-3))
     report(fs["name"], "K7_backward_g2d", **{f"{k}_normwise": v[0] for k, v in res.items()},
-           **{f"{k}_elementwise_above_floor": v[1] for k, v in res.items()})
+           **{f"{k}_elementwise_above_floor": v[1] for k, v in res.items()},
+           rows=len(ref), rows_at_threshold_pixels=int((~keep).sum()))
     for k, (nw, el) in res.items():
         assert nw <= 1e-3, (k, nw)
         assert el <= 1e-3, (k, el)
@@ -320,7 +363,8 @@ def test_adam_all_groups_vs_oracle(fs):
         a = getattr(g, f).cpu().numpy().astype(np.float64).reshape(b.shape)
         step_ref = b - pre[f].reshape(b.shape)
         err = np.abs(a - b)
-        bound = 1e-3 * np.abs(step_ref) + 2 * _ulp(b)
+        # the quaternion renorm adds 3 roundings (sum of squares, rsqrt, scale)
+        bound = 1e-3 * np.abs(step_ref) + (4 if f == "rotations" else 2) * _ulp(b)
         res[f] = (float((err / np.maximum(bound, 1e-30)).max()),
                   float(np.abs(step_ref).max()))
     for k in shapes:
@@ -371,7 +415,7 @@ def test_engine_fused_step_vs_oracle(fs):
         pre = getattr(om, f)
         step_ref = b - pre
         err = np.abs(a - b)[sel]
-        bound = 1e-3 * np.abs(step_ref)[sel] + 2 * _ulp(b)[sel]
+        bound = 1e-3 * np.abs(step_ref)[sel] + (4 if f == "rotations" else 2) * _ulp(b)[sel]
         res[f] = float((err / bound).max()) if sel.any() else 0.0
         if lr is not None:  # every selected element moved by ~lr in the oracle's direction
             assert np.all(np.sign(a - pre)[sel] == np.sign(step_ref)[sel]), f
@@ -397,12 +441,23 @@ def test_densify_bit_exact_vs_oracle(fs):
     h = g.to_numpy()
     om = orc.OMap(h["positions"], h["rotations"], h["log_scales"], h["opacity_logits"], h["sh"],
                   h["grad2d_accum"], h["grad3d_accum"], h["obs_count"])
-    # thresholds at quantiles of this map so that all three masks are busy
+    # thresholds at quantiles of this map so that all three masks are busy,
+    # placed midway between two neighbouring data values (a threshold EQUAL
+    # to a stored value would test the last ulp of exp(), which differs
+    # between CUDA's and glibc's double exp; the reference's thresholds are
+    # constants, not data values)
+    def between(v, q):
+        u = np.unique(v)
+        k = int(q * (len(u) - 1))
+        while k + 1 < len(u) and u[k + 1] - u[k] < 1e-9 * abs(u[k]):
+            k += 1
+        return float(0.5 * (u[k] + u[k + 1]))
+
     mean = om.grad2d_accum / np.maximum(om.obs_count, 1)
-    thr = float(np.quantile(mean[om.obs_count > 0], 0.95))
-    cfg = ss.DensifyConfig(grad_threshold=thr, prune_opacity=float(
-        np.quantile(1 / (1 + np.exp(-om.opacity_logits)), 0.02)))
-    ext = float(np.quantile(np.exp(om.log_scales).max(axis=1), 0.5)) / cfg.split_scale_percentile
+    thr = between(mean[om.obs_count > 0], 0.95)
+    cfg = ss.DensifyConfig(grad_threshold=thr, prune_opacity=between(
+        1 / (1 + np.exp(-om.opacity_logits)), 0.02))
+    ext = between(np.exp(om.log_scales).max(axis=1), 0.5) / cfg.split_scale_percentile
     small, large, keep = orc.densify_masks(om, cfg.grad_threshold, cfg.prune_opacity,
                                            cfg.split_scale_percentile, ext)
     normals = np.random.default_rng(7).standard_normal((2 * int(large.sum()), 3))

@@ -1,14 +1,29 @@
-"""Mapping iterations/s at the SURVEY.md 8.0 configs beyond the headline one
-(bench.py measures configs[1]): TUM-shaped S(150k, 640x480), the large
-S(1M, 1200x680) per view, and SH3 S(500k, 1200x680).  Device time of K
-CUDA-graph steps bracketed by events, L2 flushed between steps.
+"""Mapping iterations/s at the BASELINE.json configs beyond the headline one
+(bench.py measures configs[1] and configs[3]), each as north_star specifies:
 
-    python tools/bench_configs.py > profiles/r01_configs.jsonl
+* tum_densify   configs[2]: S(150k), 640x480, SH0, densify/prune AND opacity
+                reset every 100 iterations inside the timed loop (the densify
+                syncs, compacts the map + Adam moments, reallocates buffers
+                and drops the captured graph, which the next step re-captures:
+                all of that is in the time);
+* sh3_scheduled configs[4]: S(500k), 1200x680, SH3, a 64-keyframe orbit
+                driven by KeyframeScheduler(d=4, r0=8, seed=0) through
+                ScheduledMapper (adaptive, losses fed back two steps late; one
+                captured graph, each keyframe's target copied into the
+                engine's target buffer);
+* tum, replica, large_per_view, sh3: the single-view iteration (no densify,
+                one fixed keyframe) for reference.
+
+Device time = CUDA events around every step (L2 flushed between steps
+outside the events); wall = host clock around the whole timed loop.
+
+    python tools/bench_configs.py > profiles/r02_configs.jsonl
 """
 
 import json
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
@@ -16,39 +31,128 @@ import torch  # noqa: E402
 import paper_2410_00486_b200 as ss  # noqa: E402
 from paper_2410_00486_b200.scene import survey_camera, survey_scene  # noqa: E402
 
-CONFIGS = [("tum", 150_000, 640, 480, 0), ("replica", 300_000, 1200, 680, 0),
-           ("large_per_view", 1_000_000, 1200, 680, 0), ("sh3", 500_000, 1200, 680, 3)]
+SINGLE = [("tum", 150_000, 640, 480, 0), ("replica", 300_000, 1200, 680, 0),
+          ("large_per_view", 1_000_000, 1200, 680, 0), ("sh3", 500_000, 1200, 680, 3)]
+
+FLUSH = None
 
 
-def main(steps=20, warmup=5):
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    for name, n, w, h, deg in CONFIGS:
-        opts = ss.RasterOpts(sh_degree=deg)
-        cam = survey_camera(w, h)
-        tgt = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(n, 100)), cam,
-                                   opts).image.clone()
-        eng = ss.MappingEngine(ss.GaussianMap.from_scene(survey_scene(n, 0)), w, h, opts)
-        eng.fit_capacity(cam)
-        eng.enable_graph()
-        for _ in range(warmup):
-            eng.step(cam, tgt)
-        eng.synchronize()
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(steps)]
-        for a, b in ev:
-            flush.fill_(0.0)
-            a.record()
-            eng.step(cam, tgt)
-            b.record()
-        torch.cuda.synchronize()
-        ms = sum(a.elapsed_time(b) for a, b in ev) / steps
-        eng.synchronize()
-        print(json.dumps({"config": name, "gaussians": n, "image": [w, h], "sh_degree": deg,
-                          "it_per_s": 1000.0 / ms, "ms_per_step": ms,
-                          "pairs": eng.last_pair_count(), "steps": steps, "warmup": warmup,
-                          "dtype": "f32", "data": "synthetic survey scene (SURVEY.md 8d)"}),
-              flush=True)
-        del eng
+def timed(step, k):
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(k)]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for a, b in ev:
+        FLUSH.fill_(0.0)
+        a.record()
+        step()
+        b.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return [a.elapsed_time(b) for a, b in ev], wall
+
+
+def single(name, n, w, h, deg, steps=20, warmup=5):
+    opts = ss.RasterOpts(sh_degree=deg)
+    cam = survey_camera(w, h)
+    tgt = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(n, 100)), cam,
+                               opts).image.clone()
+    eng = ss.MappingEngine(ss.GaussianMap.from_scene(survey_scene(n, 0)), w, h, opts)
+    eng.fit_capacity(cam)
+    eng.enable_graph()
+    eng.target_buffer().copy_(tgt)
+    for _ in range(warmup):
+        eng.step(cam, eng.target_buffer())
+    eng.synchronize()
+    ms, _ = timed(lambda: eng.step(cam, eng.target_buffer()), steps)
+    eng.synchronize()
+    return {"config": name, "gaussians": n, "image": [w, h], "sh_degree": deg,
+            "it_per_s": 1000.0 * steps / sum(ms), "ms_per_step": sum(ms) / steps,
+            "pairs": eng.last_pair_count(), "steps": steps, "warmup": warmup,
+            "dtype": "f32", "data": "synthetic survey scene (SURVEY.md 8d)"}
+
+
+def tum_densify(iters=300):
+    """configs[2] as specified: densify/prune + opacity reset every 100."""
+    n, w, h = 150_000, 640, 480
+    opts = ss.RasterOpts(sh_degree=0)
+    cam = survey_camera(w, h)
+    tgt = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(n, 100)), cam,
+                               opts).image.clone()
+    cfg = ss.EngineConfig(densify=ss.DensifyConfig(interval=100), opacity_reset_interval=100,
+                          scene_extent=1.0)
+    eng = ss.MappingEngine(ss.GaussianMap.from_scene(survey_scene(n, 0)), w, h, opts, cfg)
+    eng.fit_capacity(cam)
+    eng.enable_graph()
+    sizes = []
+    orig = eng.densify
+
+    def densify(*a, **k):
+        r = orig(*a, **k)
+        sizes.append({"iteration": eng.iteration, "gaussians": len(eng.gmap),
+                      "cloned": r.n_cloned, "split": r.n_split, "pruned": r.n_pruned})
+        return r
+    eng.densify = densify
+    ms, wall = timed(lambda: eng.step(cam, tgt), iters)
+    eng.synchronize()
+    losses = [x[1] for x in eng.losses()]
+    return {"config": "tum_densify", "gaussians_start": n, "gaussians_end": len(eng.gmap),
+            "image": [w, h], "sh_degree": 0, "iterations": iters,
+            "it_per_s_wall": iters / wall, "it_per_s_device": 1000.0 * iters / sum(ms),
+            "densify_events": sizes, "opacity_resets": iters // 100,
+            "densify_interval": 100, "opacity_reset_interval": 100,
+            "loss_first": losses[0], "loss_last": losses[-1],
+            "timing": "all 300 iterations from the initialisation, densify + opacity reset + "
+                      "graph re-capture included (wall = host clock over the loop; device = "
+                      "sum of per-step events, which also bracket the densify kernels)",
+            "dtype": "f32", "data": "synthetic survey scene (SURVEY.md 8d)"}
+
+
+def sh3_scheduled(iters=200, warmup=20, n_kf=64):
+    """configs[4] as specified: SH3 500k, 64 orbit keyframes, adaptive
+    KeyframeScheduler(d=4, r0=8, seed=0) through ScheduledMapper."""
+    n, w, h = 500_000, 1200, 680
+    opts = ss.RasterOpts(sh_degree=3)
+    cams = [survey_camera(w, h, v, n_kf) for v in range(n_kf)]
+    tm = ss.GaussianMap.from_scene(survey_scene(n, 100))
+    targets = [ss.rasterize_forward(tm, c, opts).image.clone() for c in cams]
+    del tm
+    eng = ss.MappingEngine(ss.GaussianMap.from_scene(survey_scene(n, 0)), w, h, opts)
+    eng.fit_capacity(cams)
+    eng.enable_graph()
+    sm = ss.ScheduledMapper(eng, ss.KeyframeScheduler(d=4, r0=8, seed=0), mode="adaptive")
+    for k in range(n_kf):
+        sm.add_keyframe(k, cams[k], targets[k])
+    for _ in range(warmup):
+        sm.step()
+    sm.synchronize()
+    picks = []
+    ms, wall = timed(lambda: picks.append(sm.step()), iters)
+    sm.synchronize()
+    return {"config": "sh3_scheduled", "gaussians": n, "image": [w, h], "sh_degree": 3,
+            "keyframes": n_kf, "scheduler": "KeyframeScheduler(d=4, r0=8, seed=0), adaptive",
+            "iterations": iters, "warmup": warmup,
+            "it_per_s_wall": iters / wall, "it_per_s_device": 1000.0 * iters / sum(ms),
+            "distinct_keyframes_selected": len(set(picks)), "graphs": len(eng._graphs),
+            "pairs_capacity": eng.pair_capacity,
+            "timing": "device = per-step events (target copy into the graph's buffer "
+                      "included); wall = host clock over the loop incl. scheduler + loss feed",
+            "dtype": "f32", "data": "synthetic survey scene (SURVEY.md 8d)"}
+
+
+def main():
+    global FLUSH
+    FLUSH = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    which = sys.argv[1:] or ["tum_densify", "sh3_scheduled"] + [c[0] for c in SINGLE]
+    for name in which:
+        if name == "tum_densify":
+            line = tum_densify()
+        elif name == "sh3_scheduled":
+            line = sh3_scheduled()
+        else:
+            line = single(*[c for c in SINGLE if c[0] == name][0])
+        print(json.dumps(line), flush=True)
+        torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":
