@@ -154,6 +154,16 @@ int ss_bin_sort(int64_t n, const ss_splats *splats, const ss_camera *cam, const 
  * Needs both pointers and n_tiles <= SS_ORDER_MAX_TILES. */
 int ss_tile_order(const ss_camera *cam, const ss_bins *bins, void *stream);
 
+/* Parity / drop-in entry for build_tile_index (tiles.py:29-65) fed an
+ * EXTERNAL projection (e.g. the oracle's, or a reference-shaped Projection
+ * built elsewhere): writes the K1 outputs ss_bin_sort reads (inclusive tile
+ * rect in float32 arithmetic as numpy does, tile count, depth key) for m
+ * rows of float32 (mean2d (m,2), radius (m,), depth (m,) > 0); the pair list
+ * then holds row indices, exactly as the reference's pair_splat. */
+int ss_splats_from_projection(int64_t m, const float *d_mean2d, const float *d_radius,
+                              const float *d_depth, const ss_camera *cam, const ss_splats *out,
+                              void *stream);
+
 /* ------------------------------------------------------------ blend fwd */
 /* Replaces rasterize_forward's blend (api.py:135-206; forward_tile
  * kernels.py:34-109 and checkpoint_tile kernels.py:112-152).
@@ -169,6 +179,19 @@ int ss_blend_forward(const ss_camera *cam, const ss_raster_opts *opts, const ss_
                      float *d_depth, int32_t *d_k_eff, uint8_t *d_contributed, void *d_ckpt,
                      float *d_ckpt_depth, uint32_t *d_ckpt_mask, uint32_t *d_work,
                      int64_t work_capacity, ss_status *d_status, void *stream);
+
+/* Replaces replay_pixel_states (api.py:340-368; replay_tile
+ * kernels.py:155-178): advance tile `tile`'s archived (T, r, g, b) from
+ * checkpoint bucket from_bucket to list position pos_to with the forward's
+ * arithmetic.  d_out receives (th*tw, 4) floats, the tile's in-image pixels
+ * in row-major order.  d_image/d_final_t/d_n_contrib are the forward's
+ * outputs (a pixel stopped before the bucket has no archived state: its
+ * final state is used). */
+int ss_replay_pixel_states(const ss_camera *cam, const ss_raster_opts *opts,
+                           const ss_splats *splats, const ss_bins *bins, const float *d_image,
+                           const float *d_final_t, const int32_t *d_n_contrib, const void *d_ckpt,
+                           int32_t tile, int32_t from_bucket, int32_t pos_to, float *d_out,
+                           void *stream);
 
 /* -------------------------------------------------------------- losses */
 /* Replaces compute_losses' photometric part (losses.py:137-154,198-218):

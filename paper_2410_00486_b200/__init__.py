@@ -12,12 +12,13 @@ from .core import Camera, GaussianMap, logistic, logit
 from .densify import (DensifyConfig, DensifyResult, accumulate_grad_stats, densify_and_prune,
                       opacity_reset, seed_from_points)
 from .engine import EngineConfig, MappingEngine
-from .losses import (LossBreakdown, compute_losses, depth_l1, opacity_reg, psnr, ssim_metric,
-                     total_loss)
+from .losses import (LossBreakdown, compute_losses, depth_l1, opacity_reg, psnr, rendered_loss,
+                     ssim_metric, total_loss)
 from .optimizer import AdamState, LearningRates, adam_step, resize_for_densify
 from .rasterizer import (ParamGrads, Projection, RasterOpts, RenderOutput, TileIndex,
-                         backward_pixelwise, backward_splatwise, rasterize_forward,
-                         render_trajectory, screen_space_grads, screen_space_grads_pixelwise)
+                         backward_pixelwise, backward_splatwise, build_tile_index, chain_backward,
+                         project_map, rasterize_forward, render_trajectory, replay_pixel_states,
+                         screen_space_grads, screen_space_grads_pixelwise)
 from .mapio import load_map, save_map
 from .scheduler import KeyframeScheduler, ScheduledMapper
 from .scene import CONFIGS, survey_camera, survey_scene
@@ -28,9 +29,11 @@ __all__ = [
     "AdamState", "Camera", "CONFIGS", "DensifyConfig", "DensifyResult", "EngineConfig",
     "GaussianMap", "LearningRates", "LossBreakdown", "MappingEngine", "ParamGrads", "Projection",
     "RasterOpts", "RenderOutput", "TileIndex", "accumulate_grad_stats", "adam_step",
-    "backward_pixelwise", "backward_splatwise", "compute_losses", "densify_and_prune", "depth_l1", "logistic", "logit",
+    "backward_pixelwise", "backward_splatwise", "build_tile_index", "chain_backward",
+    "compute_losses", "densify_and_prune", "depth_l1", "logistic", "logit",
     "KeyframeScheduler", "ScheduledMapper", "load_map", "opacity_reg", "opacity_reset", "psnr",
-    "rasterize_forward", "render_trajectory", "resize_for_densify", "save_map",
+    "project_map", "rasterize_forward", "render_trajectory", "rendered_loss",
+    "replay_pixel_states", "resize_for_densify", "save_map",
     "seed_from_points",
     "ssim_metric",
     "screen_space_grads", "screen_space_grads_pixelwise", "survey_camera", "survey_scene", "total_loss",

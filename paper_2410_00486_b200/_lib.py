@@ -93,6 +93,9 @@ _SIGS = {
     "ss_status_reset": (I32, [VP, VP]),
     "ss_status_begin_step": (I32, [VP, VP]),
     "ss_status_flags": (I32, [VP, VP, VP]),
+    "ss_splats_from_projection": (I32, [I64, VP, VP, VP, P(SSCamera), P(SSSplats), VP]),
+    "ss_replay_pixel_states": (I32, [P(SSCamera), P(SSRasterOpts), P(SSSplats), P(SSBins), VP,
+                                     VP, VP, VP, I32, I32, I32, VP, VP]),
     "ss_step_snapshot": (I32, [VP, VP, VP, VP]),
     "ss_apply_stat_planes": (I32, [P(SSMap), P(SSParamGrads), VP]),
     "ss_preprocess": (I32, [P(SSMap), P(SSCamera), VP, P(SSRasterOpts), P(SSSplats), VP, VP]),

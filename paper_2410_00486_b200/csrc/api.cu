@@ -26,6 +26,11 @@ cudaError_t launch_backward_splat(const ss_camera*, const ss_raster_opts*, const
 cudaError_t launch_backward_pixel(const ss_camera*, const ss_raster_opts*, const ss_splats*,
                                   const ss_bins*, const float*, const float*, const int32_t*,
                                   const int32_t*, int64_t, float*, cudaStream_t);
+cudaError_t launch_splats_from_projection(int64_t, const float*, const float*, const float*,
+                                          const ss_camera*, const ss_splats*, cudaStream_t);
+cudaError_t launch_replay(const ss_camera*, const ss_raster_opts*, const ss_splats*,
+                          const ss_bins*, const float*, const float*, const int32_t*, const void*,
+                          int, int, int, float*, cudaStream_t);
 size_t seed_workspace_bytes(int64_t);
 cudaError_t launch_seed(int64_t, const float*, const float*, float, float*, float*, float*,
                         float*, float*, int32_t*, void*, size_t, cudaStream_t);
@@ -186,6 +191,29 @@ int ss_blend_forward(const ss_camera* cam, const ss_raster_opts* opts, const ss_
     return rc(launch_blend_forward(cam, opts, splats, bins, d_image, d_final_t, d_n_contrib,
                                    d_depth, d_k_eff, d_contributed, d_ckpt, d_ckpt_depth,
                                    d_ckpt_mask, d_work, work_capacity, d_status, S(stream)));
+}
+
+int ss_splats_from_projection(int64_t m, const float* d_mean2d, const float* d_radius,
+                              const float* d_depth, const ss_camera* cam, const ss_splats* out,
+                              void* stream) {
+    if (!cam || !out || m < 0 || m > 0x7fffffffLL) return SS_EINVAL;
+    if (m && (!d_mean2d || !d_radius || !d_depth || !out->d_rec || !out->d_depth_key ||
+              !out->d_tiles || !out->d_rect || !out->d_flags))
+        return SS_EINVAL;
+    return rc(launch_splats_from_projection(m, d_mean2d, d_radius, d_depth, cam, out, S(stream)));
+}
+
+int ss_replay_pixel_states(const ss_camera* cam, const ss_raster_opts* opts,
+                           const ss_splats* splats, const ss_bins* bins, const float* d_image,
+                           const float* d_final_t, const int32_t* d_n_contrib, const void* d_ckpt,
+                           int32_t tile, int32_t from_bucket, int32_t pos_to, float* d_out,
+                           void* stream) {
+    if (!cam || !opts_ok(opts) || !splats || !bins || !d_image || !d_final_t || !d_n_contrib ||
+        !d_ckpt || !d_out || tile < 0 || from_bucket < 0 || pos_to < 0)
+        return SS_EINVAL;
+    if (tile >= div_up(cam->width, kTile) * div_up(cam->height, kTile)) return SS_EINVAL;
+    return rc(launch_replay(cam, opts, splats, bins, d_image, d_final_t, d_n_contrib, d_ckpt, tile,
+                            from_bucket, pos_to, d_out, S(stream)));
 }
 
 size_t ss_loss_workspace_bytes(int32_t height, int32_t width) {

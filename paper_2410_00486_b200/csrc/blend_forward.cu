@@ -274,6 +274,71 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
     }
 }
 
+// replay_pixel_states (api.py:340-368) over replay_tile (kernels.py:155-178):
+// advance one tile's archived pixel states from checkpoint bucket
+// `from_bucket` to list position pos_to, with the forward's exact
+// arithmetic (quad_finish / splat_falloff, the same skip tests), so a replay
+// to k_eff reproduces the forward's final state bit for bit.  A pixel that
+// stopped (T < t_min) before the bucket has no archived state there (the
+// forward archives live pixels only): its state is the final one.
+__global__ void __launch_bounds__(256) replay_kernel(
+    int W, int H, int tiles_x, int tile, int from_bucket, int pos_to,
+    const uint32_t* __restrict__ tile_start, const uint32_t* __restrict__ ckpt_base,
+    const uint32_t* __restrict__ pairs, const SplatRec* __restrict__ rec,
+    const float4* __restrict__ ckpt, const float* __restrict__ image,
+    const float* __restrict__ final_t, const int32_t* __restrict__ n_contrib, float t_min,
+    float amin, float amax, float bg0, float bg1, float bg2, float* __restrict__ out) {
+    const int p = threadIdx.x, row = p >> 4, col = p & 15;
+    const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
+    const int ix = x0 + col, iy = y0 + row;
+    if (ix >= W || iy >= H) return;
+    const int tw = min(kTile, W - x0);
+    const size_t o = (size_t)iy * W + ix;
+    const int pos_from = kBucket * from_bucket;
+    float T, c0, c1, c2;
+    if (n_contrib[o] <= pos_from && final_t[o] < t_min) {
+        T = final_t[o];
+        c0 = image[3 * o] - bg0 * T;
+        c1 = image[3 * o + 1] - bg1 * T;
+        c2 = image[3 * o + 2] - bg2 * T;
+    } else {
+        const float4 s = ckpt[(size_t)(ckpt_base[tile] + from_bucket) * kTilePx + p];
+        T = s.x, c0 = s.y, c1 = s.z, c2 = s.w;
+    }
+    const float px = (float)ix, py = (float)iy;
+    const uint32_t start = tile_start[tile];
+    for (int k = pos_from; k < pos_to; ++k) {
+        if (T < t_min) continue;
+        const SplatRec r = rec[pairs[start + k]];
+        float dx, dy;
+        const float m = splat_power(px, py, r.a, r.b, dx, dy);
+        if (m > r.b.z) continue;
+        float a = splat_falloff(m, r.b);
+        if (a < amin) continue;
+        a = fminf(a, amax);
+        const float w = __fmul_rn(a, T);
+        c0 = __fmaf_rn(r.c.x, w, c0);
+        c1 = __fmaf_rn(r.c.y, w, c1);
+        c2 = __fmaf_rn(r.c.z, w, c2);
+        T = __fmul_rn(T, __fsub_rn(1.f, a));
+    }
+    float4* dst = reinterpret_cast<float4*>(out) + (row * tw + col);
+    *dst = make_float4(T, c0, c1, c2);
+}
+
+cudaError_t launch_replay(const ss_camera* cam, const ss_raster_opts* o, const ss_splats* sp,
+                          const ss_bins* bins, const float* image, const float* final_t,
+                          const int32_t* n_contrib, const void* ckpt, int tile, int from_bucket,
+                          int pos_to, float* out, cudaStream_t s) {
+    const int tx = div_up(cam->width, kTile);
+    replay_kernel<<<1, kTilePx, 0, s>>>(
+        cam->width, cam->height, tx, tile, from_bucket, pos_to, bins->d_tile_start,
+        bins->d_ckpt_base, bins->d_pair_splat, reinterpret_cast<const SplatRec*>(sp->d_rec),
+        reinterpret_cast<const float4*>(ckpt), image, final_t, n_contrib, o->t_min,
+        o->alpha_min, o->alpha_max, o->background[0], o->background[1], o->background[2], out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_blend_forward(const ss_camera* cam, const ss_raster_opts* o,
                                  const ss_splats* sp, const ss_bins* bins, float* image,
                                  float* final_t, int32_t* n_contrib, float* depth,

@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
     SSIM_TRACE_BEGIN
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * LT, y0 = blockIdx.y * LT;
-    const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
-    const float gs = 1.0f / (float)((double)H * W * 3);
+    const double C1d = 0.01 * 0.01, C2d = 0.03 * 0.03;
+    const double gsd = 1.0 / ((double)H * W * 3);
     double l1 = 0.0, ssum = 0.0;
     // vertical-pass task of this thread: column q, rows 4 rg .. 4 rg + 3
     const int q = t & 31, rg = t >> 5;
@@ -141,38 +141,42 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
                 vx[i] = k < LH * LH ? x[o] : 0.f;
                 vy[i] = k < LH * LH ? y[o] : 0.f;
             }
-            float hx = 0.f, hy = 0.f;
+            float hx = INFINITY, hy = INFINITY;
 #pragma unroll
             for (int i = 0; i < NL; ++i) {
                 const int k = t + 256 * i;
                 if (k < LH * LH) {
                     const int r = k / LH, cc = k - r * LH;
                     s_xy[r][cc] = make_float2(vx[i], vy[i]);
-                    hx += vx[i];
-                    hy += vy[i];
+                    hx = fminf(hx, vx[i]);
+                    hy = fminf(hy, vy[i]);
                 }
             }
-            hx = warp_sum(hx);
-            hy = warp_sum(hy);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                hx = fminf(hx, __shfl_xor_sync(0xffffffffu, hx, o));
+                hy = fminf(hy, __shfl_xor_sync(0xffffffffu, hy, o));
+            }
             if ((t & 31) == 0) {
                 s_shift[0][t >> 5] = hx;
                 s_shift[1][t >> 5] = hy;
             }
         }
         __syncthreads();
-        // The CTA's moments are taken about its halo means (cx, cy): every
+        // The CTA's moments are taken about its halo minima (cx, cy): every
         // output's window lies inside this halo, so sxx = F((x-cx)^2) -
-        // (F(x)-cx)^2 holds exactly, and centring removes most of the float32
-        // cancellation of F(x^2) - F(x)^2 (grad_image vs the float64 oracle at
-        // configs[1]: 1.1e-5 -> ~5e-6 norm-wise).
-        float cx = 0.f, cy = 0.f;
+        // (F(x)-cx)^2 holds exactly, and the shift trims the float32
+        // cancellation of F(x^2) - F(x)^2 where a tile has no black pixels
+        // (exact zeros keep the unshifted, exact arithmetic).  With the
+        // epilogue below in float64, grad_image is within ~5e-6 norm-wise and
+        // ~8e-6 max-abs of the float64 oracle at configs[1] (float32
+        // emulation: 1.2e-5 / 1.4e-5 without both).
+        float cx = INFINITY, cy = INFINITY;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            cx += s_shift[0][k];
-            cy += s_shift[1][k];
+            cx = fminf(cx, s_shift[0][k]);
+            cy = fminf(cy, s_shift[1][k]);
         }
-        cx *= 1.f / (LH * LH);
-        cy *= 1.f / (LH * LH);
         // horizontal (axis 1): 42 rows x 8 groups of 4 columns
         for (int task = t; task < LH * 8; task += 256) {
             const int r = task >> 3, c0 = (task & 7) * 4;
@@ -231,23 +235,30 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
         for (int o = 0; o < 4; ++o) {
             const int oy = y0 + 4 * rg + o;
             if (ox < W && oy < H) {
-                const float mxs = mom[0][o], mys = mom[1][o];  // means about (cx, cy)
-                const float sxx = mom[2][o] - mxs * mxs, syy = mom[3][o] - mys * mys;
-                const float sxy = mom[4][o] - mxs * mys;
-                const float mx = mxs + cx, my = mys + cy;
-                const float a1 = 2.f * mx * my + C1, a2 = 2.f * sxy + C2;
-                const float b1 = mx * mx + my * my + C1, b2 = sxx + syy + C2;
-                const float ibb = rcp_approx(b1 * b2);  // 1/b1 = b2/bb, 1/b2 = b1/bb
-                const float ss = a1 * a2 * ibb;
-                const float ga1 = gs * a2 * ibb, ga2 = gs * a1 * ibb;
-                const float gb1 = -gs * ss * (b2 * ibb), gb2 = -gs * ss * (b1 * ibb);
+                // epilogue in float64 (losses.py:99-109,119-134): ~30 flops per
+                // output, small next to the 110 float32 moment taps
+                const double mxs = mom[0][o], mys = mom[1][o];  // means about (cx, cy)
+                const double sxx = mom[2][o] - mxs * mxs, syy = mom[3][o] - mys * mys;
+                const double sxy = mom[4][o] - mxs * mys;
+                const double mx = mxs + cx, my = mys + cy;
+                const double a1 = 2.0 * mx * my + C1d, a2 = 2.0 * sxy + C2d;
+                const double b1 = mx * mx + my * my + C1d, b2 = sxx + syy + C2d;
+                // 1/(b1 b2) (then 1/b1 = b2/bb, 1/b2 = b1/bb): a float seed and two
+                // Newton steps in float64 instead of the slow IEEE double divide
+                const double bb = b1 * b2;
+                double ibb = (double)rcp_approx((float)bb);
+                ibb = ibb * fma(-bb, ibb, 2.0);
+                ibb = ibb * fma(-bb, ibb, 2.0);
+                const double ss = a1 * a2 * ibb;
+                const double ga1 = gsd * a2 * ibb, ga2 = gsd * a1 * ibb;
+                const double gb1 = -gsd * ss * (b2 * ibb), gb2 = -gsd * ss * (b1 * ibb);
                 // gradient maps are workspace: planar per channel, so the
                 // adjoint kernel's halo loads are coalesced
                 const size_t go = ((size_t)c * H + oy) * W + ox;
-                gmu[go] = 2.f * my * ga1 + 2.f * mx * gb1 - 2.f * mx * gb2 - my * 2.f * ga2;
-                gxx[go] = gb2;
-                gxy[go] = 2.f * ga2;
-                ssum += (double)ss;
+                gmu[go] = (float)(2.0 * my * ga1 + 2.0 * mx * gb1 - 2.0 * mx * gb2 - my * 2.0 * ga2);
+                gxx[go] = (float)gb2;
+                gxy[go] = (float)(2.0 * ga2);
+                ssum += ss;
                 const float2 e = s_xy[LR + 4 * rg + o][LR + q];
                 l1 += (double)fabsf(e.x - e.y);
             }
@@ -329,7 +340,7 @@ __global__ void __launch_bounds__(256, 3) ssim_bwd_kernel(int H, int W, const fl
     float(*sh)[LH][LT] = reinterpret_cast<float(*)[LH][LT]>(smem_b + 6 * LH * LP);  // [3]
     const int t = threadIdx.x;
     const int x0 = blockIdx.x * LT, y0 = blockIdx.y * LT;
-    const float inv_n = 1.0f / (float)((double)H * W * 3);
+    const double inv_nd = 1.0 / ((double)H * W * 3);
     const int q = t & 31, rg = t >> 5;
     const int ox = x0 + q;
     float gdot[4] = {0.f, 0.f, 0.f, 0.f};
@@ -414,8 +425,10 @@ __global__ void __launch_bounds__(256, 3) ssim_bwd_kernel(int H, int W, const fl
                 const float xv = x[go], yv = y[go];
                 const float d = xv - yv;
                 const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);  // np.sign(0) = 0
-                const float gx = adj[0][o] + adj[1][o] * 2.f * xv + adj[2][o] * yv;
-                const float gv = (1.0f - lam) * sgn * inv_n - lam * gx;
+                // the three adjoint terms cancel to a few digits: combine in float64
+                const double gx = (double)adj[0][o] + (double)adj[1][o] * (2.0 * xv) +
+                                  (double)adj[2][o] * yv;
+                const float gv = (float)((1.0 - lam) * sgn * inv_nd - lam * gx);
                 grad[go] = gv;
                 if (pg) pg[4 * ((size_t)oy * W + ox) + c] = gv;
                 gdot[o] += gv * xv;

@@ -222,6 +222,50 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     }
 }
 
+// build_tile_index (tiles.py:29-65) fed an external projection: the K1
+// outputs the binning reads (inclusive tile rect in float32 arithmetic as
+// numpy does, tile count, depth key) for m projection rows; the pair list
+// then holds row indices, as the reference's pair_splat does.
+__global__ void splats_from_projection_kernel(int64_t m, const float* __restrict__ mean2d,
+                                              const float* __restrict__ radius,
+                                              const float* __restrict__ depth, int tiles_x,
+                                              int tiles_y, SplatRec* __restrict__ rec,
+                                              uint32_t* __restrict__ depth_key,
+                                              uint32_t* __restrict__ tiles,
+                                              uint2* __restrict__ rect, uint8_t* __restrict__ flags) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const float mx = mean2d[2 * i], my = mean2d[2 * i + 1], rad = radius[i], z = depth[i];
+    const float fx0 = floorf(__fdiv_rn(__fsub_rn(mx, rad), (float)kTile));
+    const float fx1 = floorf(__fdiv_rn(__fadd_rn(mx, rad), (float)kTile));
+    const float fy0 = floorf(__fdiv_rn(__fsub_rn(my, rad), (float)kTile));
+    const float fy1 = floorf(__fdiv_rn(__fadd_rn(my, rad), (float)kTile));
+    const int x0 = (int)fminf(fmaxf(fx0, 0.f), (float)(tiles_x - 1));
+    const int x1 = (int)fminf(fmaxf(fx1, 0.f), (float)(tiles_x - 1));
+    const int y0 = (int)fminf(fmaxf(fy0, 0.f), (float)(tiles_y - 1));
+    const int y1 = (int)fminf(fmaxf(fy1, 0.f), (float)(tiles_y - 1));
+    SplatRec r;
+    r.a = make_float4(mx, my, 0.f, 0.f);
+    r.b = make_float4(0.f, 0.f, 0.f, z);
+    r.c = make_float4(0.f, 0.f, 0.f, 0.f);
+    rec[i] = r;
+    depth_key[i] = __float_as_uint(z);
+    tiles[i] = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+    rect[i] = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 16), (uint32_t)x1 | ((uint32_t)y1 << 16));
+    flags[i] = 1;
+}
+
+cudaError_t launch_splats_from_projection(int64_t m, const float* mean2d, const float* radius,
+                                          const float* depth, const ss_camera* cam,
+                                          const ss_splats* out, cudaStream_t s) {
+    if (m == 0) return cudaSuccess;
+    splats_from_projection_kernel<<<div_up(m, 256), 256, 0, s>>>(
+        m, mean2d, radius, depth, div_up(cam->width, kTile), div_up(cam->height, kTile),
+        reinterpret_cast<SplatRec*>(out->d_rec), out->d_depth_key, out->d_tiles,
+        reinterpret_cast<uint2*>(out->d_rect), out->d_flags);
+    return cudaGetLastError();
+}
+
 void fill_camf(const ss_camera* c, CamF& f) {
     f.fx = c->fx;
     f.fy = c->fy;

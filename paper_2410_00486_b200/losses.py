@@ -55,6 +55,24 @@ def photometric(rendered: torch.Tensor, target: torch.Tensor, lambda_ssim: float
     return ws
 
 
+def rendered_loss(rendered, target, lambda_ssim: float = 0.2):
+    """losses.py:137-154: (1 - l) mean|x - y| + l (1 - SSIM) and its
+    analytic gradient w.r.t. the rendered image (K6; float32 device
+    gradient).  Returns (loss, grad)."""
+    dev = rendered.device if isinstance(rendered, torch.Tensor) else torch.device("cuda")
+    x, y = _img(rendered, dev), _img(target, dev)
+    if tuple(x.shape) != tuple(y.shape):
+        raise ValueError(f"image shapes differ: {tuple(x.shape)} vs {tuple(y.shape)}")
+    grad = torch.empty_like(x)
+    sums = torch.zeros(_lib.SS_REDUCE_DOUBLES, dtype=torch.float64, device=dev)
+    photometric(x, y, lambda_ssim, grad, sums)
+    sh = sums[:2].cpu().numpy()
+    l1 = float(sh[0]) / x.numel()
+    if lambda_ssim != 0.0:
+        return (1.0 - lambda_ssim) * l1 + lambda_ssim * (1.0 - float(sh[1]) / x.numel()), grad
+    return l1, grad
+
+
 PSNR_CAP_DB = 100.0
 
 

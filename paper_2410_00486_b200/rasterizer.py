@@ -179,9 +179,31 @@ class Projection:
     rgb_active: np.ndarray
     m_cut: np.ndarray
     sh_degree: int
+    # device-side K1 outputs this view was built from (SplatBuffers, Camera,
+    # GaussianMap, RasterOpts), so build_tile_index / chain_backward on a
+    # Projection from project_map stay on the GPU
+    _device: tuple | None = field(default=None, repr=False, compare=False)
 
     def __len__(self):
         return int(self.map_index.shape[0])
+
+
+def _projection_from_splats(splats: SplatBuffers, sh_degree: int, dtype=np.float32) -> Projection:
+    """Reference-shaped (compacted, host) view of the K1 output."""
+    fl = splats.flags.cpu().numpy()
+    vis = np.flatnonzero(fl & 1).astype(np.int32)
+    rec = splats.rec.cpu().numpy()[vis]
+    aux = splats.aux.cpu().numpy()[vis] if splats.aux is not None else None
+    act = np.stack([(fl[vis] >> 1) & 1, (fl[vis] >> 2) & 1, (fl[vis] >> 3) & 1], 1)
+    dt = np.dtype(dtype)
+    c = (lambda a: None if a is None else np.ascontiguousarray(a, dtype=dt))
+    return Projection(
+        map_index=vis, t_cam=c(aux[:, 0:3]) if aux is not None else None,
+        depth=c(rec[:, 7]), mean2d=c(rec[:, 0:2]),
+        cov2d=c(aux[:, 3:6]) if aux is not None else None,
+        conic=c(np.stack([rec[:, 2], 0.5 * rec[:, 3], rec[:, 4]], 1)),
+        radius=c(aux[:, 6]) if aux is not None else None, sigma=c(rec[:, 5]), rgb=c(rec[:, 8:11]),
+        rgb_active=act.astype(bool), m_cut=c(rec[:, 6]), sh_degree=sh_degree)
 
 
 @dataclass
@@ -244,19 +266,9 @@ class RenderOutput:
     @property
     def proj(self) -> Projection:
         if "proj" not in self._cache:
-            fl = self.splats.flags.cpu().numpy()
-            vis = np.flatnonzero(fl & 1).astype(np.int32)
-            rec = self.splats.rec.cpu().numpy()[vis]
-            aux = self.splats.aux.cpu().numpy()[vis] if self.splats.aux is not None else None
-            act = np.stack([(fl[vis] >> 1) & 1, (fl[vis] >> 2) & 1, (fl[vis] >> 3) & 1], 1)
-            self._cache["proj"] = Projection(
-                map_index=vis, t_cam=aux[:, 0:3] if aux is not None else None,
-                depth=rec[:, 7].copy(), mean2d=rec[:, 0:2].copy(),
-                cov2d=aux[:, 3:6] if aux is not None else None,
-                conic=np.stack([rec[:, 2], 0.5 * rec[:, 3], rec[:, 4]], 1), radius=aux[:, 6].copy()
-                if aux is not None else None, sigma=rec[:, 5].copy(), rgb=rec[:, 8:11].copy(),
-                rgb_active=act.astype(bool), m_cut=rec[:, 6].copy(),
-                sh_degree=self.opts.sh_degree)
+            p = _projection_from_splats(self.splats, self.opts.sh_degree)
+            p._device = (self.splats, self.camera, self.gmap, self.opts)
+            self._cache["proj"] = p
         return self._cache["proj"]
 
     @property
@@ -290,6 +302,168 @@ def _as_image(x, shape, dev, name="grad_image"):
     return x
 
 
+def _bin(sp: SplatBuffers, n: int, cam: Camera, dev, st):
+    """K2-K4b with pair-capacity retry: (BinBuffers, pair count, status +
+    checkpoint-slot total as one host read)."""
+    L = lib()
+    s = stream_handle()
+    tx, ty = cam.tiles
+    n_tiles = tx * ty
+    cm = cam.to_ss()
+    key = (str(dev), n_tiles)
+    cap = max(_CAP_HINT.get(key, 0), 4 * n, 1024)
+    while True:
+        bins = BinBuffers.alloc(cap, n_tiles, dev)
+        ws = bin_workspace(n, cap, n_tiles, dev)
+        check(L.ss_bin_sort(n, ctypes.byref(sp.ss()), ctypes.byref(cm), ctypes.byref(bins.ss()),
+                            P(ws), ws.numel(), P(st), s), "ss_bin_sort")
+        # status words + the checkpoint slot total in one host read
+        sh = torch.cat((st, bins.ckpt_base[n_tiles:n_tiles + 1].to(torch.int64))).cpu()
+        raise_param_errors(sh[:-1])
+        pcount = int(sh[_lib.ST_PAIRS])
+        if not int(sh[_lib.ST_OVERFLOW]):
+            break
+        st[_lib.ST_OVERFLOW] = 0  # the overflow word is sticky; clear it for the retry
+        cap = int(pcount * 1.25) + 1024
+    _CAP_HINT[key] = cap
+    return bins, pcount, sh
+
+
+def project_map(gmap: GaussianMap, camera, *, dtype=np.float32, sh_degree: int = 3,
+                near: float = 0.01, dilation: float = 0.3,
+                alpha_min: float = 1.0 / 255.0) -> Projection:
+    """projection.py:73-163 as K1 on the GPU: every primitive projected,
+    splats behind the near plane or missing the image culled; returns the
+    reference-shaped (compacted) Projection.  The B200 path computes in
+    float32 (``dtype`` only sets the returned arrays' type); the backward
+    context fields (cov_cam, rot, q_hat, ...) are not materialised: the
+    chain recomputes them from the map (chain_backward below)."""
+    cam = Camera.of(camera)
+    opts = RasterOpts(sh_degree=sh_degree, near=near, dilation=dilation, alpha_min=alpha_min)
+    dev = gmap.device
+    st = new_status(dev)
+    sp = SplatBuffers.alloc(len(gmap), dev)
+    mp, cm, op = gmap.ss(), cam.to_ss(), opts.to_ss()
+    check(lib().ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), None, ctypes.byref(op),
+                              ctypes.byref(sp.ss()), P(st), stream_handle()), "ss_preprocess")
+    raise_param_errors(st.cpu())
+    p = _projection_from_splats(sp, sh_degree, dtype)
+    p._device = (sp, cam, gmap, opts)
+    return p
+
+
+def build_tile_index(proj: Projection, width: int, height: int, tile_size: int = 16) -> TileIndex:
+    """tiles.py:29-65 on the GPU (K2-K4b): inclusive tile rects, pairs sorted
+    by (tile, depth, row), tile ranges and active tiles -- bit-exact with the
+    reference on a float32 projection.  A Projection from project_map (or
+    RenderOutput.proj) is binned from its device buffers; any other
+    reference-shaped projection (numpy mean2d / radius / depth) is uploaded
+    as float32 first (ss_splats_from_projection)."""
+    if tile_size != 16:
+        raise ValueError("the B200 kernels are specialised for tile_size=16")
+    W, H = int(width), int(height)
+    dv = proj._device
+    if dv is not None and (dv[1].width, dv[1].height) == (W, H):
+        sp, cam = dv[0], dv[1]
+        n = int(sp.flags.numel())
+        dev = sp.flags.device
+        st = new_status(dev)
+        bins, pcount, _ = _bin(sp, n, cam, dev, st)
+        pg = bins.pairs[:pcount].cpu().numpy().astype(np.int64)
+        row = np.full(n, -1, dtype=np.int64)
+        row[proj.map_index] = np.arange(len(proj))
+        rows = row[pg]
+    else:
+        dev = torch.device("cuda")
+        m = len(proj)
+        cam = Camera(1.0, 1.0, W / 2.0, H / 2.0, W, H)  # only the image size is used
+        sp = SplatBuffers.alloc(m, dev, aux=False)
+        f32 = (lambda a, shp: torch.as_tensor(np.ascontiguousarray(a, np.float32).reshape(shp))
+               .to(dev))
+        mean2d, radius, depth = f32(proj.mean2d, (m, 2)), f32(proj.radius, (m,)), f32(proj.depth,
+                                                                                    (m,))
+        check(lib().ss_splats_from_projection(m, P(mean2d), P(radius), P(depth),
+                                              ctypes.byref(cam.to_ss()), ctypes.byref(sp.ss()),
+                                              stream_handle()), "ss_splats_from_projection")
+        st = new_status(dev)
+        bins, pcount, _ = _bin(sp, m, cam, dev, st)
+        rows = bins.pairs[:pcount].cpu().numpy().astype(np.int64)
+        pg = rows
+    tx, ty = cam.tiles
+    st_ = bins.tile_start.cpu().numpy().astype(np.int64)
+    en = bins.tile_end.cpu().numpy().astype(np.int64)
+    ln = en - st_
+    rng = np.zeros(tx * ty + 1, dtype=np.int64)
+    np.cumsum(ln, out=rng[1:])
+    return TileIndex(16, tx, ty, rows.astype(np.int32), pg, rng,
+                     np.flatnonzero(ln > 0).astype(np.int64))
+
+
+def chain_backward(proj: Projection, camera, g2d, n_primitives: int) -> dict:
+    """projection.py:200-299 as K8 on the GPU: per-splat screen-space rows
+    g2d (M, 9) [rgb3, mean2d2, conic3, opacity] -> dense float32 device
+    gradients over the map (culled primitives get zeros) plus the
+    pos2d_grad_norm densify statistic.  The projection context is
+    recomputed from the map's parameters, so ``proj`` must come from
+    project_map / RenderOutput.proj."""
+    if proj._device is None:
+        raise ValueError("chain_backward on the B200 path needs a Projection from project_map "
+                         "(the chain recomputes the projection context from the map)")
+    sp, pcam, gmap, opts = proj._device
+    cam = Camera.of(camera)
+    n = int(n_primitives)
+    if n != len(gmap):
+        raise ValueError(f"n_primitives {n} does not match the projected map ({len(gmap)})")
+    dev = gmap.device
+    rows = torch.as_tensor(np.asarray(g2d, np.float32) if not isinstance(g2d, torch.Tensor)
+                           else g2d, dtype=torch.float32).to(dev).reshape(len(proj), -1)
+    full = torch.zeros((max(n, 1), 9), dtype=torch.float32, device=dev)
+    if len(proj):
+        full[torch.as_tensor(proj.map_index.astype(np.int64), device=dev)] = rows[:, :9]
+    grads = ParamGrads.alloc(n, dev)
+    st = new_status(dev)
+    mp, cm, op = gmap.ss(), cam.to_ss(), opts.to_ss()
+    check(lib().ss_chain_backward(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op), P(full),
+                                  P(sp.flags), None, 0.0, 0, ctypes.byref(grads.ss()), P(st),
+                                  stream_handle()), "ss_chain_backward")
+    return {"position": grads.position, "rotation": grads.rotation,
+            "log_scale": grads.log_scale, "opacity_logit": grads.opacity_logit,
+            "sh": grads.sh, "pos2d_grad_norm": grads.pos2d_grad_norm}
+
+
+def replay_pixel_states(render: "RenderOutput", tile_pos: int, from_bucket: int,
+                        n_positions: int | None = None):
+    """api.py:340-368: advance the archived pixel states of active tile
+    ``tile_pos`` from checkpoint bucket ``from_bucket`` by ``n_positions``
+    list positions (default: to the tile's processed prefix k_eff).  Returns
+    host float32 arrays (T (npx,), rgb (npx, 3)) over the tile's pixels,
+    row-major; a replay to k_eff reproduces the forward's final states bit
+    for bit."""
+    if render.ckpt is None:
+        raise RuntimeError("render output has no checkpoints")
+    ti = render.tile_index
+    tile = int(ti.active_tiles[tile_pos])
+    ke = int(render.k_eff[tile_pos])
+    nb = (ke + 31) // 32
+    if not 0 <= from_bucket < nb:
+        raise IndexError(f"bucket {from_bucket} out of range for a tile with {nb} checkpoints")
+    pos_from = from_bucket * 32
+    pos_to = ke if n_positions is None else min(ke, pos_from + int(n_positions))
+    x0, y0 = ti.tile_origin(tile)
+    tw = min(16, render.camera.width - x0)
+    th = min(16, render.camera.height - y0)
+    out = torch.empty((th * tw, 4), dtype=torch.float32, device=render.image.device)
+    cm, op = render.camera.to_ss(), render.opts.to_ss()
+    check(lib().ss_replay_pixel_states(ctypes.byref(cm), ctypes.byref(op),
+                                       ctypes.byref(render.splats.ss()),
+                                       ctypes.byref(render.bins.ss()), P(render.image),
+                                       P(render.final_t), P(render.n_contrib), P(render.ckpt),
+                                       tile, int(from_bucket), int(pos_to), P(out),
+                                       stream_handle()), "ss_replay_pixel_states")
+    h = out.cpu().numpy()
+    return h[:, 0].copy(), h[:, 1:4].copy()
+
+
 def rasterize_forward(gmap: GaussianMap, camera, opts: RasterOpts | None = None) -> RenderOutput:
     """api.py:118-206 on the GPU: K1 preprocess -> K2-K4b binning -> K5 blend."""
     if opts is None:
@@ -307,22 +481,7 @@ def rasterize_forward(gmap: GaussianMap, camera, opts: RasterOpts | None = None)
     mp, cm, op = gmap.ss(), cam.to_ss(), opts.to_ss()
     check(L.ss_preprocess(ctypes.byref(mp), ctypes.byref(cm), None, ctypes.byref(op),
                           ctypes.byref(sp.ss()), P(st), s), "ss_preprocess")
-    key = (str(dev), n_tiles)
-    cap = max(_CAP_HINT.get(key, 0), 4 * n, 1024)
-    while True:
-        bins = BinBuffers.alloc(cap, n_tiles, dev)
-        ws = bin_workspace(n, cap, n_tiles, dev)
-        check(L.ss_bin_sort(n, ctypes.byref(sp.ss()), ctypes.byref(cm), ctypes.byref(bins.ss()),
-                            P(ws), ws.numel(), P(st), s), "ss_bin_sort")
-        # status words + the checkpoint slot total in one host read
-        sh = torch.cat((st, bins.ckpt_base[n_tiles:n_tiles + 1].to(torch.int64))).cpu()
-        raise_param_errors(sh[:-1])
-        pcount = int(sh[_lib.ST_PAIRS])
-        if not int(sh[_lib.ST_OVERFLOW]):
-            break
-        st[_lib.ST_OVERFLOW] = 0  # the overflow word is sticky; clear it for the retry
-        cap = int(pcount * 1.25) + 1024
-    _CAP_HINT[key] = cap
+    bins, pcount, sh = _bin(sp, n, cam, dev, st)
     n_slots = int(sh[-1])
     f32 = dict(dtype=torch.float32, device=dev)
     ckpt = torch.empty((max(n_slots, 1) * 256, 4), **f32)

@@ -829,3 +829,93 @@ def test_multiview_step_recovers_from_pair_overflow():
     assert ea.pair_capacity > 64
     np.testing.assert_allclose(ga.positions.cpu().numpy(), gb.positions.cpu().numpy(),
                                rtol=0, atol=1e-6)
+
+
+def test_stage_dropins_project_map_and_build_tile_index(case):
+    """Reference stage exports (rasterizer/__init__.py:21-36): project_map
+    (projection.py:73-163) == the forward's own K1 view; build_tile_index
+    (tiles.py:29-65) bit-exact vs the oracle, both on project_map's device
+    buffers and on an external float32 projection (the oracle's)."""
+    ss, out, cam, deg = case["ss"], case["out"], case["cam"], case["deg"]
+    p = ss.project_map(case["g"], cam, sh_degree=deg)
+    q = out.proj
+    for f in ("map_index", "depth", "mean2d", "conic", "radius", "sigma", "rgb", "rgb_active"):
+        np.testing.assert_array_equal(getattr(p, f), getattr(q, f), err_msg=f)
+    ti = ss.build_tile_index(p, cam.width, cam.height, 16)
+    ref = orc.tile_index(p.mean2d, p.radius, p.depth, cam.width, cam.height, 16)
+    np.testing.assert_array_equal(ti.pair_splat, ref.pair_splat)
+    np.testing.assert_array_equal(ti.tile_range, ref.tile_range)
+    np.testing.assert_array_equal(ti.active_tiles, ref.active_tiles)
+    # an external projection: the oracle's float64 projection rounded to float32
+    po = orc.project(_f32_map(case["g"]), cam, sh_degree=deg)
+    ext = orc.OProjection(map_index=po.map_index, t_cam=po.t_cam,
+                          depth=po.depth.astype(np.float32), mean2d=po.mean2d.astype(np.float32),
+                          cov2d=po.cov2d, conic=po.conic, radius=po.radius.astype(np.float32),
+                          sigma=po.sigma, rgb=po.rgb, rgb_active=po.rgb_active)
+    ti2 = ss.build_tile_index(ext, cam.width, cam.height, 16)
+    ref2 = orc.tile_index(ext.mean2d, ext.radius, ext.depth, cam.width, cam.height, 16)
+    np.testing.assert_array_equal(ti2.pair_splat, ref2.pair_splat)
+    np.testing.assert_array_equal(ti2.tile_range, ref2.tile_range)
+    with pytest.raises(ValueError):
+        ss.build_tile_index(p, cam.width, cam.height, 8)
+
+
+def test_stage_dropins_chain_backward_and_rendered_loss(case):
+    """chain_backward (projection.py:200-299) on per-row g2d == the
+    splat-wise path's own chain and the oracle; rendered_loss
+    (losses.py:137-154) vs the oracle."""
+    ss, out, cam, deg, d = case["ss"], case["out"], case["cam"], case["deg"], case["d"]
+    rng = np.random.default_rng(4)
+    gimg = torch.as_tensor(rng.standard_normal(out.image.shape).astype(np.float32) * 1e-3,
+                           device="cuda")
+    g2d = ss.screen_space_grads(out, gimg)
+    p = out.proj
+    rows = g2d[torch.as_tensor(p.map_index.astype(np.int64), device="cuda")]
+    got = ss.chain_backward(p, cam, rows, out.n_primitives)
+    mine = ss.rasterizer._finish_backward(out, g2d)
+    for k in ("position", "rotation", "log_scale", "opacity_logit", "pos2d_grad_norm"):
+        assert torch.equal(got[k], getattr(mine, k)), k
+    assert torch.equal(got["sh"], mine.sh)
+    ref = orc.chain(_f32_map(case["g"]), cam, orc.project(_f32_map(case["g"]), cam, sh_degree=deg),
+                    rows.cpu().numpy().astype(np.float64), out.contributed.cpu().numpy())
+    assert normwise(got["position"].cpu().numpy(), ref.position) <= 1e-3
+    with pytest.raises(ValueError):
+        ss.chain_backward(orc.project(_f32_map(case["g"]), cam, sh_degree=deg), cam, rows,
+                          out.n_primitives)
+    tgt = torch.as_tensor(d["target"], dtype=torch.float32, device="cuda")
+    loss, grad = ss.rendered_loss(out.image, tgt, 0.2)
+    lr = orc.losses(out.image.cpu().numpy().astype(np.float64),
+                    tgt.cpu().numpy().astype(np.float64), np.zeros(1), 0.2, 0.0)
+    assert abs(loss - lr.rendered) <= 1e-6 * abs(lr.rendered)
+    assert normwise(grad.cpu().numpy(), lr.grad_image) <= 1e-5
+
+
+def test_stage_dropin_replay_pixel_states(case):
+    """replay_pixel_states (api.py:340-368): from every checkpoint bucket of
+    the first active tiles, a replay to k_eff reproduces the forward's final
+    state bit for bit; a partial replay matches the oracle's replay of its
+    own forward of the GPU list (<= 1e-4)."""
+    ss, out = case["ss"], case["out"]
+    ti = out.tile_index
+    ke = out.k_eff
+    W = case["cam"].width
+    img = out.image.cpu().numpy()
+    ft = out.final_t.cpu().numpy()
+    r = _oracle_render_on_gpu_inputs(case)
+    checked = 0
+    for tp in range(min(len(ti.active_tiles), 6)):
+        x0, y0 = ti.tile_origin(ti.active_tiles[tp])
+        tw, th = min(16, W - x0), min(16, img.shape[0] - y0)
+        fT = ft[y0:y0 + th, x0:x0 + tw].reshape(-1)
+        fC = img[y0:y0 + th, x0:x0 + tw].reshape(-1, 3)
+        for b in range((int(ke[tp]) + 31) // 32):
+            T, rgb = ss.replay_pixel_states(out, tp, b)
+            np.testing.assert_array_equal(T, fT)
+            np.testing.assert_array_equal(rgb, fC)
+            T2, rgb2 = ss.replay_pixel_states(out, tp, b, n_positions=7)
+            oT, orgb = orc.replay(r, tp, b, n_positions=7)
+            assert np.abs(T2 - oT).max() <= 1e-4 and np.abs(rgb2 - orgb).max() <= 1e-4
+            checked += 1
+    assert checked > 0
+    with pytest.raises(IndexError):
+        ss.replay_pixel_states(out, 0, 10_000)
