@@ -376,6 +376,14 @@ int ss_densify_apply(const ss_map *map, void *d_workspace, const float *d_normal
                      const float *const *planes_in, float *const *planes_out,
                      const int32_t *plane_floats, int64_t *d_survivors, void *stream);
 
+/* Replaces resize_for_densify (optimizer.py:136-146): for each of n_planes
+ * per-Gaussian float planes (plane_floats[p] floats per row), rows
+ * [0, n_surv) of planes_out[p] = rows d_survivors[i] (int64) of planes_in[p],
+ * rows [n_surv, n_out) zeroed (the n_new fresh primitives); n_planes <= 16. */
+int ss_resize_moments(int64_t n_out, const int64_t *d_survivors, int64_t n_surv,
+                      int32_t n_planes, const float *const *planes_in, float *const *planes_out,
+                      const int32_t *plane_floats, void *stream);
+
 /* Builder extension A16: logit <- logit(min(sigma, ceiling)); opacity moments
  * zeroed (3DGS convention; absent from the reference). */
 int ss_opacity_reset(const ss_map *map, float ceiling, float *d_m_opacity, float *d_v_opacity,

@@ -12,6 +12,7 @@ from .core import Camera, GaussianMap, logistic, logit
 from .densify import (DensifyConfig, DensifyResult, accumulate_grad_stats, densify_and_prune,
                       opacity_reset, seed_from_points)
 from .engine import EngineConfig, MappingEngine
+from .errors import check_errors, error_mode, set_error_mode
 from .losses import (LossBreakdown, compute_losses, depth_l1, opacity_reg, psnr, rendered_loss,
                      ssim_metric, total_loss)
 from .optimizer import AdamState, LearningRates, adam_step, resize_for_densify
@@ -30,7 +31,7 @@ __all__ = [
     "GaussianMap", "LearningRates", "LossBreakdown", "MappingEngine", "ParamGrads", "Projection",
     "RasterOpts", "RenderOutput", "TileIndex", "accumulate_grad_stats", "adam_step",
     "backward_pixelwise", "backward_splatwise", "build_tile_index", "chain_backward",
-    "compute_losses", "densify_and_prune", "depth_l1", "logistic", "logit",
+    "check_errors", "compute_losses", "error_mode", "set_error_mode", "densify_and_prune", "depth_l1", "logistic", "logit",
     "KeyframeScheduler", "ScheduledMapper", "load_map", "opacity_reg", "opacity_reset", "psnr",
     "project_map", "rasterize_forward", "render_trajectory", "rendered_loss",
     "replay_pixel_states", "resize_for_densify", "save_map",

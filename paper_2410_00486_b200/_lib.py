@@ -93,6 +93,7 @@ _SIGS = {
     "ss_status_reset": (I32, [VP, VP]),
     "ss_status_begin_step": (I32, [VP, VP]),
     "ss_status_flags": (I32, [VP, VP, VP]),
+    "ss_resize_moments": (I32, [I64, VP, I64, I32, VP, VP, VP, VP]),
     "ss_splats_from_projection": (I32, [I64, VP, VP, VP, P(SSCamera), P(SSSplats), VP]),
     "ss_replay_pixel_states": (I32, [P(SSCamera), P(SSRasterOpts), P(SSSplats), P(SSBins), VP,
                                      VP, VP, VP, I32, I32, I32, VP, VP]),
@@ -166,3 +167,22 @@ def check(rc: int, what: str):
 
 def exported_symbols():
     return list(_SIGS)
+
+
+def traced(name: str):
+    """NVTX range around an API call (nsys / ncu --nvtx timelines show the
+    mapping path's stages; a no-op cost without a profiler attached)."""
+    import functools
+
+    import torch
+
+    def deco(fn):
+        @functools.wraps(fn)
+        def wrapper(*a, **k):
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*a, **k)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        return wrapper
+    return deco

@@ -57,6 +57,8 @@ cudaError_t launch_stats(const ss_map*, const ss_param_grads*, const uint8_t*, c
 cudaError_t launch_apply_stat_planes(const ss_map*, const ss_param_grads*, cudaStream_t);
 cudaError_t launch_opacity_reset(const ss_map*, float, float*, float*, cudaStream_t);
 size_t densify_workspace_bytes(int64_t);
+cudaError_t launch_resize_moments(int64_t, const int64_t*, int64_t, int, const float* const*,
+                                  float* const*, const int32_t*, cudaStream_t);
 cudaError_t launch_densify_count(const ss_map*, float, float, double, void*, int64_t*, uint8_t*,
                                  cudaStream_t);
 cudaError_t launch_densify_apply(const ss_map*, void*, const float*, uint64_t, float, float,
@@ -339,6 +341,19 @@ int ss_densify_apply(const ss_map* map, void* d_workspace, const float* d_normal
     return rc(launch_densify_apply(map, d_workspace, d_normals, seed, clone_step, shrink_log,
                                    out, n_planes, planes_in, planes_out, plane_floats, 0,
                                    d_survivors, S(stream)));
+}
+
+int ss_resize_moments(int64_t n_out, const int64_t* d_survivors, int64_t n_surv,
+                      int32_t n_planes, const float* const* planes_in, float* const* planes_out,
+                      const int32_t* plane_floats, void* stream) {
+    if (n_out < 0 || n_surv < 0 || n_surv > n_out || n_planes < 0 || n_planes > 16)
+        return SS_EINVAL;
+    if (n_surv > 0 && !d_survivors) return SS_EINVAL;
+    for (int p = 0; p < n_planes; ++p)
+        if (!planes_out[p] || (n_surv > 0 && !planes_in[p]) || plane_floats[p] < 1)
+            return SS_EINVAL;
+    return rc(launch_resize_moments(n_out, d_survivors, n_surv, n_planes, planes_in, planes_out,
+                                    plane_floats, S(stream)));
 }
 
 int ss_opacity_reset(const ss_map* map, float ceiling, float* d_m_opacity, float* d_v_opacity,

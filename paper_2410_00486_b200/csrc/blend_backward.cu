@@ -242,33 +242,14 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
     const bool hi = lane >= 16;            // lane's splats live in the second bucket
     const int sh = (2 * lane) & 31;        // their bit pair in that bucket's mask
     const int64_t count = min(*work_count, work_cap);
-    // schedule built by bwd_schedule_kernel (mode 0: the forward's list)
-    const uint32_t mode = work_counter[1];
-    const uint32_t mu = mode >> 1;
-    const uint32_t* sched_start =
-        reinterpret_cast<const uint32_t*>(work) + (2 * work_cap - (n_tiles + (int64_t)mu + 2));
-    const uint32_t* sched_tiles = sched_start + mu + 1;
-
     for (;;) {
         uint32_t item = 0;
         if (lane == 0) item = atomicAdd(work_counter, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if ((int64_t)item >= count) break;
-        int tile, u;
-        if (mode & 1u) {
-            uint32_t lo = 0, hi_ = mu;  // largest u with start[u] <= item
-            while (hi_ - lo > 1) {
-                const uint32_t mid = (lo + hi_) >> 1;
-                if (sched_start[mid] <= item) lo = mid;
-                else hi_ = mid;
-            }
-            u = (int)lo;
-            tile = (int)sched_tiles[item - sched_start[lo]];
-        } else {
-            const uint2 wk = work[item];
-            tile = (int)wk.x;
-            u = (int)wk.y;
-        }
+        // (tile, unit) in bwd_schedule_kernel's longest-first order
+        const uint2 wk = work[item];
+        const int tile = (int)wk.x, u = (int)wk.y;
         const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
         const uint32_t start = tile_start[tile];
         const int ke = k_eff[tile];
@@ -416,18 +397,310 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
     }
 }
 
+// --------------------------------------------------------------------------
+// Sparse two-phase variant (the default).  The wavefront above evaluates
+// every (pixel, list position) slot of a unit and zeroes the ones the pixel
+// did not blend; at the bench workload only 25 % of those slots are blended
+// (15 % after 250 training iterations: low opacities, long lists), so ~80 %
+// of its FMA / MUFU work is predicated away.  Here a CTA of 256 threads
+// takes one checkpoint bucket (tile, 32 list positions) at a time:
+//
+//   phase 1 (thread = pixel): walk the set bits of the pixel's blend mask
+//     in list order from the bucket's checkpoint -- exactly the pairs the
+//     forward blended, with its arithmetic (splat_power / splat_falloff) --
+//     and emit per blended pair w = alpha T and the alpha-path gradient
+//     da = alpha dL/dalpha (kernels.py:342-364), written SPLAT-MAJOR into
+//     shared memory: the slot of (pixel, position k) is known before the
+//     walk from per-warp ballots of the masks (rank among the pixels that
+//     blended k);
+//   phase 2 (8 threads per list position): each position's pairs are summed
+//     into its 9 (10) screen-space gradients, the 8 partial rows are
+//     combined with shuffles and committed with one red.add row per
+//     (tile, splat), as in the wavefront.
+//
+// Work is proportional to the blended pairs; there is no cross-lane state
+// passing and no ramp.  Shared memory holds the worst case of one bucket
+// (32 x 256 pairs).
+constexpr int kSpThreads = kTilePx;             // one thread per tile pixel
+constexpr int kSpWarps = kSpThreads / 32;
+constexpr int kSpMaxPairs = kBucket * kTilePx;  // every pixel blends every position
+constexpr int kSpRuns = kBucket * (kTilePx / 64);  // runs of <= 64 pairs per position
+
+struct SpShared {
+    float2 wd[kSpMaxPairs];         // (alpha T, alpha dL/dalpha) per blended pair, splat-major
+    uint8_t pid[kSpMaxPairs];       // tile-local pixel of the pair
+    float4 g[kTilePx];              // per pixel (g_r, g_g, g_b, g_depth)
+    float2 xy[kTilePx];             // per pixel (x, y)
+    SplatRec rec[kUnit];            // the unit's 64 list positions
+    uint32_t sid[kUnit];
+    uint32_t bal[kSpWarps][kBucket];  // per warp, per position: which lanes blended it
+    uint32_t off[kBucket][kSpWarps];  // slot base of (position, warp)
+    uint32_t run[kSpRuns];            // phase-2 runs: begin | len << 13 | position << 20
+    int nrun;
+    int next;
+};
+
+// 32 x 32 bit-matrix transpose across a warp: lane l holds row l (bit k =
+// M[l][k]); returns column `lane` (bit l = M[l][lane]).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+    const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int j = 16 >> s;
+        const uint32_t m = masks[s];
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+        x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+    }
+    return x;
+}
+
+template <bool DEPTH>
+__global__ void __launch_bounds__(kSpThreads, 2) backward_sparse_kernel(
+    int W, int H, int tiles_x, const uint32_t* __restrict__ tile_start,
+    const uint32_t* __restrict__ ckpt_base, const int32_t* __restrict__ k_eff,
+    const uint32_t* __restrict__ pairs, const SplatRec* __restrict__ rec, float amax,
+    const float* __restrict__ image, const float* __restrict__ grad_image,
+    const float4* __restrict__ pixgrad, const float* __restrict__ depth_img,
+    const float* __restrict__ grad_depth, const int32_t* __restrict__ n_contrib,
+    const float4* __restrict__ ckpt, const float* __restrict__ ckpt_depth,
+    const uint32_t* __restrict__ ckpt_mask, const uint2* __restrict__ work,
+    const int64_t* __restrict__ work_count, int64_t work_cap, uint32_t* work_counter,
+    float* __restrict__ g2d, uint8_t* __restrict__ contributed) {
+    constexpr int NC = DEPTH ? 10 : 9;
+    extern __shared__ __align__(16) unsigned char sp_smem[];
+    SpShared& S = *reinterpret_cast<SpShared*>(sp_smem);
+    PDL_WAIT();
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int64_t count = min(*work_count, work_cap);
+    // phase-2 role: group grp of 8 threads (sub-lane sub) takes runs grp, grp + 32, ...
+    const int grp = t >> 3, sub = t & 7;
+    if (t == 0) S.next = (int)atomicAdd(work_counter, 1u);
+    __syncthreads();
+
+    for (;;) {
+        const uint32_t item = (uint32_t)S.next;
+        if ((int64_t)item >= count) break;
+        __syncthreads();  // everyone has read S.next
+        // the next item's index is fetched now; its latency hides under this one
+        if (t == 0) S.next = (int)atomicAdd(work_counter, 1u);
+        const uint2 wk = work[item];  // (tile, unit), longest-first order
+        const int tile = (int)wk.x, u = (int)wk.y;
+        const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
+        const uint32_t start = tile_start[tile];
+        const int ke = k_eff[tile];
+        const uint32_t cb = ckpt_base[tile];
+        const int kb0 = u * kUnit;
+        const int nbk = min(2, (ke - kb0 + kBucket - 1) / kBucket);  // buckets of the unit
+        // ---- every global load of the unit issued up front: the pixel's
+        //      n_contrib, both buckets' masks and states, its gradient; the
+        //      64 positions' records (validity is applied after the loads)
+        const int ix = x0 + (t & 15), iy = y0 + (t >> 4);
+        const bool inimg = ix < W && iy < H;
+        const size_t o = inimg ? (size_t)iy * W + ix : 0;
+        const size_t slot0 = (size_t)(cb + 2 * u) * kTilePx + t;
+        const int nct = inimg ? n_contrib[o] : 0;
+        uint32_t m0 = ckpt_mask[slot0];
+        uint32_t m1 = nbk > 1 ? ckpt_mask[slot0 + kTilePx] : 0u;
+        const float4 ck0 = ckpt[slot0];
+        const float4 ck1 = nbk > 1 ? ckpt[slot0 + kTilePx] : make_float4(1.f, 0.f, 0.f, 0.f);
+        float cd0 = 0.f, cd1 = 0.f;
+        if (DEPTH) {
+            cd0 = ckpt_depth[slot0];
+            cd1 = nbk > 1 ? ckpt_depth[slot0 + kTilePx] : 0.f;
+        }
+        float4 pg = make_float4(0.f, 0.f, 0.f, 0.f);
+        float gd = 0.f;
+        if (inimg) {
+            if (pixgrad) {
+                pg = pixgrad[o];
+            } else {
+                pg.x = grad_image[3 * o];
+                pg.y = grad_image[3 * o + 1];
+                pg.z = grad_image[3 * o + 2];
+                pg.w = pg.x * image[3 * o] + pg.y * image[3 * o + 1] + pg.z * image[3 * o + 2];
+            }
+            if (DEPTH) {
+                gd = grad_depth ? grad_depth[o] : 0.f;
+                if (!pixgrad) pg.w += gd * depth_img[o];
+            }
+        }
+        if (t < kUnit) {
+            const int k = kb0 + t;
+            uint32_t sg = 0xffffffffu;
+            if (k < ke) {
+                sg = pairs[start + k];
+                S.rec[t] = rec[sg];
+            }
+            S.sid[t] = sg;
+        }
+        const float px = (float)ix, py = (float)iy;
+        S.g[t] = make_float4(pg.x, pg.y, pg.z, gd);
+        S.xy[t] = make_float2(px, py);
+        // a bucket's mask and state exist for pixels still blending at its start
+        m0 = nct > kb0 ? m0 : 0u;
+        m1 = nct > kb0 + kBucket ? m1 : 0u;
+        for (int half = 0; half < nbk; ++half) {
+            const uint32_t mask = half ? m1 : m0;
+            const float4 ck = half ? ck1 : ck0;
+            float T = ck.x;
+            float G = pg.x * ck.y + pg.y * ck.z + pg.z * ck.w;
+            if (DEPTH) G += gd * (half ? cd1 : cd0);
+            const SplatRec* R32 = S.rec + kBucket * half;
+            // per warp and position: the lanes that blended it -- the warp's
+            // 32 x 32 bit matrix of masks transposed in 5 butterfly stages
+            S.bal[wid][lane] = warp_transpose32(mask, lane);
+            __syncthreads();
+            // slot bases (position-major, warps in order inside a position) and
+            // the phase-2 runs (<= 64 consecutive pairs of one position)
+            if (wid == 0) {
+                uint32_t c[kSpWarps], tot = 0;
+#pragma unroll
+                for (int w = 0; w < kSpWarps; ++w) {
+                    c[w] = tot;
+                    tot += __popc(S.bal[w][lane]);
+                }
+                uint32_t inc = tot;  // inclusive scans of the totals and run counts
+                const uint32_t nr = (tot + 63u) >> 6;
+                uint32_t rinc = nr;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xffffffffu, inc, d);
+                    const uint32_t rv = __shfl_up_sync(0xffffffffu, rinc, d);
+                    if (lane >= d) {
+                        inc += v;
+                        rinc += rv;
+                    }
+                }
+                const uint32_t base = inc - tot;
+#pragma unroll
+                for (int w = 0; w < kSpWarps; ++w) S.off[lane][w] = base + c[w];
+                for (uint32_t j = 0; j < nr; ++j) {
+                    const uint32_t b = base + 64u * j;
+                    S.run[rinc - nr + j] = b | (min(64u, base + tot - b) << 13) | ((uint32_t)lane << 20);
+                }
+                if (lane == 31) S.nrun = (int)rinc;
+            }
+            __syncthreads();
+            // ---- phase 1: the pixel's blended pairs in list order; the next
+            //      pair's record is loaded while this one computes
+            if (mask) {
+                uint32_t m = mask;
+                const uint32_t lt = lanemask_lt();
+                int k = __ffs(m) - 1;
+                m &= m - 1;
+                SplatRec R = R32[k];
+                for (;;) {
+                    const bool more = m != 0u;
+                    const int kn = more ? __ffs(m) - 1 : k;
+                    m &= m - 1;
+                    const SplatRec Rn = R32[kn];
+                    float dx, dy;
+                    const float a0 = splat_falloff(splat_power(px, py, R.a, R.b, dx, dy), R.b);
+                    const float a = fminf(a0, amax);
+                    const float w = __fmul_rn(a, T);
+                    float grgb = fmaf(pg.z, R.c.z, fmaf(pg.y, R.c.y, pg.x * R.c.x));
+                    if (DEPTH) grgb = fmaf(gd, R.b.w, grgb);
+                    const float Gafter = fmaf(grgb, w, G);
+                    const float om = __fsub_rn(1.f, a);
+                    // dL/da = T (g . rgb) - (g . image - G_after) / (1 - a); 0 when clamped
+                    const float dal = fmaf(T, grgb, (Gafter - pg.w) * rcp_approx(om));
+                    const float da = dal * (a != amax ? a : 0.f);
+                    T = __fmul_rn(T, om);
+                    G = Gafter;
+                    const uint32_t r = S.off[k][wid] + __popc(S.bal[wid][k] & lt);
+                    S.wd[r] = make_float2(w, da);
+                    S.pid[r] = (uint8_t)t;
+                    if (!more) break;
+                    k = kn;
+                    R = Rn;
+                }
+            }
+            __syncthreads();
+            // ---- phase 2: runs of <= 64 pairs of one position, 8 threads each;
+            //      one red.add row per run
+            const int nrun = S.nrun;
+            // the group's lanes (groups of a warp may run different numbers of runs)
+            const uint32_t gmask = 0xffu << (8 * (grp & 3));
+            for (int ri = grp; ri < nrun; ri += kSpThreads / 8) {
+                const uint32_t rw = S.run[ri];
+                const uint32_t rb = rw & 8191u, rl = (rw >> 13) & 127u;
+                const int kq = (int)(rw >> 20);
+                const float4 A = R32[kq].a, B = R32[kq].b;
+                const f32x2 mxy = pk2(A.x, A.y);
+                f32x2 acc_rg = pk2(0.f, 0.f), s_d = acc_rg, s_xxy = acc_rg;
+                float acc_b = 0.f, acc_z = 0.f, s_da = 0.f, s_yy = 0.f;
+#pragma unroll 2
+                for (uint32_t r = rb + sub; r < rb + rl; r += 8) {
+                    const float2 wd = S.wd[r];
+                    const int p = S.pid[r];
+                    const float4 g = S.g[p];
+                    const float2 xy = S.xy[p];
+                    acc_rg = fma2(pk2(wd.x, wd.x), pk2(g.x, g.y), acc_rg);
+                    acc_b = fmaf(wd.x, g.z, acc_b);
+                    if (DEPTH) acc_z = fmaf(wd.x, g.w, acc_z);
+                    const f32x2 dxy = sub2(pk2(xy.x, xy.y), mxy);
+                    const f32x2 txy = mul2(pk2(wd.y, wd.y), dxy);
+                    s_da += wd.y;
+                    s_d = add2(s_d, txy);
+                    float tx, ty, dx, dy;
+                    upk2(txy, tx, ty);
+                    upk2(dxy, dx, dy);
+                    s_xxy = fma2(pk2(tx, tx), dxy, s_xxy);
+                    s_yy = fmaf(ty, dy, s_yy);
+                }
+                float acc[NC];
+                upk2(acc_rg, acc[0], acc[1]);
+                acc[2] = acc_b;
+                float s_dx, s_dy, s_xx, s_xy;
+                upk2(s_d, s_dx, s_dy);
+                upk2(s_xxy, s_xx, s_xy);
+#pragma unroll
+                for (int d = 1; d < 8; d <<= 1) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) acc[c] += __shfl_xor_sync(gmask, acc[c], d);
+                    if (DEPTH) acc_z += __shfl_xor_sync(gmask, acc_z, d);
+                    s_da += __shfl_xor_sync(gmask, s_da, d);
+                    s_dx += __shfl_xor_sync(gmask, s_dx, d);
+                    s_dy += __shfl_xor_sync(gmask, s_dy, d);
+                    s_xx += __shfl_xor_sync(gmask, s_xx, d);
+                    s_xy += __shfl_xor_sync(gmask, s_xy, d);
+                    s_yy += __shfl_xor_sync(gmask, s_yy, d);
+                }
+                if (sub == 0) {
+                    // splat-constant factors once (see the wavefront's commit)
+                    const float c1 = 0.5f * A.w;
+                    acc[3] = A.z * s_dx + c1 * s_dy;
+                    acc[4] = c1 * s_dx + B.x * s_dy;
+                    acc[5] = -0.5f * s_xx;
+                    acc[6] = -s_xy;
+                    acc[7] = -0.5f * s_yy;
+                    acc[8] = s_da / B.y;
+                    if (DEPTH) acc[NC - 1] = acc_z;
+                    const uint32_t sg = S.sid[kBucket * half + kq];
+                    float* row = g2d + (size_t)sg * NC;
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        if (acc[c] != 0.f) atomicAdd(row + c, acc[c]);
+                    if (contributed) contributed[sg] = 1;
+                }
+            }
+            __syncthreads();  // the bucket's shared state is reused by the next one
+        }
+    }
+}
+
 // Longest-units-first schedule.  A unit's size is roughly the number of
 // pixels still blending at its first bucket, so earlier units of a tile are
 // larger, and tiles with more units are the deeper ones.  Handing units out
 // unit-index-major with the tiles of each index in descending unit count
 // approximates longest-processing-time-first and shortens the tail of the
 // persistent backward.  One CTA builds it from k_eff: tiles counting-sorted
-// by unit count, descending (S), and start[u] = sum over u' < u of #tiles
-// with more than u' units; item c is unit u (largest u with start[u] <= c)
-// of tile S[c - start[u]].  Written at the end of the work buffer (past the
-// forward's list); the mode word (high half of the status block's counter
-// word) = 1 | max_units << 1, or 0 to keep the forward's list (more than
-// kMaxUnits units in a tile, too many tiles, or no room).
+// by unit count, descending (S; the tiles with more than u units are a
+// prefix of S), start[u] = sum over u' < u of #tiles with more than u'
+// units; item start[u] + i is unit u of tile S[i].  The list is written IN
+// PLACE over the forward's (same items, any order), so the backward reads
+// its items with one load.  Tiles with more than kMaxUnits units, or more
+// than kSchedTiles tiles: the forward's list is kept.
 constexpr int kMaxUnits = 1024;
 constexpr int kSchedTiles = 16384;  // 4K frames at 16 px tiles fit
 
@@ -437,13 +710,12 @@ __global__ void __launch_bounds__(1024) bwd_schedule_kernel(uint32_t* counter,
                                                             int64_t wl_cap,
                                                             const int64_t* __restrict__ total) {
     __shared__ uint32_t h[kMaxUnits + 1];
+    __shared__ uint32_t s_start[kMaxUnits + 1];
     __shared__ uint16_t s_nb[kSchedTiles];
     __shared__ uint32_t s_max;
     const int t = threadIdx.x;
-    if (n_tiles > kSchedTiles) {
-        if (t == 0) counter[1] = 0u;
-        return;
-    }
+    if (t == 0) counter[1] = 0u;  // items are read as work[item] (kept for the ABI word)
+    if (n_tiles > kSchedTiles) return;
     for (int v = t; v <= kMaxUnits; v += blockDim.x) h[v] = 0u;
     if (t == 0) s_max = 0u;
 #pragma unroll 8
@@ -459,13 +731,7 @@ __global__ void __launch_bounds__(1024) bwd_schedule_kernel(uint32_t* counter,
     atomicMax(&s_max, m);
     __syncthreads();
     const uint32_t mu = s_max;
-    const int64_t off = wl_cap - ((int64_t)n_tiles + mu + 2);
-    if (mu > (uint32_t)kMaxUnits || off < 2 * min(*total, wl_cap / 2)) {
-        if (t == 0) counter[1] = 0u;  // keep the forward's list
-        return;
-    }
-    uint32_t* start = wl + off;    // [mu + 1]
-    uint32_t* S = start + mu + 1;  // [n_tiles]
+    if (mu > (uint32_t)kMaxUnits || *total > wl_cap / 2) return;  // keep the forward's list
     if (t == 0) {
         uint32_t above = 0;
         for (int v = (int)mu; v >= 0; --v) {  // h[v] -> #tiles with more than v units
@@ -475,20 +741,21 @@ __global__ void __launch_bounds__(1024) bwd_schedule_kernel(uint32_t* counter,
         }
         uint32_t pre = 0;
         for (uint32_t u = 0; u < mu; ++u) {
-            start[u] = pre;
+            s_start[u] = pre;
             pre += h[u];
         }
-        start[mu] = pre;
+        s_start[mu] = pre;
     }
     __syncthreads();
     for (int q = t; q < n_tiles; q += blockDim.x) {
         const uint32_t nb = s_nb[q];
-        if (nb != 0) S[atomicAdd(&h[nb], 1u)] = (uint32_t)q;
-    }
-    __syncthreads();
-    if (t == 0) {
-        __threadfence();
-        counter[1] = 1u | (mu << 1);
+        if (nb == 0) continue;
+        const uint32_t pos = atomicAdd(&h[nb], 1u);  // this tile's index in S
+        for (uint32_t u = 0; u < nb; ++u) {
+            const uint32_t c = s_start[u] + pos;
+            wl[2 * c] = (uint32_t)q;
+            wl[2 * c + 1] = u;
+        }
     }
 }
 
@@ -531,11 +798,34 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
     int tx = div_up(cam->width, kTile), ty = div_up(cam->height, kTile);
     launch_pdl(bwd_clear_kernel, dim3(div_up(n * ncol > 4 ? n * ncol / 4 : 1, 256)), dim3(256),
                0, s, g2d, (int64_t)n * ncol, contributed, n, counter);
-    const int threads = 32 * kBwdWarps;
-    const size_t smem = 0;
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static const bool wavefront = [] {
+        const char* e = getenv("SS_BWD_SPARSE");  // 1: the sparse two-phase kernel
+        return !(e && e[0] == '1');
+    }();
+    if (!wavefront) {
+        const size_t sm_bytes = sizeof(SpShared);
+        auto go = [&](auto kern) -> cudaError_t {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)sm_bytes);
+            if (e != cudaSuccess) return e;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSpThreads, sm_bytes);
+            if (per_sm < 1) per_sm = 1;
+            launch_pdl(kern, dim3(sms * per_sm), dim3(kSpThreads), sm_bytes, s,
+                cam->width, cam->height, tx, bins->d_tile_start, bins->d_ckpt_base, k_eff,
+                bins->d_pair_splat, reinterpret_cast<const SplatRec*>(sp->d_rec), o->alpha_max,
+                image, grad_image, pixgrad, depth, grad_depth, n_contrib,
+                reinterpret_cast<const float4*>(ckpt), ckpt_depth, ckpt_mask,
+                reinterpret_cast<const uint2*>(work), &st->bucket_count, work_cap, counter, g2d,
+                contributed);
+            return cudaGetLastError();
+        };
+        return depthf ? go(backward_sparse_kernel<true>) : go(backward_sparse_kernel<false>);
+    }
+    const int threads = 32 * kBwdWarps;
+    const size_t smem = 0;
     auto go = [&](auto kern) -> cudaError_t {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
         if (per_sm < 1) per_sm = 1;

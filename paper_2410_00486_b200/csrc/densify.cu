@@ -275,4 +275,43 @@ cudaError_t launch_densify_apply(const ss_map* mp, void* ws, const float* normal
     return cudaGetLastError();
 }
 
+// resize_for_densify (optimizer.py:136-146) for a moment set: per plane,
+// out[i] = in[survivors[i]] for i < n_surv, zero rows after (n_new fresh
+// primitives).  One launch for every plane (grid.y = plane).
+struct ResizePlanes {
+    const float* in[16];
+    float* out[16];
+    int32_t k[16];
+};
+
+__global__ void resize_moments_kernel(int64_t n_out, const int64_t* __restrict__ surv,
+                                      int64_t n_surv, ResizePlanes P) {
+    const int pl = blockIdx.y;
+    const int k = P.k[pl];
+    const int64_t nf = n_out * k;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nf;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e / k, c = e - row * k;
+        P.out[pl][e] = row < n_surv ? P.in[pl][surv[row] * k + c] : 0.f;
+    }
+}
+
+cudaError_t launch_resize_moments(int64_t n_out, const int64_t* surv, int64_t n_surv,
+                                  int n_planes, const float* const* pin, float* const* pout,
+                                  const int32_t* pk, cudaStream_t s) {
+    if (n_planes == 0 || n_out == 0) return cudaSuccess;
+    ResizePlanes P = {};
+    int kmax = 1;
+    for (int p = 0; p < n_planes; ++p) {
+        P.in[p] = pin[p];
+        P.out[p] = pout[p];
+        P.k[p] = pk[p];
+        kmax = pk[p] > kmax ? pk[p] : kmax;
+    }
+    const int64_t nf = n_out * kmax;
+    const int blocks = (int)((nf + 255) / 256 < 4096 ? (nf + 255) / 256 : 4096);
+    resize_moments_kernel<<<dim3(blocks, n_planes), 256, 0, s>>>(n_out, surv, n_surv, P);
+    return cudaGetLastError();
+}
+
 }  // namespace ss

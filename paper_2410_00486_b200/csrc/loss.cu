@@ -206,10 +206,10 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
         }
         __syncthreads();
         // vertical (axis 0): column q, 4 consecutive rows
-        float mom[5][4];
+        float mom[2][4];
+        double mom2[3][4];  // second moments: the vertical taps accumulate in float64
         {
             f32x2 v2[14], o2[4];
-            float v[14];
 #pragma unroll
             for (int i = 0; i < 14; ++i) {
                 const float2 e = shp[4 * rg + i][q];
@@ -218,17 +218,28 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
             taps4x2(v2, win, o2);
 #pragma unroll
             for (int o = 0; o < 4; ++o) upk2(o2[o], mom[0][o], mom[1][o]);
+            float vx[14], vy[14], vm[14];
 #pragma unroll
             for (int i = 0; i < 14; ++i) {
                 const float2 e = shq[4 * rg + i][q];
-                v2[i] = pk2(e.x, e.y);
+                vx[i] = e.x;
+                vy[i] = e.y;
+                vm[i] = shm[4 * rg + i][q];
             }
-            taps4x2(v2, win, o2);
 #pragma unroll
-            for (int o = 0; o < 4; ++o) upk2(o2[o], mom[2][o], mom[3][o]);
+            for (int o = 0; o < 4; ++o) {
+                double axx = 0.0, ayy = 0.0, axy = 0.0;
 #pragma unroll
-            for (int i = 0; i < 14; ++i) v[i] = shm[4 * rg + i][q];
-            taps4(v, win, mom[4]);
+                for (int m = 0; m < 11; ++m) {
+                    const double wd = (double)win.w[m];
+                    axx = fma(wd, (double)vx[o + m], axx);
+                    ayy = fma(wd, (double)vy[o + m], ayy);
+                    axy = fma(wd, (double)vm[o + m], axy);
+                }
+                mom2[0][o] = axx;
+                mom2[1][o] = ayy;
+                mom2[2][o] = axy;
+            }
         }
         const int ox = x0 + q;
 #pragma unroll
@@ -238,8 +249,8 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
                 // epilogue in float64 (losses.py:99-109,119-134): ~30 flops per
                 // output, small next to the 110 float32 moment taps
                 const double mxs = mom[0][o], mys = mom[1][o];  // means about (cx, cy)
-                const double sxx = mom[2][o] - mxs * mxs, syy = mom[3][o] - mys * mys;
-                const double sxy = mom[4][o] - mxs * mys;
+                const double sxx = mom2[0][o] - mxs * mxs, syy = mom2[1][o] - mys * mys;
+                const double sxy = mom2[2][o] - mxs * mys;
                 const double mx = mxs + cx, my = mys + cy;
                 const double a1 = 2.0 * mx * my + C1d, a2 = 2.0 * sxy + C2d;
                 const double b1 = mx * mx + my * my + C1d, b2 = sxx + syy + C2d;

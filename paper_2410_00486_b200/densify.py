@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from ._lib import check, lib
+from ._lib import check, lib, traced
 from .core import GaussianMap
 from .rasterizer import ParamGrads, P, stream_handle
 
@@ -50,6 +50,7 @@ class DensifyResult:
     n_pruned: int
 
 
+@traced("ss.seed_from_points")
 def seed_from_points(points, colors, scene_extent: float = 1.0, device=None):
     """densify.py:53-83 on the GPU: one isotropic primitive per point, scale =
     mean distance to the 3 nearest neighbours in the cloud (exact kNN on a
@@ -88,6 +89,7 @@ def seed_from_points(points, colors, scene_extent: float = 1.0, device=None):
     return out["positions"], out["rotations"], out["log_scales"], out["opacity_logits"], sh
 
 
+@traced("ss.accumulate_grad_stats")
 def accumulate_grad_stats(gmap: GaussianMap, grads: ParamGrads) -> GaussianMap:
     """densify.py:86-100."""
     if len(grads) != len(gmap):
@@ -115,6 +117,7 @@ def densify_count(gmap: GaussianMap, config: DensifyConfig, scene_extent: float)
     return ws, counts.cpu().numpy(), mask[:n]
 
 
+@traced("ss.densify_and_prune")
 def densify_and_prune(gmap: GaussianMap, config: DensifyConfig, scene_extent: float,
                       rng=None, normals=None, extra_planes=()) -> DensifyResult:
     """densify.py:103-173, in place on ``gmap``.

@@ -32,7 +32,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import check, lib
+from ._lib import check, lib, traced
 from .core import Camera, GaussianMap
 from .densify import DensifyConfig, densify_and_prune, opacity_reset
 from .optimizer import AdamState, LearningRates
@@ -155,7 +155,9 @@ class MappingEngine:
         self._pdev.copy_(slot, non_blocking=True)
 
     def _mark(self, name):
-        """Stage boundary for the per-kernel timing bench.py reports."""
+        """Stage boundary: an NVTX marker (profiler timelines) and, when
+        profiling, an event for the per-kernel timing bench.py reports."""
+        torch.cuda.nvtx.mark("ss." + name)
         if self.profile is not None:
             ev = torch.cuda.Event(enable_timing=True)
             ev.record()
@@ -291,6 +293,7 @@ class MappingEngine:
         rec.event.record()
 
     # ---------------------------------------------------------- main step
+    @traced("ss.MappingEngine.step")
     def step(self, camera, target: torch.Tensor, target_depth: torch.Tensor | None = None):
         """One fused mapping iteration (single view, single GPU)."""
         self._maybe_densify()
@@ -471,6 +474,7 @@ class MappingEngine:
             self.synchronize()
             opacity_reset(self.gmap, self.state, cfg.opacity_reset_ceiling)
 
+    @traced("ss.MappingEngine.densify")
     def densify(self, normals=None):
         """densify_and_prune + resize_for_densify as one compaction
         (trainer.py:187-193)."""
@@ -548,6 +552,7 @@ class MappingEngine:
                                         pin_memory=True)
         return self._flat, self._fss
 
+    @traced("ss.MappingEngine.multiview_step")
     def multiview_step(self, cameras, targets, target_depths=None, allreduce=None,
                        add_reg: bool = True):
         """Keyframe batch: the sum of per-view gradients

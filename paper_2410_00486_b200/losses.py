@@ -14,8 +14,8 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _lib
-from ._lib import check, lib
+from . import _lib, errors
+from ._lib import check, lib, traced
 from .rasterizer import P, stream_handle
 
 SSIM_WINDOW = 11
@@ -26,15 +26,33 @@ SSIM_C2 = 0.03 ** 2
 
 @dataclass
 class LossBreakdown:
-    """losses.py:185-195."""
+    """losses.py:185-195.  The scalars are Python floats; in deferred error
+    mode (errors.py) they are read from the device when first used."""
 
-    l1: float
-    ssim_loss: float
-    rendered: float
-    opacity_reg: float
-    total: float
-    grad_image: torch.Tensor
-    grad_opacity_logit: torch.Tensor
+    _SCALARS = ("l1", "ssim_loss", "rendered", "opacity_reg", "total")
+
+    def __init__(self, l1=None, ssim_loss=None, rendered=None, opacity_reg=None, total=None,
+                 grad_image=None, grad_opacity_logit=None, resolve=None):
+        self._resolve = resolve
+        self._vals = None if resolve is not None else dict(
+            l1=l1, ssim_loss=ssim_loss, rendered=rendered, opacity_reg=opacity_reg, total=total)
+        self.grad_image = grad_image
+        self.grad_opacity_logit = grad_opacity_logit
+
+    def _get(self, k):
+        if self._vals is None:
+            self._vals = self._resolve()
+            self._resolve = None
+        return self._vals[k]
+
+    l1 = property(lambda self: self._get("l1"))
+    ssim_loss = property(lambda self: self._get("ssim_loss"))
+    rendered = property(lambda self: self._get("rendered"))
+    opacity_reg = property(lambda self: self._get("opacity_reg"))
+    total = property(lambda self: self._get("total"))
+
+    def __repr__(self):
+        return "LossBreakdown(" + ", ".join(f"{k}={self._get(k)!r}" for k in self._SCALARS) + ")"
 
 
 def _img(x, dev):
@@ -55,6 +73,7 @@ def photometric(rendered: torch.Tensor, target: torch.Tensor, lambda_ssim: float
     return ws
 
 
+@traced("ss.rendered_loss")
 def rendered_loss(rendered, target, lambda_ssim: float = 0.2):
     """losses.py:137-154: (1 - l) mean|x - y| + l (1 - SSIM) and its
     analytic gradient w.r.t. the rendered image (K6; float32 device
@@ -101,6 +120,7 @@ def psnr(a, b) -> float:
     return min(PSNR_CAP_DB, 10.0 * float(np.log10(1.0 / mse)))
 
 
+@traced("ss.compute_losses")
 def compute_losses(rendered, target, opacity_logits, lambda_ssim: float = 0.2,
                    lambda_o: float = 0.001) -> LossBreakdown:
     """losses.py:198-228."""
@@ -120,15 +140,20 @@ def compute_losses(rendered, target, opacity_logits, lambda_ssim: float = 0.2,
     g_logit = torch.empty(n, dtype=torch.float32, device=dev)
     check(lib().ss_opacity_reg(n, P(logits), float(lambda_o), P(g_logit), 0, P(osum),
                                stream_handle()), "ss_opacity_reg")
-    sh = torch.cat((sums[:2], osum[:1])).cpu().numpy()  # one host read
+    dsums = torch.cat((sums[:2], osum[:1]))
     npx = H * W * 3
-    l1 = float(sh[0] / npx)
-    ssim_loss = 1.0 - float(sh[1] / npx) if lambda_ssim != 0.0 else 0.0
-    rendered_val = (1.0 - lambda_ssim) * l1 + lambda_ssim * ssim_loss
-    reg = float(sh[2] / n) if n else 0.0
-    return LossBreakdown(l1=l1, ssim_loss=ssim_loss, rendered=rendered_val, opacity_reg=reg,
-                         total=rendered_val + lambda_o * reg, grad_image=grad,
-                         grad_opacity_logit=g_logit)
+
+    def resolve():
+        sh = dsums.cpu().numpy()  # one host read
+        l1 = float(sh[0] / npx)
+        ssim_loss = 1.0 - float(sh[1] / npx) if lambda_ssim != 0.0 else 0.0
+        rendered_val = (1.0 - lambda_ssim) * l1 + lambda_ssim * ssim_loss
+        reg = float(sh[2] / n) if n else 0.0
+        return dict(l1=l1, ssim_loss=ssim_loss, rendered=rendered_val, opacity_reg=reg,
+                    total=rendered_val + lambda_o * reg)
+    if errors.deferred():
+        return LossBreakdown(grad_image=grad, grad_opacity_logit=g_logit, resolve=resolve)
+    return LossBreakdown(**resolve(), grad_image=grad, grad_opacity_logit=g_logit)
 
 
 def opacity_reg(opacities):

@@ -11,12 +11,14 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 
 from . import _lib
-from ._lib import check, lib
+from ._lib import check, lib, traced
 from .core import GaussianMap
-from .rasterizer import P, ParamGrads, finite_flags, stream_handle
+from . import errors
+from .rasterizer import P, ParamGrads, finite_flags, finite_flags_device, stream_handle
 
 PARAM_SHAPES = {
     "position": (3,),
@@ -105,6 +107,7 @@ class AdamState:
         return g
 
 
+@traced("ss.adam_step")
 def adam_step(gmap: GaussianMap, grads: ParamGrads, state: AdamState, sh_degree: int | None = None):
     """optimizer.py:101-133.  Returns (gmap, state)."""
     if len(grads) != len(gmap):
@@ -113,13 +116,25 @@ def adam_step(gmap: GaussianMap, grads: ParamGrads, state: AdamState, sh_degree:
     named = (("position", grads.position), ("rotation", grads.rotation),
              ("log_scale", grads.log_scale), ("opacity_logit", grads.opacity_logit),
              ("sh_dc", grads.sh_dc), ("sh_rest", grads.sh_rest))
-    # the finite checks and the "sh_rest in use" test as one host read
-    extra = () if state.sh_rest_active else ((grads.sh_rest != 0).any(),)
-    host = finite_flags([t for _, t in named], extra)
-    for (name, _), good in zip(named, host):
-        if not good:
-            raise FloatingPointError(f"non-finite gradient for parameter '{name}'")
-    upd_rest = state.sh_rest_active or bool(host[len(named)])
+
+    def raise_nonfinite(flags):
+        for (name, _), good in zip(named, [bool(v) for v in flags]):
+            if not good:
+                raise FloatingPointError(f"non-finite gradient for parameter '{name}'")
+    deferred = errors.deferred()
+    if deferred:
+        # the check stays on the device (errors.py); the Adam kernel leaves
+        # Gaussians with non-finite gradients untouched.  sh_rest is updated
+        # unless the gradients are known to come from an SH-0 render (then they
+        # are exactly 0 and so are the moments: the skip is bit-exact)
+        errors.defer(finite_flags_device([t for _, t in named]), raise_nonfinite)
+        upd_rest = state.sh_rest_active or grads.sh_degree is None or grads.sh_degree > 0
+    else:
+        # the finite checks and the "sh_rest in use" test as one host read
+        extra = () if state.sh_rest_active else ((grads.sh_rest != 0).any(),)
+        host = finite_flags([t for _, t in named], extra)
+        raise_nonfinite(host[:len(named)])
+        upd_rest = state.sh_rest_active or bool(host[len(named)])
     state.sh_rest_active = upd_rest
     state.step_count += 1
     st = torch.empty(_lib.STATUS_WORDS, dtype=torch.int64, device=gmap.device)
@@ -130,18 +145,42 @@ def adam_step(gmap: GaussianMap, grads: ParamGrads, state: AdamState, sh_degree:
     check(lib().ss_adam_step(ctypes.byref(mp), ctypes.byref(gr), ctypes.byref(state.planes("m")),
                              ctypes.byref(state.planes("v")), ctypes.byref(hp), P(st), s),
           "ss_adam_step")
-    if int(st[_lib.ST_ZERO_QUAT].item()) != _lib.INT64_MAX:
-        raise ValueError("zero-norm quaternion in map")
+    def raise_zero_quat(h):
+        if int(h[0]) != _lib.INT64_MAX:
+            raise ValueError("zero-norm quaternion in map")
+    if deferred:
+        errors.defer(st[_lib.ST_ZERO_QUAT:_lib.ST_ZERO_QUAT + 1], raise_zero_quat)
+    else:
+        raise_zero_quat(st[_lib.ST_ZERO_QUAT:_lib.ST_ZERO_QUAT + 1].cpu())
     return gmap, state
 
 
+@traced("ss.resize_for_densify")
 def resize_for_densify(state: AdamState, survivors, n_new: int) -> AdamState:
-    """optimizer.py:136-146: gather moments of survivors, append zeros."""
+    """optimizer.py:136-146: moments of the survivors gathered in order, zero
+    rows appended for the n_new fresh primitives (one ss_resize_moments
+    launch for every m / v plane)."""
+    dev = next(iter(state.m.values())).device
+    surv = torch.as_tensor(survivors, dtype=torch.int64).to(dev).reshape(-1)
+    n_old = next(iter(state.m.values())).shape[0]
+    if surv.numel() and (int(surv.min()) < 0 or int(surv.max()) >= n_old):
+        raise ValueError("survivor index out of range")
+    n_out = int(surv.numel()) + int(n_new)
+    pin, pout, pk, names = [], [], [], []
     for d in (state.m, state.v):
-        for name, t in list(d.items()):
-            surv = torch.as_tensor(survivors, device=t.device, dtype=torch.int64)
-            if surv.numel() and (int(surv.min()) < 0 or int(surv.max()) >= t.shape[0]):
-                raise ValueError("survivor index out of range")
-            z = torch.zeros((n_new,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-            d[name] = torch.cat([t.index_select(0, surv), z]).contiguous()
+        for name, t in d.items():
+            out = torch.empty((n_out,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
+            k = int(t[0].numel()) if t.shape[0] else int(np.prod(t.shape[1:], dtype=np.int64))
+            pin.append(t.contiguous())
+            pout.append(out)
+            pk.append(max(k, 1))
+            names.append((d, name))
+    n_pl = len(pin)
+    arr_in = (ctypes.c_void_p * n_pl)(*[p.data_ptr() for p in pin])
+    arr_out = (ctypes.c_void_p * n_pl)(*[p.data_ptr() for p in pout])
+    arr_k = (ctypes.c_int32 * n_pl)(*pk)
+    check(lib().ss_resize_moments(n_out, P(surv), int(surv.numel()), n_pl, arr_in, arr_out,
+                                  arr_k, stream_handle()), "ss_resize_moments")
+    for (d, name), out in zip(names, pout):
+        d[name] = out
     return state

@@ -18,8 +18,8 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _lib
-from ._lib import check, lib
+from . import _lib, errors
+from ._lib import check, lib, traced
 from .core import Camera, GaussianMap
 
 G2D_COLS = 9
@@ -146,6 +146,15 @@ def finite_flags(tensors, extra=()):
     it = iter(host.tolist())
     flags = [bool(next(it)) if t.numel() else True for t in tensors]
     return flags + [bool(v) for v in it]
+
+
+def finite_flags_device(tensors):
+    """Device bool tensor: [all(isfinite(t)) for t in tensors] (no host read)."""
+    nonempty = [t for t in tensors if t.numel()]
+    vals = iter(torch._foreach_norm(nonempty, float("inf")) if nonempty else [])
+    dev = tensors[0].device if tensors else torch.device("cuda")
+    one = torch.ones((), dtype=torch.bool, device=dev)
+    return torch.stack([torch.isfinite(next(vals)) if t.numel() else one for t in tensors])
 
 
 def raise_param_errors(st_host):
@@ -317,8 +326,10 @@ def _bin(sp: SplatBuffers, n: int, cam: Camera, dev, st):
         ws = bin_workspace(n, cap, n_tiles, dev)
         check(L.ss_bin_sort(n, ctypes.byref(sp.ss()), ctypes.byref(cm), ctypes.byref(bins.ss()),
                             P(ws), ws.numel(), P(st), s), "ss_bin_sort")
-        # status words + the checkpoint slot total in one host read
-        sh = torch.cat((st, bins.ckpt_base[n_tiles:n_tiles + 1].to(torch.int64))).cpu()
+        # status words + the checkpoint slot total in one host read (with every
+        # check a deferred-error call left pending, errors.py)
+        sh = errors.read_with_pending(
+            torch.cat((st, bins.ckpt_base[n_tiles:n_tiles + 1].to(torch.int64))))
         raise_param_errors(sh[:-1])
         pcount = int(sh[_lib.ST_PAIRS])
         if not int(sh[_lib.ST_OVERFLOW]):
@@ -329,6 +340,7 @@ def _bin(sp: SplatBuffers, n: int, cam: Camera, dev, st):
     return bins, pcount, sh
 
 
+@traced("ss.project_map")
 def project_map(gmap: GaussianMap, camera, *, dtype=np.float32, sh_degree: int = 3,
                 near: float = 0.01, dilation: float = 0.3,
                 alpha_min: float = 1.0 / 255.0) -> Projection:
@@ -352,6 +364,7 @@ def project_map(gmap: GaussianMap, camera, *, dtype=np.float32, sh_degree: int =
     return p
 
 
+@traced("ss.build_tile_index")
 def build_tile_index(proj: Projection, width: int, height: int, tile_size: int = 16) -> TileIndex:
     """tiles.py:29-65 on the GPU (K2-K4b): inclusive tile rects, pairs sorted
     by (tile, depth, row), tile ranges and active tiles -- bit-exact with the
@@ -362,7 +375,7 @@ def build_tile_index(proj: Projection, width: int, height: int, tile_size: int =
     if tile_size != 16:
         raise ValueError("the B200 kernels are specialised for tile_size=16")
     W, H = int(width), int(height)
-    dv = proj._device
+    dv = getattr(proj, "_device", None)
     if dv is not None and (dv[1].width, dv[1].height) == (W, H):
         sp, cam = dv[0], dv[1]
         n = int(sp.flags.numel())
@@ -399,6 +412,7 @@ def build_tile_index(proj: Projection, width: int, height: int, tile_size: int =
                      np.flatnonzero(ln > 0).astype(np.int64))
 
 
+@traced("ss.chain_backward")
 def chain_backward(proj: Projection, camera, g2d, n_primitives: int) -> dict:
     """projection.py:200-299 as K8 on the GPU: per-splat screen-space rows
     g2d (M, 9) [rgb3, mean2d2, conic3, opacity] -> dense float32 device
@@ -406,7 +420,7 @@ def chain_backward(proj: Projection, camera, g2d, n_primitives: int) -> dict:
     pos2d_grad_norm densify statistic.  The projection context is
     recomputed from the map's parameters, so ``proj`` must come from
     project_map / RenderOutput.proj."""
-    if proj._device is None:
+    if getattr(proj, "_device", None) is None:
         raise ValueError("chain_backward on the B200 path needs a Projection from project_map "
                          "(the chain recomputes the projection context from the map)")
     sp, pcam, gmap, opts = proj._device
@@ -431,6 +445,7 @@ def chain_backward(proj: Projection, camera, g2d, n_primitives: int) -> dict:
             "sh": grads.sh, "pos2d_grad_norm": grads.pos2d_grad_norm}
 
 
+@traced("ss.replay_pixel_states")
 def replay_pixel_states(render: "RenderOutput", tile_pos: int, from_bucket: int,
                         n_positions: int | None = None):
     """api.py:340-368: advance the archived pixel states of active tile
@@ -464,6 +479,7 @@ def replay_pixel_states(render: "RenderOutput", tile_pos: int, from_bucket: int,
     return h[:, 0].copy(), h[:, 1:4].copy()
 
 
+@traced("ss.rasterize_forward")
 def rasterize_forward(gmap: GaussianMap, camera, opts: RasterOpts | None = None) -> RenderOutput:
     """api.py:118-206 on the GPU: K1 preprocess -> K2-K4b binning -> K5 blend."""
     if opts is None:
@@ -518,6 +534,7 @@ class ParamGrads:
     sh_rest: torch.Tensor
     pos2d_grad_norm: torch.Tensor
     contributed: torch.Tensor
+    sh_degree: int | None = None  # of the render they came from (None: unknown)
 
     def __len__(self):
         return int(self.position.shape[0])
@@ -544,12 +561,20 @@ class ParamGrads:
         return g
 
     def validate_finite(self):
-        """api.py:74-79 (one fused reduction, one host read)."""
+        """api.py:74-79 (one fused reduction, one host read; in deferred error
+        mode the check stays on the device and raises later, errors.py)."""
         names = ("position", "rotation", "log_scale", "opacity_logit", "sh_dc", "sh_rest")
-        for k, good in zip(names, finite_flags([getattr(self, k) for k in names])):
-            if not good:
-                raise FloatingPointError(
-                    f"non-finite gradient in {'sh' if k.startswith('sh') else k}")
+
+        def raiser(flags):
+            for k, good in zip(names, [bool(v) for v in flags]):
+                if not good:
+                    raise FloatingPointError(
+                        f"non-finite gradient in {'sh' if k.startswith('sh') else k}")
+        tensors = [getattr(self, k) for k in names]
+        if errors.deferred():
+            errors.defer(finite_flags_device(tensors), raiser)
+        else:
+            raiser(finite_flags(tensors))
         return self
 
 
@@ -592,6 +617,7 @@ def screen_space_grads(render: RenderOutput, grad_image, grad_depth=None):
     return g2d[:n]
 
 
+@traced("ss.backward_splatwise")
 def backward_splatwise(render: RenderOutput, grad_image, n_workers=None,
                        grad_depth=None) -> ParamGrads:
     """api.py:275-337: K7 splat-wise backward + K8 chain to parameters."""
@@ -619,6 +645,7 @@ def screen_space_grads_pixelwise(render: RenderOutput, grad_image):
     return g2d[:n]
 
 
+@traced("ss.backward_pixelwise")
 def backward_pixelwise(render: RenderOutput, grad_image, n_workers=None) -> ParamGrads:
     """api.py:227-272: pixel-parallel backward + K8 chain to parameters (the
     reference's alternative to backward_splatwise; no checkpoints needed)."""
@@ -632,6 +659,7 @@ def _finish_backward(render: RenderOutput, g2d) -> ParamGrads:
     dev = render.image.device
     grads = ParamGrads.alloc(n, dev)
     grads.contributed = render.contributed.clone()
+    grads.sh_degree = render.opts.sh_degree
     mp, cm, op = render.gmap.ss(), render.camera.to_ss(), render.opts.to_ss()
     check(lib().ss_chain_backward(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op), P(g2d),
                                   P(render.splats.flags), None, 0.0, 0, ctypes.byref(grads.ss()),

@@ -315,20 +315,29 @@ def test_full_iteration_matches_reference_golden(case):
     for name in ("position", "rotation", "log_scale", "opacity_logit"):
         a = getattr(gr, name).cpu().numpy()
         assert normwise(a, d["g_" + name]) <= 1e-3, name
-        assert floored_rel(a, d["g_" + name], 1e-2) <= 5e-2, name
+        # entries above 1e-3 x max within 1e-3
+        assert floored_rel(a, d["g_" + name], 1e-3) <= 1e-3, name
     assert normwise(gr.sh.cpu().numpy(), expand_sh(d["g_sh"])) <= 1e-3
     st = ss.AdamState.for_map(g)
     ss.adam_step(g, gr, st)
     ss.accumulate_grad_stats(g, gr)
     h = g.to_numpy()
-    # first Adam step moves every element by ~lr*sign(g): compare where the
-    # reference gradient is not within float32 noise of zero
-    for name, gname in (("positions", "g_position"), ("log_scales", "g_log_scale"),
-                        ("opacity_logits", "g_opacity_logit")):
+    pre = dict(zip(("positions", "rotations", "log_scales", "opacity_logits"), case["arrs"]))
+    # first Adam step moves every element by ~lr * sign(g): where the
+    # reference gradient is above float32 noise (1e-3 x max), the GPU's step
+    # equals the reference's within 1e-3 of the step (+ float32 ulps of the
+    # parameter; 4 for the renormalised quaternions) -- a reversed step fails
+    for name, gname in (("positions", "g_position"), ("rotations", "g_rotation"),
+                        ("log_scales", "g_log_scale"), ("opacity_logits", "g_opacity_logit")):
         ref_g = d[gname]
         ok = np.abs(ref_g) > 1e-3 * np.abs(ref_g).max()
-        a, b = h[name][ok], d["post_" + name][ok]
-        assert np.abs(a - b).max() <= 1e-3 * np.abs(b).max(), name
+        if name == "rotations":
+            ok = np.repeat(ok.any(axis=1, keepdims=True), 4, axis=1)
+        b = d["post_" + name]
+        step = b - np.asarray(pre[name], np.float64).reshape(b.shape)
+        ulps = (4 if name == "rotations" else 2) * np.spacing(np.abs(b).astype(np.float32))
+        bound = 1e-3 * np.abs(step) + ulps
+        assert (np.abs(h[name] - b)[ok] <= bound[ok]).all(), name
     np.testing.assert_array_equal(h["obs_count"], d["post_obs_count"])
 
 
@@ -919,3 +928,73 @@ def test_stage_dropin_replay_pixel_states(case):
     assert checked > 0
     with pytest.raises(IndexError):
         ss.replay_pixel_states(out, 0, 10_000)
+
+
+def test_deferred_error_mode_same_results_and_late_raise(case):
+    """errors.set_error_mode("deferred"): the train_one sequence gives the same
+    map as eager mode with two host reads per iteration; a non-finite gradient
+    is raised by the next rasterize_forward (its status read), and the
+    Gaussian it belongs to was not updated."""
+    ss, d, cam, deg = case["ss"], case["d"], case["cam"], case["deg"]
+    tgt = torch.as_tensor(d["target"], dtype=torch.float32, device="cuda")
+    opts = ss.RasterOpts(sh_degree=deg)
+
+    def iteration(g, st, poison=False):
+        out = ss.rasterize_forward(g, cam, opts)
+        lb = ss.compute_losses(out.image, tgt, g.opacity_logits)
+        gr = ss.backward_splatwise(out, lb.grad_image)
+        gr.opacity_logit += lb.grad_opacity_logit
+        if poison:
+            gr.position[3, 0] = float("nan")
+        ss.adam_step(g, gr, st)
+        ss.accumulate_grad_stats(g, gr)
+        return lb
+
+    ga, gb = ss.GaussianMap.from_arrays(*case["arrs"]), ss.GaussianMap.from_arrays(*case["arrs"])
+    sa, sb = ss.AdamState.for_map(ga), ss.AdamState.for_map(gb)
+    la = [iteration(ga, sa).total for _ in range(2)]
+    ss.set_error_mode("deferred")
+    try:
+        lbs = [iteration(gb, sb) for _ in range(2)]
+        lb_ = [x.total for x in lbs]
+        ss.check_errors()
+        for f in ("positions", "rotations", "log_scales", "opacity_logits", "sh_dc"):
+            assert torch.equal(getattr(ga, f), getattr(gb, f)), f
+        assert la == lb_
+        before = gb.positions[3].clone()
+        iteration(gb, sb, poison=True)  # no raise here
+        assert torch.equal(gb.positions[3], before)
+        with pytest.raises(FloatingPointError, match="non-finite gradient"):
+            ss.rasterize_forward(gb, cam, opts)
+    finally:
+        ss.errors.take_pending()
+        ss.set_error_mode("eager")
+
+
+def test_resize_for_densify_matches_reference_golden():
+    """resize_for_densify (optimizer.py:136-146) on the GPU after the GPU
+    densify of tests/golden/densify.npz: the position moments equal the
+    reference's m_post_position (survivor rows gathered, fresh rows zero),
+    bit for bit in float32; every plane's fresh tail is zero."""
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    d = load("densify")
+    g = ss.GaussianMap.from_arrays(d["pre_positions"], d["pre_rotations"], d["pre_log_scales"],
+                                   d["pre_opacity_logits"], d["pre_sh"])
+    g.grad2d_accum = torch.as_tensor(d["pre_grad2d_accum"], dtype=torch.float32, device="cuda")
+    g.grad3d_accum = torch.as_tensor(d["pre_grad3d_accum"], dtype=torch.float32, device="cuda")
+    g.obs_count = torch.as_tensor(d["pre_obs_count"], dtype=torch.int32, device="cuda")
+    st = ss.AdamState.for_map(g)
+    st.m["position"].copy_(torch.as_tensor(d["m_pre_position"], dtype=torch.float32))
+    st.v["rotation"].uniform_(0.0, 1.0)
+    res = ss.densify_and_prune(g, ss.DensifyConfig(), float(d["extent"]), normals=d["normals"])
+    st = ss.resize_for_densify(st, res.survivors, res.n_new)
+    np.testing.assert_array_equal(st.m["position"].cpu().numpy(),
+                                  d["m_post_position"].astype(np.float32))
+    kept = int(res.survivors.numel())
+    for dct in (st.m, st.v):
+        for k, t in dct.items():
+            assert t.shape[0] == len(g), k
+            assert float(t[kept:].abs().max()) == 0.0 if res.n_new else True, k
+    with pytest.raises(ValueError):
+        ss.resize_for_densify(st, torch.tensor([len(g) + 5]), 0)

@@ -1,0 +1,70 @@
+"""compute-sanitizer over one small mapping iteration of every path the
+library launches (API forward / loss / splat-wise and pixel-wise backward /
+chain / Adam / densify, the fused engine step, a keyframe batch, seeding,
+replay): memcheck (out-of-bounds and misaligned accesses) and racecheck
+(shared-memory hazards) must report 0 errors.  The reference's one known
+race -- several threads setting the same `contributed` flag to 1
+(api.py:142, kernels.py:94-95) -- is a same-value global store, which
+neither tool flags."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {repo!r}); sys.path.insert(0, {tests!r})
+import paper_2410_00486_b200 as ss
+from paper_2410_00486_b200.scene import survey_camera, survey_scene
+from helpers import fixture_camera, fixture_scene, load
+d = load("iter_sh3_small")
+cam = fixture_camera(d)
+g = ss.GaussianMap.from_arrays(*fixture_scene(d))
+opts = ss.RasterOpts(sh_degree=3)
+tgt = torch.as_tensor(d["target"], dtype=torch.float32, device="cuda")
+out = ss.rasterize_forward(g, cam, opts)
+lb = ss.compute_losses(out.image, tgt, g.opacity_logits)
+gr = ss.backward_splatwise(out, lb.grad_image)
+gp = ss.backward_pixelwise(out, lb.grad_image)
+st = ss.AdamState.for_map(g)
+ss.adam_step(g, gr, st)
+ss.accumulate_grad_stats(g, gr)
+ss.replay_pixel_states(out, 0, 0)
+ti = ss.build_tile_index(ss.project_map(g, cam, sh_degree=3), cam.width, cam.height, 16)
+res = ss.densify_and_prune(g, ss.DensifyConfig(grad_threshold=1e-7), 1.0, rng=3)
+st = ss.resize_for_densify(st, res.survivors, res.n_new)
+eng = ss.MappingEngine(ss.GaussianMap.from_scene(survey_scene(2000, 1)), 64, 48,
+                       ss.RasterOpts(sh_degree=0))
+cams = [survey_camera(64, 48, v, 2) for v in range(2)]
+tg = [torch.rand(48, 64, 3, device="cuda") for _ in cams]
+for _ in range(2):
+    eng.step(cams[0], tg[0])
+eng.multiview_step(cams, tg)
+eng.synchronize()
+ss.seed_from_points(np.random.default_rng(0).uniform(-1, 1, (300, 3)),
+                    np.random.default_rng(1).uniform(0, 1, (300, 3)))
+torch.cuda.synchronize()
+print("iteration ok")
+"""
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+def test_compute_sanitizer_reports_no_errors(tool, tmp_path):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    san = "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(san):
+        pytest.skip("compute-sanitizer not installed")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = tmp_path / "it.py"
+    path.write_text(SCRIPT.format(repo=repo, tests=os.path.join(repo, "tests")))
+    r = subprocess.run([san, f"--tool={tool}", "--error-exitcode=3", sys.executable, str(path)],
+                       capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert "iteration ok" in out, out[-3000:]
+    assert r.returncode == 0 and "ERROR SUMMARY: 0 errors" in out, out[-3000:]

@@ -19,14 +19,22 @@ def it():
     gr.opacity_logit += lb.grad_opacity_logit
     ss.adam_step(g, gr, st)
     ss.accumulate_grad_stats(g, gr)
-for _ in range(3): it()
-torch.cuda.synchronize()
-t = time.perf_counter()
-K = 20
-for _ in range(K): it()
-torch.cuda.synchronize()
-dt = (time.perf_counter() - t) / K
-print(f"API path (rasterize_forward + compute_losses + backward_splatwise + adam_step + stats): {dt*1e3:.3f} ms/it, {1/dt:.0f} it/s")
+    return lb.total  # the scheduler's loss feed (trainer.py:209)
+def timed(mode):
+    ss.set_error_mode(mode)
+    for _ in range(3): it()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    K = 20
+    for _ in range(K): it()
+    torch.cuda.synchronize()
+    ss.check_errors()
+    dt = (time.perf_counter() - t) / K
+    print(f"API path, {mode} errors (rasterize_forward + compute_losses + backward_splatwise + "
+          f"adam_step + stats, loss read each iteration): {dt*1e3:.3f} ms/it, {1/dt:.0f} it/s")
+    ss.set_error_mode("eager")
+timed("eager")
+timed("deferred")
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU, torch.profiler.ProfilerActivity.CUDA]) as p:
     it(); torch.cuda.synchronize()
 print(p.key_averages().table(sort_by="self_cpu_time_total", row_limit=12))
