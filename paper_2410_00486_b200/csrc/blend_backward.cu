@@ -398,45 +398,43 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
 }
 
 // --------------------------------------------------------------------------
-// Sparse two-phase variant (the default).  The wavefront above evaluates
+// Sparse variant (opt-in: SS_BWD_SPARSE=1).  The wavefront above evaluates
 // every (pixel, list position) slot of a unit and zeroes the ones the pixel
 // did not blend; at the bench workload only 25 % of those slots are blended
-// (15 % after 250 training iterations: low opacities, long lists), so ~80 %
-// of its FMA / MUFU work is predicated away.  Here a CTA of 256 threads
-// takes one checkpoint bucket (tile, 32 list positions) at a time:
+// (15 % after 250 training iterations: low opacities, long lists).  Here
+// only blended pairs are evaluated.  A CTA of 256 threads (one per tile
+// pixel) takes a unit (tile, 2 checkpoint buckets); per bucket each WARP
+// works on its own 32 pixels without CTA barriers:
 //
-//   phase 1 (thread = pixel): walk the set bits of the pixel's blend mask
-//     in list order from the bucket's checkpoint -- exactly the pairs the
+//   phase 1 (lane = pixel): walk the set bits of the pixel's blend mask in
+//     list order from the bucket's checkpoint -- exactly the pairs the
 //     forward blended, with its arithmetic (splat_power / splat_falloff) --
-//     and emit per blended pair w = alpha T and the alpha-path gradient
-//     da = alpha dL/dalpha (kernels.py:342-364), written SPLAT-MAJOR into
-//     shared memory: the slot of (pixel, position k) is known before the
-//     walk from per-warp ballots of the masks (rank among the pixels that
-//     blended k);
-//   phase 2 (8 threads per list position): each position's pairs are summed
-//     into its 9 (10) screen-space gradients, the 8 partial rows are
-//     combined with shuffles and committed with one red.add row per
-//     (tile, splat), as in the wavefront.
+//     and store per pair w = alpha T and da = alpha dL/dalpha
+//     (kernels.py:342-364) position-major in the warp's shared-memory
+//     region; the slot of (pixel, position) comes from the warp's 32 x 32
+//     mask matrix transposed in registers (rank among the warp's pixels that
+//     blended the position);
+//   phase 2 (lane = list position): sum the position's pairs (<= 32) into
+//     its 9 (10) screen-space gradients -- no shuffles -- and park them in
+//     shared memory;
 //
-// Work is proportional to the blended pairs; there is no cross-lane state
-// passing and no ramp.  Shared memory holds the worst case of one bucket
-// (32 x 256 pairs).
-constexpr int kSpThreads = kTilePx;             // one thread per tile pixel
+// then one CTA barrier, the 8 warps' rows are summed per position and
+// committed with one red.add row per (tile, splat), as in the wavefront.
+constexpr int kSpThreads = kTilePx;  // one thread per tile pixel
 constexpr int kSpWarps = kSpThreads / 32;
-constexpr int kSpMaxPairs = kBucket * kTilePx;  // every pixel blends every position
-constexpr int kSpRuns = kBucket * (kTilePx / 64);  // runs of <= 64 pairs per position
+constexpr int kSpWarpPairs = 32 * kBucket;  // a warp's pixels x a bucket's positions
+constexpr int kSpPart = 10;                // parked row: 9 (10) gradients + pair count
 
 struct SpShared {
-    float2 wd[kSpMaxPairs];         // (alpha T, alpha dL/dalpha) per blended pair, splat-major
-    uint8_t pid[kSpMaxPairs];       // tile-local pixel of the pair
-    float4 g[kTilePx];              // per pixel (g_r, g_g, g_b, g_depth)
-    float2 xy[kTilePx];             // per pixel (x, y)
-    SplatRec rec[kUnit];            // the unit's 64 list positions
+    float2 wd[kSpWarps][kSpWarpPairs];     // (alpha T, alpha dL/dalpha), position-major
+    uint8_t pid[kSpWarps][kSpWarpPairs];   // lane (pixel) of the pair
+    float part[2][kSpWarps][kBucket][kSpPart + 1];  // per warp, per position (double-buffered)
+    uint32_t bal[kSpWarps][kBucket];       // lanes that blended each position
+    uint32_t base[kSpWarps][kBucket + 1];  // position slot ranges in the warp's region
+    float4 g[kTilePx];                     // per pixel (g_r, g_g, g_b, g_depth)
+    float2 xy[kTilePx];                    // per pixel (x, y)
+    SplatRec rec[kUnit];                   // the unit's 64 list positions
     uint32_t sid[kUnit];
-    uint32_t bal[kSpWarps][kBucket];  // per warp, per position: which lanes blended it
-    uint32_t off[kBucket][kSpWarps];  // slot base of (position, warp)
-    uint32_t run[kSpRuns];            // phase-2 runs: begin | len << 13 | position << 20
-    int nrun;
     int next;
 };
 
@@ -472,15 +470,14 @@ __global__ void __launch_bounds__(kSpThreads, 2) backward_sparse_kernel(
     PDL_WAIT();
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int64_t count = min(*work_count, work_cap);
-    // phase-2 role: group grp of 8 threads (sub-lane sub) takes runs grp, grp + 32, ...
-    const int grp = t >> 3, sub = t & 7;
     if (t == 0) S.next = (int)atomicAdd(work_counter, 1u);
     __syncthreads();
+    int par = 0;  // parked-row buffer of the current bucket
 
     for (;;) {
         const uint32_t item = (uint32_t)S.next;
         if ((int64_t)item >= count) break;
-        __syncthreads();  // everyone has read S.next
+        __syncthreads();  // everyone has read S.next and finished the last commit
         // the next item's index is fetched now; its latency hides under this one
         if (t == 0) S.next = (int)atomicAdd(work_counter, 1u);
         const uint2 wk = work[item];  // (tile, unit), longest-first order
@@ -536,9 +533,12 @@ __global__ void __launch_bounds__(kSpThreads, 2) backward_sparse_kernel(
         const float px = (float)ix, py = (float)iy;
         S.g[t] = make_float4(pg.x, pg.y, pg.z, gd);
         S.xy[t] = make_float2(px, py);
+        __syncthreads();  // records and pixel data visible to every warp
         // a bucket's mask and state exist for pixels still blending at its start
         m0 = nct > kb0 ? m0 : 0u;
         m1 = nct > kb0 + kBucket ? m1 : 0u;
+        float2* WD = S.wd[wid];
+        uint8_t* PID = S.pid[wid];
         for (int half = 0; half < nbk; ++half) {
             const uint32_t mask = half ? m1 : m0;
             const float4 ck = half ? ck1 : ck0;
@@ -546,54 +546,26 @@ __global__ void __launch_bounds__(kSpThreads, 2) backward_sparse_kernel(
             float G = pg.x * ck.y + pg.y * ck.z + pg.z * ck.w;
             if (DEPTH) G += gd * (half ? cd1 : cd0);
             const SplatRec* R32 = S.rec + kBucket * half;
-            // per warp and position: the lanes that blended it -- the warp's
-            // 32 x 32 bit matrix of masks transposed in 5 butterfly stages
-            S.bal[wid][lane] = warp_transpose32(mask, lane);
-            __syncthreads();
-            // slot bases (position-major, warps in order inside a position) and
-            // the phase-2 runs (<= 64 consecutive pairs of one position)
-            if (wid == 0) {
-                uint32_t c[kSpWarps], tot = 0;
+            // lane k: which of the warp's pixels blended position k, and the
+            // slot range of position k in the warp's region
+            const uint32_t balk = warp_transpose32(mask, lane);
+            const uint32_t cnt = __popc(balk);
+            uint32_t inc = cnt;
 #pragma unroll
-                for (int w = 0; w < kSpWarps; ++w) {
-                    c[w] = tot;
-                    tot += __popc(S.bal[w][lane]);
-                }
-                uint32_t inc = tot;  // inclusive scans of the totals and run counts
-                const uint32_t nr = (tot + 63u) >> 6;
-                uint32_t rinc = nr;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint32_t v = __shfl_up_sync(0xffffffffu, inc, d);
-                    const uint32_t rv = __shfl_up_sync(0xffffffffu, rinc, d);
-                    if (lane >= d) {
-                        inc += v;
-                        rinc += rv;
-                    }
-                }
-                const uint32_t base = inc - tot;
-#pragma unroll
-                for (int w = 0; w < kSpWarps; ++w) S.off[lane][w] = base + c[w];
-                for (uint32_t j = 0; j < nr; ++j) {
-                    const uint32_t b = base + 64u * j;
-                    S.run[rinc - nr + j] = b | (min(64u, base + tot - b) << 13) | ((uint32_t)lane << 20);
-                }
-                if (lane == 31) S.nrun = (int)rinc;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += v;
             }
-            __syncthreads();
+            S.bal[wid][lane] = balk;
+            S.base[wid][lane] = inc - cnt;
+            if (lane == 31) S.base[wid][kBucket] = inc;
+            __syncwarp();
             // ---- phase 1: the pixel's blended pairs in list order; the next
-            //      pair's record is loaded while this one computes
+            //      pair's record is loaded while this one computes (two record
+            //      registers used in turn)
             if (mask) {
-                uint32_t m = mask;
                 const uint32_t lt = lanemask_lt();
-                int k = __ffs(m) - 1;
-                m &= m - 1;
-                SplatRec R = R32[k];
-                for (;;) {
-                    const bool more = m != 0u;
-                    const int kn = more ? __ffs(m) - 1 : k;
-                    m &= m - 1;
-                    const SplatRec Rn = R32[kn];
+                auto term = [&](int k, const SplatRec& R) {
                     float dx, dy;
                     const float a0 = splat_falloff(splat_power(px, py, R.a, R.b, dx, dy), R.b);
                     const float a = fminf(a0, amax);
@@ -607,34 +579,48 @@ __global__ void __launch_bounds__(kSpThreads, 2) backward_sparse_kernel(
                     const float da = dal * (a != amax ? a : 0.f);
                     T = __fmul_rn(T, om);
                     G = Gafter;
-                    const uint32_t r = S.off[k][wid] + __popc(S.bal[wid][k] & lt);
-                    S.wd[r] = make_float2(w, da);
-                    S.pid[r] = (uint8_t)t;
-                    if (!more) break;
-                    k = kn;
-                    R = Rn;
+                    const uint32_t r = S.base[wid][k] + __popc(S.bal[wid][k] & lt);
+                    WD[r] = make_float2(w, da);
+                    PID[r] = (uint8_t)lane;
+                };
+                uint32_t m = mask;
+                int k = __ffs(m) - 1;
+                m &= m - 1;
+                SplatRec R = R32[k];
+                for (;;) {
+                    if (!m) {
+                        term(k, R);
+                        break;
+                    }
+                    const int k2 = __ffs(m) - 1;
+                    m &= m - 1;
+                    const SplatRec R2 = R32[k2];
+                    term(k, R);
+                    if (!m) {
+                        term(k2, R2);
+                        break;
+                    }
+                    k = __ffs(m) - 1;
+                    m &= m - 1;
+                    R = R32[k];
+                    term(k2, R2);
                 }
             }
-            __syncthreads();
-            // ---- phase 2: runs of <= 64 pairs of one position, 8 threads each;
-            //      one red.add row per run
-            const int nrun = S.nrun;
-            // the group's lanes (groups of a warp may run different numbers of runs)
-            const uint32_t gmask = 0xffu << (8 * (grp & 3));
-            for (int ri = grp; ri < nrun; ri += kSpThreads / 8) {
-                const uint32_t rw = S.run[ri];
-                const uint32_t rb = rw & 8191u, rl = (rw >> 13) & 127u;
-                const int kq = (int)(rw >> 20);
-                const float4 A = R32[kq].a, B = R32[kq].b;
+            __syncwarp();
+            // ---- phase 2: lane k sums position k's pairs of this warp
+            {
+                const float4 A = R32[lane].a, B = R32[lane].b;
                 const f32x2 mxy = pk2(A.x, A.y);
                 f32x2 acc_rg = pk2(0.f, 0.f), s_d = acc_rg, s_xxy = acc_rg;
                 float acc_b = 0.f, acc_z = 0.f, s_da = 0.f, s_yy = 0.f;
-#pragma unroll 2
-                for (uint32_t r = rb + sub; r < rb + rl; r += 8) {
-                    const float2 wd = S.wd[r];
-                    const int p = S.pid[r];
-                    const float4 g = S.g[p];
-                    const float2 xy = S.xy[p];
+                const uint32_t r1 = inc;
+                const float4* Gw = S.g + 32 * wid;
+                const float2* XYw = S.xy + 32 * wid;
+                for (uint32_t r = inc - cnt; r < r1; ++r) {
+                    const float2 wd = WD[r];
+                    const int p = PID[r];
+                    const float4 g = Gw[p];
+                    const float2 xy = XYw[p];
                     acc_rg = fma2(pk2(wd.x, wd.x), pk2(g.x, g.y), acc_rg);
                     acc_b = fmaf(wd.x, g.z, acc_b);
                     if (DEPTH) acc_z = fmaf(wd.x, g.w, acc_z);
@@ -648,43 +634,44 @@ __global__ void __launch_bounds__(kSpThreads, 2) backward_sparse_kernel(
                     s_xxy = fma2(pk2(tx, tx), dxy, s_xxy);
                     s_yy = fmaf(ty, dy, s_yy);
                 }
-                float acc[NC];
-                upk2(acc_rg, acc[0], acc[1]);
-                acc[2] = acc_b;
+                // the splat-constant factors (linear: summing the warps' rows
+                // afterwards gives the same result)
                 float s_dx, s_dy, s_xx, s_xy;
                 upk2(s_d, s_dx, s_dy);
                 upk2(s_xxy, s_xx, s_xy);
+                float* row = S.part[par][wid][lane];
+                upk2(acc_rg, row[0], row[1]);
+                row[2] = acc_b;
+                const float c1 = 0.5f * A.w;
+                row[3] = A.z * s_dx + c1 * s_dy;
+                row[4] = c1 * s_dx + B.x * s_dy;
+                row[5] = -0.5f * s_xx;
+                row[6] = -s_xy;
+                row[7] = -0.5f * s_yy;
+                row[8] = cnt ? s_da / B.y : 0.f;
+                if (DEPTH) row[9] = acc_z;
+                row[kSpPart] = (float)cnt;
+            }
+            __syncthreads();  // every warp's rows are parked
+            // ---- commit: sum the 8 warps' rows per (position, column)
+            {
+                const int k = t >> 3, c0 = t & 7;
+                const uint32_t sg = S.sid[kBucket * half + k];
+                float n = 0.f;
 #pragma unroll
-                for (int d = 1; d < 8; d <<= 1) {
+                for (int w = 0; w < kSpWarps; ++w) n += S.part[par][w][k][kSpPart];
+                if (n > 0.f) {
+                    float* grow = g2d + (size_t)sg * NC;
+                    for (int c = c0; c < NC; c += 8) {
+                        float v = 0.f;
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) acc[c] += __shfl_xor_sync(gmask, acc[c], d);
-                    if (DEPTH) acc_z += __shfl_xor_sync(gmask, acc_z, d);
-                    s_da += __shfl_xor_sync(gmask, s_da, d);
-                    s_dx += __shfl_xor_sync(gmask, s_dx, d);
-                    s_dy += __shfl_xor_sync(gmask, s_dy, d);
-                    s_xx += __shfl_xor_sync(gmask, s_xx, d);
-                    s_xy += __shfl_xor_sync(gmask, s_xy, d);
-                    s_yy += __shfl_xor_sync(gmask, s_yy, d);
-                }
-                if (sub == 0) {
-                    // splat-constant factors once (see the wavefront's commit)
-                    const float c1 = 0.5f * A.w;
-                    acc[3] = A.z * s_dx + c1 * s_dy;
-                    acc[4] = c1 * s_dx + B.x * s_dy;
-                    acc[5] = -0.5f * s_xx;
-                    acc[6] = -s_xy;
-                    acc[7] = -0.5f * s_yy;
-                    acc[8] = s_da / B.y;
-                    if (DEPTH) acc[NC - 1] = acc_z;
-                    const uint32_t sg = S.sid[kBucket * half + kq];
-                    float* row = g2d + (size_t)sg * NC;
-#pragma unroll
-                    for (int c = 0; c < NC; ++c)
-                        if (acc[c] != 0.f) atomicAdd(row + c, acc[c]);
-                    if (contributed) contributed[sg] = 1;
+                        for (int w = 0; w < kSpWarps; ++w) v += S.part[par][w][k][c];
+                        if (v != 0.f) atomicAdd(grow + c, v);
+                    }
+                    if (contributed && c0 == 0) contributed[sg] = 1;
                 }
             }
-            __syncthreads();  // the bucket's shared state is reused by the next one
+            par ^= 1;
         }
     }
 }

@@ -958,9 +958,15 @@ def test_deferred_error_mode_same_results_and_late_raise(case):
         lbs = [iteration(gb, sb) for _ in range(2)]
         lb_ = [x.total for x in lbs]
         ss.check_errors()
-        for f in ("positions", "rotations", "log_scales", "opacity_logits", "sh_dc"):
-            assert torch.equal(getattr(ga, f), getattr(gb, f)), f
-        assert la == lb_
+        # g2d rows are float atomics: two runs agree to rounding, and Adam's
+        # +-lr steps bound the effect of near-zero gradient sign flips
+        lr = dict(positions=1.6e-4, rotations=1e-3, log_scales=5e-3, opacity_logits=5e-2,
+                  sh_dc=2.5e-3)
+        for f, r in lr.items():
+            d_ = (getattr(ga, f) - getattr(gb, f)).abs()
+            assert float(d_.max()) <= 4 * r + 1e-5, f
+            assert float((d_ > 1e-3 * r + 1e-6).float().mean()) < 0.01, f
+        np.testing.assert_allclose(la, lb_, rtol=1e-5)
         before = gb.positions[3].clone()
         iteration(gb, sb, poison=True)  # no raise here
         assert torch.equal(gb.positions[3], before)
