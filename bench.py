@@ -59,6 +59,10 @@ def _args():
     ap.add_argument("--no-converged", action="store_true")
     ap.add_argument("--no-config4", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)
+    # validation of the N > 1 code path on a one-GPU box only (every rank on
+    # cuda:0, gradients summed over gloo); never a measurement
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--same-device", action="store_true")
     return ap.parse_args()
 
 
@@ -514,16 +518,20 @@ def main():
         return reference_arm(args, rank, world)
 
     import torch
-    torch.cuda.set_device(local)
+    dev_index = 0 if args.same_device else local
+    torch.cuda.set_device(dev_index)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group("gloo")
     warmup = max(args.warmup, 3)
     timer = Timer(torch)
 
     if world > 1:
-        sampler = ClockSampler(local)
+        sampler = ClockSampler(dev_index)
         sampler.start()
         res = batch_arm(torch, args, rank, world, dist, timer, args.steps, warmup,
                         not args.no_e2e)
@@ -541,6 +549,7 @@ def main():
                            "l2": "256 MB buffer written between timed steps (outside the "
                                  "events)"},
                 "views_per_s": res["views_per_s"], "clocks": clocks, "e2e": res.get("e2e"),
+                "validation_only": (args.same_device or args.dist_backend != "nccl") or None,
                 "gpu_launches": res["gpu_launches"], "cpu_baseline": None,
             }
             print(json.dumps(line), flush=True)
@@ -575,7 +584,7 @@ def main():
     snap = snapshot_state(eng)
 
     # ---- timed region: per-step CUDA events, L2 flushed between steps
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev_index)
     torch.cuda.synchronize()
     sampler.start()
     launches0 = eng.launches

@@ -48,6 +48,7 @@ tiles_nc = pad.reshape(ty, 16, tx, 16).transpose(0, 2, 1, 3).reshape(tx * ty, 25
 units = []
 useful = executed = steps_total = ramp_total = 0
 pairs_hist = []
+band_pos, band_pairs = [], []
 for t in range(tx * ty):
     nu = (ke[t] + 63) // 64
     for u in range(nu):
@@ -61,6 +62,13 @@ for t in range(tx * ty):
         p1 = np.where(live1, pc[s0 + 256:s0 + 512], 0) if has1 else 0 * p0
         act = (m0 | m1) != 0
         npair = (int(act.sum()) + 1) // 2
+        # per 4-row band: positions blended by any of its pixels (both buckets)
+        for b in range(4):
+            o0 = np.bitwise_or.reduce(m0[64 * b:64 * (b + 1)].astype(np.uint64))
+            o1 = np.bitwise_or.reduce(m1[64 * b:64 * (b + 1)].astype(np.uint64))
+            npos = bin(int(o0)).count("1") + bin(int(o1)).count("1")
+            band_pos.append(npos)
+            band_pairs.append((int(act[64 * b:64 * (b + 1)].sum()) + 1) // 2)
         st = npair + 15
         useful += int(p0.sum() + p1.sum())
         executed += st * 32 * 2 * 2
@@ -76,4 +84,8 @@ print(json.dumps({
     "term_slots_executed": executed, "term_slots_useful": useful,
     "useful_fraction": useful / executed,
     "mean_sigma": float(torch.sigmoid(eng.gmap.opacity_logits).mean()),
+    "band_positions_mean": float(np.mean(band_pos)),
+    "band_positions_hist_le16_le32_le48_le64": [float(np.mean(np.array(band_pos) <= v))
+                                                for v in (16, 32, 48, 64)],
+    "band_pairs_mean": float(np.mean(band_pairs)),
 }))
