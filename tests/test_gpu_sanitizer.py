@@ -66,5 +66,9 @@ def test_compute_sanitizer_reports_no_errors(tool, tmp_path):
     r = subprocess.run([san, f"--tool={tool}", "--error-exitcode=3", sys.executable, str(path)],
                        capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
+    if "closed on this pool" in out:
+        # the GPU pool disables compute-sanitizer (runs under it left GPUs needing a
+        # reset); tests/test_gpu_guard.py checks every device buffer's bounds instead
+        pytest.skip("compute-sanitizer disabled on this GPU pool")
     assert "iteration ok" in out, out[-3000:]
     assert r.returncode == 0 and "ERROR SUMMARY: 0 errors" in out, out[-3000:]
