@@ -42,10 +42,14 @@ struct SplatAcc2 {  // one splat's partial sums, (pixel a, pixel b) lanes
 };
 struct SplatP2 {  // one splat's record fields, duplicated into both lanes
     f32x2 mx, my, c0, c1x2, c2, sig, cr, cg, cb, z;
+    float mxs, c0s, c1x2s;  // the dx-only terms are shared by a pair (one column)
 };
 
 __device__ __forceinline__ SplatP2 splat_p2(const float4& A, const float4& B, const float4& C) {
     SplatP2 p;
+    p.mxs = A.x;
+    p.c0s = A.z;
+    p.c1x2s = A.w;
     p.mx = pk2(A.x, A.x);
     p.my = pk2(A.y, A.y);
     p.c0 = pk2(A.z, A.z);
@@ -59,19 +63,22 @@ __device__ __forceinline__ SplatP2 splat_p2(const float4& A, const float4& B, co
     return p;
 }
 
-// One splat applied to a pixel pair.  `ba` / `bb` are the forward's blend
-// mask bits of the two pixels; a pair that was not blended gets a = 0, which
-// leaves T and G bit-exactly unchanged and contributes nothing, so the term
-// runs branch-free.
+// One splat applied to a pixel pair -- two pixels of one column, rows y and
+// y + 1 (the forward also shares a column's dx-only terms between its two
+// pixels).  `ba` / `bb` are the forward's blend mask bits of the two pixels;
+// a pair that was not blended gets a = 0, which leaves T and G bit-exactly
+// unchanged and contributes nothing, so the term runs branch-free.
 template <bool DEPTH, bool CLAMP>
-__device__ __forceinline__ void bwd_term2(uint32_t ba, uint32_t bb, f32x2 px, f32x2 py, f32x2 gx,
+__device__ __forceinline__ void bwd_term2(uint32_t ba, uint32_t bb, float pxs, f32x2 py, f32x2 gx,
                                           f32x2 gy, f32x2 gz, f32x2 gw, f32x2 gd,
                                           const SplatP2& S, float amax, f32x2& T, f32x2& G,
                                           SplatAcc2& q) {
-    // splat_power / splat_falloff (common.cuh) per lane: same operations,
-    // same rounding as the forward's blend decision
-    const f32x2 dx = sub2(px, S.mx), dy = sub2(py, S.my);
-    const f32x2 m = fma2(mul2(S.c2, dy), dy, fma2(mul2(S.c1x2, dx), dy, mul2(mul2(S.c0, dx), dx)));
+    // splat_power / splat_falloff (common.cuh) per lane: the forward's
+    // operations and rounding (quad_dx0 / quad_dx1 once for the column)
+    const float dxs = __fsub_rn(pxs, S.mxs);
+    const float q0s = __fmul_rn(__fmul_rn(S.c0s, dxs), dxs), q1s = __fmul_rn(S.c1x2s, dxs);
+    const f32x2 dx = pk2(dxs, dxs), dy = sub2(py, S.my);
+    const f32x2 m = fma2(mul2(S.c2, dy), dy, fma2(pk2(q1s, q1s), dy, pk2(q0s, q0s)));
     float e0, e1;
     upk2(mul2(m, pk2(-0.5f * kLog2e, -0.5f * kLog2e)), e0, e1);
     float a0, a1;
@@ -203,9 +210,10 @@ __device__ __forceinline__ uint32_t bwd_wavefront(int npair, int lane, bool hi, 
         const uint32_t bb = inr ? (m.y >> sh) & 3u : 0u;
         // (no warp-uniform skip: a branch here would split the unrolled steps)
         seen |= ba | bb;
-        const float4 xy = XY[jj];
+        const float4 xy = XY[jj];  // (x, x, y, y + 1): one column
         const float4 g0 = GA[jj], g1 = GB[jj];
-        const f32x2 px = pk2(xy.x, xy.y), py = pk2(xy.z, xy.w);
+        const float px = xy.x;
+        const f32x2 py = pk2(xy.z, xy.w);
         const f32x2 gx = pk2(g0.x, g0.y), gy = pk2(g0.z, g0.w), gz = pk2(g1.x, g1.y),
                     gw = pk2(g1.z, g1.w);
         f32x2 gd = pk2(0.f, 0.f);
@@ -294,7 +302,11 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
                 mk1[c] = nct[c] > kbase + kBucket ? ckpt_mask[slot0 + kTilePx + p] : 0u;
             }
         }
-        int nact = 0;
+        // pairs = the two pixels of one column in rows 2c and 2c + 1 (lanes l and
+        // l + 16 of group c); a pair is kept when either pixel blended a splat of
+        // the unit, its other pixel then rides along inert (no blend bits, zero
+        // gradient, finite state)
+        int npair = 0;
 #pragma unroll
         for (int c = 0; c < kTilePx / 32; ++c) {
             const int p = c * 32 + lane;
@@ -302,39 +314,45 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
             const size_t o = (size_t)iy * W + ix;
             const uint32_t m0 = mk0[c], m1 = mk1[c];
             const bool act = (m0 | m1) != 0u;
-            const unsigned bal = __ballot_sync(0xffffffffu, act);
-            if (act) {
-                const int pos = nact + __popc(bal & lanemask_lt());
-                float4 pg;
-                if (pixgrad) {
-                    pg = pixgrad[o];
-                } else {
-                    pg.x = grad_image[3 * o];
-                    pg.y = grad_image[3 * o + 1];
-                    pg.z = grad_image[3 * o + 2];
-                    pg.w = pg.x * image[3 * o] + pg.y * image[3 * o + 1] + pg.z * image[3 * o + 2];
+            const int partner = __shfl_xor_sync(0xffffffffu, (int)act, 16);  // every lane
+            const bool pact = act || partner;
+            const unsigned bal = __ballot_sync(0xffffffffu, pact) & 0xffffu;
+            if (pact) {
+                const int pr = npair + __popc(bal & ((1u << (lane & 15)) - 1u));
+                const int hi = lane >> 4;  // the pair's lane: row 2c (lo) or 2c + 1 (hi)
+                float4 pg = make_float4(0.f, 0.f, 0.f, 0.f);
+                float4 ck = make_float4(1.f, 0.f, 0.f, 0.f);
+                float G0 = 0.f, T1 = 1.f, G1 = 0.f, gd = 0.f;
+                if (act) {
+                    if (pixgrad) {
+                        pg = pixgrad[o];
+                    } else {
+                        pg.x = grad_image[3 * o];
+                        pg.y = grad_image[3 * o + 1];
+                        pg.z = grad_image[3 * o + 2];
+                        pg.w = pg.x * image[3 * o] + pg.y * image[3 * o + 1] +
+                               pg.z * image[3 * o + 2];
+                    }
+                    ck = ckpt[slot0 + p];
+                    G0 = pg.x * ck.y + pg.y * ck.z + pg.z * ck.w;
+                    if (DEPTH) {
+                        gd = grad_depth ? grad_depth[o] : 0.f;
+                        if (!pixgrad) pg.w += gd * depth_img[o];
+                        G0 += gd * ckpt_depth[slot0 + p];
+                    }
+                    // state at the second bucket's start (only pixels still
+                    // blending there have that checkpoint; the others get an
+                    // inert finite state: their second-bucket bits are 0)
+                    if (m1 != 0u) {
+                        const float4 c2 = ckpt[slot0 + kTilePx + p];
+                        T1 = c2.x;
+                        G1 = pg.x * c2.y + pg.y * c2.z + pg.z * c2.w;
+                        if (DEPTH) G1 += gd * ckpt_depth[slot0 + kTilePx + p];
+                    }
                 }
-                const float4 ck = ckpt[slot0 + p];
-                float G0 = pg.x * ck.y + pg.y * ck.z + pg.z * ck.w;
-                if (DEPTH) {
-                    const float gd = grad_depth ? grad_depth[o] : 0.f;
-                    if (!pixgrad) pg.w += gd * depth_img[o];
-                    G0 += gd * ckpt_depth[slot0 + p];
-                    sD[wid][pos] = gd;
-                }
-                // state at the second bucket's start (only pixels still
-                // blending there have that checkpoint; the others get an
-                // inert finite state: their second-bucket bits are 0)
-                float T1 = 0.f, G1 = 0.f;
-                if (m1 != 0u) {
-                    const float4 c2 = ckpt[slot0 + kTilePx + p];
-                    T1 = c2.x;
-                    G1 = pg.x * c2.y + pg.y * c2.z + pg.z * c2.w;
-                    if (DEPTH)
-                        G1 += (grad_depth ? grad_depth[o] : 0.f) * ckpt_depth[slot0 + kTilePx + p];
-                }
+                if (DEPTH) sD[wid][2 * pr + hi] = gd;
                 BwdList& L = sL[wid];
-                const int ps = (pos >> 1) * 4 + (pos & 1);  // pair-interleaved slots
+                const int ps = pr * 4 + hi;  // pair-interleaved slots
                 L.ga[ps] = pg.x;
                 L.ga[ps + 2] = pg.y;
                 L.gb[ps] = pg.z;
@@ -343,26 +361,12 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
                 L.s[ps + 2] = G0;
                 L.s2[ps] = T1;
                 L.s2[ps + 2] = G1;
-                L.ma[pos] = m0;
-                L.mb[pos] = m1;
+                L.ma[2 * pr + hi] = m0;
+                L.mb[2 * pr + hi] = m1;
                 L.xy[ps] = (float)ix;
                 L.xy[ps + 2] = (float)iy;
             }
-            nact += __popc(bal);
-        }
-        // odd count: pad the last pair with an inert pixel (no blend bits,
-        // zero gradient, finite state)
-        if ((nact & 1) && lane == 0) {
-            BwdList& L = sL[wid];
-            const int ps = (nact >> 1) * 4 + 1;
-            L.ga[ps] = L.ga[ps + 2] = L.gb[ps] = L.gb[ps + 2] = 0.f;
-            L.s[ps] = 1.f;
-            L.s[ps + 2] = 0.f;
-            L.s2[ps] = 1.f;
-            L.s2[ps + 2] = 0.f;
-            L.ma[nact] = L.mb[nact] = 0u;
-            L.xy[ps] = L.xy[ps + 2] = 0.f;
-            if (DEPTH) sD[wid][nact] = 0.f;
+            npair += __popc(bal);
         }
         __syncwarp();
         // ---- diagonal wavefront over the active pixel pairs; lane i applies
@@ -374,7 +378,7 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
         const f32x2 z2 = pk2(0.f, 0.f);
         SplatAcc2 q0 = {z2, z2, z2, z2, z2, z2, z2, z2, z2, z2}, q1 = q0;
         const SplatP2 S0 = splat_p2(A0, B0, C0), S1 = splat_p2(A1, B1, C1);
-        const int npair = (nact + 1) >> 1;
+
         uint32_t seen;
         // the clamp at alpha_max can only bind for splats with sigma >= alpha_max
         const bool clamp = __any_sync(0xffffffffu, (k0 < ke && B0.y >= amax * 0.999999f) ||
