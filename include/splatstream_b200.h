@@ -198,8 +198,8 @@ int ss_replay_pixel_states(const ss_camera *cam, const ss_raster_opts *opts,
  * (1-l) mean|x-y| + l (1 - SSIM), 11x11 Gaussian window, mirror padding.
  * d_sums receives (sum |x-y|, sum SSIM) as doubles; d_grad (h,w,3) the
  * analytic gradient; optional d_pixgrad (h,w,4) float4 (g_r, g_g, g_b,
- * g . x) for ss_backward_splat (lambda_ssim != 0 only).  Needs height,
- * width >= 6 when lambda_ssim != 0. */
+ * g . x) for ss_backward_splat (lambda_ssim != 0 only; d_grad may then be
+ * NULL).  Needs height, width >= 6 when lambda_ssim != 0. */
 size_t ss_loss_workspace_bytes(int32_t height, int32_t width);
 int ss_loss_l1_ssim(int32_t height, int32_t width, const float *d_x, const float *d_y,
                     float lambda_ssim, float *d_grad, float *d_pixgrad, double *d_sums,
@@ -375,6 +375,14 @@ int ss_densify_apply(const ss_map *map, void *d_workspace, const float *d_normal
                      float clone_step, float shrink_log, const ss_map *out, int32_t n_planes,
                      const float *const *planes_in, float *const *planes_out,
                      const int32_t *plane_floats, int64_t *d_survivors, void *stream);
+
+/* The drop-in API's finite checks (ParamGrads.validate_finite, api.py:74-79;
+ * adam_step, optimizer.py:111-113) in one launch over up to 8 float32
+ * tensors (host arrays of device pointers and element counts): d_flags[t] =
+ * 1 if tensor t holds a non-finite value, d_flags[n + t] = 1 if it holds a
+ * non-zero value, else 0 (2 n int32, zeroed by the call). */
+int ss_check_finite(int32_t n_tensors, const float *const *d_tensors, const int64_t *counts,
+                    int32_t *d_flags, void *stream);
 
 /* Replaces resize_for_densify (optimizer.py:136-146): for each of n_planes
  * per-Gaussian float planes (plane_floats[p] floats per row), rows

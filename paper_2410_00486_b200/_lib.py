@@ -94,6 +94,7 @@ _SIGS = {
     "ss_status_begin_step": (I32, [VP, VP]),
     "ss_status_flags": (I32, [VP, VP, VP]),
     "ss_resize_moments": (I32, [I64, VP, I64, I32, VP, VP, VP, VP]),
+    "ss_check_finite": (I32, [I32, VP, VP, VP, VP]),
     "ss_splats_from_projection": (I32, [I64, VP, VP, VP, P(SSCamera), P(SSSplats), VP]),
     "ss_replay_pixel_states": (I32, [P(SSCamera), P(SSRasterOpts), P(SSSplats), P(SSBins), VP,
                                      VP, VP, VP, I32, I32, I32, VP, VP]),

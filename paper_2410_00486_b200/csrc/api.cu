@@ -57,6 +57,8 @@ cudaError_t launch_stats(const ss_map*, const ss_param_grads*, const uint8_t*, c
 cudaError_t launch_apply_stat_planes(const ss_map*, const ss_param_grads*, cudaStream_t);
 cudaError_t launch_opacity_reset(const ss_map*, float, float*, float*, cudaStream_t);
 size_t densify_workspace_bytes(int64_t);
+cudaError_t launch_check_finite(int, const float* const*, const int64_t*, int32_t*,
+                                cudaStream_t);
 cudaError_t launch_resize_moments(int64_t, const int64_t*, int64_t, int, const float* const*,
                                   float* const*, const int32_t*, cudaStream_t);
 cudaError_t launch_densify_count(const ss_map*, float, float, double, void*, int64_t*, uint8_t*,
@@ -225,7 +227,8 @@ size_t ss_loss_workspace_bytes(int32_t height, int32_t width) {
 int ss_loss_l1_ssim(int32_t height, int32_t width, const float* d_x, const float* d_y,
                     float lambda_ssim, float* d_grad, float* d_pixgrad, double* d_sums,
                     void* d_workspace, size_t workspace_bytes, void* stream) {
-    if (!d_x || !d_y || !d_grad || !d_sums || height <= 0 || width <= 0) return SS_EINVAL;
+    if (!d_x || !d_y || !d_sums || height <= 0 || width <= 0) return SS_EINVAL;
+    if (!d_grad && !d_pixgrad) return SS_EINVAL;  // d_grad may be NULL when d_pixgrad is given
     if (lambda_ssim != 0.0f && (height < 6 || width < 6)) return SS_EINVAL;
     if (workspace_bytes < loss_workspace_bytes(height, width)) return SS_ECAPACITY;
     if (d_pixgrad && lambda_ssim == 0.0f) return SS_EINVAL;
@@ -341,6 +344,14 @@ int ss_densify_apply(const ss_map* map, void* d_workspace, const float* d_normal
     return rc(launch_densify_apply(map, d_workspace, d_normals, seed, clone_step, shrink_log,
                                    out, n_planes, planes_in, planes_out, plane_floats, 0,
                                    d_survivors, S(stream)));
+}
+
+int ss_check_finite(int32_t n_tensors, const float* const* d_tensors, const int64_t* counts,
+                    int32_t* d_flags, void* stream) {
+    if (n_tensors < 1 || n_tensors > 8 || !d_tensors || !counts || !d_flags) return SS_EINVAL;
+    for (int t = 0; t < n_tensors; ++t)
+        if (counts[t] < 0 || (counts[t] > 0 && !d_tensors[t])) return SS_EINVAL;
+    return rc(launch_check_finite(n_tensors, d_tensors, counts, d_flags, S(stream)));
 }
 
 int ss_resize_moments(int64_t n_out, const int64_t* d_survivors, int64_t n_surv,

@@ -776,4 +776,47 @@ cudaError_t launch_opacity_reset(const ss_map* mp, float ceiling, float* m, floa
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------- finite check
+// api.py:74-79 / optimizer.py:111-113 for up to 8 float tensors in one
+// launch: flags[t] |= 1 when tensor t holds a non-finite value, flags[n + t]
+// |= 1 when it holds a non-zero value (adam_step's "sh_rest in use" test).
+// The caller zeroes flags (2n int32) first.
+struct FiniteSet {
+    const float* p[8];
+    int64_t n[8];
+};
+
+__global__ void check_finite_kernel(int nt, FiniteSet S, int32_t* __restrict__ flags) {
+    for (int t = 0; t < nt; ++t) {
+        bool bad = false, nz = false;
+        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < S.n[t];
+             e += (int64_t)gridDim.x * blockDim.x) {
+            const float v = S.p[t][e];
+            bad |= !isfinite(v);
+            nz |= v != 0.f;
+        }
+        const unsigned bb = __ballot_sync(0xffffffffu, bad), bn = __ballot_sync(0xffffffffu, nz);
+        if ((threadIdx.x & 31) == 0) {
+            if (bb) atomicOr(flags + t, 1);
+            if (bn) atomicOr(flags + nt + t, 1);
+        }
+    }
+}
+
+cudaError_t launch_check_finite(int nt, const float* const* ptrs, const int64_t* counts,
+                                int32_t* flags, cudaStream_t s) {
+    FiniteSet S = {};
+    int64_t mx = 1;
+    for (int t = 0; t < nt; ++t) {
+        S.p[t] = ptrs[t];
+        S.n[t] = counts[t];
+        mx = counts[t] > mx ? counts[t] : mx;
+    }
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int32_t) * 2 * nt, s);
+    if (e != cudaSuccess) return e;
+    const int blocks = (int)((mx + 255) / 256 < 1184 ? (mx + 255) / 256 : 1184);
+    check_finite_kernel<<<blocks, 256, 0, s>>>(nt, S, flags);
+    return cudaGetLastError();
+}
+
 }  // namespace ss

@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(256, 3) ssim_bwd_kernel(int H, int W, const fl
                 const double gx = (double)adj[0][o] + (double)adj[1][o] * (2.0 * xv) +
                                   (double)adj[2][o] * yv;
                 const float gv = (float)((1.0 - lam) * sgn * inv_nd - lam * gx);
-                grad[go] = gv;
+                if (grad) grad[go] = gv;  // the engine only needs pixgrad
                 if (pg) pg[4 * ((size_t)oy * W + ox) + c] = gv;
                 gdot[o] += gv * xv;
             }

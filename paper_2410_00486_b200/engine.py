@@ -257,8 +257,10 @@ class MappingEngine:
                                          self.work_cap, P(self.status), stream_handle()),
                   "ss_backward_schedule")
         use_pg = self.cfg.lambda_ssim != 0.0 and not self.opts.with_depth
+        # with pixgrad the backward never reads grad_image: it is not written
         check(L.ss_loss_l1_ssim(self.H, self.W, P(self.image), P(target),
-                                float(self.cfg.lambda_ssim), P(self.grad_image),
+                                float(self.cfg.lambda_ssim),
+                                None if use_pg else P(self.grad_image),
                                 P(self.pixgrad) if use_pg else None, P(self.sums),
                                 P(self.loss_ws), self.loss_ws.numel(), s), "ss_loss_l1_ssim")
         if self.opts.with_depth:

@@ -117,9 +117,9 @@ def adam_step(gmap: GaussianMap, grads: ParamGrads, state: AdamState, sh_degree:
              ("log_scale", grads.log_scale), ("opacity_logit", grads.opacity_logit),
              ("sh_dc", grads.sh_dc), ("sh_rest", grads.sh_rest))
 
-    def raise_nonfinite(flags):
-        for (name, _), good in zip(named, [bool(v) for v in flags]):
-            if not good:
+    def raise_nonfinite(bad):
+        for (name, _), b in zip(named, [int(v) for v in bad[:len(named)]]):
+            if b:
                 raise FloatingPointError(f"non-finite gradient for parameter '{name}'")
     deferred = errors.deferred()
     if deferred:
@@ -127,14 +127,13 @@ def adam_step(gmap: GaussianMap, grads: ParamGrads, state: AdamState, sh_degree:
         # Gaussians with non-finite gradients untouched.  sh_rest is updated
         # unless the gradients are known to come from an SH-0 render (then they
         # are exactly 0 and so are the moments: the skip is bit-exact)
-        errors.defer(finite_flags_device([t for _, t in named]), raise_nonfinite)
+        errors.defer(finite_flags_device([t for _, t in named])[:len(named)], raise_nonfinite)
         upd_rest = state.sh_rest_active or grads.sh_degree is None or grads.sh_degree > 0
     else:
-        # the finite checks and the "sh_rest in use" test as one host read
-        extra = () if state.sh_rest_active else ((grads.sh_rest != 0).any(),)
-        host = finite_flags([t for _, t in named], extra)
-        raise_nonfinite(host[:len(named)])
-        upd_rest = state.sh_rest_active or bool(host[len(named)])
+        # the finite checks and the "sh_rest in use" test: one kernel, one host read
+        host = finite_flags([t for _, t in named], extra_nonzero=True)
+        raise_nonfinite([0 if good else 1 for good in host[:len(named)]])
+        upd_rest = state.sh_rest_active or bool(host[2 * len(named) - 1])
     state.sh_rest_active = upd_rest
     state.step_count += 1
     st = torch.empty(_lib.STATUS_WORDS, dtype=torch.int64, device=gmap.device)

@@ -134,27 +134,29 @@ def new_status(dev):
     return st
 
 
-def finite_flags(tensors, extra=()):
-    """[all(isfinite(t)) for t in tensors] + [bool(e) for e in extra] with one
-    fused max-|x| reduction over the tensors (torch._foreach_norm, inf-norm:
-    NaN and inf propagate, finite values cannot overflow) and ONE host read.
-    `extra`: 0-d device tensors read back in the same transfer."""
-    nonempty = [t for t in tensors if t.numel()]
-    vals = list(torch._foreach_norm(nonempty, float("inf"))) if nonempty else []
-    host = torch.stack([torch.isfinite(v) for v in vals] + [e.bool() for e in extra]).cpu() \
-        if (vals or extra) else torch.zeros(0, dtype=torch.bool)
-    it = iter(host.tolist())
-    flags = [bool(next(it)) if t.numel() else True for t in tensors]
-    return flags + [bool(v) for v in it]
-
-
 def finite_flags_device(tensors):
-    """Device bool tensor: [all(isfinite(t)) for t in tensors] (no host read)."""
-    nonempty = [t for t in tensors if t.numel()]
-    vals = iter(torch._foreach_norm(nonempty, float("inf")) if nonempty else [])
-    dev = tensors[0].device if tensors else torch.device("cuda")
-    one = torch.ones((), dtype=torch.bool, device=dev)
-    return torch.stack([torch.isfinite(next(vals)) if t.numel() else one for t in tensors])
+    """Device int32 flags (2 n): [t] = tensor t holds a non-finite value,
+    [n + t] = it holds a non-zero value -- one ss_check_finite launch, no
+    host read."""
+    ts = [t.contiguous() if t.dtype == torch.float32 else t.float().contiguous()
+          for t in tensors]
+    n = len(ts)
+    flags = torch.empty(2 * n, dtype=torch.int32, device=ts[0].device)
+    ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() if t.numel() else None for t in ts])
+    cnts = (ctypes.c_int64 * n)(*[t.numel() for t in ts])
+    check(lib().ss_check_finite(n, ptrs, cnts, P(flags), stream_handle()), "ss_check_finite")
+    return flags
+
+
+def finite_flags(tensors, extra_nonzero=False):
+    """[all(isfinite(t)) for t in tensors] (+ [any(t != 0)] per tensor with
+    extra_nonzero) from one kernel and ONE host read."""
+    if not tensors:
+        return []
+    h = finite_flags_device(tensors).cpu().tolist()
+    n = len(tensors)
+    out = [h[t] == 0 for t in range(n)]
+    return out + ([h[n + t] != 0 for t in range(n)] if extra_nonzero else [])
 
 
 def raise_param_errors(st_host):
@@ -565,16 +567,16 @@ class ParamGrads:
         mode the check stays on the device and raises later, errors.py)."""
         names = ("position", "rotation", "log_scale", "opacity_logit", "sh_dc", "sh_rest")
 
-        def raiser(flags):
-            for k, good in zip(names, [bool(v) for v in flags]):
-                if not good:
+        def raiser(bad):
+            for k, b in zip(names, [int(v) for v in bad[:len(names)]]):
+                if b:
                     raise FloatingPointError(
                         f"non-finite gradient in {'sh' if k.startswith('sh') else k}")
         tensors = [getattr(self, k) for k in names]
         if errors.deferred():
-            errors.defer(finite_flags_device(tensors), raiser)
+            errors.defer(finite_flags_device(tensors)[:len(names)], raiser)
         else:
-            raiser(finite_flags(tensors))
+            raiser([0 if good else 1 for good in finite_flags(tensors)])
         return self
 
 

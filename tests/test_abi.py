@@ -72,14 +72,13 @@ def test_product_raises_without_gpu():
         ss.GaussianMap(10)
 
 
-def test_finite_flags_host_logic():
-    """finite_flags: one fused inf-norm reduction per call, empty tensors
-    count as finite, extra 0-d flags appended in order (CPU tensors here)."""
-    import torch
-    from paper_2410_00486_b200.rasterizer import finite_flags
-    nan, inf = float("nan"), float("inf")
-    got = finite_flags([torch.ones(3), torch.tensor([nan, 1.0]), torch.zeros(0),
-                        torch.tensor([3e38, -3e38]), torch.tensor([-inf])],
-                       (torch.tensor(True), torch.tensor(False)))
-    assert got == [True, False, True, True, False, True, False]
-    assert finite_flags([]) == []
+def test_check_finite_rejects_bad_arguments():
+    """ss_check_finite (the drop-in API's finite checks) validates its
+    arguments before touching the device."""
+    from paper_2410_00486_b200 import _lib
+    L = _lib.lib()
+    ptrs = (ctypes.c_void_p * 1)(None)
+    cnts = (ctypes.c_int64 * 1)(5)
+    assert L.ss_check_finite(0, ptrs, cnts, ctypes.c_void_p(8), None) == _lib.SS_EINVAL
+    assert L.ss_check_finite(9, ptrs, cnts, ctypes.c_void_p(8), None) == _lib.SS_EINVAL
+    assert L.ss_check_finite(1, ptrs, cnts, ctypes.c_void_p(8), None) == _lib.SS_EINVAL
