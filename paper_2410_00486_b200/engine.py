@@ -368,14 +368,18 @@ class MappingEngine:
         self.launches += self._launches_per_step()
         self._snapshot(rec)
 
-    def _launches_per_step(self):
-        k = (KERNELS_PER_CALL["step_fb"] + binning_kernels(self.n_tiles, len(self.gmap))
-             + KERNELS_PER_CALL["chain_adam"] + KERNELS_PER_CALL["snapshot"])
+    def _launches_fb(self, depth_loss: bool):
+        """Library kernels one _forward_backward enqueues (K1-K7 of a view)."""
+        k = KERNELS_PER_CALL["step_fb"] + binning_kernels(self.n_tiles, len(self.gmap))
         if self.n_tiles <= _lib.ORDER_MAX_TILES:
             k += KERNELS_PER_CALL["tile_order"]
-        if self.opts.with_depth and self.cfg.depth_weight:
-            k += 3
+        if depth_loss:
+            k += 3  # ss_depth_l1
         return k
+
+    def _launches_per_step(self):
+        return (self._launches_fb(bool(self.opts.with_depth and self.cfg.depth_weight))
+                + KERNELS_PER_CALL["chain_adam"] + KERNELS_PER_CALL["snapshot"])
 
     def _drain(self, lag: int):
         """Consume status snapshots older than `lag` steps; recover overflow."""
@@ -583,8 +587,11 @@ class MappingEngine:
             flat.zero_()
             losses = []
             for v, (cam, tgt, td) in enumerate(views):
+                depth_loss = bool(self.opts.with_depth and td is not None
+                                  and self.cfg.depth_weight != 0.0)
                 while True:
                     mp, cm, op = self._forward_backward(cam, tgt, td, v)
+                    self.launches += self._launches_fb(depth_loss)
                     if not sync_each:
                         break
                     row = self.status.cpu().numpy()
@@ -594,14 +601,17 @@ class MappingEngine:
                     self._alloc_pair_buffers(max(
                         self._cap, int(int(row[_lib.ST_PAIRS]) * self.cfg.pair_margin) + 4096))
                     check(L.ss_status_reset(P(self.status), s), "ss_status_reset")
+                    self.launches += 1
                 check(L.ss_chain_backward(ctypes.byref(mp), ctypes.byref(cm), ctypes.byref(op),
                                           P(self.g2d), P(self.splats.flags),
                                           P(self.contributed), lon if v == 0 else 0.0,
                                           _lib.SS_CHAIN_ACCUMULATE | _lib.SS_CHAIN_STAT_PLANES,
                                           ctypes.byref(fss), P(self.status), s),
                       "ss_chain_backward")
+                self.launches += 1
                 losses.append(self.sums[:2].clone())
             check(L.ss_status_flags(P(self.status), P(self._flat_tail), s), "ss_status_flags")
+            self.launches += 1
             if allreduce is not None:
                 allreduce(flat)
             # one host read: this rank's status row + the (reduced) flags
@@ -618,6 +628,7 @@ class MappingEngine:
             # some rank overflowed: every rank redoes the step, view by view
             # with a read per view (the rare path), so the collectives match
             check(L.ss_status_reset(P(self.status), s), "ss_status_reset")
+            self.launches += 1
             losses, row, flags = run_views(sync_each=True)
         if flags[1] > 0:
             self._check_errors(row)
@@ -632,6 +643,7 @@ class MappingEngine:
                              P(self.status), s), "ss_adam_step")
         check(L.ss_apply_stat_planes(ctypes.byref(mp), ctypes.byref(fss), s),
               "ss_apply_stat_planes")
+        self.launches += 2  # Adam + statistics planes
         self._mv_unchecked = True
         self.iteration += 1
         self.since_densify += 1
