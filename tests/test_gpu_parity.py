@@ -783,34 +783,60 @@ def test_seed_large_cloud_vs_oracle_and_engine_insert():
     assert len(eng.losses()) == 2
 
 
-def test_engine_launch_count_matches_profiler():
-    """MappingEngine.launches (bench.py's gpu_launches) equals the library
-    kernels CUPTI sees in graph-replayed steps, side-stream kernels included."""
-    _need_gpu()
-    import paper_2410_00486_b200 as ss
-    from paper_2410_00486_b200.scene import survey_camera, survey_scene
-    n, w, h = 20000, 320, 240
-    g = ss.GaussianMap.from_scene(survey_scene(n, 0))
-    cam = survey_camera(w, h)
-    opts = ss.RasterOpts(sh_degree=0)
-    tgt = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(n, 100)), cam,
-                               opts).image.clone()
-    eng = ss.MappingEngine(g, w, h, opts)
-    eng.fit_capacity(cam)
+_LAUNCH_COUNT = r"""
+import sys
+sys.path.insert(0, {repo!r})
+import torch
+import paper_2410_00486_b200 as ss
+from paper_2410_00486_b200.scene import survey_camera, survey_scene
+n, w, h, V = 20000, 320, 240, {views}
+opts = ss.RasterOpts(sh_degree=0)
+cams = [survey_camera(w, h, v, V) for v in range(V)]
+tm = ss.GaussianMap.from_scene(survey_scene(n, 100))
+tg = [ss.rasterize_forward(tm, c, opts).image.clone() for c in cams]
+eng = ss.MappingEngine(ss.GaussianMap.from_scene(survey_scene(n, 0)), w, h, opts)
+eng.fit_capacity(cams)
+if V == 1:
     eng.enable_graph()
-    for _ in range(3):
-        eng.step(cam, tgt)
+    run = lambda: eng.step(cams[0], tg[0])
+else:
+    run = lambda: eng.multiview_step(cams, tg)
+for _ in range(3):
+    run()
+eng.synchronize()
+torch.cuda.synchronize()
+l0 = eng.launches
+with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+    for _ in range(4):
+        run()
     eng.synchronize()
-    steps = 4
-    l0 = eng.launches
-    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
-        for _ in range(steps):
-            eng.step(cam, tgt)
-        eng.synchronize()
-    ours = sum(e.count for e in prof.key_averages() if e.key.startswith("ss::")
-               or "ss::" in e.key.split("(")[0])
-    assert eng.launches - l0 == ours
-    assert ours == steps * eng._launches_per_step()
+    torch.cuda.synchronize()
+ours = sum(e.count for e in prof.key_averages() if e.key.startswith("ss::")
+           or "ss::" in e.key.split("(")[0])
+per = eng._launches_per_step() if V == 1 else -1
+print("COUNTS", eng.launches - l0, ours, per)
+"""
+
+
+@pytest.mark.parametrize("views", [1, 3])
+def test_engine_launch_count_matches_profiler(views):
+    """MappingEngine.launches (bench.py's gpu_launches) equals the library
+    kernels CUPTI sees: graph-replayed single-view steps (side-stream kernels
+    included) and keyframe-batch steps.  Each count runs in a fresh process
+    (one profiler session per process)."""
+    _need_gpu()
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _LAUNCH_COUNT.format(repo=repo, views=views)],
+                       capture_output=True, text=True, timeout=600)
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("COUNTS")]
+    assert line, r.stdout[-2000:] + r.stderr[-2000:]
+    counted, seen, per = (int(v) for v in line[0].split()[1:])
+    assert counted == seen > 0
+    if views == 1:
+        assert seen == 4 * per
 
 
 def test_multiview_step_recovers_from_pair_overflow():
