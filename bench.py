@@ -550,6 +550,8 @@ def main():
                                  "events)"},
                 "views_per_s": res["views_per_s"], "clocks": clocks, "e2e": res.get("e2e"),
                 "validation_only": (args.same_device or args.dist_backend != "nccl") or None,
+                "scaling_reference": "the N = 1 point of this workload is the `config4` block "
+                                     "of the N = 1 line (whose `value` is configs[1])",
                 "gpu_launches": res["gpu_launches"], "cpu_baseline": None,
             }
             print(json.dumps(line), flush=True)
