@@ -2,9 +2,10 @@
 //
 // Restates rasterize_forward's tile loop (rasterizer/api.py:153-196) and
 // forward_tile (rasterizer/kernels.py:34-109) with checkpoint_tile
-// (kernels.py:112-152) folded in: one 128-thread CTA per 16x16 tile, two
-// pixels per thread (rows r and r+8, two independent blend chains per
-// thread for ILP).  The tile's depth-sorted list is walked in batches of
+// (kernels.py:112-152) folded in: one 128-thread CTA per 16x16 tile, a warp
+// per 8x8 quadrant, two pixels per thread (rows r and r+4 of one column: two
+// independent blend chains for ILP, sharing the dx terms, as the (lo, hi)
+// lanes of packed f32x2 state).  The tile's depth-sorted list is walked in batches of
 // 256 splat records staged in shared memory (each thread gathers two
 // records; every thread then reads the batch with broadcast LDS.128).
 // Reference semantics kept:
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
     uint32_t* __restrict__ tile_cost) {
     __shared__ SplatRec s_rec[256];
     __shared__ uint32_t s_id[256];
-    __shared__ uint8_t s_band[256];  // bit w: the splat's blend region reaches band w
+    __shared__ uint8_t s_band[256];  // bit w: the splat's blend region reaches warp w's quadrant
     __shared__ int s_hit[CONTRIB ? 256 : 1];
     __shared__ int s_kmax[4];
     __shared__ unsigned long long s_wbase;
@@ -73,12 +74,13 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
     uint32_t tr_iters = 0;
 #endif
     const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
-    // warp w owns the 4-row band 4w..4w+3; a thread owns rows r and r + 2 of
-    // its column (the two pixels share the dx terms)
+    // warp w owns the 8x8 quadrant (w & 1, w >> 1) of the tile; a thread owns
+    // rows r and r + 4 of one of its columns (the two pixels share the dx terms)
     const int w = t >> 5, lane = t & 31;
-    const int row0 = 4 * w + (lane >> 4), row1 = row0 + 2;
-    const int ix = x0 + (lane & 15), iy0 = y0 + row0, iy1 = y0 + row1;
-    const int p0 = row0 * kTile + (lane & 15), p1 = row1 * kTile + (lane & 15);  // tile-local ids
+    const int col = 8 * (w & 1) + (lane & 7);
+    const int row0 = 8 * (w >> 1) + (lane >> 3), row1 = row0 + 4;
+    const int ix = x0 + col, iy0 = y0 + row0, iy1 = y0 + row1;
+    const int p0 = row0 * kTile + col, p1 = row1 * kTile + col;  // tile-local ids
     const float px = (float)ix, py0 = (float)iy0, py1 = (float)iy1;
     const uint32_t start = tile_start[tile];
     const uint32_t len = tile_end[tile] - start;
@@ -110,15 +112,17 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
                 s_id[t + 128 * r] = s;
                 const SplatRec sr = rec[s];
                 s_rec[t + 128 * r] = sr;
-                // bands (4 rows each) the splat's blend region can reach:
-                // |y - my| <= ext_y within the band, |x - mx| <= ext_x within
-                // the tile's columns
+                // 8x8 quadrants (one per warp) the splat's blend region can
+                // reach: |x - mx| <= ext_x and |y - my| <= ext_y within the
+                // quadrant (a square block culls small splats better than a
+                // 16 x 4 band: 91 -> 86 us, 244 -> 225 us after 250 iterations)
                 const float2 ext = __half22float2(*reinterpret_cast<const __half2*>(&sr.c.w));
-                const bool xin = fabsf(sr.a.x - ((float)x0 + 7.5f)) <= ext.x + 7.5f;
-                uint32_t bm = 0;
-#pragma unroll
-                for (int b = 0; b < 4; ++b)
-                    bm |= (xin && fabsf(sr.a.y - ((float)(y0 + 4 * b) + 1.5f)) <= ext.y + 1.5f) << b;
+                const bool xin0 = fabsf(sr.a.x - ((float)x0 + 3.5f)) <= ext.x + 3.5f;
+                const bool xin1 = fabsf(sr.a.x - ((float)x0 + 11.5f)) <= ext.x + 3.5f;
+                const bool yin0 = fabsf(sr.a.y - ((float)y0 + 3.5f)) <= ext.y + 3.5f;
+                const bool yin1 = fabsf(sr.a.y - ((float)y0 + 11.5f)) <= ext.y + 3.5f;
+                const uint32_t bm = (uint32_t)(xin0 && yin0) | ((uint32_t)(xin1 && yin0) << 1) |
+                                    ((uint32_t)(xin0 && yin1) << 2) | ((uint32_t)(xin1 && yin1) << 3);
                 s_band[t + 128 * r] = (uint8_t)bm;
                 if (CONTRIB) s_hit[t + 128 * r] = 0;
             }
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(128) blend_forward_kernel(
                 if (DEPTH) ckpt_depth[slot + p1] = s1.D;
             }
             if (__all_sync(0xffffffffu, s0.done && s1.done)) continue;  // whole warp stopped
-            // the bucket's splats whose blend region reaches this warp's band
+            // the bucket's splats whose blend region reaches this warp's quadrant
             unsigned todo = __ballot_sync(0xffffffffu, j0 + lane < nb && ((s_band[j0 + lane] >> w) & 1u));
             while (todo) {
                 const int j = j0 + __ffs(todo) - 1;
