@@ -26,6 +26,12 @@
 // equals T (g . rgb) - (g . image - G_after) / (1 - a), so two floats move
 // per shuffle instead of four.  Warps are persistent and pull work units
 // from the list the forward appended.
+//
+// Three kernels share this structure: backward_quad_kernel (default) runs
+// one chain per 8x8 quadrant of the tile over only the positions that
+// quadrant blended; backward_splat_kernel (SS_BWD_UNIT=1) one chain per
+// bucket over the whole tile; backward_sparse_kernel (SS_BWD_SPARSE=1)
+// evaluates only the blended pairs in two phases.
 #include "common.cuh"
 
 namespace ss {
@@ -396,6 +402,463 @@ __global__ void __launch_bounds__(32 * kBwdWarps) backward_splat_kernel(
         if (k1 < ke) {
             bwd_commit<NC>(q1, A1, B1, g2d + (size_t)s1 * NC);
             if (contributed && (seen & 2u)) contributed[s1] = 1;
+        }
+        __syncwarp();
+    }
+}
+
+// --------------------------------------------------------------------------
+// Quadrant chains (default).  A pixel of the tile only blends the splats
+// whose blend region reaches its 8x8 quadrant, and at the bench workload a
+// quadrant's pixels together blend ~22 of a unit's 64 list positions (the
+// forward iterates per quadrant too).  The unit is therefore split into one
+// chain per quadrant: the quadrant's active column pairs (<= 32) flow
+// through only the positions some pixel of that quadrant blended (the OR
+// of its pixels' blend masks, compacted in list order), starting from the
+// state at the unit start -- the positions left out did not touch these
+// pixels, so every blended term still sees exactly the reference's state.
+// A chain of <= 32 positions runs on a half-warp (2 positions per lane,
+// np + ceil(n/2) - 1 steps); a quadrant with more is split at the bucket
+// boundary (the second part starts from the second bucket's checkpoint).
+// The two half-warps take two chains at a time, longest first.  A position
+// appears in several chains: each chain folds its per-splat sums into a
+// per-warp shared row, and the position's owner lane commits the row with
+// one red.add per (tile, splat) column as before.
+//
+// The chain carries (T, G - g . image) instead of (T, G): dL/dalpha needs
+// only G_after - g . image, so g . image leaves the per-step loads.
+constexpr int kQWarps = 2;
+constexpr int kQPairs = kTilePx / 2;  // pair slots: quadrant q at [32 q, 32 q + 32); + 1 inert slot
+
+template <bool DEPTH>
+struct QuadList {
+    static constexpr int NC = DEPTH ? 10 : 9;
+    float4 ga[kQPairs + 1];        // per pair: (gx, gx', gy, gy')
+    float4 gb[kQPairs + 1];        // (gz, gz', y, y + 1)
+    float4 s[kQPairs + 1];         // (T, T', G - gw, G' - gw') at the unit start
+    float4 s2[kQPairs + 1];        // the same at the second bucket's start
+    uint4 m[kQPairs + 1];          // blend masks (bucket 0 lo, hi; bucket 1 lo, hi)
+    float px[kQPairs + 1];         // the pair's column x
+    float2 gd[DEPTH ? kQPairs + 1 : 1];  // depth gradient (lo, hi)
+    float acc[kUnit][NC];          // raw per-splat sums of the unit, over its chains
+    uint32_t sid[kUnit];           // the unit's splats (records are re-read through L1/L2)
+    uint8_t qpos[4][kUnit];        // per quadrant: its positions, compacted in list order
+};
+
+template <typename T>
+__device__ __forceinline__ T sel4(int q, T a, T b, T c, T d) {
+    return q == 0 ? a : q == 1 ? b : q == 2 ? c : d;
+}
+
+// One splat applied to a pixel pair of a chain (bwd_term2 with the state
+// (T, G - g . image)).
+template <bool DEPTH, bool CLAMP>
+__device__ __forceinline__ void chain_term2(uint32_t ba, uint32_t bb, float pxs, f32x2 py,
+                                            f32x2 gx, f32x2 gy, f32x2 gz, f32x2 gd,
+                                            const SplatP2& S, float amax, f32x2& T, f32x2& G,
+                                            SplatAcc2& q) {
+    const float dxs = __fsub_rn(pxs, S.mxs);
+    const float q0s = __fmul_rn(__fmul_rn(S.c0s, dxs), dxs), q1s = __fmul_rn(S.c1x2s, dxs);
+    const f32x2 dx = pk2(dxs, dxs), dy = sub2(py, S.my);
+    const f32x2 m = fma2(mul2(S.c2, dy), dy, fma2(pk2(q1s, q1s), dy, pk2(q0s, q0s)));
+    float e0, e1;
+    upk2(mul2(m, pk2(-0.5f * kLog2e, -0.5f * kLog2e)), e0, e1);
+    float a0, a1;
+    upk2(mul2(S.sig, pk2(ex2_approx(e0), ex2_approx(e1))), a0, a1);
+    if (CLAMP) {
+        a0 = fminf(a0, amax);
+        a1 = fminf(a1, amax);
+    }
+    a0 = ba ? a0 : 0.f;
+    a1 = bb ? a1 : 0.f;
+    const f32x2 a = pk2(a0, a1);
+    const f32x2 w = mul2(a, T);
+    f32x2 grgb = fma2(gz, S.cb, fma2(gy, S.cg, mul2(gx, S.cr)));
+    if (DEPTH) {
+        grgb = fma2(gd, S.z, grgb);
+        q.rz = fma2(w, gd, q.rz);
+    }
+    const f32x2 Gafter = fma2(grgb, w, G);
+    q.r0 = fma2(w, gx, q.r0);
+    q.r1 = fma2(w, gy, q.r1);
+    q.r2 = fma2(w, gz, q.r2);
+    // dL/da = T (g . rgb) - (g . image - G_after) / (1 - a)   (kernels.py:342-364)
+    const f32x2 om = sub2(pk2(1.f, 1.f), a);
+    float o0, o1;
+    upk2(om, o0, o1);
+    const f32x2 dal = fma2(T, grgb, mul2(Gafter, pk2(rcp_approx(o0), rcp_approx(o1))));
+    const f32x2 da =
+        mul2(dal, CLAMP ? pk2(a0 != amax ? a0 : 0.f, a1 != amax ? a1 : 0.f) : a);
+    const f32x2 tx = mul2(da, dx), ty = mul2(da, dy);
+    q.s_da = add2(q.s_da, da);
+    q.s_dx = add2(q.s_dx, tx);
+    q.s_dy = add2(q.s_dy, ty);
+    q.s_xx = fma2(tx, dx, q.s_xx);
+    q.s_xy = fma2(tx, dy, q.s_xy);
+    q.s_yy = fma2(ty, dy, q.s_yy);
+    T = mul2(T, om);
+    G = Gafter;
+}
+
+// The half-warp wavefront of one chain: lane hl applies its positions pa,
+// pb (-1: none) to pair j = step - hl of the chain's pairs [lb, lb + np);
+// lanes off the diagonal read the inert slot (no blend bits).
+template <bool DEPTH, bool CLAMP>
+__device__ __forceinline__ void quad_wavefront(int steps, int np, int hl, int lb, int pa, int pb,
+                                               const QuadList<DEPTH>& L,
+                                               const float4* __restrict__ S4, const SplatP2& S0,
+                                               const SplatP2& S1, float amax, SplatAcc2& q0,
+                                               SplatAcc2& q1) {
+    f32x2 T = pk2(0.f, 0.f), G = T;
+    const bool wa = pa >= 32, wb = pb >= 32;
+    const uint32_t bitA = pa >= 0 ? 1u << (pa & 31) : 0u;
+    const uint32_t bitB = pb >= 0 ? 1u << (pb & 31) : 0u;
+#pragma unroll 1
+    for (int st = 0; st < steps; ++st) {
+        T = shfl_up2(T);
+        G = shfl_up2(G);
+        const int j = st - hl;
+        const bool inr = (unsigned)j < (unsigned)np;
+        const int jj = inr ? lb + j : kQPairs;
+        const uint4 m = L.m[jj];
+        if (hl == 0 && inr) {
+            const float4 s = S4[jj];
+            T = pk2(s.x, s.y);
+            G = pk2(s.z, s.w);
+        }
+        const uint32_t xa0 = (wa ? m.z : m.x) & bitA, xa1 = (wa ? m.w : m.y) & bitA;
+        const uint32_t xb0 = (wb ? m.z : m.x) & bitB, xb1 = (wb ? m.w : m.y) & bitB;
+        const float pxs = L.px[jj];
+        const float4 g0 = L.ga[jj], g1 = L.gb[jj];
+        const f32x2 py = pk2(g1.z, g1.w);
+        const f32x2 gx = pk2(g0.x, g0.y), gy = pk2(g0.z, g0.w), gz = pk2(g1.x, g1.y);
+        f32x2 gd = pk2(0.f, 0.f);
+        if (DEPTH) {
+            const float2 d = L.gd[jj];
+            gd = pk2(d.x, d.y);
+        }
+        chain_term2<DEPTH, CLAMP>(xa0, xa1, pxs, py, gx, gy, gz, gd, S0, amax, T, G, q0);
+        chain_term2<DEPTH, CLAMP>(xb0, xb1, pxs, py, gx, gy, gz, gd, S1, amax, T, G, q1);
+    }
+}
+
+template <bool DEPTH>
+__device__ __forceinline__ void quad_fold(QuadList<DEPTH>& L, int p, const SplatAcc2& q) {
+    if (p < 0) return;
+    float* row = L.acc[p];
+    row[0] += hsum(q.r0);
+    row[1] += hsum(q.r1);
+    row[2] += hsum(q.r2);
+    row[3] += hsum(q.s_da);
+    row[4] += hsum(q.s_dx);
+    row[5] += hsum(q.s_dy);
+    row[6] += hsum(q.s_xx);
+    row[7] += hsum(q.s_xy);
+    row[8] += hsum(q.s_yy);
+    if (DEPTH) row[9] += hsum(q.rz);
+}
+
+// One round: lanes 0-15 run chain ida, lanes 16-31 chain idb (-1: idle).
+// Chain id = 2 q + part: a quadrant with <= 32 positions is one chain
+// (part 0: both buckets from the unit start), one with more is split at the
+// bucket boundary (part 0: bucket 0; part 1: bucket 1 from its checkpoint).
+template <bool DEPTH>
+__device__ __forceinline__ void quad_round(QuadList<DEPTH>& L, const SplatRec* __restrict__ rec,
+                                           int lane, int ida, int idb, const int (&qn0)[4],
+                                           const int (&qn1)[4], const int (&qnp)[4],
+                                           float amax) {
+    const bool hi = lane >= 16;
+    const int hl = lane & 15;
+    const int id = hi ? idb : ida;
+    int np = 0, off = 0, n = 0, q = 0;
+    bool second = false;
+    if (id >= 0) {
+        q = id >> 1;
+        const int n0 = sel4(q, qn0[0], qn0[1], qn0[2], qn0[3]);
+        const int n1 = sel4(q, qn1[0], qn1[1], qn1[2], qn1[3]);
+        const bool split = n0 + n1 > 32;
+        second = (id & 1) != 0;
+        off = second ? n0 : 0;
+        n = split ? (second ? n1 : n0) : n0 + n1;
+        np = sel4(q, qnp[0], qnp[1], qnp[2], qnp[3]);
+    }
+    const int pa = 2 * hl < n ? L.qpos[q][off + 2 * hl] : -1;
+    const int pb = 2 * hl + 1 < n ? L.qpos[q][off + 2 * hl + 1] : -1;
+    float4 A0 = make_float4(0.f, 0.f, 0.f, 0.f), B0 = make_float4(0.f, 1.f, -1.f, 0.f), C0 = A0;
+    float4 A1 = A0, B1 = B0, C1 = C0;
+    if (pa >= 0) {
+        const SplatRec r = rec[L.sid[pa]];
+        A0 = r.a;
+        B0 = r.b;
+        C0 = r.c;
+    }
+    if (pb >= 0) {
+        const SplatRec r = rec[L.sid[pb]];
+        A1 = r.a;
+        B1 = r.b;
+        C1 = r.c;
+    }
+    int steps = n > 0 ? np + (n + 1) / 2 - 1 : 0;
+    steps = max(steps, __shfl_xor_sync(0xffffffffu, steps, 16));
+    const f32x2 z2 = pk2(0.f, 0.f);
+    SplatAcc2 q0 = {z2, z2, z2, z2, z2, z2, z2, z2, z2, z2}, q1 = q0;
+    const SplatP2 S0 = splat_p2(A0, B0, C0), S1 = splat_p2(A1, B1, C1);
+    const float4* S4 = second ? L.s2 : L.s;
+    const bool clamp = __any_sync(0xffffffffu, (pa >= 0 && B0.y >= amax * 0.999999f) ||
+                                                   (pb >= 0 && B1.y >= amax * 0.999999f));
+    if (clamp)
+        quad_wavefront<DEPTH, true>(steps, np, hl, q * 32, pa, pb, L, S4, S0, S1, amax, q0, q1);
+    else
+        quad_wavefront<DEPTH, false>(steps, np, hl, q * 32, pa, pb, L, S4, S0, S1, amax, q0, q1);
+    // fold into the unit's rows; the two half-warps' chains may share
+    // positions, so they take turns
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if ((int)hi == h) {
+            quad_fold(L, pa, q0);
+            quad_fold(L, pb, q1);
+        }
+        __syncwarp();
+    }
+}
+
+template <bool DEPTH>
+__global__ void __launch_bounds__(32 * kQWarps, 8) backward_quad_kernel(
+    int W, int H, int tiles_x, const uint32_t* __restrict__ tile_start,
+    const uint32_t* __restrict__ ckpt_base, const int32_t* __restrict__ k_eff,
+    const uint32_t* __restrict__ pairs, const SplatRec* __restrict__ rec, float amax,
+    const float* __restrict__ image, const float* __restrict__ grad_image,
+    const float4* __restrict__ pixgrad, const float* __restrict__ depth_img,
+    const float* __restrict__ grad_depth, const int32_t* __restrict__ n_contrib,
+    const float4* __restrict__ ckpt, const float* __restrict__ ckpt_depth,
+    const uint32_t* __restrict__ ckpt_mask, const uint2* __restrict__ work,
+    const int64_t* __restrict__ work_count, int64_t work_cap, uint32_t* work_counter,
+    float* __restrict__ g2d, uint8_t* __restrict__ contributed, int n_tiles) {
+    constexpr int NC = DEPTH ? 10 : 9;
+    __shared__ QuadList<DEPTH> sQ[kQWarps];
+    PDL_WAIT();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    QuadList<DEPTH>& L = sQ[wid];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        L.acc[2 * lane][c] = 0.f;
+        L.acc[2 * lane + 1][c] = 0.f;
+    }
+    if (lane == 0) {  // the inert slot read by lanes off the diagonal
+        L.ga[kQPairs] = make_float4(0.f, 0.f, 0.f, 0.f);
+        L.gb[kQPairs] = make_float4(0.f, 0.f, 0.f, 0.f);
+        L.s[kQPairs] = make_float4(1.f, 1.f, 0.f, 0.f);
+        L.s2[kQPairs] = make_float4(1.f, 1.f, 0.f, 0.f);
+        L.m[kQPairs] = make_uint4(0u, 0u, 0u, 0u);
+        L.px[kQPairs] = 0.f;
+        if (DEPTH) L.gd[kQPairs] = make_float2(0.f, 0.f);
+    }
+    const int64_t count = min(*work_count, work_cap);
+    for (;;) {
+        uint32_t item = 0;
+        if (lane == 0) item = atomicAdd(work_counter, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if ((int64_t)item >= count) break;
+        const uint2 wk = work[item];
+        const int tile = (int)wk.x, u = (int)wk.y;
+        const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
+        const uint32_t start = tile_start[tile];
+        const int ke = k_eff[tile];
+        const int kbase = u * kUnit;
+        const int k0 = kbase + 2 * lane, k1 = k0 + 1;
+        // ---- the unit's splats (the lane's two positions)
+        const uint32_t s0 = k0 < ke ? pairs[start + k0] : 0u;
+        const uint32_t s1 = k1 < ke ? pairs[start + k1] : 0u;
+        L.sid[2 * lane] = s0;
+        L.sid[2 * lane + 1] = s1;
+        // ---- the lane's 8 pixels (rows 2c + (lane >> 4), column lane & 15)
+        const size_t slot0 = (size_t)(ckpt_base[tile] + 2 * u) * kTilePx;
+        uint32_t mk0[kTilePx / 32], mk1[kTilePx / 32];
+        {
+            int nct[kTilePx / 32];
+#pragma unroll
+            for (int c = 0; c < kTilePx / 32; ++c) {
+                const int p = c * 32 + lane;
+                const int ix = x0 + (p & 15), iy = y0 + (p >> 4);
+                nct[c] = (ix < W && iy < H) ? n_contrib[(size_t)iy * W + ix] : 0;
+            }
+#pragma unroll
+            for (int c = 0; c < kTilePx / 32; ++c) {
+                const int p = c * 32 + lane;
+                mk0[c] = nct[c] > kbase ? ckpt_mask[slot0 + p] : 0u;
+                mk1[c] = nct[c] > kbase + kBucket ? ckpt_mask[slot0 + kTilePx + p] : 0u;
+            }
+        }
+        // ---- per quadrant: the positions its pixels blended (both buckets),
+        //      compacted in list order; their union = the splats that
+        //      contributed in this unit
+        int qn0[4], qn1[4];
+        uint32_t u0 = 0u, u1 = 0u;
+        {
+            uint32_t t0 = 0, t1 = 0, b0 = 0, b1 = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                t0 |= mk0[c];
+                t1 |= mk1[c];
+                b0 |= mk0[c + 4];
+                b1 |= mk1[c + 4];
+            }
+            const bool right = (lane & 8) != 0;
+            const unsigned lt = lanemask_lt();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t v0 = q < 2 ? t0 : b0, v1 = q < 2 ? t1 : b1;
+                const bool mine = (q & 1) ? right : !right;
+                const uint32_t m0 = __reduce_or_sync(0xffffffffu, mine ? v0 : 0u);
+                const uint32_t m1 = __reduce_or_sync(0xffffffffu, mine ? v1 : 0u);
+                qn0[q] = __popc(m0);
+                qn1[q] = __popc(m1);
+                if ((m0 >> lane) & 1u) L.qpos[q][__popc(m0 & lt)] = (uint8_t)lane;
+                if ((m1 >> lane) & 1u) L.qpos[q][qn0[q] + __popc(m1 & lt)] = (uint8_t)(32 + lane);
+                u0 |= m0;
+                u1 |= m1;
+            }
+        }
+        // ---- compact each quadrant's active column pairs (rows 2c, 2c + 1)
+        //      into its 32-slot region of the list
+        int qnp[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int c = 0; c < kTilePx / 32; ++c) {
+            const int p = c * 32 + lane;
+            const int ix = x0 + (p & 15), iy = y0 + (p >> 4);
+            const size_t o = (size_t)iy * W + ix;
+            const uint32_t m0 = mk0[c], m1 = mk1[c];
+            const bool act = (m0 | m1) != 0u;
+            const int partner = __shfl_xor_sync(0xffffffffu, (int)act, 16);  // every lane
+            const bool pact = act || partner;
+            const unsigned bal = __ballot_sync(0xffffffffu, pact) & 0xffffu;
+            const int qbase = c < 4 ? 0 : 2;
+            if (pact) {
+                const bool right = (lane & 8) != 0;
+                const int q = qbase + (right ? 1 : 0);
+                const unsigned grp = right ? 0xff00u : 0x00ffu;
+                const int pr = q * 32 + (right ? qnp[qbase + 1] : qnp[qbase]) +
+                               __popc(bal & grp & ((1u << (lane & 15)) - 1u));
+                const int hi = lane >> 4;  // the pair's lane: row 2c (lo) or 2c + 1 (hi)
+                float4 pg = make_float4(0.f, 0.f, 0.f, 0.f);
+                float T0 = 1.f, G0 = 0.f, T1 = 1.f, G1 = 0.f, gd = 0.f;
+                if (act) {
+                    if (pixgrad) {
+                        pg = pixgrad[o];
+                    } else {
+                        pg.x = grad_image[3 * o];
+                        pg.y = grad_image[3 * o + 1];
+                        pg.z = grad_image[3 * o + 2];
+                        pg.w = pg.x * image[3 * o] + pg.y * image[3 * o + 1] +
+                               pg.z * image[3 * o + 2];
+                    }
+                    const float4 ck = ckpt[slot0 + p];
+                    T0 = ck.x;
+                    G0 = pg.x * ck.y + pg.y * ck.z + pg.z * ck.w;
+                    if (DEPTH) {
+                        gd = grad_depth ? grad_depth[o] : 0.f;
+                        if (!pixgrad) pg.w += gd * depth_img[o];
+                        G0 += gd * ckpt_depth[slot0 + p];
+                    }
+                    G0 -= pg.w;
+                    // state at the second bucket's start (used by split chains;
+                    // pixels not blending there get an inert finite state)
+                    if (m1 != 0u) {
+                        const float4 c2 = ckpt[slot0 + kTilePx + p];
+                        T1 = c2.x;
+                        G1 = pg.x * c2.y + pg.y * c2.z + pg.z * c2.w;
+                        if (DEPTH) G1 += gd * ckpt_depth[slot0 + kTilePx + p];
+                        G1 -= pg.w;
+                    }
+                }
+                float* fga = reinterpret_cast<float*>(&L.ga[pr]);
+                float* fgb = reinterpret_cast<float*>(&L.gb[pr]);
+                float* fs = reinterpret_cast<float*>(&L.s[pr]);
+                float* fs2 = reinterpret_cast<float*>(&L.s2[pr]);
+                uint32_t* fm = reinterpret_cast<uint32_t*>(&L.m[pr]);
+                fga[hi] = pg.x;
+                fga[2 + hi] = pg.y;
+                fgb[hi] = pg.z;
+                fgb[2 + hi] = (float)iy;
+                fs[hi] = T0;
+                fs[2 + hi] = G0;
+                fs2[hi] = T1;
+                fs2[2 + hi] = G1;
+                fm[hi] = m0;
+                fm[2 + hi] = m1;
+                if (DEPTH) reinterpret_cast<float*>(&L.gd[pr])[hi] = gd;
+                if (!hi) L.px[pr] = (float)ix;
+            }
+            qnp[qbase] += __popc(bal & 0x00ffu);
+            qnp[qbase + 1] += __popc(bal & 0xff00u);
+        }
+        __syncwarp();
+        // ---- chains sorted by length (steps), longest first, two per round
+        int key[8], cid[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int n0 = qn0[q], n1 = qn1[q];
+            const bool split = n0 + n1 > 32;
+            cid[2 * q] = 2 * q;
+            cid[2 * q + 1] = 2 * q + 1;
+            const int na = split ? n0 : n0 + n1;
+            key[2 * q] = na > 0 ? qnp[q] + (na + 1) / 2 - 1 : -1;
+            key[2 * q + 1] = (split && n1 > 0) ? qnp[q] + (n1 + 1) / 2 - 1 : -1;
+        }
+#define SS_CX(a, b)                         \
+    if (key[a] < key[b]) {                  \
+        const int tk = key[a], tq = cid[a]; \
+        key[a] = key[b];                    \
+        cid[a] = cid[b];                    \
+        key[b] = tk;                        \
+        cid[b] = tq;                        \
+    }
+        // Batcher's odd-even merge sort network for 8 (19 compare-exchanges)
+        SS_CX(0, 1) SS_CX(2, 3) SS_CX(4, 5) SS_CX(6, 7)
+        SS_CX(0, 2) SS_CX(1, 3) SS_CX(4, 6) SS_CX(5, 7)
+        SS_CX(1, 2) SS_CX(5, 6)
+        SS_CX(0, 4) SS_CX(1, 5) SS_CX(2, 6) SS_CX(3, 7)
+        SS_CX(2, 4) SS_CX(3, 5)
+        SS_CX(1, 2) SS_CX(3, 4) SS_CX(5, 6)
+#undef SS_CX
+#pragma unroll 1
+        for (int r = 0; r < 4; ++r) {
+            const int ka = sel4(r, key[0], key[2], key[4], key[6]);
+            const int kb = sel4(r, key[1], key[3], key[5], key[7]);
+            if (ka < 0) break;
+            const int ia = sel4(r, cid[0], cid[2], cid[4], cid[6]);
+            const int ib = kb >= 0 ? sel4(r, cid[1], cid[3], cid[5], cid[7]) : -1;
+            quad_round<DEPTH>(L, rec, lane, ia, ib, qn0, qn1, qnp, amax);
+        }
+        // ---- commit: lane l owns positions 2l, 2l + 1
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int p = 2 * lane + h;
+            if (kbase + p < ke) {
+                const uint32_t sg = h ? s1 : s0;
+                const float4 A = rec[sg].a, B = rec[sg].b;
+                float* r = L.acc[p];
+                const float c1 = 0.5f * A.w;
+                float acc[NC];
+                acc[0] = r[0];
+                acc[1] = r[1];
+                acc[2] = r[2];
+                acc[3] = A.z * r[4] + c1 * r[5];
+                acc[4] = c1 * r[4] + B.x * r[5];
+                acc[5] = -0.5f * r[6];
+                acc[6] = -r[7];
+                acc[7] = -0.5f * r[8];
+                acc[8] = r[3] / B.y;
+                if (DEPTH) acc[NC - 1] = r[9];
+                float* row = g2d + (size_t)sg * NC;
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    if (acc[c] != 0.f) atomicAdd(row + c, acc[c]);
+                const uint32_t um = p < 32 ? u0 : u1;
+                if (contributed && ((um >> (p & 31)) & 1u)) contributed[sg] = 1;
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c) L.acc[p][c] = 0.f;
         }
         __syncwarp();
     }
@@ -796,6 +1259,10 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
         const char* e = getenv("SS_BWD_SPARSE");  // 1: the sparse two-phase kernel
         return !(e && e[0] == '1');
     }();
+    static const bool unit_chains = [] {
+        const char* e = getenv("SS_BWD_UNIT");  // 1: one chain per bucket over the whole tile
+        return e && e[0] == '1';
+    }();
     if (!wavefront) {
         const size_t sm_bytes = sizeof(SpShared);
         auto go = [&](auto kern) -> cudaError_t {
@@ -829,7 +1296,22 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
             contributed, tx * ty);
         return cudaGetLastError();
     };
-    return depthf ? go(backward_splat_kernel<true>) : go(backward_splat_kernel<false>);
+    if (unit_chains)
+        return depthf ? go(backward_splat_kernel<true>) : go(backward_splat_kernel<false>);
+    const int qthreads = 32 * kQWarps;
+    auto goq = [&](auto kern) -> cudaError_t {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, qthreads, 0);
+        if (per_sm < 1) per_sm = 1;
+        launch_pdl(kern, dim3(sms * per_sm), dim3(qthreads), 0, s,
+            cam->width, cam->height, tx, bins->d_tile_start, bins->d_ckpt_base, k_eff,
+            bins->d_pair_splat, reinterpret_cast<const SplatRec*>(sp->d_rec), o->alpha_max, image,
+            grad_image, pixgrad, depth, grad_depth, n_contrib,
+            reinterpret_cast<const float4*>(ckpt), ckpt_depth, ckpt_mask,
+            reinterpret_cast<const uint2*>(work), &st->bucket_count, work_cap, counter, g2d,
+            contributed, tx * ty);
+        return cudaGetLastError();
+    };
+    return depthf ? goq(backward_quad_kernel<true>) : goq(backward_quad_kernel<false>);
 }
 
 }  // namespace ss

@@ -49,6 +49,10 @@ units = []
 useful = executed = steps_total = ramp_total = 0
 pairs_hist = []
 band_pos, band_pairs = [], []
+quad_steps = 0  # per-quadrant chains (see below)
+seg_steps = 0
+GROUPS = [(8, 8), (16, 4), (8, 4), (4, 8), (4, 4), (16, 2), (8, 2)]
+grp_stats = {}
 for t in range(tx * ty):
     nu = (ke[t] + 63) // 64
     for u in range(nu):
@@ -69,6 +73,81 @@ for t in range(tx * ty):
             npos = bin(int(o0)).count("1") + bin(int(o1)).count("1")
             band_pos.append(npos)
             band_pairs.append((int(act[64 * b:64 * (b + 1)].sum()) + 1) // 2)
+        # quadrant chains: per 8x8 quadrant the positions blended by any of its
+        # pixels (both buckets) and its active column pairs; a chain of n <= 32
+        # positions runs np + ceil(n/2) - 1 steps in a half-warp, n > 32 splits
+        # at the bucket boundary; jobs sorted by length, paired per round
+        jobs = []  # (active pairs, positions) per chain
+        a2 = act.reshape(8, 2, 16)  # (c, row parity, col)
+        for q in range(4):
+            rows = slice(0, 8) if q < 2 else slice(8, 16)
+            cols = slice(0, 8) if q % 2 == 0 else slice(8, 16)
+            mq0 = m0.reshape(16, 16)[rows, cols].astype(np.uint64)
+            mq1 = m1.reshape(16, 16)[rows, cols].astype(np.uint64)
+            o0 = int(np.bitwise_or.reduce(mq0.ravel()))
+            o1 = int(np.bitwise_or.reduce(mq1.ravel()))
+            n0, n1 = bin(o0).count("1"), bin(o1).count("1")
+            cq = slice(0, 4) if q < 2 else slice(4, 8)
+            npq = int((a2[cq, 0, cols] | a2[cq, 1, cols]).sum())
+            if n0 + n1 == 0:
+                continue
+            if n0 + n1 <= 32:
+                jobs.append((npq, n0 + n1))
+            else:
+                jobs.append((npq, n0))
+                if n1:
+                    jobs.append((npq, n1))
+        stp = sorted((p + (n + 1) // 2 - 1 for p, n in jobs), reverse=True)
+        quad_steps += sum(stp[0::2])
+        # segments: chains (2 positions per lane) packed first-fit-decreasing
+        # into rounds of 32 lanes; a round runs max(np + L - 1) steps
+        rounds = []
+        for p, n in sorted(jobs, key=lambda j: -(j[0] + (j[1] + 1) // 2)):
+            L = (n + 1) // 2
+            for r in rounds:
+                if r[0] + L <= 32:
+                    r[0] += L
+                    r[1] = max(r[1], p + L - 1)
+                    break
+            else:
+                rounds.append([L, p + L - 1])
+        seg_steps += sum(r[1] for r in rounds)
+        # the same packing for other pixel-group shapes (gw columns x gh rows)
+        M0 = m0.reshape(16, 16).astype(np.uint64)
+        M1 = m1.reshape(16, 16).astype(np.uint64)
+        A = act.reshape(16, 16)
+        for (gw, gh) in GROUPS:
+            chains = []
+            for gy in range(0, 16, gh):
+                for gx in range(0, 16, gw):
+                    o0 = int(np.bitwise_or.reduce(M0[gy:gy + gh, gx:gx + gw].ravel()))
+                    o1 = int(np.bitwise_or.reduce(M1[gy:gy + gh, gx:gx + gw].ravel()))
+                    n0, n1 = bin(o0).count("1"), bin(o1).count("1")
+                    if n0 + n1 == 0:
+                        continue
+                    aa = A[gy:gy + gh, gx:gx + gw].reshape(gh // 2, 2, gw)
+                    npg = int((aa[:, 0] | aa[:, 1]).sum())
+                    if n0 + n1 <= 32:
+                        chains.append((npg, n0 + n1))
+                    else:
+                        chains.append((npg, n0))
+                        if n1:
+                            chains.append((npg, n1))
+            rr = []
+            for pp, nn in sorted(chains, key=lambda j: -(j[0] + (j[1] + 1) // 2)):
+                L = (nn + 1) // 2
+                for r in rr:
+                    if r[0] + L <= 32:
+                        r[0] += L
+                        r[1] = max(r[1], pp + L - 1)
+                        break
+                else:
+                    rr.append([L, pp + L - 1])
+            g = grp_stats.setdefault((gw, gh), [0, 0, 0, 0])
+            g[0] += sum(r[1] for r in rr)
+            g[1] += len(rr)
+            g[2] += len(chains)
+            g[3] += sum(nn for _, nn in chains)
         st = npair + 15
         useful += int(p0.sum() + p1.sum())
         executed += st * 32 * 2 * 2
@@ -88,4 +167,11 @@ print(json.dumps({
     "band_positions_hist_le16_le32_le48_le64": [float(np.mean(np.array(band_pos) <= v))
                                                 for v in (16, 32, 48, 64)],
     "band_pairs_mean": float(np.mean(band_pairs)),
+    "quadrant_chain_steps": quad_steps, "quadrant_vs_wavefront": quad_steps / steps_total,
+    "segment_rounds_steps": seg_steps, "segments_vs_wavefront": seg_steps / steps_total,
+    "groups": {"%dx%d" % k: {"vs_wavefront": round(v[0] / steps_total, 4),
+                             "rounds_per_unit": round(v[1] / len(ph), 2),
+                             "chains_per_unit": round(v[2] / len(ph), 2),
+                             "positions_per_chain": round(v[3] / max(v[2], 1), 1)}
+               for k, v in grp_stats.items()},
 }))
