@@ -156,6 +156,13 @@ __device__ __forceinline__ void bwd_commit(const SplatAcc2& q, const float4& A, 
         if (acc[c] != 0.f) atomicAdd(row + c, acc[c]);
 }
 
+// shfl.up by one lane across the warp (chains as lane segments)
+__device__ __forceinline__ f32x2 shfl_up2w(f32x2 v) {
+    float lo, hi;
+    upk2(v, lo, hi);
+    return pk2(__shfl_up_sync(0xffffffffu, lo, 1), __shfl_up_sync(0xffffffffu, hi, 1));
+}
+
 // shfl.up by one lane inside each half-warp (the two buckets' chains)
 __device__ __forceinline__ f32x2 shfl_up2(f32x2 v) {
     float lo, hi;
@@ -443,6 +450,8 @@ struct QuadList {
     float acc[kUnit][NC];          // raw per-splat sums of the unit, over its chains
     uint32_t sid[kUnit];           // the unit's splats (records are re-read through L1/L2)
     uint8_t qpos[4][kUnit];        // per quadrant: its positions, compacted in list order
+    uint8_t lanejob[8][32];        // per round and lane: chain id << 5 | lane in its segment, 255 idle
+    int32_t rsteps[8];             // per round: the longest chain's step count
 };
 
 template <typename T>
@@ -515,8 +524,8 @@ __device__ __forceinline__ void quad_wavefront(int steps, int np, int hl, int lb
     const uint32_t bitB = pb >= 0 ? 1u << (pb & 31) : 0u;
 #pragma unroll 1
     for (int st = 0; st < steps; ++st) {
-        T = shfl_up2(T);
-        G = shfl_up2(G);
+        T = shfl_up2w(T);
+        G = shfl_up2w(G);
         const int j = st - hl;
         const bool inr = (unsigned)j < (unsigned)np;
         const int jj = inr ? lb + j : kQPairs;
@@ -546,30 +555,28 @@ template <bool DEPTH>
 __device__ __forceinline__ void quad_fold(QuadList<DEPTH>& L, int p, const SplatAcc2& q) {
     if (p < 0) return;
     float* row = L.acc[p];
-    row[0] += hsum(q.r0);
-    row[1] += hsum(q.r1);
-    row[2] += hsum(q.r2);
-    row[3] += hsum(q.s_da);
-    row[4] += hsum(q.s_dx);
-    row[5] += hsum(q.s_dy);
-    row[6] += hsum(q.s_xx);
-    row[7] += hsum(q.s_xy);
-    row[8] += hsum(q.s_yy);
-    if (DEPTH) row[9] += hsum(q.rz);
+    atomicAdd(row + 0, hsum(q.r0));
+    atomicAdd(row + 1, hsum(q.r1));
+    atomicAdd(row + 2, hsum(q.r2));
+    atomicAdd(row + 3, hsum(q.s_da));
+    atomicAdd(row + 4, hsum(q.s_dx));
+    atomicAdd(row + 5, hsum(q.s_dy));
+    atomicAdd(row + 6, hsum(q.s_xx));
+    atomicAdd(row + 7, hsum(q.s_xy));
+    atomicAdd(row + 8, hsum(q.s_yy));
+    if (DEPTH) atomicAdd(row + 9, hsum(q.rz));
 }
 
-// One round: lanes 0-15 run chain ida, lanes 16-31 chain idb (-1: idle).
-// Chain id = 2 q + part: a quadrant with <= 32 positions is one chain
-// (part 0: both buckets from the unit start), one with more is split at the
-// bucket boundary (part 0: bucket 0; part 1: bucket 1 from its checkpoint).
+// One round: the lane runs chain `id` (-1: idle) as lane hl of its segment;
+// `steps` = the longest chain of the round.  Chain id = 2 q + part: a
+// quadrant with <= 32 positions is one chain (part 0: both buckets from the
+// unit start), one with more is split at the bucket boundary (part 0:
+// bucket 0; part 1: bucket 1 from its checkpoint).
 template <bool DEPTH>
 __device__ __forceinline__ void quad_round(QuadList<DEPTH>& L, const SplatRec* __restrict__ rec,
-                                           int lane, int ida, int idb, const int (&qn0)[4],
+                                           int id, int hl, int steps, const int (&qn0)[4],
                                            const int (&qn1)[4], const int (&qnp)[4],
                                            float amax) {
-    const bool hi = lane >= 16;
-    const int hl = lane & 15;
-    const int id = hi ? idb : ida;
     int np = 0, off = 0, n = 0, q = 0;
     bool second = false;
     if (id >= 0) {
@@ -598,8 +605,6 @@ __device__ __forceinline__ void quad_round(QuadList<DEPTH>& L, const SplatRec* _
         B1 = r.b;
         C1 = r.c;
     }
-    int steps = n > 0 ? np + (n + 1) / 2 - 1 : 0;
-    steps = max(steps, __shfl_xor_sync(0xffffffffu, steps, 16));
     const f32x2 z2 = pk2(0.f, 0.f);
     SplatAcc2 q0 = {z2, z2, z2, z2, z2, z2, z2, z2, z2, z2}, q1 = q0;
     const SplatP2 S0 = splat_p2(A0, B0, C0), S1 = splat_p2(A1, B1, C1);
@@ -610,16 +615,10 @@ __device__ __forceinline__ void quad_round(QuadList<DEPTH>& L, const SplatRec* _
         quad_wavefront<DEPTH, true>(steps, np, hl, q * 32, pa, pb, L, S4, S0, S1, amax, q0, q1);
     else
         quad_wavefront<DEPTH, false>(steps, np, hl, q * 32, pa, pb, L, S4, S0, S1, amax, q0, q1);
-    // fold into the unit's rows; the two half-warps' chains may share
-    // positions, so they take turns
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        if ((int)hi == h) {
-            quad_fold(L, pa, q0);
-            quad_fold(L, pb, q1);
-        }
-        __syncwarp();
-    }
+    // fold into the unit's rows (chains of different quadrants may share
+    // positions: shared-memory atomics)
+    quad_fold(L, pa, q0);
+    quad_fold(L, pb, q1);
 }
 
 template <bool DEPTH>
@@ -821,15 +820,51 @@ __global__ void __launch_bounds__(32 * kQWarps, 8) backward_quad_kernel(
         SS_CX(2, 4) SS_CX(3, 5)
         SS_CX(1, 2) SS_CX(3, 4) SS_CX(5, 6)
 #undef SS_CX
-#pragma unroll 1
-        for (int r = 0; r < 4; ++r) {
-            const int ka = sel4(r, key[0], key[2], key[4], key[6]);
-            const int kb = sel4(r, key[1], key[3], key[5], key[7]);
-            if (ka < 0) break;
-            const int ia = sel4(r, cid[0], cid[2], cid[4], cid[6]);
-            const int ib = kb >= 0 ? sel4(r, cid[1], cid[3], cid[5], cid[7]) : -1;
-            quad_round<DEPTH>(L, rec, lane, ia, ib, qn0, qn1, qnp, amax);
+        // first-fit decreasing: chain i (2 positions per lane, L_i lanes)
+        // goes to the first round with L_i free lanes; each lane records its
+        // (chain, segment lane) per round in shared memory
+        int nr = 0;
+        {
+            int used[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                used[r] = 0;
+                L.lanejob[r][lane] = 255;
+            }
+            if (lane < 8) L.rsteps[lane] = 0;
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (key[i] >= 0) {
+                    const int q = cid[i] >> 1;
+                    const int n0 = sel4(q, qn0[0], qn0[1], qn0[2], qn0[3]);
+                    const int n1 = sel4(q, qn1[0], qn1[1], qn1[2], qn1[3]);
+                    const int n = n0 + n1 > 32 ? ((cid[i] & 1) ? n1 : n0) : n0 + n1;
+                    const int Lc = (n + 1) >> 1;
+                    int rs = -1, o = 0;
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+                        if (rs < 0 && r <= nr && used[r] + Lc <= 32) {
+                            rs = r;
+                            o = used[r];
+                        }
+#pragma unroll
+                    for (int r = 0; r < 8; ++r)
+                        if (r == rs) used[r] += Lc;
+                    nr = max(nr, rs + 1);
+                    if (lane >= o && lane < o + Lc) L.lanejob[rs][lane] = (uint8_t)(cid[i] << 5 | (lane - o));
+                    if (lane == 0) L.rsteps[rs] = max(L.rsteps[rs], key[i]);
+                }
+            }
+            __syncwarp();
         }
+#pragma unroll 1
+        for (int r = 0; r < nr; ++r) {
+            const int code = L.lanejob[r][lane];
+            quad_round<DEPTH>(L, rec, code != 255 ? code >> 5 : -1, code & 31,
+                              L.rsteps[r], qn0, qn1, qnp, amax);
+        }
+        __syncwarp();
         // ---- commit: lane l owns positions 2l, 2l + 1
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
