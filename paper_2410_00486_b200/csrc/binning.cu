@@ -775,7 +775,6 @@ __device__ __forceinline__ void fe_walk(const uint4* __restrict__ drec,
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) endw = max(endw, __shfl_xor_sync(0xffffffffu, endw, d));
         const uint32_t a1 = min(rlo + endw, q1);
-        const uint32_t pw = wx | (wy << 16);
 #pragma unroll 2
         for (uint32_t e0 = q - rlo; e0 < a1 - rlo; e0 += 32) {
             const uint32_t e = e0 + l;
@@ -807,27 +806,19 @@ __device__ __forceinline__ void fe_walk(const uint4* __restrict__ drec,
                 if (in) atomicAdd(word, 1u << sh);
             } else {
                 const uint32_t gid = __shfl_sync(0xffffffffu, cur.y, o);
-                // earlier lanes of the step with the same tile
+                // rank = the tile's counter before this pair.  The step's
+                // pairs take their counters splat by splat (one predicated
+                // atomic per splat of the step, in depth order); a splat's
+                // tiles are distinct, so within one atomic every lane owns
+                // its own 16-bit half and the returned half is exact
                 const int o_first = __shfl_sync(0xffffffffu, o, 0);
-                const int o_last = __shfl_sync(0xffffffffu, in ? o : 0, 31 - __clz(__ballot_sync(0xffffffffu, in)));
-                uint32_t inrank = 0;
+                const int o_last =
+                    __shfl_sync(0xffffffffu, in ? o : 0, 31 - __clz(__ballot_sync(0xffffffffu, in)));
+                uint32_t old = 0;
 #pragma unroll 1
-                for (int o2 = o_first; o2 < o_last; ++o2) {
-                    const uint32_t r2 = __shfl_sync(0xffffffffu, rel, o2);
-                    const uint32_t xy2 = __shfl_sync(0xffffffffu, cur.z, o2);
-                    const uint32_t p2 = __shfl_sync(0xffffffffu, pw, o2);
-                    const uint32_t dx = tx - (xy2 & 0xffffu), dy = ty - (xy2 >> 16);
-                    const uint32_t w2 = p2 & 0xffffu;
-                    if (in && o2 < o && dx < w2 && dy < (p2 >> 16) && r2 + dy * w2 + dx >= e0)
-                        ++inrank;
-                }
-                uint32_t before = 0;
-                if (in) before = (*word >> sh) & 0xffffu;
-                __syncwarp();
-                if (in) {
-                    atomicAdd(word, 1u << sh);
-                    fn(tile, before + inrank, gid);
-                }
+                for (int k = o_first; k <= o_last; ++k)
+                    if (in && o == k) old = atomicAdd(word, 1u << sh);
+                if (in) fn(tile, (old >> sh) & 0xffffu, gid);
             }
             __syncwarp();
         }
@@ -854,12 +845,21 @@ __device__ void fe_direct(const FeArgs& a, cooperative_groups::grid_group& grid,
 
     // ---- this CTA's depth-sort chunk: pair counts, chunk total
     uint32_t sid[ITEMS], cnt[ITEMS], off[ITEMS];
+    uint2 rct[ITEMS];
     uint32_t wtot = 0;
 #pragma unroll
     for (int r = 0; r < ITEMS; ++r) {
         const uint32_t j = base + wbase + r * 32 + l;
         sid[r] = j < a.n ? order[j] : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+        const uint32_t j = base + wbase + r * 32 + l;
         cnt[r] = j < a.n ? a.tiles[sid[r]] : 0u;
+        rct[r] = j < a.n ? a.rect[sid[r]] : make_uint2(0u, 0u);  // loaded with the count
+    }
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
         uint32_t x = cnt[r];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -880,7 +880,7 @@ __device__ void fe_direct(const FeArgs& a, cooperative_groups::grid_group& grid,
         if (j < a.n) {
             uint4 d = make_uint4(wpre + off[r], sid[r], 0u, 0u);
             if (cnt[r]) {
-                const uint2 rc = a.rect[sid[r]];
+                const uint2 rc = rct[r];
                 d.z = rc.x;
                 d.w = ((rc.y & 0xffffu) - (rc.x & 0xffffu) + 1) |
                       (((rc.y >> 16) - (rc.x >> 16) + 1) << 16);
@@ -951,15 +951,26 @@ __device__ void fe_direct(const FeArgs& a, cooperative_groups::grid_group& grid,
     };
     // placer-warp counters -> exclusive prefix over the warps (per tile);
     // returns nothing, totals land in tot (may alias nothing)
+    // (two tiles per 32-bit word: the 16-bit halves never carry, a tile's
+    // count in one piece is < 2^16; the G words of a column are loaded
+    // before the running sum walks them)
     auto prefix_warps = [&](uint32_t* tot) {
-        for (uint32_t q = t; q < NT; q += kFeThreads) {
+        const uint32_t NW = NT2 / 2;
+        for (uint32_t k = t; k < NW; k += kFeThreads) {
+            uint32_t v[32];
+#pragma unroll
+            for (int g = 0; g < 32; ++g) v[g] = g < (int)G ? sm[(size_t)g * NW + k] : 0u;
             uint32_t run = 0;
-            for (uint32_t g = 0; g < G; ++g) {
-                const uint32_t c = s_c16[(size_t)g * NT2 + q];
-                s_c16[(size_t)g * NT2 + q] = (uint16_t)run;
-                run += c;
+#pragma unroll
+            for (int g = 0; g < 32; ++g)
+                if (g < (int)G) {
+                    sm[(size_t)g * NW + k] = run;
+                    run += v[g];
+                }
+            if (tot) {
+                if (2 * k < NT) tot[2 * k] = run & 0xffffu;
+                if (2 * k + 1 < NT) tot[2 * k + 1] = run >> 16;
             }
-            if (tot) tot[q] = run;
         }
     };
     auto zero_c16 = [&]() {
@@ -969,7 +980,9 @@ __device__ void fe_direct(const FeArgs& a, cooperative_groups::grid_group& grid,
     if (npieces <= 1) {
         count_piece(p0, p1);
         __syncthreads();
+        FE_STAMP(12);
         prefix_warps(s_base);
+        FE_STAMP(13);
     } else {
         for (uint32_t q0 = p0 + w * 32 * 64; q0 < p1; q0 += kFeWarps * 32 * 64)
             fe_walk<2>(a.drec, s_cb, cshift, a.n, q0, min(p1, q0 + 32 * 64), a.tiles_x, s_base,
@@ -1177,6 +1190,7 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
         }
         FE_STAMP(1 + 2 * p);
         grid.sync();
+        FE_STAMP(20 + p);
         if (p == 0 && a.direct) {
             if (w == 0) {
                 uint32_t kand = 0xffffffffu, kor = 0u;
@@ -1229,6 +1243,7 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
             }
         }
         __syncthreads();
+        if (p == 1) FE_STAMP(7);
         const uint32_t col = t < 256 ? s_part[0][t] : 0u;
         const uint32_t tot = t < 256 ? s_part[0][256 + t] : 0u;
         const uint32_t excl = block_excl_scan<kFeThreads>(t < 256 ? tot : 0u, s_warp);
@@ -1244,6 +1259,7 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
             }
         }
         __syncthreads();
+        if (p == 1) FE_STAMP(8);
         for (uint32_t i = t; i < nloc; i += kFeThreads) {
             const uint32_t k = s_keys[i];
             const uint32_t d = (k >> shift) & 255u;
@@ -1251,6 +1267,7 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
             vout[gp] = s_vals[i];
             if (p < lastp) kout[gp] = k;
         }
+        if (p == 1) FE_STAMP(9);
         grid.sync();
         FE_STAMP(2 + 2 * p);
         ksrc = kout;

@@ -2,13 +2,13 @@
 
 Needs the library built with -DSS_FE_TRACE, e.g. on the GPU box:
     make -C paper_2410_00486_b200/csrc clean
-    make -C paper_2410_00486_b200/csrc FLAGS+=-DSS_FE_TRACE
+    make -C paper_2410_00486_b200/csrc EXTRA=-DSS_FE_TRACE
     python tools/trace_front.py
 Stamps (globaltimer, per CTA): 0 start, 1+2p / 2+2p depth pass p before /
 after its second grid barrier; direct emission: 10/11 around the chunk-sum
-barrier, 12/13 around the records barrier, 14/15 around the count barrier
-(pass 1 before 14), 16/17 around the column-prefix barrier, 18 tile starts
-done, 19 pass 2 done."""
+barrier, 12 count walk done, 13 warp prefix done, 14/15 around the count
+barrier, 16/17 around the column-prefix barrier, 18 tile starts done, 19
+rank walk done; 20+p after depth pass p's first barrier."""
 import ctypes
 import os
 import sys
