@@ -13,7 +13,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
     > gpurun_out/ncu_launches.log 2>&1
 timeout 300 python tools/profile_step.py > gpurun_out/plain2.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
-    -k regex:"backward_splat|blend_forward|bin_front|ssim_bwd|ssim_fwd|chain_adam|preprocess" -c 7 \
+    -k regex:"backward_quad|blend_forward|bin_front|ssim_bwd|ssim_fwd|chain_adam|preprocess" -c 7 \
     -o gpurun_out/full python tools/profile_step.py > gpurun_out/ncu_full.log 2>&1
 tail -2 gpurun_out/bench_default.log | cut -c1-300; tail -2 gpurun_out/bench_reference.log | cut -c1-300
 tail -2 gpurun_out/smoke.log; tail -2 gpurun_out/ncu_full.log

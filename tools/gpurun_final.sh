@@ -18,15 +18,16 @@ PROF_ITERS=6 timeout 300 python tools/bwd_stats.py > $O/bwd_stats.jsonl 2>&1
 PROF_ITERS=250 timeout 300 python tools/bwd_stats.py >> $O/bwd_stats.jsonl 2>&1
 timeout 300 python tools/api_timing.py > $O/api_timing.txt 2>&1
 SS_BWD_SPARSE=1 timeout 600 python bench.py --no-cpu-baseline --no-config4 > $O/bench_sparse.log 2>&1
+SS_BWD_UNIT=1 timeout 600 python bench.py --no-cpu-baseline --no-config4 > $O/bench_unit_chains.log 2>&1
 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-converged --no-config4 --no-e2e > $O/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
     --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-converged --no-config4 --no-e2e \
     > $O/ncu_launches.log 2>&1
 timeout 300 python tools/profile_step.py > $O/plain2.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
-    -k regex:"backward_splat|blend_forward|bin_front|ssim_bwd|ssim_fwd|chain_adam|preprocess" -c 7 \
+    -k regex:"backward_quad|blend_forward|bin_front|ssim_bwd|ssim_fwd|chain_adam|preprocess" -c 7 \
     -o $O/full python tools/profile_step.py > $O/ncu_full.log 2>&1
 PROF_WARM=250 PROF_STEPS=1 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
-    -k regex:"backward_splat|blend_forward|bin_front|ssim_bwd|ssim_fwd|chain_adam|preprocess" -c 7 \
+    -k regex:"backward_quad|blend_forward|bin_front|ssim_bwd|ssim_fwd|chain_adam|preprocess" -c 7 \
     -o $O/conv_full python tools/profile_step.py > $O/ncu_conv.log 2>&1
 tail -3 $O/pytest_gpu.log; tail -2 $O/bench_default.log | cut -c1-300; tail -2 $O/bench_reference.log | cut -c1-300; tail -2 $O/smoke.log

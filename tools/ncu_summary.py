@@ -11,7 +11,7 @@ import json
 import sys
 
 KEYS = {"bin_front": "bin_front_kernel", "blend_forward": "blend_forward_kernel",
-        "ssim_bwd": "ssim_bwd_kernel", "backward": "backward_splat_kernel",
+        "ssim_bwd": "ssim_bwd_kernel", "backward": "backward_quad_kernel",
         "chain_adam": "chain_adam_kernel", "ssim_fwd": "ssim_fwd_kernel",
         "preprocess": "preprocess_kernel"}
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3,
