@@ -60,6 +60,10 @@ struct GaussGrad {
     float n2d;
 };
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ float rsqrt_approx(float x) {
     float y;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -477,23 +481,46 @@ __global__ void __launch_bounds__(256, REST ? 2 : 4) chain_adam_kernel(
     int32_t* __restrict__ obs_count, ss_status* st) {
     PDL_WAIT();
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n || st->pair_overflow) return;
+    if (i >= n) return;
+    // every independent load first (the parameters are needed by Adam
+    // whether or not the Gaussian is visible; a culled Gaussian's g2d row is
+    // zero), then the overflow word and the flag test
+    const uint8_t fl = flags[i];
+    const float opi = opl[i];
+    float p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+    const float4 q4 = rot[i];
+    float l[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
+    float dc[3] = {shdc[3 * i], shdc[3 * i + 1], shdc[3 * i + 2]};
+    float g[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) g[k] = g2d[NC * i + k];
+    // the Adam moments this thread updates after the chain: their lines are
+    // requested now (no registers held), so those loads hit L1
+    prefetch_l1(M.d_position + 3 * i);
+    prefetch_l1(V.d_position + 3 * i);
+    prefetch_l1(M.d_log_scale + 3 * i);
+    prefetch_l1(V.d_log_scale + 3 * i);
+    prefetch_l1(M.d_sh_dc + 3 * i);
+    prefetch_l1(V.d_sh_dc + 3 * i);
+    prefetch_l1(M.d_rotation + 4 * i);
+    prefetch_l1(V.d_rotation + 4 * i);
+    prefetch_l1(M.d_opacity + i);
+    prefetch_l1(V.d_opacity + i);
+    if (contributed) {
+        prefetch_l1(contributed + i);
+        prefetch_l1(grad2d_accum + i);
+        prefetch_l1(grad3d_accum + 3 * i);
+        prefetch_l1(obs_count + i);
+    }
     CamC cam = cam_v;
     AdamHP hp = hp_v;
     if (d_cam) load_camc(d_cam, cam);  // graph replay: per-step values from device memory
     if (d_hp) load_hp(d_hp, hp);
+    if (st->pair_overflow) return;
     GaussGrad o = {};
-    const uint8_t fl = flags[i];
-    const float opi = opl[i];
     float rest_g[REST ? 45 : 1];
     if (fl & 1) {
-        float p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
-        float l[3] = {ls[3 * i], ls[3 * i + 1], ls[3 * i + 2]};
-        float dc[3] = {shdc[3 * i], shdc[3 * i + 1], shdc[3 * i + 2]};
-        float g[NC];
-#pragma unroll
-        for (int k = 0; k < NC; ++k) g[k] = g2d[NC * i + k];
-        chain_one<NC>(p, rot[i], l, opi, dc, shrest + 45 * i, cam, deg, dilation, g, fl, o,
+        chain_one<NC>(p, q4, l, opi, dc, shrest + 45 * i, cam, deg, dilation, g, fl, o,
                       REST ? rest_g : nullptr);
     } else if (REST) {
 #pragma unroll
