@@ -155,10 +155,11 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
                   (my - rad <= (float)(cam.H - 1)) && (qn2 != 0.0f);
             if (vis) {
                 // tiles.py:42-47: inclusive rect, float32 arithmetic as numpy
-                float fx0 = floorf(__fdiv_rn(__fsub_rn(mx, rad), (float)kTile));
-                float fx1 = floorf(__fdiv_rn(__fadd_rn(mx, rad), (float)kTile));
-                float fy0 = floorf(__fdiv_rn(__fsub_rn(my, rad), (float)kTile));
-                float fy1 = floorf(__fdiv_rn(__fadd_rn(my, rad), (float)kTile));
+                // (x / 16 and x * (1/16) round identically: a power of two)
+                float fx0 = floorf(__fmul_rn(__fsub_rn(mx, rad), 1.0f / kTile));
+                float fx1 = floorf(__fmul_rn(__fadd_rn(mx, rad), 1.0f / kTile));
+                float fy0 = floorf(__fmul_rn(__fsub_rn(my, rad), 1.0f / kTile));
+                float fy1 = floorf(__fmul_rn(__fadd_rn(my, rad), 1.0f / kTile));
                 int x0 = (int)fminf(fmaxf(fx0, 0.f), (float)(tiles_x - 1));
                 int x1 = (int)fminf(fmaxf(fx1, 0.f), (float)(tiles_x - 1));
                 int y0 = (int)fminf(fmaxf(fy0, 0.f), (float)(tiles_y - 1));
@@ -167,12 +168,21 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
                 rc = make_uint2((uint32_t)x0 | ((uint32_t)y0 << 16),
                                 (uint32_t)x1 | ((uint32_t)y1 << 16));
                 // colour (projection.py:147-155)
-                float u[3] = {p[0] - cam.c[0], p[1] - cam.c[1], p[2] - cam.c[2]};
-                float vl = fmaxf(sqrtf(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]), 1e-12f);
-                float d[3] = {u[0] / vl, u[1] / vl, u[2] / vl};
                 float rgb[3];
                 bool act[3];
-                sh_color(d, sh_degree, dc, sh_rest + 45 * i, rgb, act);
+                if (sh_degree == 0) {  // view-independent: no direction needed
+#pragma unroll
+                    for (int ch = 0; ch < 3; ++ch) {
+                        const float raw = kSH_C0 * dc[ch] + 0.5f;
+                        act[ch] = raw > 0.f;
+                        rgb[ch] = fmaxf(raw, 0.f);
+                    }
+                } else {
+                    float u[3] = {p[0] - cam.c[0], p[1] - cam.c[1], p[2] - cam.c[2]};
+                    float vl = fmaxf(sqrtf(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]), 1e-12f);
+                    float d[3] = {u[0] / vl, u[1] / vl, u[2] / vl};
+                    sh_color(d, sh_degree, dc, sh_rest + 45 * i, rgb, act);
+                }
                 fl = 1u | (act[0] ? 2u : 0u) | (act[1] ? 4u : 0u) | (act[2] ? 8u : 0u);
                 r.a = make_float4(mx, my, P.c / det, 2.0f * (-P.b / det));
                 r.b = make_float4(P.a / det, sg, mcut, P.t[2]);
@@ -236,10 +246,10 @@ __global__ void splats_from_projection_kernel(int64_t m, const float* __restrict
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= m) return;
     const float mx = mean2d[2 * i], my = mean2d[2 * i + 1], rad = radius[i], z = depth[i];
-    const float fx0 = floorf(__fdiv_rn(__fsub_rn(mx, rad), (float)kTile));
-    const float fx1 = floorf(__fdiv_rn(__fadd_rn(mx, rad), (float)kTile));
-    const float fy0 = floorf(__fdiv_rn(__fsub_rn(my, rad), (float)kTile));
-    const float fy1 = floorf(__fdiv_rn(__fadd_rn(my, rad), (float)kTile));
+    const float fx0 = floorf(__fmul_rn(__fsub_rn(mx, rad), 1.0f / kTile));
+    const float fx1 = floorf(__fmul_rn(__fadd_rn(mx, rad), 1.0f / kTile));
+    const float fy0 = floorf(__fmul_rn(__fsub_rn(my, rad), 1.0f / kTile));
+    const float fy1 = floorf(__fmul_rn(__fadd_rn(my, rad), 1.0f / kTile));
     const int x0 = (int)fminf(fmaxf(fx0, 0.f), (float)(tiles_x - 1));
     const int x1 = (int)fminf(fmaxf(fx1, 0.f), (float)(tiles_x - 1));
     const int y0 = (int)fminf(fmaxf(fy0, 0.f), (float)(tiles_y - 1));
