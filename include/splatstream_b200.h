@@ -180,6 +180,19 @@ int ss_blend_forward(const ss_camera *cam, const ss_raster_opts *opts, const ss_
                      float *d_ckpt_depth, uint32_t *d_ckpt_mask, uint32_t *d_work,
                      int64_t work_capacity, ss_status *d_status, void *stream);
 
+/* RenderOutput.contributed (api.py:82-105; set in forward_tile,
+ * kernels.py:94-95) from the forward's blend masks: d_contributed[i] = 1
+ * for every Gaussian that was blended into at least one pixel, else 0
+ * (n entries).  d_work / work_capacity / d_status are the work list and
+ * status ss_blend_forward filled.  ss_blend_forward with d_contributed ==
+ * NULL skips the per-pair flag in its blend loop; this entry derives the
+ * same set afterwards. */
+int ss_contributed_from_masks(const ss_camera *cam, const ss_bins *bins,
+                              const int32_t *d_n_contrib, const int32_t *d_k_eff,
+                              const uint32_t *d_ckpt_mask, const uint32_t *d_work,
+                              int64_t work_capacity, const ss_status *d_status, int64_t n,
+                              uint8_t *d_contributed, void *stream);
+
 /* Replaces replay_pixel_states (api.py:340-368; replay_tile
  * kernels.py:155-178): advance tile `tile`'s archived (T, r, g, b) from
  * checkpoint bucket from_bucket to list position pos_to with the forward's

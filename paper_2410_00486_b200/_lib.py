@@ -96,6 +96,8 @@ _SIGS = {
     "ss_resize_moments": (I32, [I64, VP, I64, I32, VP, VP, VP, VP]),
     "ss_check_finite": (I32, [I32, VP, VP, VP, VP]),
     "ss_splats_from_projection": (I32, [I64, VP, VP, VP, P(SSCamera), P(SSSplats), VP]),
+    "ss_contributed_from_masks": (I32, [P(SSCamera), P(SSBins), VP, VP, VP, VP, I64, VP, I64, VP,
+                                        VP]),
     "ss_replay_pixel_states": (I32, [P(SSCamera), P(SSRasterOpts), P(SSSplats), P(SSBins), VP,
                                      VP, VP, VP, I32, I32, I32, VP, VP]),
     "ss_step_snapshot": (I32, [VP, VP, VP, VP]),

@@ -31,6 +31,10 @@ cudaError_t launch_splats_from_projection(int64_t, const float*, const float*, c
 cudaError_t launch_replay(const ss_camera*, const ss_raster_opts*, const ss_splats*,
                           const ss_bins*, const float*, const float*, const int32_t*, const void*,
                           int, int, int, float*, cudaStream_t);
+cudaError_t launch_contributed(const ss_camera* cam, const ss_bins* bins, const int32_t* n_contrib,
+                               const int32_t* k_eff, const uint32_t* ckpt_mask,
+                               const uint32_t* work, int64_t work_cap, const ss_status* st,
+                               uint8_t* contributed, int64_t n, cudaStream_t s);
 size_t seed_workspace_bytes(int64_t);
 cudaError_t launch_seed(int64_t, const float*, const float*, float, float*, float*, float*,
                         float*, float*, int32_t*, void*, size_t, cudaStream_t);
@@ -218,6 +222,19 @@ int ss_replay_pixel_states(const ss_camera* cam, const ss_raster_opts* opts,
     if (tile >= div_up(cam->width, kTile) * div_up(cam->height, kTile)) return SS_EINVAL;
     return rc(launch_replay(cam, opts, splats, bins, d_image, d_final_t, d_n_contrib, d_ckpt, tile,
                             from_bucket, pos_to, d_out, S(stream)));
+}
+
+int ss_contributed_from_masks(const ss_camera* cam, const ss_bins* bins,
+                              const int32_t* d_n_contrib, const int32_t* d_k_eff,
+                              const uint32_t* d_ckpt_mask, const uint32_t* d_work,
+                              int64_t work_capacity, const ss_status* d_status, int64_t n,
+                              uint8_t* d_contributed, void* stream) {
+    if (!cam || !bins || !d_n_contrib || !d_k_eff || !d_ckpt_mask || !d_work || !d_status ||
+        !d_contributed || n < 0 || work_capacity < 0)
+        return SS_EINVAL;
+    if (n == 0) return SS_OK;
+    return rc(launch_contributed(cam, bins, d_n_contrib, d_k_eff, d_ckpt_mask, d_work,
+                                 work_capacity, d_status, d_contributed, n, S(stream)));
 }
 
 size_t ss_loss_workspace_bytes(int32_t height, int32_t width) {

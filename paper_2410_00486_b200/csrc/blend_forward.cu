@@ -374,6 +374,71 @@ cudaError_t launch_blend_forward(const ss_camera* cam, const ss_raster_opts* o,
     return cudaGetLastError();
 }
 
+// The splats that blended at least one pixel (kernels.py:94-95), from the
+// forward's per-(pixel, bucket) blend masks instead of a per-pair flag in
+// the blend loop: a warp per backward work unit (tile, two buckets) of the
+// forward's list; the OR of the masks of the pixels still blending at a
+// bucket's start names its contributing list positions.  (The engine never
+// needs this: the backward derives the same set.)
+__global__ void __launch_bounds__(256) contributed_kernel(
+    int W, int H, int tiles_x, const uint32_t* __restrict__ tile_start,
+    const uint32_t* __restrict__ ckpt_base, const uint32_t* __restrict__ pairs,
+    const int32_t* __restrict__ n_contrib, const int32_t* __restrict__ k_eff,
+    const uint32_t* __restrict__ ckpt_mask, const uint2* __restrict__ work,
+    const int64_t* __restrict__ work_count, int64_t work_cap, uint8_t* __restrict__ contributed) {
+    const int lane = threadIdx.x & 31;
+    const int64_t count = min(*work_count, work_cap);
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t it = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); it < count;
+         it += nw) {
+        const uint2 wk = work[it];
+        const int tile = (int)wk.x, u = (int)wk.y;
+        const int x0 = (tile % tiles_x) * kTile, y0 = (tile / tiles_x) * kTile;
+        const int ke = k_eff[tile];
+        const int kbase = u * kUnit;
+        const bool two = kbase + kBucket < ke;
+        const size_t slot0 = (size_t)(ckpt_base[tile] + 2 * u) * kTilePx;
+        uint32_t o0 = 0u, o1 = 0u;
+        int nct[kTilePx / 32];
+        uint32_t m0[kTilePx / 32], m1[kTilePx / 32];
+#pragma unroll
+        for (int c = 0; c < kTilePx / 32; ++c) {  // every load of the unit in flight
+            const int p = c * 32 + lane;
+            const int ix = x0 + (p & 15), iy = y0 + (p >> 4);
+            nct[c] = (ix < W && iy < H) ? n_contrib[(size_t)iy * W + ix] : 0;
+            m0[c] = ckpt_mask[slot0 + p];
+            m1[c] = two ? ckpt_mask[slot0 + kTilePx + p] : 0u;
+        }
+#pragma unroll
+        for (int c = 0; c < kTilePx / 32; ++c) {
+            o0 |= nct[c] > kbase ? m0[c] : 0u;
+            o1 |= nct[c] > kbase + kBucket ? m1[c] : 0u;
+        }
+        o0 = __reduce_or_sync(0xffffffffu, o0);
+        o1 = __reduce_or_sync(0xffffffffu, o1);
+        const uint32_t start = tile_start[tile] + kbase;
+        if ((o0 >> lane) & 1u) contributed[pairs[start + lane]] = 1;
+        if ((o1 >> lane) & 1u) contributed[pairs[start + kBucket + lane]] = 1;
+    }
+}
+
+cudaError_t launch_contributed(const ss_camera* cam, const ss_bins* bins, const int32_t* n_contrib,
+                               const int32_t* k_eff, const uint32_t* ckpt_mask,
+                               const uint32_t* work, int64_t work_cap, const ss_status* st,
+                               uint8_t* contributed, int64_t n, cudaStream_t s) {
+    const int tx = div_up(cam->width, kTile);
+    cudaError_t e = cudaMemsetAsync(contributed, 0, (size_t)n, s);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    contributed_kernel<<<sms * 8, 256, 0, s>>>(cam->width, cam->height, tx, bins->d_tile_start,
+                                                bins->d_ckpt_base, bins->d_pair_splat, n_contrib,
+                                                k_eff, ckpt_mask,
+                                                reinterpret_cast<const uint2*>(work),
+                                                &st->bucket_count, work_cap, contributed);
+    return cudaGetLastError();
+}
 }  // namespace ss
 
 #ifdef SS_FWD_TRACE

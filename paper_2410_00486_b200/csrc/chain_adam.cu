@@ -813,19 +813,42 @@ struct FiniteSet {
     int64_t n[8];
 };
 
-__global__ void check_finite_kernel(int nt, FiniteSet S, int32_t* __restrict__ flags) {
+// validate_finite (api.py:74-79) and the non-zero tests over up to 8
+// tensors in one launch: 16-byte loads where the tensor is aligned, four in
+// flight per thread, and one flag update per CTA and tensor (block OR), so
+// the flag words see ~a thousand atomics instead of one per warp.
+__global__ void __launch_bounds__(256) check_finite_kernel(int nt, FiniteSet S,
+                                                           int32_t* __restrict__ flags) {
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int t = 0; t < nt; ++t) {
+        const float* p = S.p[t];
+        const int64_t n = S.n[t];
         bool bad = false, nz = false;
-        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < S.n[t];
-             e += (int64_t)gridDim.x * blockDim.x) {
-            const float v = S.p[t][e];
+        auto test = [&](float v) {
             bad |= !isfinite(v);
             nz |= v != 0.f;
+        };
+        const int64_t n4 = (reinterpret_cast<uintptr_t>(p) & 15) ? 0 : n / 4;
+        const float4* p4 = reinterpret_cast<const float4*>(p);
+        int64_t e = tid;
+        for (; e + 3 * stride < n4; e += 4 * stride) {
+            const float4 a = p4[e], b = p4[e + stride], c = p4[e + 2 * stride],
+                         d = p4[e + 3 * stride];
+            test(a.x), test(a.y), test(a.z), test(a.w), test(b.x), test(b.y), test(b.z), test(b.w);
+            test(c.x), test(c.y), test(c.z), test(c.w), test(d.x), test(d.y), test(d.z), test(d.w);
         }
-        const unsigned bb = __ballot_sync(0xffffffffu, bad), bn = __ballot_sync(0xffffffffu, nz);
-        if ((threadIdx.x & 31) == 0) {
+        for (; e < n4; e += stride) {
+            const float4 a = p4[e];
+            test(a.x), test(a.y), test(a.z), test(a.w);
+        }
+        for (int64_t k = 4 * n4 + tid; k < n; k += stride) test(p[k]);
+        const bool bb = __syncthreads_or(bad), bn = __syncthreads_or(nz);
+        if (threadIdx.x == 0) {
             if (bb) atomicOr(flags + t, 1);
-            if (bn) atomicOr(flags + nt + t, 1);
+            // the non-zero word is usually set by the first CTAs: skip the atomic then
+            if (bn && *reinterpret_cast<volatile int32_t*>(flags + nt + t) == 0)
+                atomicOr(flags + nt + t, 1);
         }
     }
 }
@@ -841,7 +864,9 @@ cudaError_t launch_check_finite(int nt, const float* const* ptrs, const int64_t*
     }
     cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int32_t) * 2 * nt, s);
     if (e != cudaSuccess) return e;
-    const int blocks = (int)((mx + 255) / 256 < 1184 ? (mx + 255) / 256 : 1184);
+    // enough CTAs for every SM (about 16 floats per thread and round)
+    const int64_t want = (mx / 16 + 255) / 256;
+    const int blocks = (int)(want < 1 ? 1 : (want < 1184 ? want : 1184));
     check_finite_kernel<<<blocks, 256, 0, s>>>(nt, S, flags);
     return cudaGetLastError();
 }

@@ -243,7 +243,7 @@ class RenderOutput:
     final_t: torch.Tensor    # (H, W)
     n_contrib: torch.Tensor  # (H, W) int32
     k_eff_tiles: torch.Tensor  # (T,) int32, per tile (all tiles)
-    contributed: torch.Tensor  # (N,) bool
+    contributed_buf: torch.Tensor | None  # (N,) bool once derived (see `contributed`)
     opts: RasterOpts
     camera: Camera
     n_primitives: int
@@ -259,6 +259,22 @@ class RenderOutput:
     status: torch.Tensor
     depth: torch.Tensor | None = None
     _cache: dict = field(default_factory=dict)
+
+    @property
+    def contributed(self) -> torch.Tensor:
+        """(N,) bool: Gaussians blended into at least one pixel (kernels.py:94-95),
+        derived from the forward's blend masks on first use (one kernel)."""
+        if self.contributed_buf is None:
+            n = self.n_primitives
+            dev = self.image.device
+            buf = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+            check(lib().ss_contributed_from_masks(
+                ctypes.byref(self.camera.to_ss()), ctypes.byref(self.bins.ss()),
+                P(self.n_contrib), P(self.k_eff_tiles), P(self.ckpt_mask), P(self.work),
+                self.work_capacity, P(self.status), n, P(buf), stream_handle()),
+                "ss_contributed_from_masks")
+            self.contributed_buf = buf[:n].view(torch.bool)
+        return self.contributed_buf
 
     @property
     def acc_rgb(self) -> torch.Tensor:
@@ -510,15 +526,14 @@ def rasterize_forward(gmap: GaussianMap, camera, opts: RasterOpts | None = None)
     n_contrib = torch.empty((H, W), dtype=torch.int32, device=dev)
     depth = torch.empty((H, W), **f32) if opts.with_depth else None
     k_eff = torch.empty(n_tiles, dtype=torch.int32, device=dev)
-    contributed = torch.zeros(n, dtype=torch.uint8, device=dev)
     work_cap = max(n_slots, 1)
     work = torch.empty((work_cap, 2), dtype=torch.int32, device=dev)
     check(L.ss_blend_forward(ctypes.byref(cm), ctypes.byref(op), ctypes.byref(sp.ss()),
                              ctypes.byref(bins.ss()), P(image), P(final_t), P(n_contrib), P(depth),
-                             P(k_eff), P(contributed), P(ckpt), P(ckpt_depth), P(ckpt_mask),
+                             P(k_eff), None, P(ckpt), P(ckpt_depth), P(ckpt_mask),
                              P(work), work_cap, P(st), s), "ss_blend_forward")
     return RenderOutput(image=image, final_t=final_t, n_contrib=n_contrib, k_eff_tiles=k_eff,
-                        contributed=contributed.bool(), opts=opts, camera=cam, n_primitives=n,
+                        contributed_buf=None, opts=opts, camera=cam, n_primitives=n,
                         gmap=gmap, splats=sp, bins=bins, pair_count=pcount,
                         ckpt=ckpt if opts.with_checkpoints else None, ckpt_depth=ckpt_depth,
                         ckpt_mask=ckpt_mask, work=work, work_capacity=work_cap, status=st, depth=depth)
