@@ -130,10 +130,21 @@ def adam_step(gmap: GaussianMap, grads: ParamGrads, state: AdamState, sh_degree:
         errors.defer(finite_flags_device([t for _, t in named])[:len(named)], raise_nonfinite)
         upd_rest = state.sh_rest_active or grads.sh_degree is None or grads.sh_degree > 0
     else:
-        # the finite checks and the "sh_rest in use" test: one kernel, one host read
-        host = finite_flags([t for _, t in named], extra_nonzero=True)
-        raise_nonfinite([0 if good else 1 for good in host[:len(named)]])
-        upd_rest = state.sh_rest_active or bool(host[2 * len(named) - 1])
+        # the finite checks and the "sh_rest in use" test: one kernel, one host
+        # read -- for the tensors backward_splatwise's eager check has not
+        # already passed unmodified (ParamGrads.known_finite)
+        known = [grads.known_finite(k, t) if hasattr(grads, "known_finite") else (False, None)
+                 for k, t in named]
+        todo = [i for i, (ok, _) in enumerate(known) if not ok]
+        bad = [0] * len(named)
+        nonzero = [nz for _, nz in known]
+        if todo:
+            host = finite_flags([named[i][1] for i in todo], extra_nonzero=True)
+            for j, i in enumerate(todo):
+                bad[i] = 0 if host[j] else 1
+                nonzero[i] = host[len(todo) + j]
+        raise_nonfinite(bad)
+        upd_rest = state.sh_rest_active or bool(nonzero[len(named) - 1])
     state.sh_rest_active = upd_rest
     state.step_count += 1
     st = torch.empty(_lib.STATUS_WORDS, dtype=torch.int64, device=gmap.device)

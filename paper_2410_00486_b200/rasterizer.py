@@ -126,6 +126,10 @@ class BinBuffers:
 
 
 _CAP_HINT: dict = {}
+# per (device, tile grid): the last forward's per-tile blend cost, which the
+# next call's binning turns into the costliest-first CTA order (the forward's
+# results do not depend on it; only its tail does)
+_COST_HINT: dict = {}
 
 
 def new_status(dev):
@@ -341,6 +345,10 @@ def _bin(sp: SplatBuffers, n: int, cam: Camera, dev, st):
     cap = max(_CAP_HINT.get(key, 0), 4 * n, 1024)
     while True:
         bins = BinBuffers.alloc(cap, n_tiles, dev)
+        cost = _COST_HINT.get(key)
+        if cost is None:
+            cost = _COST_HINT[key] = bins.tile_cost
+        bins.tile_cost = cost
         ws = bin_workspace(n, cap, n_tiles, dev)
         check(L.ss_bin_sort(n, ctypes.byref(sp.ss()), ctypes.byref(cm), ctypes.byref(bins.ss()),
                             P(ws), ws.numel(), P(st), s), "ss_bin_sort")
@@ -552,6 +560,9 @@ class ParamGrads:
     pos2d_grad_norm: torch.Tensor
     contributed: torch.Tensor
     sh_degree: int | None = None  # of the render they came from (None: unknown)
+    # tensors an eager check found finite: name -> (id, torch version, any
+    # non-zero); adam_step re-checks only tensors replaced or modified since
+    _finite_ok: dict = field(default_factory=dict, repr=False, compare=False)
 
     def __len__(self):
         return int(self.position.shape[0])
@@ -591,8 +602,23 @@ class ParamGrads:
         if errors.deferred():
             errors.defer(finite_flags_device(tensors)[:len(names)], raiser)
         else:
-            raiser([0 if good else 1 for good in finite_flags(tensors)])
+            host = finite_flags(tensors, extra_nonzero=True)
+            raiser([0 if good else 1 for good in host[:len(names)]])
+            self.note_finite(names, tensors, host[len(names):])
         return self
+
+    def note_finite(self, names, tensors, nonzero):
+        for k, t, nz in zip(names, tensors, nonzero):
+            self._finite_ok[k] = (id(t), t._version, bool(nz))
+
+    def known_finite(self, name, t):
+        """(known finite, any non-zero) for tensor `t` held as `name`: a
+        tensor an eager check passed and nothing has modified in place since
+        (torch version counter) needs no second reduction."""
+        rec = self._finite_ok.get(name)
+        if rec is not None and rec[0] == id(t) and rec[1] == t._version:
+            return True, rec[2]
+        return False, None
 
 
 def render_trajectory(gmap: GaussianMap, cameras, opts: RasterOpts | None = None):
