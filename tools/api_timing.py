@@ -38,3 +38,22 @@ timed("deferred")
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU, torch.profiler.ProfilerActivity.CUDA]) as p:
     it(); torch.cuda.synchronize()
 print(p.key_averages().table(sort_by="self_cpu_time_total", row_limit=12))
+# device kernels of one iteration, by time
+evs = [e for e in p.events() if e.device_type.name == "CUDA"]
+evs.sort(key=lambda e: e.time_range.start)
+span = evs[-1].time_range.end - evs[0].time_range.start
+busy = {}
+for e in evs:
+    busy.setdefault(e.name[:70], []).append(e.time_range.end - e.time_range.start)
+print(f"one iteration: device span {span:.1f} us, {len(evs)} device ops")
+for k, v in sorted(busy.items(), key=lambda kv: -sum(kv[1]))[:30]:
+    print(f"  {sum(v):8.1f} us  x{len(v):2d}  {k}")
+gaps = []
+for a, b in zip(evs[:-1], evs[1:]):
+    g = b.time_range.start - a.time_range.end
+    if g > 5:
+        gaps.append((g, a.name[:40], b.name[:40]))
+gaps.sort(reverse=True)
+print("largest gaps:")
+for g in gaps[:10]:
+    print(f"  {g[0]:8.1f} us  {g[1]} -> {g[2]}")
