@@ -1243,7 +1243,6 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
             }
         }
         __syncthreads();
-        if (p == 1) FE_STAMP(7);
         const uint32_t col = t < 256 ? s_part[0][t] : 0u;
         const uint32_t tot = t < 256 ? s_part[0][256 + t] : 0u;
         const uint32_t excl = block_excl_scan<kFeThreads>(t < 256 ? tot : 0u, s_warp);
@@ -1259,7 +1258,6 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
             }
         }
         __syncthreads();
-        if (p == 1) FE_STAMP(8);
         for (uint32_t i = t; i < nloc; i += kFeThreads) {
             const uint32_t k = s_keys[i];
             const uint32_t d = (k >> shift) & 255u;
@@ -1267,7 +1265,6 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
             vout[gp] = s_vals[i];
             if (p < lastp) kout[gp] = k;
         }
-        if (p == 1) FE_STAMP(9);
         grid.sync();
         FE_STAMP(2 + 2 * p);
         ksrc = kout;
