@@ -104,6 +104,30 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     CamF cam = cam_v;
     if (d_cam) load_camf(d_cam, cam);  // graph replay: camera from device memory
+    // SH bands 1-3 (sh_degree > 0): a thread's 45-float row is strided 180 B
+    // from its neighbour's, so the CTA's 256 rows (one contiguous span) are
+    // staged through shared memory with coalesced loads first
+    extern __shared__ __align__(16) float s_rest[];
+    const float* my_rest = sh_rest + 45 * i;
+    if (sh_degree > 0) {
+        const int64_t r0 = blockIdx.x * (int64_t)blockDim.x;
+        const int64_t nr = min((int64_t)blockDim.x, n - r0);
+        const float* src = sh_rest + 45 * r0;
+        if (nr == blockDim.x && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+            // every 16-byte piece of the span in flight at once (cp.async, no registers)
+            const int n4 = 45 * (int)nr / 4;
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_rest);
+            for (int k = threadIdx.x; k < n4; k += blockDim.x)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * k),
+                             "l"(src + 4 * k)
+                             : "memory");
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        } else {
+            for (int k = threadIdx.x; k < 45 * nr; k += blockDim.x) s_rest[k] = src[k];
+        }
+        __syncthreads();
+        my_rest = s_rest + 45 * threadIdx.x;
+    }
     bool vis = false;
     if (i < n) {
         float p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
@@ -121,7 +145,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
             // non-short-circuit: all 45 loads in flight (a && chain waits on each)
             bool rf = true;
 #pragma unroll 15
-            for (int k = 0; k < 45; ++k) rf &= finitef(sh_rest[45 * i + k]);
+            for (int k = 0; k < 45; ++k) rf &= finitef(my_rest[k]);
             fin = fin && rf;
         }
         if (!fin) report_first(&status->first_nonfinite_param, i);
@@ -181,7 +205,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
                     float u[3] = {p[0] - cam.c[0], p[1] - cam.c[1], p[2] - cam.c[2]};
                     float vl = fmaxf(sqrtf(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]), 1e-12f);
                     float d[3] = {u[0] / vl, u[1] / vl, u[2] / vl};
-                    sh_color(d, sh_degree, dc, sh_rest + 45 * i, rgb, act);
+                    sh_color(d, sh_degree, dc, my_rest, rgb, act);
                 }
                 fl = 1u | (act[0] ? 2u : 0u) | (act[1] ? 4u : 0u) | (act[2] ? 8u : 0u);
                 r.a = make_float4(mx, my, P.c / det, 2.0f * (-P.b / det));
@@ -299,7 +323,13 @@ cudaError_t launch_preprocess(const ss_map* map, const ss_camera* cam, const ss_
     int tx = div_up(cam->width, kTile), ty = div_up(cam->height, kTile);
     int threads = 256;
     int blocks = div_up(map->n, threads);
-    launch_pdl(preprocess_kernel, dim3(blocks), dim3(threads), 0, s,
+    const size_t smem = o->sh_degree > 0 ? sizeof(float) * 45 * threads : 0;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(preprocess_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    launch_pdl(preprocess_kernel, dim3(blocks), dim3(threads), smem, s,
         map->n, map->d_positions, reinterpret_cast<const float4*>(map->d_rotations),
         map->d_log_scales, map->d_opacity_logits, map->d_sh_dc, map->d_sh_rest, cf, d_cam,
         o->sh_degree, o->near_plane, o->dilation, logf(o->alpha_min), tx, ty,
