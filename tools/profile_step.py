@@ -15,7 +15,7 @@ H = int(os.environ.get("PROF_H", 680))
 steps = int(os.environ.get("PROF_STEPS", 2))
 g = ss.GaussianMap.from_scene(survey_scene(n, 0))
 cam = survey_camera(W, H)
-opts = ss.RasterOpts(sh_degree=0)
+opts = ss.RasterOpts(sh_degree=int(os.environ.get("PROF_DEG", 0)))
 tgt = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(n, 100)), cam, opts).image
 eng = ss.MappingEngine(g, W, H, opts)
 eng.fit_capacity(cam)
