@@ -168,10 +168,14 @@ class MappingEngine:
         self._graphs.clear()
         n = len(self.gmap)
         dev = self.dev
+        self.splats = self.g2d = self.contributed = None  # blocks reusable below
         self.splats = SplatBuffers.alloc(n, dev, aux=False)
         ncol = 10 if self.opts.with_depth else 9
         self.g2d = torch.empty((max(n, 1), ncol), dtype=torch.float32, device=dev)
         self.contributed = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)
+        self._flat = None
+        if getattr(self, "image", None) is not None:
+            return  # the image-sized buffers do not depend on the map size
         f32 = dict(dtype=torch.float32, device=dev)
         self.image = torch.empty((self.H, self.W, 3), **f32)
         self.final_t = torch.empty((self.H, self.W), **f32)
@@ -194,6 +198,10 @@ class MappingEngine:
         self._graphs.clear()
         n = len(self.gmap)
         self._cap = int(cap)
+        # drop the old buffers first so the caching allocator can hand their
+        # blocks to the new ones
+        self.bins = self.bin_ws = self.ckpt = self.ckpt_depth = self.ckpt_mask = None
+        self.work = None
         self.bins = BinBuffers.alloc(self._cap, self.n_tiles, self.dev)
         self.bin_ws = bin_workspace(n, self._cap, self.n_tiles, self.dev)
         slots = self._cap // 32 + self.n_tiles + 1
@@ -357,16 +365,34 @@ class MappingEngine:
             key = tdep is not None
             g = self._graphs.get(key)
             if g is None:
-                torch.cuda.synchronize()
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    self._body(rec.camera, tgt, tdep)
+                g = self._capture(lambda: self._body(rec.camera, tgt, tdep))
                 self._graphs[key] = g
             g.replay()
         else:
             self._body(rec.camera, rec.target, rec.target_depth)
         self.launches += self._launches_per_step()
         self._snapshot(rec)
+
+    def _capture(self, body):
+        """Capture body() into a CUDA graph on a side stream.  Not through
+        torch.cuda.graph(): its entry empties the device and pinned-host
+        allocator caches (and may run gc), so the next allocations go back to
+        cudaMalloc / cudaHostAlloc -- tens to hundreds of ms, at every
+        re-capture after a densify."""
+        torch.cuda.synchronize()
+        if getattr(self, "_cap_stream", None) is None or self._cap_stream.device != self.dev:
+            self._cap_stream = torch.cuda.Stream(device=self.dev)
+        g = torch.cuda.CUDAGraph()
+        cs = self._cap_stream
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            g.capture_begin()
+            try:
+                body()
+            finally:
+                g.capture_end()
+        torch.cuda.current_stream().wait_stream(cs)
+        return g
 
     def _launches_fb(self, depth_loss: bool):
         """Library kernels one _forward_backward enqueues (K1-K7 of a view)."""
@@ -508,7 +534,16 @@ class MappingEngine:
         self._graphs.clear()
         if len(self.gmap) != n:
             self._alloc_map_buffers()
-            self._alloc_pair_buffers(max(self._cap * len(self.gmap) // max(n, 1), 4096))
+            # pair buffers only grow: a shrunken map keeps them (no cudaMalloc of
+            # hundreds of MB at a prune); the binning workspace is re-sized only
+            # if the new map needs more
+            need = max(self._cap * len(self.gmap) // max(n, 1), 4096)
+            ws = int(lib().ss_bin_workspace_bytes(len(self.gmap), self._cap, self.n_tiles))
+            if need > self._cap:
+                self._alloc_pair_buffers(need)
+            elif ws > self.bin_ws.numel():
+                self.bin_ws = None
+                self.bin_ws = bin_workspace(len(self.gmap), self._cap, self.n_tiles, self.dev)
         return res
 
     def add_points(self, points, colors):
