@@ -349,13 +349,14 @@ def restore_state(eng, snap):
     eng.iteration = snap[4]
 
 
-def e2e_single(torch, eng, cam, tgt, steps):
+def e2e_single(torch, eng, cam, tgt, steps, restore=None):
     """The public API call a user makes per keyframe iteration, with host
-    buffers: the target uploaded from pinned host memory each step (copy
-    stream, double-buffered so the upload of step k+1 overlaps step k) and
-    the step's loss/status snapshot read back (wall clock)."""
+    buffers: the target uploaded from pinned host memory each step straight
+    into one of the engine's two target slots (copy stream, so the upload of
+    step k+1 overlaps step k), and the step's loss/status snapshot read back
+    (wall clock)."""
     host_tgt = tgt.cpu().pin_memory()
-    bufs = [torch.empty_like(tgt), torch.empty_like(tgt)]
+    bufs = [eng.target_buffer(slot=0), eng.target_buffer(slot=1)]
     copy_stream = torch.cuda.Stream()
     uploaded = [torch.cuda.Event(), torch.cuda.Event()]
     consumed = [torch.cuda.Event(), torch.cuda.Event()]
@@ -381,8 +382,18 @@ def e2e_single(torch, eng, cam, tgt, steps):
     upload(1)
     eng.synchronize()
     torch.cuda.synchronize()
+    # both slot graphs captured outside the timed loop (as the bench's own slot is)
+    for k in range(2):
+        main.wait_event(uploaded[k])
+        eng.step(cam, bufs[k])
+        consumed[k].record(main)
+        upload(k + 2)
+    eng.synchronize()
+    if restore is not None:  # time the same iterations as the device-timed value
+        restore()
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for k in range(steps):
+    for k in range(2, steps + 2):
         step(k)
     eng.synchronize()  # every step's loss is on the host
     wall = time.perf_counter() - t0
@@ -391,8 +402,9 @@ def e2e_single(torch, eng, cam, tgt, steps):
             "h2d_bytes_per_step": int(host_tgt.numel() * 4),
             "d2h_bytes_per_step": int(eng._host.shape[1] * 8),
             "timing": "wall clock over the same iterations as the device-timed value (state "
-                      "restored), pinned host target upload per step (copy stream, "
-                      "double-buffered) + per-step loss/status read back"}
+                      "restored), pinned host target upload per step into the engine's other "
+                      "target slot (copy stream, double-buffered) + per-step loss/status read "
+                      "back"}
 
 
 def stage_times(torch, eng, step, k=5):
@@ -605,7 +617,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         restore_state(eng, snap)
-        e2e = e2e_single(torch, eng, cam, tgt, args.steps)
+        e2e = e2e_single(torch, eng, cam, tgt, args.steps, restore=lambda: restore_state(eng, snap))
 
     # ---- converged regime: iterations 251-270 of the same training run
     converged = None
@@ -628,7 +640,8 @@ def main():
                      "roofline": c_rf["roof"]}
         if not args.no_e2e:
             restore_state(eng, csnap)
-            converged["e2e"] = e2e_single(torch, eng, cam, tgt, args.steps)
+            converged["e2e"] = e2e_single(torch, eng, cam, tgt, args.steps,
+                                          restore=lambda: restore_state(eng, csnap))
     del eng
     torch.cuda.empty_cache()
 

@@ -191,6 +191,7 @@ class MappingEngine:
                                    dtype=torch.uint8, device=dev)
         if getattr(self, "_tgt_buf", None) is None:
             self._tgt_buf = torch.zeros((self.H, self.W, 3), **f32)
+            self._tgt_buf1 = None
             self._tdep_buf = None
         self._flat = None
 
@@ -335,20 +336,32 @@ class MappingEngine:
                               P(self.status), stream_handle()), "ss_chain_adam")
         self._mark("chain_adam")
 
-    def target_buffer(self, depth: bool = False) -> torch.Tensor:
-        """The engine's fixed keyframe-target buffer ((H, W, 3), or (H, W)
-        for the depth target) that the captured graph reads.  step() copies
-        its target here (stream-ordered, device to device) unless the caller
-        passes this buffer itself, so every keyframe shares ONE graph."""
+    def target_buffer(self, depth: bool = False, slot: int = 0) -> torch.Tensor:
+        """The engine's keyframe-target staging buffers ((H, W, 3), or (H, W)
+        for the depth target) that the captured graphs read.  step() copies
+        its target into slot 0 (stream-ordered, device to device) unless the
+        caller passes one of these buffers itself.  There are two RGB slots,
+        each with its own graph, so a caller can upload keyframe k + 1 into
+        one slot (e.g. from pinned host memory on a copy stream) while step
+        k still reads the other: no device-to-device copy per step."""
         if depth:
             if self._tdep_buf is None:
                 self._tdep_buf = torch.zeros((self.H, self.W), dtype=torch.float32,
                                              device=self.dev)
             return self._tdep_buf
-        return self._tgt_buf
+        if slot not in (0, 1):
+            raise ValueError("target slot must be 0 or 1")
+        if slot == 1 and self._tgt_buf1 is None:
+            self._tgt_buf1 = torch.zeros((self.H, self.W, 3), dtype=torch.float32,
+                                         device=self.dev)
+        return self._tgt_buf if slot == 0 else self._tgt_buf1
 
     def _stage_target(self, rec: StepRecord):
-        tgt = self.target_buffer()
+        """(target buffer, depth buffer, slot) the graph of this step reads."""
+        slot = 0
+        if self._tgt_buf1 is not None and rec.target.data_ptr() == self._tgt_buf1.data_ptr():
+            slot = 1
+        tgt = self.target_buffer(slot=slot)
         if rec.target.data_ptr() != tgt.data_ptr():
             tgt.copy_(rec.target.reshape(tgt.shape), non_blocking=True)
         tdep = None
@@ -356,13 +369,13 @@ class MappingEngine:
             tdep = self.target_buffer(depth=True)
             if rec.target_depth.data_ptr() != tdep.data_ptr():
                 tdep.copy_(rec.target_depth.reshape(tdep.shape), non_blocking=True)
-        return tgt, tdep
+        return tgt, tdep, slot
 
     def _run(self, rec: StepRecord):
         self._stage_params(rec)
         if self.use_graph and self.profile is None:
-            tgt, tdep = self._stage_target(rec)
-            key = tdep is not None
+            tgt, tdep, slot = self._stage_target(rec)
+            key = (tdep is not None, slot)
             g = self._graphs.get(key)
             if g is None:
                 g = self._capture(lambda: self._body(rec.camera, tgt, tdep))
