@@ -718,6 +718,21 @@ __global__ void __launch_bounds__(32 * kQWarps, 8) backward_quad_kernel(
                 u1 |= m1;
             }
         }
+        // ---- the compaction's per-pixel rows (gradient, both checkpoints) are
+        //      requested into L1 now, so its eight column-pair rounds do not each
+        //      wait a DRAM round trip
+#pragma unroll
+        for (int c = 0; c < kTilePx / 32; ++c) {
+            const int p = c * 32 + lane;
+            const int ix = x0 + (p & 15), iy = y0 + (p >> 4);
+            if ((mk0[c] | mk1[c]) != 0u) {
+                const size_t o = (size_t)iy * W + ix;
+                if (pixgrad) asm volatile("prefetch.global.L1 [%0];" ::"l"(pixgrad + o));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(ckpt + slot0 + p));
+                if (mk1[c] != 0u)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(ckpt + slot0 + kTilePx + p));
+            }
+        }
         // ---- compact each quadrant's active column pairs (rows 2c, 2c + 1)
         //      into its 32-slot region of the list
         int qnp[4] = {0, 0, 0, 0};
