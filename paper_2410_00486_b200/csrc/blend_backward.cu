@@ -555,16 +555,16 @@ template <bool DEPTH>
 __device__ __forceinline__ void quad_fold(QuadList<DEPTH>& L, int p, const SplatAcc2& q) {
     if (p < 0) return;
     float* row = L.acc[p];
-    atomicAdd(row + 0, hsum(q.r0));
-    atomicAdd(row + 1, hsum(q.r1));
-    atomicAdd(row + 2, hsum(q.r2));
-    atomicAdd(row + 3, hsum(q.s_da));
-    atomicAdd(row + 4, hsum(q.s_dx));
-    atomicAdd(row + 5, hsum(q.s_dy));
-    atomicAdd(row + 6, hsum(q.s_xx));
-    atomicAdd(row + 7, hsum(q.s_xy));
-    atomicAdd(row + 8, hsum(q.s_yy));
-    if (DEPTH) atomicAdd(row + 9, hsum(q.rz));
+    row[0] += hsum(q.r0);
+    row[1] += hsum(q.r1);
+    row[2] += hsum(q.r2);
+    row[3] += hsum(q.s_da);
+    row[4] += hsum(q.s_dx);
+    row[5] += hsum(q.s_dy);
+    row[6] += hsum(q.s_xx);
+    row[7] += hsum(q.s_xy);
+    row[8] += hsum(q.s_yy);
+    if (DEPTH) row[9] += hsum(q.rz);
 }
 
 // One round: the lane runs chain `id` (-1: idle) as lane hl of its segment;
@@ -574,7 +574,8 @@ __device__ __forceinline__ void quad_fold(QuadList<DEPTH>& L, int p, const Splat
 // bucket 0; part 1: bucket 1 from its checkpoint).
 template <bool DEPTH>
 __device__ __forceinline__ void quad_round(QuadList<DEPTH>& L, const SplatRec* __restrict__ rec,
-                                           int id, int hl, int steps, const int (&qn0)[4],
+                                           int id, int hl, int steps, uint32_t chains,
+                                           const int (&qn0)[4],
                                            const int (&qn1)[4], const int (&qnp)[4],
                                            float amax) {
     int np = 0, off = 0, n = 0, q = 0;
@@ -615,10 +616,18 @@ __device__ __forceinline__ void quad_round(QuadList<DEPTH>& L, const SplatRec* _
         quad_wavefront<DEPTH, true>(steps, np, hl, q * 32, pa, pb, L, S4, S0, S1, amax, q0, q1);
     else
         quad_wavefront<DEPTH, false>(steps, np, hl, q * 32, pa, pb, L, S4, S0, S1, amax, q0, q1);
-    // fold into the unit's rows (chains of different quadrants may share
-    // positions: shared-memory atomics)
-    quad_fold(L, pa, q0);
-    quad_fold(L, pb, q1);
+    // fold into the unit's rows: chains of different quadrants may share
+    // positions, so the round's chains take turns (a chain's own positions
+    // are distinct: plain read-modify-writes, no atomics)
+    while (chains) {
+        const int c = __ffs(chains) - 1;
+        chains &= chains - 1u;
+        if (id == c) {
+            quad_fold(L, pa, q0);
+            quad_fold(L, pb, q1);
+        }
+        __syncwarp();
+    }
 }
 
 template <bool DEPTH>
@@ -868,7 +877,11 @@ __global__ void __launch_bounds__(32 * kQWarps, 8) backward_quad_kernel(
                         if (r == rs) used[r] += Lc;
                     nr = max(nr, rs + 1);
                     if (lane >= o && lane < o + Lc) L.lanejob[rs][lane] = (uint8_t)(cid[i] << 5 | (lane - o));
-                    if (lane == 0) L.rsteps[rs] = max(L.rsteps[rs], key[i]);
+                    if (lane == 0) {  // steps | chain ids of the round << 16
+                        const int cur = L.rsteps[rs];
+                        L.rsteps[rs] = max(cur & 0xffff, key[i]) | (cur & ~0xffff) |
+                                       (1 << (16 + cid[i]));
+                    }
                 }
             }
             __syncwarp();
@@ -876,8 +889,9 @@ __global__ void __launch_bounds__(32 * kQWarps, 8) backward_quad_kernel(
 #pragma unroll 1
         for (int r = 0; r < nr; ++r) {
             const int code = L.lanejob[r][lane];
-            quad_round<DEPTH>(L, rec, code != 255 ? code >> 5 : -1, code & 31,
-                              L.rsteps[r], qn0, qn1, qnp, amax);
+            const int rs = L.rsteps[r];
+            quad_round<DEPTH>(L, rec, code != 255 ? code >> 5 : -1, code & 31, rs & 0xffff,
+                              (uint32_t)rs >> 16, qn0, qn1, qnp, amax);
         }
         __syncwarp();
         // ---- commit: lane l owns positions 2l, 2l + 1
