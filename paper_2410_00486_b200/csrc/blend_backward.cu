@@ -738,7 +738,9 @@ __global__ void __launch_bounds__(32 * kQWarps, 8) backward_quad_kernel(
                 const size_t o = (size_t)iy * W + ix;
                 if (pixgrad) asm volatile("prefetch.global.L1 [%0];" ::"l"(pixgrad + o));
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(ckpt + slot0 + p));
-                if (mk1[c] != 0u)
+                const int q = (c < 4 ? 0 : 2) + ((lane & 8) ? 1 : 0);
+                if (mk1[c] != 0u && sel4(q, qn0[0] + qn1[0], qn0[1] + qn1[1], qn0[2] + qn1[2],
+                                         qn0[3] + qn1[3]) > 32)
                     asm volatile("prefetch.global.L1 [%0];" ::"l"(ckpt + slot0 + kTilePx + p));
             }
         }
@@ -784,9 +786,12 @@ __global__ void __launch_bounds__(32 * kQWarps, 8) backward_quad_kernel(
                         G0 += gd * ckpt_depth[slot0 + p];
                     }
                     G0 -= pg.w;
-                    // state at the second bucket's start (used by split chains;
-                    // pixels not blending there get an inert finite state)
-                    if (m1 != 0u) {
+                    // state at the second bucket's start: only split chains (a
+                    // quadrant with > 32 positions) start there; pixels not
+                    // blending there, or in unsplit quadrants, get an inert
+                    // finite state (never read)
+                    if (m1 != 0u && sel4(q, qn0[0] + qn1[0], qn0[1] + qn1[1],
+                                         qn0[2] + qn1[2], qn0[3] + qn1[3]) > 32) {
                         const float4 c2 = ckpt[slot0 + kTilePx + p];
                         T1 = c2.x;
                         G1 = pg.x * c2.y + pg.y * c2.z + pg.z * c2.w;
