@@ -1061,3 +1061,33 @@ def test_ragged_image_sizes_match_oracle(w, h):
     mine = g2d[out.proj.map_index]
     for cols in ((0, 3), (3, 5), (5, 8), (8, 9)):
         assert normwise(mine[:, cols[0]:cols[1]], ref[:, cols[0]:cols[1]]) <= 1e-3, cols
+
+
+def test_depth_extension_mid_size_matches_oracle():
+    """The DEPTH instantiations of the blend and the quadrant-chain backward at a
+    scene with many units per tile and split chains (30k Gaussians, 320x240):
+    depth / alpha images and the 10-column g2d vs the oracle on the GPU's list."""
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    from paper_2410_00486_b200.scene import survey_camera, survey_scene
+    cam = survey_camera(320, 240)
+    g = ss.GaussianMap.from_scene(survey_scene(30000, 31))
+    out = ss.rasterize_forward(g, cam, ss.RasterOpts(sh_degree=0, with_depth=True))
+    assert int(out.k_eff_tiles.max()) > 64  # several units per tile
+    po = _gpu_proj_as_oracle(out)
+    ti = out.tile_index
+    oti = orc.OTileIndex(16, ti.tiles_x, ti.tiles_y, ti.pair_splat, ti.tile_range,
+                         ti.active_tiles)
+    r = orc.forward(po, oti, cam.width, cam.height, out.n_primitives, with_depth=True,
+                    m_cut=out.proj.m_cut.astype(np.float64))
+    assert np.abs(out.depth.cpu().numpy() - r.depth).max() <= 1e-4 * max(1.0, r.depth.max())
+    assert np.abs(out.alpha.cpu().numpy() - r.alpha).max() <= 1e-4
+    rng = np.random.default_rng(10)
+    gi = rng.standard_normal(out.image.shape).astype(np.float32) * 1e-3
+    gd = rng.standard_normal(out.depth.shape).astype(np.float32) * 1e-3
+    g2d = ss.screen_space_grads(out, torch.as_tensor(gi, device="cuda"),
+                                torch.as_tensor(gd, device="cuda")).cpu().numpy()
+    ref = orc.backward_splat(r, gi.astype(np.float64), gd.astype(np.float64))
+    mine = g2d[out.proj.map_index]
+    for cols in ((0, 3), (3, 5), (5, 8), (8, 9), (9, 10)):
+        assert normwise(mine[:, cols[0]:cols[1]], ref[:, cols[0]:cols[1]]) <= 1e-3, cols
