@@ -71,6 +71,28 @@ def single_workload(args):
             "(BASELINE configs[1])")
 
 
+L2_NOTE = ("GPU arm: 256 MB buffer written between timed steps (outside the events); "
+           "reference arm: host cores, no device cache")
+
+
+def single_config(args):
+    """The config object both arms print for the single-view workload."""
+    w = max(args.warmup, 3)
+    return {"workload": single_workload(args), "gaussians": args.n,
+            "image": [args.width, args.height], "sh_degree": 0, "l2": L2_NOTE,
+            "phase": f"iterations {w + 1}-{w + args.steps} from the survey initialisation; "
+                     "`converged` = iterations 251-270",
+            "parallelism": "single GPU"}
+
+
+def batch_config(world):
+    """The config object both arms print for the keyframe-batch workload."""
+    return {"workload": batch_workload(world), "gaussians": BATCH["n"],
+            "image": [BATCH["width"], BATCH["height"]], "sh_degree": 0,
+            "views_per_step": BATCH["views"],
+            "parallelism": f"keyframe-sharded x{world} (NCCL all-reduce)", "l2": L2_NOTE}
+
+
 def batch_workload(world):
     return (f"large map S({BATCH['n']}, {BATCH['width']}x{BATCH['height']}) SH0, fixed "
             f"keyframe batch of {BATCH['views']} views per step sharded over {world} GPU(s), "
@@ -282,11 +304,11 @@ def reference_arm(args, rank, world):
     warm = max(args.warmup, 3) if world == 1 else 1
     if world > 1:
         times, threads = run_cpu_batch_steps(warm + args.steps, budget_s=170.0)
-        workload, unit = batch_workload(world), "it/s"
+        config, unit = batch_config(world), "it/s"
         sample = "oracle keyframe-batch steps (8 views of S(1M) each, float64)"
     else:
         times, threads = run_cpu_iterations(args, warm + args.steps, budget_s=150.0)
-        workload, unit = single_workload(args), "it/s"
+        config, unit = single_config(args), "it/s"
         sample = "full float64 train_one iterations of the oracle restatement (oracle/)"
     timed = times[warm:] if len(times) > warm else times
     it_s = len(timed) / sum(timed)
@@ -296,7 +318,7 @@ def reference_arm(args, rank, world):
         "ms_per_step": 1000.0 * sum(timed) / len(timed), "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": workload},
+        "config": config,
         "cpu_baseline": {"value": it_s, "unit": unit, "cores": threads, "kind": "port",
                          "sample": f"{len(timed)} timed {sample}, {threads} OpenMP threads on "
                                    f"'{cpu_model()}' ({len(times) - len(timed)} untimed "
@@ -554,12 +576,7 @@ def main():
                 "steps": args.steps, "warmup": warmup, "ms_per_step": res["ms_per_step"],
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic",
-                "config": {"workload": batch_workload(world), "gaussians": BATCH["n"],
-                           "image": [BATCH["width"], BATCH["height"]], "sh_degree": 0,
-                           "views_per_step": BATCH["views"],
-                           "parallelism": f"keyframe-sharded x{world} (NCCL all-reduce)",
-                           "l2": "256 MB buffer written between timed steps (outside the "
-                                 "events)"},
+                "config": batch_config(world),
                 "views_per_s": res["views_per_s"], "clocks": clocks, "e2e": res.get("e2e"),
                 "validation_only": (args.same_device or args.dist_backend != "nccl") or None,
                 "scaling_reference": "the N = 1 point of this workload is the `config4` block "
@@ -669,13 +686,9 @@ def main():
         "steps": args.steps, "warmup": warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": single_workload(args), "gaussians": N, "image": [W, H],
-                   "sh_degree": 0, "pairs": rf["P"], "visible": rf["M"],
-                   "checkpoint_slots": rf["C"], "backward_units": rf["U"],
-                   "l2": "256 MB buffer written between timed steps (outside the events)",
-                   "phase": f"iterations {warmup + 1}-{warmup + args.steps} from the survey "
-                            "initialisation; `converged` = iterations 251-270",
-                   "parallelism": "single GPU"},
+        "config": single_config(args),
+        "workload_stats": {"pairs": rf["P"], "visible": rf["M"], "checkpoint_slots": rf["C"],
+                           "backward_units": rf["U"]},
         "roofline": rf["roof"],
         "iteration_roofline": {"algorithmic_MB": it_bytes / 1e6,
                                "achieved_GBs": it_bytes * value / 1e9,
