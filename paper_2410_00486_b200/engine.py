@@ -118,6 +118,7 @@ class MappingEngine:
         self._host = torch.zeros((self._slots, _lib.SNAPSHOT_DOUBLES), dtype=torch.float64,
                                  pin_memory=True)
         self._graphs: dict = {}
+        self._cam_last = None  # (caller's camera, its key, Camera, ss_camera)
         self._alloc_map_buffers()
         self._alloc_pair_buffers(self._cap)
         self.profile = None  # list of (stage, start event, end event) when profiling
@@ -145,11 +146,35 @@ class MappingEngine:
         base = self._pdev.data_ptr()
         return ctypes.c_void_p(base), ctypes.c_void_p(base + 128)
 
+    def _slot_event(self, it):
+        """The snapshot event of slot it % slots (created once: a slot's
+        record is drained long before the slot comes round again)."""
+        if getattr(self, "_events", None) is None:
+            self._events = [None] * self._slots
+        k = it % self._slots
+        if self._events[k] is None:
+            self._events[k] = torch.cuda.Event()
+        return self._events[k]
+
+    def _camera_of(self, camera):
+        """Camera.of(camera) and its ss_camera struct, reused while the caller
+        passes the same, unchanged camera object (host time before the step's
+        first launch: the GPU waits for it)."""
+        key = (camera.fx, camera.fy, camera.cx, camera.cy, int(camera.width),
+               int(camera.height), np.asarray(camera.R).tobytes(), np.asarray(camera.t).tobytes())
+        c = self._cam_last
+        if c is not None and c[0] is camera and c[1] == key:
+            return c[2]
+        cam = Camera.of(camera)
+        self._cam_last = (camera, key, cam, cam.to_ss())
+        return cam
+
     def _stage_params(self, rec):
         """Write the step's camera + Adam values into its pinned slot and
         enqueue the host->device copy."""
         slot = self._phost[rec.slot % self._pslots]
-        cm = rec.camera.to_ss()
+        c = self._cam_last
+        cm = c[3] if c is not None and c[2] is rec.camera else rec.camera.to_ss()
         ctypes.memmove(slot.data_ptr(), ctypes.addressof(cm), ctypes.sizeof(cm))
         ctypes.memmove(slot.data_ptr() + 128, ctypes.addressof(rec.hp), ctypes.sizeof(rec.hp))
         self._pdev.copy_(slot, non_blocking=True)
@@ -308,11 +333,11 @@ class MappingEngine:
     def step(self, camera, target: torch.Tensor, target_depth: torch.Tensor | None = None):
         """One fused mapping iteration (single view, single GPU)."""
         self._maybe_densify()
-        cam = Camera.of(camera)
+        cam = self._camera_of(camera)
         self.state.step_count += 1
         hp = self.state.hparams(self.opts.sh_degree > 0)
         rec = StepRecord(self.iteration, cam, target, target_depth, hp,
-                         self.iteration % self._slots, torch.cuda.Event())
+                         self.iteration % self._slots, self._slot_event(self.iteration))
         self._run(rec)
         self._records.append(rec)
         self.iteration += 1
