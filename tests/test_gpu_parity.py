@@ -1091,3 +1091,35 @@ def test_depth_extension_mid_size_matches_oracle():
     mine = g2d[out.proj.map_index]
     for cols in ((0, 3), (3, 5), (5, 8), (8, 9), (9, 10)):
         assert normwise(mine[:, cols[0]:cols[1]], ref[:, cols[0]:cols[1]]) <= 1e-3, cols
+
+
+@pytest.mark.parametrize("deg", [1, 2])
+def test_sh_degrees_1_2_match_oracle(deg):
+    """SH degrees between the fixtures' 0 and 3 (sh_basis / colors_from_sh,
+    sh.py:37-70,122-132; sh_basis_grad, sh.py:73-119): projected colour and
+    active mask, and the chain's SH / position / rotation gradients vs the
+    oracle on the same g2d."""
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    d = load("iter_sh3_small")
+    cam = fixture_camera(d)
+    g = ss.GaussianMap.from_arrays(*fixture_scene(d))
+    out = ss.rasterize_forward(g, cam, ss.RasterOpts(sh_degree=deg))
+    p = out.proj
+    ref = orc.project(_f32_map(g), cam, sh_degree=deg)
+    np.testing.assert_array_equal(p.map_index, ref.map_index)
+    assert np.abs(p.rgb - ref.rgb).max() <= 1e-5
+    np.testing.assert_array_equal(p.rgb_active, ref.rgb_active)
+    rng = np.random.default_rng(40 + deg)
+    gimg = rng.standard_normal(out.image.shape).astype(np.float32) * 1e-3
+    g2d = ss.screen_space_grads(out, torch.as_tensor(gimg, device="cuda"))
+    grads = ss.rasterizer._finish_backward(out, g2d)
+    mi = out.proj.map_index
+    oref = orc.chain(_f32_map(g), cam, ref, g2d.cpu().numpy().astype(np.float64)[mi],
+                     out.contributed.cpu().numpy())
+    for name in ("position", "rotation", "log_scale", "opacity_logit"):
+        assert normwise(getattr(grads, name).cpu().numpy(), getattr(oref, name)) <= 1e-3, name
+    sh = grads.sh.cpu().numpy()
+    assert normwise(sh, oref.sh) <= 1e-3
+    nb = (deg + 1) ** 2
+    assert np.abs(sh[:, nb:]).max() == 0.0  # bands above the degree get no gradient
