@@ -51,6 +51,7 @@ pairs_hist = []
 band_pos, band_pairs = [], []
 quad_steps = 0  # per-quadrant chains (see below)
 seg_steps = 0
+seg_need = seg_have = 0
 GROUPS = [(8, 8), (16, 4), (8, 4), (4, 8), (4, 4), (16, 2), (8, 2)]
 grp_stats = {}
 for t in range(tx * ty):
@@ -112,6 +113,9 @@ for t in range(tx * ty):
             else:
                 rounds.append([L, p + L - 1])
         seg_steps += sum(r[1] for r in rounds)
+        # lane-steps the chains need vs the rounds' 32 lanes x longest chain
+        seg_need += sum((p + (n + 1) // 2 - 1) * ((n + 1) // 2) for p, n in jobs)
+        seg_have += 32 * sum(r[1] for r in rounds)
         # the same packing for other pixel-group shapes (gw columns x gh rows)
         M0 = m0.reshape(16, 16).astype(np.uint64)
         M1 = m1.reshape(16, 16).astype(np.uint64)
@@ -169,6 +173,7 @@ print(json.dumps({
     "band_pairs_mean": float(np.mean(band_pairs)),
     "quadrant_chain_steps": quad_steps, "quadrant_vs_wavefront": quad_steps / steps_total,
     "segment_rounds_steps": seg_steps, "segments_vs_wavefront": seg_steps / steps_total,
+    "segment_lane_utilisation": seg_need / max(seg_have, 1),
     "groups": {"%dx%d" % k: {"vs_wavefront": round(v[0] / steps_total, 4),
                              "rounds_per_unit": round(v[1] / len(ph), 2),
                              "chains_per_unit": round(v[2] / len(ph), 2),
