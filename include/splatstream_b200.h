@@ -255,6 +255,25 @@ int ss_backward_splat(const ss_camera *cam, const ss_raster_opts *opts, const ss
                       const uint32_t *d_work, int64_t work_capacity,
                       int64_t n, float *d_g2d, uint8_t *d_contributed, const ss_status *d_status,
                       void *stream);
+/* The clearing ss_backward_splat does first (d_g2d rows, d_contributed when
+ * non-NULL, the work-unit counter in d_status), as its own launch: run it
+ * ahead of time -- e.g. on a second stream beside the loss kernels, after
+ * ss_backward_schedule on that stream -- and call ss_backward_splat_ex with
+ * SS_BWD_SKIP_CLEAR.  g2d_cols 9 or 10 (with depth). */
+int ss_backward_clear(int64_t n, int32_t g2d_cols, float *d_g2d, uint8_t *d_contributed,
+                      ss_status *d_status, void *stream);
+#define SS_BWD_SKIP_CLEAR 1
+/* ss_backward_splat with flags (0 or SS_BWD_SKIP_CLEAR: the rows were
+ * cleared by ss_backward_clear, stream-ordered before this call). */
+int ss_backward_splat_ex(const ss_camera *cam, const ss_raster_opts *opts,
+                         const ss_splats *splats, const ss_bins *bins, const float *d_image,
+                         const float *d_grad_image, const float *d_pixgrad,
+                         const float *d_depth, const float *d_grad_depth,
+                         const int32_t *d_n_contrib, const int32_t *d_k_eff, const void *d_ckpt,
+                         const float *d_ckpt_depth, const uint32_t *d_ckpt_mask,
+                         const uint32_t *d_work, int64_t work_capacity, int64_t n,
+                         float *d_g2d, uint8_t *d_contributed, const ss_status *d_status,
+                         int32_t flags, void *stream);
 
 /* Flat per-Gaussian gradient / moment layout (planes of n floats):
  * position 3, rotation 4, log_scale 3, opacity 1, sh_dc 3, sh_rest 45. */

@@ -35,6 +35,7 @@ class SSStatus(ctypes.Structure):
 
 
 ORDER_MAX_TILES = 16384  # SS_ORDER_MAX_TILES
+SS_BWD_SKIP_CLEAR = 1  # ss_backward_splat_ex flag: rows cleared by ss_backward_clear
 STATUS_WORDS = 10  # 80-byte ss_status as int64 words (word 8 holds a double)
 SNAPSHOT_DOUBLES = 11  # ss_step_snapshot row: 8 status words, opacity sum, 2 loss sums
 SN_OPACITY_SUM, SN_L1_SUM, SN_SSIM_SUM = 8, 9, 10
@@ -114,6 +115,10 @@ _SIGS = {
     "ss_depth_l1": (I32, [I32, I32, VP, VP, F32, VP, VP, VP]),
     "ss_backward_splat": (I32, [P(SSCamera), P(SSRasterOpts), P(SSSplats), P(SSBins), VP, VP,
                                 VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP]),
+    "ss_backward_clear": (I32, [I64, I32, VP, VP, VP, VP]),
+    "ss_backward_splat_ex": (I32, [P(SSCamera), P(SSRasterOpts), P(SSSplats), P(SSBins), VP, VP,
+                                   VP, VP, VP, VP, VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, I32,
+                                   VP]),
     "ss_backward_pixel": (I32, [VP, VP, VP, VP, VP, VP, VP, VP, I64, VP, VP]),
     "ss_seed_workspace_bytes": (SZ, [I64]),
     "ss_seed_from_points": (I32, [I64, VP, VP, F32, VP, VP, VP, VP, VP, VP, VP, SZ, VP]),

@@ -22,7 +22,8 @@ cudaError_t launch_backward_splat(const ss_camera*, const ss_raster_opts*, const
                                   const float*, const float*, const int32_t*, const int32_t*,
                                   const void*, const float*, const uint32_t*, const uint32_t*,
                                   int64_t, int64_t, float*, uint8_t*, const ss_status*, uint32_t*,
-                                  cudaStream_t);
+                                  bool, cudaStream_t);
+cudaError_t launch_backward_clear(int64_t, int, float*, uint8_t*, uint32_t*, cudaStream_t);
 cudaError_t launch_backward_pixel(const ss_camera*, const ss_raster_opts*, const ss_splats*,
                                   const ss_bins*, const float*, const float*, const int32_t*,
                                   const int32_t*, int64_t, float*, cudaStream_t);
@@ -276,6 +277,13 @@ int ss_backward_schedule(const ss_camera* cam, const int32_t* d_k_eff, uint32_t*
                                        S(stream)));
 }
 
+int ss_backward_clear(int64_t n, int32_t g2d_cols, float* d_g2d, uint8_t* d_contributed,
+                      ss_status* d_status, void* stream) {
+    if (n < 0 || (g2d_cols != 9 && g2d_cols != 10) || !d_g2d || !d_status) return SS_EINVAL;
+    uint32_t* counter = reinterpret_cast<uint32_t*>(&d_status->reserved);
+    return rc(launch_backward_clear(n, g2d_cols, d_g2d, d_contributed, counter, S(stream)));
+}
+
 int ss_backward_splat(const ss_camera* cam, const ss_raster_opts* opts, const ss_splats* splats,
                       const ss_bins* bins, const float* d_image, const float* d_grad_image,
                       const float* d_pixgrad, const float* d_depth, const float* d_grad_depth,
@@ -284,6 +292,22 @@ int ss_backward_splat(const ss_camera* cam, const ss_raster_opts* opts, const ss
                       const uint32_t* d_work, int64_t work_capacity,
                       int64_t n, float* d_g2d, uint8_t* d_contributed, const ss_status* d_status,
                       void* stream) {
+    return ss_backward_splat_ex(cam, opts, splats, bins, d_image, d_grad_image, d_pixgrad,
+                                d_depth, d_grad_depth, d_n_contrib, d_k_eff, d_ckpt,
+                                d_ckpt_depth, d_ckpt_mask, d_work, work_capacity, n, d_g2d,
+                                d_contributed, d_status, 0, stream);
+}
+
+int ss_backward_splat_ex(const ss_camera* cam, const ss_raster_opts* opts,
+                         const ss_splats* splats, const ss_bins* bins, const float* d_image,
+                         const float* d_grad_image, const float* d_pixgrad,
+                         const float* d_depth, const float* d_grad_depth,
+                         const int32_t* d_n_contrib, const int32_t* d_k_eff, const void* d_ckpt,
+                         const float* d_ckpt_depth, const uint32_t* d_ckpt_mask,
+                         const uint32_t* d_work, int64_t work_capacity, int64_t n,
+                         float* d_g2d, uint8_t* d_contributed, const ss_status* d_status,
+                         int32_t flags, void* stream) {
+    if (flags & ~SS_BWD_SKIP_CLEAR) return SS_EINVAL;
     if (!cam || !opts_ok(opts) || !splats || !bins || !d_image || !d_grad_image ||
         !d_n_contrib || !d_k_eff || !d_ckpt || !d_ckpt_mask || !d_work || !d_g2d || !d_status)
         return SS_EINVAL;
@@ -294,7 +318,7 @@ int ss_backward_splat(const ss_camera* cam, const ss_raster_opts* opts, const ss
                                     reinterpret_cast<const float4*>(d_pixgrad), d_depth,
                                     d_grad_depth, d_n_contrib, d_k_eff, d_ckpt, d_ckpt_depth,
                                     d_ckpt_mask, d_work, work_capacity, n, d_g2d, d_contributed,
-                                    d_status, counter, S(stream)));
+                                    d_status, counter, !(flags & SS_BWD_SKIP_CLEAR), S(stream)));
 }
 
 int ss_backward_pixel(const ss_camera* cam, const ss_raster_opts* opts, const ss_splats* splats,

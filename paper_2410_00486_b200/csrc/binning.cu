@@ -658,7 +658,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
 #ifdef SS_FE_TRACE
 // diagnostics build only (tools/trace_front.py): per CTA, globaltimer stamps
 // at the phase boundaries of bin_front_kernel
-constexpr int kFeTraceSlots = 24;
+constexpr int kFeTraceSlots = 40;
 __device__ unsigned long long g_fe_trace[160 * kFeTraceSlots];
 __device__ __forceinline__ void fe_stamp(int slot) {
     if (threadIdx.x == 0 && slot < kFeTraceSlots) {
@@ -1243,6 +1243,7 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
             }
         }
         __syncthreads();
+        FE_STAMP(24 + 4 * p);
         const uint32_t col = t < 256 ? s_part[0][t] : 0u;
         const uint32_t tot = t < 256 ? s_part[0][256 + t] : 0u;
         const uint32_t excl = block_excl_scan<kFeThreads>(t < 256 ? tot : 0u, s_warp);
@@ -1258,6 +1259,7 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
             }
         }
         __syncthreads();
+        FE_STAMP(25 + 4 * p);
         for (uint32_t i = t; i < nloc; i += kFeThreads) {
             const uint32_t k = s_keys[i];
             const uint32_t d = (k >> shift) & 255u;
@@ -1265,6 +1267,7 @@ __global__ void __launch_bounds__(kFeThreads, 1) bin_front_kernel(FeArgs a) {
             vout[gp] = s_vals[i];
             if (p < lastp) kout[gp] = k;
         }
+        FE_STAMP(26 + 4 * p);
         grid.sync();
         FE_STAMP(2 + 2 * p);
         ksrc = kout;
@@ -1686,6 +1689,10 @@ cudaError_t launch_scan_u32(const uint32_t* in, int64_t n, uint32_t* out, int64_
 }  // namespace ss
 
 #ifdef SS_FE_TRACE
+extern "C" int ss_debug_fe_trace_clear() {
+    static const unsigned long long zeros[160 * ss::kFeTraceSlots] = {};
+    return (int)cudaMemcpyToSymbol(ss::g_fe_trace, zeros, sizeof(zeros));
+}
 extern "C" int ss_debug_fe_trace(void* host, size_t bytes) {
     if (bytes > sizeof(ss::g_fe_trace)) bytes = sizeof(ss::g_fe_trace);
     return (int)cudaMemcpyFromSymbol(host, ss::g_fe_trace, bytes);

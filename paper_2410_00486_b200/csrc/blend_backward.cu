@@ -1305,6 +1305,16 @@ cudaError_t launch_backward_schedule(const ss_camera* cam, const int32_t* k_eff,
     return cudaGetLastError();
 }
 
+// one launch clears the gradient rows, the contributed marks and the
+// work-unit counter (also usable ahead of time on another stream: the
+// engine runs it beside the loss kernels, ss_backward_clear)
+cudaError_t launch_backward_clear(int64_t n, int ncol, float* g2d, uint8_t* contributed,
+                                  uint32_t* counter, cudaStream_t s) {
+    launch_pdl(bwd_clear_kernel, dim3(div_up(n * ncol > 4 ? n * ncol / 4 : 1, 256)), dim3(256),
+               0, s, g2d, (int64_t)n * ncol, contributed, n, counter);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
                                   const ss_splats* sp, const ss_bins* bins, const float* image,
                                   const float* grad_image, const float4* pixgrad,
@@ -1313,14 +1323,11 @@ cudaError_t launch_backward_splat(const ss_camera* cam, const ss_raster_opts* o,
                                   const float* ckpt_depth, const uint32_t* ckpt_mask,
                                   const uint32_t* work, int64_t work_cap, int64_t n, float* g2d,
                                   uint8_t* contributed, const ss_status* st, uint32_t* counter,
-                                  cudaStream_t s) {
+                                  bool clear, cudaStream_t s) {
     const bool depthf = o->with_depth != 0;
     const int ncol = depthf ? 10 : 9;
-    // one launch clears the gradient rows, the contributed marks and the
-    // work-unit counter
     int tx = div_up(cam->width, kTile), ty = div_up(cam->height, kTile);
-    launch_pdl(bwd_clear_kernel, dim3(div_up(n * ncol > 4 ? n * ncol / 4 : 1, 256)), dim3(256),
-               0, s, g2d, (int64_t)n * ncol, contributed, n, counter);
+    if (clear) launch_backward_clear(n, ncol, g2d, contributed, counter, s);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

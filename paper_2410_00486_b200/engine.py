@@ -32,7 +32,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import check, lib, traced
+from ._lib import SS_BWD_SKIP_CLEAR, check, lib, traced
 from .core import Camera, GaussianMap
 from .densify import DensifyConfig, densify_and_prune, opacity_reset
 from .optimizer import AdamState, LearningRates
@@ -290,6 +290,11 @@ class MappingEngine:
             check(L.ss_backward_schedule(ctypes.byref(cm), P(self.k_eff), P(self.work),
                                          self.work_cap, P(self.status), stream_handle()),
                   "ss_backward_schedule")
+            # the backward's clearing of the g2d rows (last read by the
+            # previous step's chain+Adam) off the critical path as well
+            check(L.ss_backward_clear(n, 10 if self.opts.with_depth else 9, P(self.g2d),
+                                      P(self.contributed), P(self.status), stream_handle()),
+                  "ss_backward_clear")
         use_pg = self.cfg.lambda_ssim != 0.0 and not self.opts.with_depth
         # with pixgrad the backward never reads grad_image: it is not written
         check(L.ss_loss_l1_ssim(self.H, self.W, P(self.image), P(target),
@@ -306,13 +311,14 @@ class MappingEngine:
                 self.grad_depth.zero_()
         self._mark("loss")
         torch.cuda.current_stream().wait_stream(side)
-        check(L.ss_backward_splat(ctypes.byref(cm), ctypes.byref(op), ctypes.byref(spss),
-                                  ctypes.byref(bss), P(self.image), P(self.grad_image),
-                                  P(self.pixgrad) if use_pg else None, P(self.depth),
-                                  P(self.grad_depth), P(self.n_contrib), P(self.k_eff),
-                                  P(self.ckpt), P(self.ckpt_depth), P(self.ckpt_mask),
-                                  P(self.work), self.work_cap, n, P(self.g2d),
-                                  P(self.contributed), P(self.status), s), "ss_backward_splat")
+        check(L.ss_backward_splat_ex(ctypes.byref(cm), ctypes.byref(op), ctypes.byref(spss),
+                                     ctypes.byref(bss), P(self.image), P(self.grad_image),
+                                     P(self.pixgrad) if use_pg else None, P(self.depth),
+                                     P(self.grad_depth), P(self.n_contrib), P(self.k_eff),
+                                     P(self.ckpt), P(self.ckpt_depth), P(self.ckpt_mask),
+                                     P(self.work), self.work_cap, n, P(self.g2d),
+                                     P(self.contributed), P(self.status), SS_BWD_SKIP_CLEAR, s),
+              "ss_backward_splat_ex")
         self._mark("backward")
         return mp, cm, op
 

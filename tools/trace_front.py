@@ -8,7 +8,10 @@ Stamps (globaltimer, per CTA): 0 start, 1+2p / 2+2p depth pass p before /
 after its second grid barrier; direct emission: 10/11 around the chunk-sum
 barrier, 12 count walk done, 13 warp prefix done, 14/15 around the count
 barrier, 16/17 around the column-prefix barrier, 18 tile starts done, 19
-rank walk done; 20+p after depth pass p's first barrier."""
+rank walk done; 20+p after depth pass p's first barrier; 24+4p column
+histograms loaded, 25+4p local reorder done, 26+4p scatter done (before the
+pass's second barrier).  The buffer is cleared (zeros read back first) so
+stale stamps of skipped passes do not show."""
 import ctypes
 import os
 import sys
@@ -29,13 +32,17 @@ opts = ss.RasterOpts(sh_degree=0)
 tgt = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(n, 100)), cam, opts).image
 eng = ss.MappingEngine(g, W, H, opts)
 eng.fit_capacity(cam)
-for _ in range(6):
+for _ in range(5):
     eng.step(cam, tgt)
 eng.synchronize()
 L = _lib.lib()
 fn = L.ss_debug_fe_trace
 fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-S = 24
+clr = L.ss_debug_fe_trace_clear
+S = 40
+assert clr() == 0
+eng.step(cam, tgt)
+eng.synchronize()
 buf = np.zeros(160 * S, np.uint64)
 assert fn(buf.ctypes.data, buf.nbytes) == 0
 tr = buf.reshape(160, S).astype(np.int64)
