@@ -106,3 +106,40 @@ def test_adam_step_rechecks_only_modified_gradients():
     with pytest.raises(FloatingPointError, match="position"):
         ss.adam_step(g, gr, st)
     assert torch.equal(before, g.positions)
+
+
+def test_backward_clear_ahead_equals_backward_splat():
+    """ss_backward_clear + ss_backward_splat_ex(SS_BWD_SKIP_CLEAR) -- the
+    engine's split, the clear on a second stream -- gives the rows
+    ss_backward_splat gives whatever the buffer held before (up to the order
+    of the per-tile red.add rows); bad flags / column counts are rejected."""
+    _need_gpu()
+    from paper_2410_00486_b200 import _lib
+    from paper_2410_00486_b200.rasterizer import P, screen_space_grads, stream_handle
+    ss, g, cam = _scene(seed=14)
+    opts = ss.RasterOpts(sh_degree=0)
+    out = ss.rasterize_forward(g, cam, opts)
+    gi = torch.randn_like(out.image)
+    want = screen_space_grads(out, gi)
+    n = out.n_primitives
+    L = _lib.lib()
+    cm, op = out.camera.to_ss(), out.opts.to_ss()
+    g2d = torch.full((n, 9), float("nan"), device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        assert L.ss_backward_schedule(ctypes.byref(cm), P(out.k_eff_tiles), P(out.work),
+                                      out.work_capacity, P(out.status), stream_handle()) == 0
+        assert L.ss_backward_clear(n, 9, P(g2d), None, P(out.status), stream_handle()) == 0
+    torch.cuda.current_stream().wait_stream(side)
+    args = (ctypes.byref(cm), ctypes.byref(op), ctypes.byref(out.splats.ss()),
+            ctypes.byref(out.bins.ss()), P(out.image), P(gi), None, P(out.depth), None,
+            P(out.n_contrib), P(out.k_eff_tiles), P(out.ckpt), P(out.ckpt_depth),
+            P(out.ckpt_mask), P(out.work), out.work_capacity, n, P(g2d), None, P(out.status))
+    assert L.ss_backward_splat_ex(*args, 2, stream_handle()) == _lib.SS_EINVAL
+    assert L.ss_backward_splat_ex(*args, _lib.SS_BWD_SKIP_CLEAR, stream_handle()) == 0
+    torch.cuda.synchronize()
+    assert torch.isfinite(g2d).all()
+    scale = want.abs().amax(dim=0)
+    assert ((g2d - want).abs() <= 1e-5 * scale + 1e-30).all()
+    assert L.ss_backward_clear(n, 8, P(g2d), None, P(out.status), None) == _lib.SS_EINVAL
