@@ -143,3 +143,44 @@ def test_backward_clear_ahead_equals_backward_splat():
     scale = want.abs().amax(dim=0)
     assert ((g2d - want).abs() <= 1e-5 * scale + 1e-30).all()
     assert L.ss_backward_clear(n, 8, P(g2d), None, P(out.status), None) == _lib.SS_EINVAL
+
+
+@pytest.mark.parametrize("depth", [False, True])
+def test_warp_forward_bit_identical_to_cta_forward(depth):
+    """The per-warp forward (default) and the CTA-batched forward (taken when
+    the blend loop's contributed flags are asked for) write the same image,
+    transmittance, n_contrib, k_eff, depth, checkpoints and blend masks, bit
+    for bit, at a scene with long tile lists (many buckets per tile)."""
+    _need_gpu()
+    from paper_2410_00486_b200 import _lib
+    from paper_2410_00486_b200.rasterizer import P, stream_handle
+    ss, g, cam = _scene(n=30000, seed=15)
+    out = ss.rasterize_forward(g, cam, ss.RasterOpts(sh_degree=0, with_depth=depth))
+    assert int(out.k_eff_tiles.max()) > 64
+    L = _lib.lib()
+    res = []
+    for flag in (None, torch.zeros(len(g), dtype=torch.uint8, device="cuda")):
+        bufs = dict(img=torch.empty_like(out.image), ft=torch.empty_like(out.final_t),
+                    nc=torch.empty_like(out.n_contrib), ke=torch.empty_like(out.k_eff_tiles),
+                    ck=torch.full_like(out.ckpt, -7.0),
+                    cm=torch.full_like(out.ckpt_mask, 0x5A5A5A5A),
+                    work=torch.empty_like(out.work))
+        if depth:
+            bufs["d"] = torch.empty_like(out.depth)
+            bufs["cd"] = torch.full_like(out.ckpt_depth, -7.0)
+        st = torch.empty(_lib.STATUS_WORDS, dtype=torch.int64, device="cuda")
+        assert L.ss_status_reset(P(st), stream_handle()) == 0
+        rc = L.ss_blend_forward(ctypes.byref(out.camera.to_ss()), ctypes.byref(out.opts.to_ss()),
+                                ctypes.byref(out.splats.ss()), ctypes.byref(out.bins.ss()),
+                                P(bufs["img"]), P(bufs["ft"]), P(bufs["nc"]),
+                                P(bufs.get("d")), P(bufs["ke"]), P(flag), P(bufs["ck"]),
+                                P(bufs.get("cd")), P(bufs["cm"]), P(bufs["work"]),
+                                out.work_capacity, P(st), stream_handle())
+        assert rc == 0
+        torch.cuda.synchronize()
+        res.append(bufs)
+    a, b = res
+    for k in a:
+        if k == "work":
+            continue  # same entries, order of the tiles' appends differs
+        assert torch.equal(a[k], b[k]), k

@@ -5,7 +5,7 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/abb
 D=paper_2410_00486_b200/csrc
 mkdir -p /tmp/abb_base && cp $D/*.cu $D/*.cuh /tmp/abb_base/
-mkdir -p /tmp/abb_lib
+rm -rf /tmp/abb_lib; mkdir -p /tmp/abb_lib
 make -s -C $D > /dev/null 2>&1 && cp paper_2410_00486_b200/libss_b200.so /tmp/abb_lib/base.so
 for d in tools/_ab_*/; do
   v=$(basename $d); v=${v#_ab_}

@@ -4,7 +4,8 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/abn
 D=paper_2410_00486_b200/csrc
-mkdir -p /tmp/abn_base && cp $D/*.cu $D/*.cuh /tmp/abn_base/
+rm -rf /tmp/abn_base; mkdir -p /tmp/abn_base && cp $D/*.cu $D/*.cuh /tmp/abn_base/
+make -s -C $D > /dev/null 2>&1
 run() {
   PROF_WARM=5 timeout 200 python tools/profile_kernels.py > gpurun_out/abn/$1_early.txt 2>&1
   PROF_WARM=250 timeout 300 python tools/profile_kernels.py > gpurun_out/abn/$1_conv.txt 2>&1
