@@ -10,7 +10,7 @@ import csv
 import json
 import sys
 
-KEYS = {"bin_front": "bin_front_kernel", "blend_forward": "blend_forward_kernel",
+KEYS = {"bin_front": "bin_front_kernel", "blend_forward": "blend_forward_",
         "ssim_bwd": "ssim_bwd_kernel", "backward": "backward_quad_kernel",
         "chain_adam": "chain_adam_kernel", "ssim_fwd": "ssim_fwd_kernel",
         "preprocess": "preprocess_kernel"}
