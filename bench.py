@@ -379,17 +379,15 @@ def e2e_single(torch, eng, cam, tgt, steps, restore=None):
     (wall clock)."""
     host_tgt = tgt.cpu().pin_memory()
     bufs = [eng.target_buffer(slot=0), eng.target_buffer(slot=1)]
-    copy_stream = torch.cuda.Stream()
-    uploaded = [torch.cuda.Event(), torch.cuda.Event()]
+    uploaded = [None, None]
     consumed = [torch.cuda.Event(), torch.cuda.Event()]
     main = torch.cuda.current_stream()
 
     def upload(k):
+        # MappingEngine.upload_target: row chunks on concurrent copy streams,
+        # after the slot's previous reader
         b = k % 2
-        with torch.cuda.stream(copy_stream):
-            copy_stream.wait_event(consumed[b])
-            bufs[b].copy_(host_tgt, non_blocking=True)
-            uploaded[b].record(copy_stream)
+        uploaded[b] = eng.upload_target(host_tgt, b, after=consumed[b])
 
     def step(k):
         b = k % 2
@@ -419,14 +417,14 @@ def e2e_single(torch, eng, cam, tgt, steps, restore=None):
         step(k)
     eng.synchronize()  # every step's loss is on the host
     wall = time.perf_counter() - t0
-    copy_stream.synchronize()
+    torch.cuda.synchronize()
     return {"value": steps / wall, "unit": "it/s", "steps": steps,
             "h2d_bytes_per_step": int(host_tgt.numel() * 4),
             "d2h_bytes_per_step": int(eng._host.shape[1] * 8),
             "timing": "wall clock over the same iterations as the device-timed value (state "
                       "restored), pinned host target upload per step into the engine's other "
-                      "target slot (copy stream, double-buffered) + per-step loss/status read "
-                      "back"}
+                      "target slot (MappingEngine.upload_target: row chunks on 4 copy streams, "
+                      "double-buffered) + per-step loss/status read back"}
 
 
 def stage_times(torch, eng, step, k=5):

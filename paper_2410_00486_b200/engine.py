@@ -387,6 +387,46 @@ class MappingEngine:
                                          device=self.dev)
         return self._tgt_buf if slot == 0 else self._tgt_buf1
 
+    def upload_target(self, host: torch.Tensor, slot: int, after=None, chunks: int = 4):
+        """Upload one keyframe target (H, W, 3) float32 from pinned host
+        memory into target slot `slot`, split into row chunks copied
+        concurrently on `chunks` copy streams (one pinned host-to-device copy
+        of 9.8 MB ran at 22 GB/s on a box where four concurrent chunks ran
+        at 34 GB/s; on a fast host both reach ~50).  `after`: an event the
+        copies wait for (the slot's previous reader).  Returns the event a
+        step reading the slot must wait on (torch.cuda.current_stream()
+        .wait_event), or pass the buffer to step() after it."""
+        dst = self.target_buffer(slot=slot)
+        if tuple(host.shape) != tuple(dst.shape) or host.dtype != torch.float32:
+            raise ValueError(f"target must be float32 {tuple(dst.shape)}, got "
+                             f"{host.dtype} {tuple(host.shape)}")
+        if host.device.type != "cpu" or not host.is_pinned():
+            raise ValueError("upload_target needs a pinned host tensor (tensor.pin_memory())")
+        k = max(1, min(int(chunks), 8))
+        streams = getattr(self, "_copy_streams", None)
+        if streams is None or len(streams) < k or streams[0].device != self.dev:
+            streams = self._copy_streams = [torch.cuda.Stream(device=self.dev)
+                                            for _ in range(k)]
+        src, out = host.reshape(self.H, -1), dst.reshape(self.H, -1)
+        # events reused per slot (a wait already issued keeps the state it saw)
+        evs = getattr(self, "_upload_events", {})
+        self._upload_events = evs
+        if (slot, k) not in evs:
+            evs[(slot, k)] = [torch.cuda.Event() for _ in range(k + 1)]
+        done = evs[(slot, k)]
+        for i in range(k):
+            r0, r1 = i * self.H // k, (i + 1) * self.H // k
+            st = streams[i]
+            if after is not None:
+                st.wait_event(after)
+            with torch.cuda.stream(st):
+                out[r0:r1].copy_(src[r0:r1], non_blocking=True)
+            done[i].record(st)
+        for ev in done[1:k]:
+            streams[0].wait_event(ev)
+        done[k].record(streams[0])
+        return done[k]
+
     def _stage_target(self, rec: StepRecord):
         """(target buffer, depth buffer, slot) the graph of this step reads."""
         slot = 0

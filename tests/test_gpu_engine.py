@@ -334,3 +334,42 @@ def test_scheduled_mapper_matches_oracle_trainer_selection():
         assert abs(sm.kf_loss[k] - v) <= 1e-3 * abs(v), (k, sm.kf_loss[k], v)
     assert len(eng._graphs) == 1
 
+
+
+def test_upload_target_chunked_copy_and_errors():
+    """MappingEngine.upload_target: the row chunks copied on concurrent copy
+    streams reassemble the keyframe exactly in the requested slot, ordered
+    after `after`; a step fed the slot matches a step fed the same target
+    through step()'s own staging copy; wrong dtype / shape / unpinned host
+    memory are rejected."""
+    _need_gpu()
+    import paper_2410_00486_b200 as ss
+    from paper_2410_00486_b200.scene import survey_camera, survey_scene
+    cam = survey_camera(160, 120)
+    opts = ss.RasterOpts(sh_degree=0)
+    tgt = ss.rasterize_forward(ss.GaussianMap.from_scene(survey_scene(4000, 71)), cam,
+                               opts).image
+    host = tgt.cpu().pin_memory()
+    e1 = ss.MappingEngine(ss.GaussianMap.from_scene(survey_scene(4000, 72)), 160, 120, opts)
+    e2 = ss.MappingEngine(ss.GaussianMap.from_scene(survey_scene(4000, 72)), 160, 120, opts)
+    for k in (1, 3, 4):
+        before = torch.cuda.Event()
+        before.record()
+        ev = e1.upload_target(host, 1, after=before, chunks=k)
+        torch.cuda.current_stream().wait_event(ev)
+        assert torch.equal(e1.target_buffer(slot=1), tgt), k
+    for _ in range(3):
+        ev = e1.upload_target(host, 1)
+        torch.cuda.current_stream().wait_event(ev)
+        e1.step(cam, e1.target_buffer(slot=1))
+        e2.step(cam, tgt)
+    e1.synchronize()
+    e2.synchronize()
+    # (the backward's per-tile red.add rows sum in any order: last-bit noise)
+    assert torch.allclose(e1.gmap.positions, e2.gmap.positions, rtol=0, atol=1e-5)
+    with pytest.raises(ValueError):
+        e1.upload_target(host.double().pin_memory(), 0)
+    with pytest.raises(ValueError):
+        e1.upload_target(tgt.cpu(), 0)
+    with pytest.raises(ValueError):
+        e1.upload_target(host[:-1].clone().pin_memory(), 0)
