@@ -427,6 +427,21 @@ def e2e_single(torch, eng, cam, tgt, steps, restore=None):
                       "double-buffered) + per-step loss/status read back"}
 
 
+def e2e_median(torch, eng, cam, tgt, steps, restore, reps=3):
+    """e2e_single `reps` times over the same iterations (state restored
+    before each): the median run, with every run's value listed (the boxes'
+    host-to-device rate swings within minutes, `tools/e2e_probe.py`)."""
+    runs = []
+    for _ in range(reps):
+        restore()
+        runs.append(e2e_single(torch, eng, cam, tgt, steps, restore=restore))
+    runs.sort(key=lambda r: r["value"])
+    med = dict(runs[len(runs) // 2])
+    med["runs"] = [round(r["value"], 1) for r in runs]
+    med["timing"] += f"; median of {reps} runs"
+    return med
+
+
 def stage_times(torch, eng, step, k=5):
     """Per-stage device times from instrumented (event-bracketed, non-graph)
     steps, outside any timed region."""
@@ -631,8 +646,7 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        restore_state(eng, snap)
-        e2e = e2e_single(torch, eng, cam, tgt, args.steps, restore=lambda: restore_state(eng, snap))
+        e2e = e2e_median(torch, eng, cam, tgt, args.steps, restore=lambda: restore_state(eng, snap))
 
     # ---- converged regime: iterations 251-270 of the same training run
     converged = None
@@ -654,8 +668,7 @@ def main():
                      "backward_units": c_rf["U"], "stage_ms": c_stage,
                      "roofline": c_rf["roof"]}
         if not args.no_e2e:
-            restore_state(eng, csnap)
-            converged["e2e"] = e2e_single(torch, eng, cam, tgt, args.steps,
+            converged["e2e"] = e2e_median(torch, eng, cam, tgt, args.steps,
                                           restore=lambda: restore_state(eng, csnap))
     del eng
     torch.cuda.empty_cache()
