@@ -54,6 +54,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 struct SsimWindow {
     float w[11];
+    double wd[11];  // the same weights widened (exact), for the float64 vertical taps
 };
 
 __device__ __forceinline__ int reflect1(int i, int n) {
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(256, 3) ssim_fwd_kernel(int H, int W, const fl
                 double axx = 0.0, ayy = 0.0, axy = 0.0;
 #pragma unroll
                 for (int m = 0; m < 11; ++m) {
-                    const double wd = (double)win.w[m];
+                    const double wd = win.wd[m];
                     axx = fma(wd, (double)vx[o + m], axx);
                     ayy = fma(wd, (double)vy[o + m], ayy);
                     axy = fma(wd, (double)vm[o + m], axy);
@@ -513,7 +514,10 @@ static SsimWindow make_window() {
         v[m] = exp(-(xx * xx) / (2 * 1.5 * 1.5));
         s += v[m];
     }
-    for (int m = 0; m < 11; ++m) w.w[m] = (float)(v[m] / s);
+    for (int m = 0; m < 11; ++m) {
+        w.w[m] = (float)(v[m] / s);
+        w.wd[m] = (double)w.w[m];
+    }
     return w;
 }
 
